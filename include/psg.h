@@ -1,0 +1,224 @@
+/*
+ * psg.h — C ABI of the B200-native SparkNet data-parallel hot path (libpsg.so).
+ *
+ * The reference (`/root/reference/proj`, "parasgd") is header-only C++ with no FFI
+ * layer; its drop-in surface is the declarations in model.hpp / weights.hpp /
+ * data.hpp / schemes.hpp.  This header is the thin C boundary that a C++ (or
+ * ctypes / cgo / JNI) host binds to; every entry point below names the
+ * reference interface it replaces.  Plain pointers and sizes only, no torch
+ * types.  All host-visible tensors use the reference's layouts:
+ *   images  : [n, c, h, w] row-major (NCHW), as Batch::images (batch.hpp:11-16)
+ *   weights : WeightCollection order (weights.hpp:19-86): layer declaration
+ *             order x {kernel, bias} x row-major; conv kernels [F, C/G, kh, kw],
+ *             linear weights [O, D] with D flattened in CHW order
+ *             (model.hpp:409).
+ * Internally the device keeps activations NHWC and conv kernels [F, kh, kw, C/G];
+ * the boundary converts.
+ *
+ * Error model: every call returns a status code; the message of
+ * the last failure on the calling thread is psg_last_error().
+ *   PSG_EINVAL   <-> std::invalid_argument  (structure / shape / argument errors)
+ *   PSG_ERUNTIME <-> std::runtime_error     (non-finite values, missing data)
+ *   PSG_ECUDA    <-> CUDA / NCCL failures
+ *   PSG_ELOGIC   <-> std::logic_error
+ */
+#ifndef PSG_H_
+#define PSG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSG_ABI_VERSION 1
+
+enum psg_status {
+  PSG_OK = 0,
+  PSG_EINVAL = 1,
+  PSG_ERUNTIME = 2,
+  PSG_ECUDA = 3,
+  PSG_ELOGIC = 4
+};
+
+/* LayerKind (net_spec.hpp:11) plus the Caffe kinds the BASELINE configs need. */
+enum psg_layer_kind {
+  PSG_LAYER_DATA = 0,
+  PSG_LAYER_LABEL = 1,
+  PSG_LAYER_CONV = 2,
+  PSG_LAYER_POOL = 3,
+  PSG_LAYER_LINEAR = 4,
+  PSG_LAYER_RELU = 5,
+  PSG_LAYER_SOFTMAX_LOSS = 6,
+  PSG_LAYER_LRN = 7,      /* extension: Caffe LRN ACROSS_CHANNELS */
+  PSG_LAYER_DROPOUT = 8,  /* extension: Caffe dropout (counter-hash mask) */
+  PSG_LAYER_CONCAT = 9    /* extension: channel concat (reserved) */
+};
+
+enum psg_pool_method { PSG_POOL_MAX = 0, PSG_POOL_AVE = 1 };
+
+enum psg_precision {
+  PSG_PRECISION_FP32 = 0, /* strict mode: fp32 SIMT FFMA, 1e-5 parity bar */
+  PSG_PRECISION_TF32 = 1  /* fast mode: tcgen05 kind::tf32, fp32 accumulate, 1e-2 bar */
+};
+
+enum psg_average_mode {
+  PSG_AVERAGE_FAST = 0,    /* NCCL allreduce-sum x 1/K */
+  PSG_AVERAGE_ORDERED = 1  /* ascending-k fp64 accumulation, /K, one rounding (weights.hpp:90-107) */
+};
+
+/*
+ * One declarative layer: LayerSpec (net_spec.hpp:28-38) widened with Caffe
+ * geometry.  Zero/defaults (psg_layer_desc_init) reproduce the reference:
+ * stride 1, no pad, group 1, floor-mode pooling, lr/decay multipliers 1.
+ */
+typedef struct psg_layer_desc {
+  int kind;                /* psg_layer_kind */
+  char name[48];
+  int n_inputs;
+  int inputs[8];           /* indices of earlier layers (topological order) */
+  int batch, channels, height, width; /* data: [b,c,h,w]; label: batch */
+  int num_output;          /* conv filters / linear outputs */
+  int kernel_h, kernel_w;
+  int stride_h, stride_w;
+  int pad_h, pad_w;
+  int group;
+  int pool;                /* psg_pool_method */
+  int ceil_mode;           /* 0: reference floor mode (model.hpp:244); 1: Caffe ceil */
+  int local_size;          /* LRN */
+  double alpha, beta, k;   /* LRN */
+  double dropout_ratio;    /* dropout */
+  double loss_weight;      /* softmax loss (1.0 = reference) */
+  double lr_mult_w, lr_mult_b, decay_mult_w, decay_mult_b;
+} psg_layer_desc;
+
+/* Fills defaults; name is truncated to 47 bytes. */
+void psg_layer_desc_init(psg_layer_desc* d, int kind, const char* name);
+
+typedef struct psg_ctx psg_ctx;
+typedef struct psg_dataset psg_dataset;
+typedef struct psg_net psg_net;
+typedef struct psg_comm psg_comm;
+typedef struct psg_buffer psg_buffer;
+
+const char* psg_last_error(void);
+int psg_abi_version(void);
+int psg_device_count(int* n);
+
+/* ---- host-side reference semantics (bit-exact integer work) ---------------- */
+/* splitmix64 / derive_seed (rng.hpp:11-25). */
+uint64_t psg_splitmix64(uint64_t x);
+uint64_t psg_derive_seed(uint64_t base, const uint64_t* parts, int nparts);
+/* shard() permutation + split (data.hpp:261-288): perm[n], offsets[workers+1]. */
+int psg_shard(size_t n, int workers, uint64_t seed, uint64_t* perm, uint64_t* offsets);
+/* worker_stream_seed (data.hpp:386-388). */
+uint64_t psg_worker_stream_seed(uint64_t global_seed, int worker_id);
+/* ShardBatchIterator::start_epoch order (data.hpp:338-343). */
+int psg_epoch_order(const uint64_t* shard_indices, size_t n, uint64_t stream_seed,
+                    uint64_t epoch, uint64_t* order);
+/* generate_synthetic (data.hpp:111-155), NCHW fp64 on the host. */
+int psg_generate_synthetic(int classes, size_t c, size_t h, size_t w, size_t per_class,
+                           double separation, uint64_t seed, uint64_t variant, double* images,
+                           int32_t* labels);
+
+/* ---- device context --------------------------------------------------------- */
+int psg_ctx_create(int device, psg_ctx** out);
+int psg_ctx_destroy(psg_ctx* ctx);
+int psg_ctx_sync(psg_ctx* ctx);
+
+/* ---- datasets: Dataset (data.hpp:21-41) resident in HBM --------------------- */
+int psg_dataset_upload_f64(psg_ctx* ctx, const double* images, const int32_t* labels, size_t n,
+                           int c, int h, int w, int num_classes, psg_dataset** out);
+int psg_dataset_upload_f32(psg_ctx* ctx, const float* images, const int32_t* labels, size_t n,
+                           int c, int h, int w, int num_classes, psg_dataset** out);
+/* Host generator (bit-exact with the reference) followed by upload. */
+int psg_dataset_synthetic(psg_ctx* ctx, int classes, int c, int h, int w, size_t per_class,
+                          double separation, uint64_t seed, uint64_t variant, psg_dataset** out);
+int psg_dataset_size(const psg_dataset* ds, size_t* n);
+int psg_dataset_destroy(psg_dataset* ds);
+
+/* ---- nets: class Net (model.hpp:50-597) ------------------------------------- */
+/* Net(NetSpec, seed) (model.hpp:52-55, init at :200-283). */
+int psg_net_create(psg_ctx* ctx, const psg_layer_desc* layers, int n_layers, uint64_t seed,
+                   psg_net** out);
+int psg_net_destroy(psg_net* net);
+int psg_net_num_classes(const psg_net* net, int* classes);
+/* Flat parameter count P (sum of WeightCollection tensor volumes). */
+int psg_net_param_count(const psg_net* net, size_t* n);
+/* WeightCollection structure: tensors in order; layer index, tensor slot
+ * (0 kernel / 1 bias), rank and reference-order shape, flat offset. */
+int psg_net_num_tensors(const psg_net* net, int* n);
+int psg_net_tensor_info(const psg_net* net, int t, int* layer, int* slot, int* rank,
+                        int64_t shape[4], size_t* offset);
+int psg_net_set_precision(psg_net* net, int precision);
+/* set_sgd (model.hpp:60-66) + weight decay extension (0 = reference). */
+int psg_net_set_sgd(psg_net* net, double learning_rate, double momentum, double weight_decay);
+/* get_weights / set_weights (model.hpp:140-171); fp32 <-> fp64 exact widening,
+ * round-to-nearest narrowing.  Momentum untouched by set. */
+int psg_net_get_weights_f64(psg_net* net, double* flat, size_t n);
+int psg_net_set_weights_f64(psg_net* net, const double* flat, size_t n);
+int psg_net_get_velocity_f64(psg_net* net, double* flat, size_t n);
+int psg_net_reset_velocity(psg_net* net);
+/* forward(Batch) (model.hpp:74-78): loss + probabilities [n, classes]. */
+int psg_net_forward(psg_net* net, const double* images, const int32_t* labels, size_t n,
+                    double* loss, double* probs);
+/* backward(Batch) (model.hpp:83-86): gradient in WeightCollection order. */
+int psg_net_backward(psg_net* net, const double* images, const int32_t* labels, size_t n,
+                     double* loss, double* grads);
+/* apply_update(grads) (model.hpp:90-107). */
+int psg_net_apply_update(psg_net* net, const double* grads, size_t n);
+/* Per-layer state of the last forward/backward, reference NCHW order (parity harness). */
+int psg_net_layer_shape(const psg_net* net, int layer, int64_t shape[4]);
+int psg_net_layer_output(psg_net* net, int layer, double* out, size_t n);
+int psg_net_layer_grad(psg_net* net, int layer, double* out, size_t n);
+/* set_training_data(make_worker_iterator(...)) with the shard kept on device:
+ * ShardBatchIterator semantics (data.hpp:312-351). */
+int psg_net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* shard_indices,
+                         size_t count, size_t batch, uint64_t stream_seed);
+/* Continue from another net's iterator position (the warm-start master shares
+ * worker 0's stream, schemes.hpp:314). Copies the iterator state. */
+int psg_net_copy_stream_state(psg_net* dst, const psg_net* src);
+/* train(steps) (model.hpp:111-118); enqueued on the net's stream.  A non-finite
+ * value raises PSG_ERUNTIME at the next psg_net_sync (sticky device flag). */
+int psg_net_train(psg_net* net, long steps);
+int psg_net_sync(psg_net* net);
+/* Device time of the last psg_net_train call's kernels (CUDA events on the
+ * net's stream), ms; valid after psg_net_sync. */
+int psg_net_last_train_ms(psg_net* net, float* ms);
+int psg_net_last_loss(psg_net* net, double* loss);
+/* set_validation_data(SequentialBatchIterator) + test(steps) (model.hpp:122-136). */
+int psg_net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch);
+int psg_net_test(psg_net* net, long steps, double* accuracy);
+/* Kernel launches of one training step (device-side work count). */
+int psg_net_kernels_per_step(const psg_net* net, int* launches);
+
+/* ---- averaging: weights_mean (weights.hpp:90-107) ---------------------------- */
+/* K nets on one device: ordered mean written back into every net. */
+int psg_average_local(psg_net* const* nets, int count);
+/* NCCL communicators (one per rank/device). */
+int psg_comm_unique_id(unsigned char id[128]);
+int psg_comm_create(psg_ctx* ctx, int nranks, int rank, const unsigned char id[128],
+                    psg_comm** out);
+int psg_comm_create_all(psg_ctx* const* ctxs, int ndev, psg_comm** out);
+int psg_comm_destroy(psg_comm* comm);
+/* In-place average of every net's flat parameters across the communicator.
+ * count = nets driven by this caller (1 per process, or ndev in one process). */
+int psg_comm_average(psg_comm* const* comms, psg_net* const* nets, int count, int mode);
+int psg_comm_broadcast(psg_comm* const* comms, psg_net* const* nets, int count, int root);
+
+/* ---- raw flat buffers (averaging-only sweep) -------------------------------- */
+int psg_buffer_create(psg_ctx* ctx, size_t n, psg_buffer** out);
+int psg_buffer_fill_uniform(psg_buffer* buf, uint64_t seed, double lo, double hi);
+int psg_buffer_read(psg_buffer* buf, float* host, size_t n);
+int psg_buffer_write(psg_buffer* buf, const float* host, size_t n);
+int psg_buffer_destroy(psg_buffer* buf);
+int psg_buffer_average_local(psg_buffer* const* bufs, int count);
+int psg_comm_average_buffer(psg_comm* const* comms, psg_buffer* const* bufs, int count,
+                            int mode, float* device_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSG_H_ */
