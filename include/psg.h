@@ -176,9 +176,11 @@ int psg_net_layer_grad(psg_net* net, int layer, double* out, size_t n);
  * ShardBatchIterator semantics (data.hpp:312-351). */
 int psg_net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* shard_indices,
                          size_t count, size_t batch, uint64_t stream_seed);
-/* Continue from another net's iterator position (the warm-start master shares
- * worker 0's stream, schemes.hpp:314). Copies the iterator state. */
-int psg_net_copy_stream_state(psg_net* dst, const psg_net* src);
+/* Iterator position (epoch, cursor) of the attached shard stream.  Lets a host
+ * share one ShardBatchIterator between nets (the warm-start master consumes
+ * worker 0's stream, schemes.hpp:314). */
+int psg_net_get_stream_position(const psg_net* net, uint64_t* epoch, uint64_t* cursor);
+int psg_net_set_stream_position(psg_net* net, uint64_t epoch, uint64_t cursor);
 /* train(steps) (model.hpp:111-118); enqueued on the net's stream.  A non-finite
  * value raises PSG_ERUNTIME at the next psg_net_sync (sticky device flag). */
 int psg_net_train(psg_net* net, long steps);

@@ -1,0 +1,519 @@
+// HBM-bound kernels of the training step (NHWC, fp32).  Every reduction is a
+// fixed-order gather (no float atomics), so a step is bitwise reproducible.
+#include <algorithm>
+#include <cfloat>
+
+#include "psg_internal.h"
+
+namespace psg {
+namespace {
+
+inline int grid_for(size_t n, int block = 256, int max_blocks = 148 * 16) {
+  const size_t b = (n + block - 1) / block;
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(b, max_blocks)));
+}
+
+#define GRID_STRIDE(i, n)                                                          \
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < (n); \
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:11-16
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// ------------------------------------------------------------------ pool ---
+// model.hpp:369-406 (max, strict '>' so the first maximum in (u, v) scan order
+// wins) with Caffe padding / ceil windows; AVE divides by the window clipped to
+// the padded extent.  route = (u * kw + v) relative to the unclipped window.
+__global__ void pool_fwd_k(PoolGeom g, const float* __restrict__ x, float* __restrict__ y,
+                           uint8_t* __restrict__ route) {
+  const size_t total = static_cast<size_t>(g.n) * g.OH * g.OW * g.C;
+  GRID_STRIDE(i, total) {
+    const int c = static_cast<int>(i % g.C);
+    size_t t = i / g.C;
+    const int ow = static_cast<int>(t % g.OW);
+    t /= g.OW;
+    const int oh = static_cast<int>(t % g.OH);
+    const int b = static_cast<int>(t / g.OH);
+    const int hs0 = oh * g.sh - g.ph, ws0 = ow * g.sw - g.pw;
+    const int he0 = hs0 + g.kh, we0 = ws0 + g.kw;
+    const int hs = max(hs0, 0), ws = max(ws0, 0), he = min(he0, g.H), we = min(we0, g.W);
+    const float* xb = x + static_cast<size_t>(b) * g.H * g.W * g.C + c;
+    if (g.method == PSG_POOL_AVE) {
+      const int size = (min(he0, g.H + g.ph) - hs0) * (min(we0, g.W + g.pw) - ws0);
+      float acc = 0.f;
+      for (int r = hs; r < he; ++r)
+        for (int s = ws; s < we; ++s) acc += xb[(static_cast<size_t>(r) * g.W + s) * g.C];
+      y[i] = acc / static_cast<float>(size);
+    } else {
+      float best = xb[(static_cast<size_t>(hs) * g.W + ws) * g.C];
+      int arg = (hs - hs0) * g.kw + (ws - ws0);
+      for (int r = hs; r < he; ++r) {
+        for (int s = ws; s < we; ++s) {
+          const float v = xb[(static_cast<size_t>(r) * g.W + s) * g.C];
+          if (v > best) {
+            best = v;
+            arg = (r - hs0) * g.kw + (s - ws0);
+          }
+        }
+      }
+      y[i] = best;
+      route[i] = static_cast<uint8_t>(arg);
+    }
+  }
+}
+
+// model.hpp:492-498 as a deterministic gather: each input sums, in ascending
+// output order, the dy of the covering windows that routed to it.
+__global__ void pool_bwd_k(PoolGeom g, const float* __restrict__ dy,
+                           const uint8_t* __restrict__ route, float* __restrict__ dx,
+                           int accumulate) {
+  const size_t total = static_cast<size_t>(g.n) * g.H * g.W * g.C;
+  GRID_STRIDE(i, total) {
+    const int c = static_cast<int>(i % g.C);
+    size_t t = i / g.C;
+    const int w = static_cast<int>(t % g.W);
+    t /= g.W;
+    const int h = static_cast<int>(t % g.H);
+    const int b = static_cast<int>(t / g.H);
+    // windows with oh*sh - ph <= h < oh*sh - ph + kh
+    const int ohl = max(0, (h + g.ph - g.kh + g.sh) / g.sh), ohh = min(g.OH - 1, (h + g.ph) / g.sh);
+    const int owl = max(0, (w + g.pw - g.kw + g.sw) / g.sw), owh = min(g.OW - 1, (w + g.pw) / g.sw);
+    const size_t obase = static_cast<size_t>(b) * g.OH * g.OW;
+    float acc = 0.f;
+    for (int oh = ohl; oh <= ohh; ++oh) {
+      const int hs0 = oh * g.sh - g.ph;
+      if (h < hs0 || h >= hs0 + g.kh) continue;
+      for (int ow = owl; ow <= owh; ++ow) {
+        const int ws0 = ow * g.sw - g.pw;
+        if (w < ws0 || w >= ws0 + g.kw) continue;
+        const size_t o = (obase + static_cast<size_t>(oh) * g.OW + ow) * g.C + c;
+        if (g.method == PSG_POOL_AVE) {
+          const int size =
+              (min(hs0 + g.kh, g.H + g.ph) - hs0) * (min(ws0 + g.kw, g.W + g.pw) - ws0);
+          acc += dy[o] / static_cast<float>(size);
+        } else if (route[o] == (h - hs0) * g.kw + (w - ws0)) {
+          acc += dy[o];
+        }
+      }
+    }
+    dx[i] = accumulate ? dx[i] + acc : acc;
+  }
+}
+
+// ------------------------------------------------------------------ relu ---
+__global__ void relu_fwd_k(const float* __restrict__ x, float* __restrict__ y, size_t n) {
+  const size_t n4 = n / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4* y4 = reinterpret_cast<float4*>(y);
+  GRID_STRIDE(i, n4) {
+    float4 v = x4[i];
+    v.x = v.x > 0.f ? v.x : 0.f;
+    v.y = v.y > 0.f ? v.y : 0.f;
+    v.z = v.z > 0.f ? v.z : 0.f;
+    v.w = v.w > 0.f ? v.w : 0.f;
+    y4[i] = v;
+  }
+  GRID_STRIDE(j, n - n4 * 4) {
+    const size_t i = n4 * 4 + j;
+    y[i] = x[i] > 0.f ? x[i] : 0.f;
+  }
+}
+
+__global__ void relu_bwd_k(const float* __restrict__ x, const float* __restrict__ dy,
+                           float* __restrict__ dx, size_t n, int accumulate) {
+  GRID_STRIDE(i, n) {
+    const float g = x[i] > 0.f ? dy[i] : 0.f;  // model.hpp:489
+    dx[i] = accumulate ? dx[i] + g : g;
+  }
+}
+
+// ------------------------------------------------------------------- lrn ---
+// Caffe LRN ACROSS_CHANNELS on NHWC: the channel window is contiguous.
+__global__ void lrn_fwd_k(LrnGeom g, const float* __restrict__ x, float* __restrict__ y,
+                          float* __restrict__ scale) {
+  const size_t total = static_cast<size_t>(g.pixels) * g.C;
+  const int pre = (g.size - 1) / 2, post = g.size - pre - 1;
+  const float a = g.alpha / g.size;
+  GRID_STRIDE(i, total) {
+    const int c = static_cast<int>(i % g.C);
+    const float* row = x + (i - c);
+    const int lo = max(0, c - pre), hi = min(g.C - 1, c + post);
+    float acc = 0.f;
+    for (int q = lo; q <= hi; ++q) acc += row[q] * row[q];
+    const float s = g.k + a * acc;
+    scale[i] = s;
+    y[i] = x[i] * powf(s, -g.beta);
+  }
+}
+
+__global__ void lrn_bwd_k(LrnGeom g, const float* __restrict__ x, const float* __restrict__ y,
+                          const float* __restrict__ scale, const float* __restrict__ dy,
+                          float* __restrict__ dx, int accumulate) {
+  const size_t total = static_cast<size_t>(g.pixels) * g.C;
+  const int pre = (g.size - 1) / 2, post = g.size - pre - 1;
+  const float ratio = 2.f * g.alpha * g.beta / g.size;
+  GRID_STRIDE(i, total) {
+    const int c = static_cast<int>(i % g.C);
+    const size_t base = i - c;
+    const int lo = max(0, c - post), hi = min(g.C - 1, c + pre);
+    float acc = 0.f;
+    for (int q = lo; q <= hi; ++q) acc += dy[base + q] * y[base + q] / scale[base + q];
+    const float v = dy[i] * powf(scale[i], -g.beta) - ratio * x[i] * acc;
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+
+// --------------------------------------------------------------- dropout ---
+// Keep-mask = splitmix64(mix(base ^ step) + nchw_index) >> 40 >= ratio * 2^24.
+__device__ __forceinline__ float drop_mask(const DropGeom& g, uint64_t base, size_t i,
+                                           uint32_t thresh, float keep) {
+  const int c = static_cast<int>(i % g.C);
+  size_t t = i / g.C;
+  const int w = static_cast<int>(t % g.W);
+  t /= g.W;
+  const int h = static_cast<int>(t % g.H);
+  const size_t b = t / g.H;
+  const uint64_t nchw = ((b * g.C + c) * g.H + h) * g.W + w;
+  const uint32_t u = static_cast<uint32_t>(mix64(base + nchw) >> 40);
+  return u >= thresh ? keep : 0.f;
+}
+
+__global__ void dropout_fwd_k(DropGeom g, const float* __restrict__ x, float* __restrict__ y,
+                              const uint64_t* __restrict__ d_step, int train) {
+  const size_t total = static_cast<size_t>(g.n) * g.C * g.H * g.W;
+  if (!train) {
+    GRID_STRIDE(i, total) y[i] = x[i];
+    return;
+  }
+  const uint64_t base = mix64(g.base_seed ^ *d_step);
+  const uint32_t thresh = static_cast<uint32_t>(static_cast<double>(g.ratio) * 16777216.0);
+  const float keep = static_cast<float>(1.0 / (1.0 - static_cast<double>(g.ratio)));
+  GRID_STRIDE(i, total) y[i] = x[i] * drop_mask(g, base, i, thresh, keep);
+}
+
+__global__ void dropout_bwd_k(DropGeom g, const float* __restrict__ dy, float* __restrict__ dx,
+                              const uint64_t* __restrict__ d_step, int accumulate) {
+  const size_t total = static_cast<size_t>(g.n) * g.C * g.H * g.W;
+  const uint64_t base = mix64(g.base_seed ^ *d_step);
+  const uint32_t thresh = static_cast<uint32_t>(static_cast<double>(g.ratio) * 16777216.0);
+  const float keep = static_cast<float>(1.0 / (1.0 - static_cast<double>(g.ratio)));
+  GRID_STRIDE(i, total) {
+    const float v = dy[i] * drop_mask(g, base, i, thresh, keep);
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+
+// ---------------------------------------------------------- softmax-loss ---
+// model.hpp:429-451 + :463-475.  One warp per row; the row math runs in fp64
+// (tiny), probabilities and the loss seed are rounded once to fp32.
+__global__ void softmax_loss_k(const float* __restrict__ logits, const int32_t* __restrict__ labels,
+                               int n, int C, double scale, float* __restrict__ probs,
+                               float* __restrict__ dlogits, double* __restrict__ row_loss) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (warp >= n) return;
+  const float* row = logits + static_cast<size_t>(warp) * C;
+  float mx = -FLT_MAX;
+  for (int j = lane; j < C; j += 32) mx = fmaxf(mx, row[j]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double sum = 0.0;
+  for (int j = lane; j < C; j += 32) sum += exp(static_cast<double>(row[j]) - mx);
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const int y = labels[warp];
+  for (int j = lane; j < C; j += 32) {
+    const double p = exp(static_cast<double>(row[j]) - mx) / sum;
+    probs[static_cast<size_t>(warp) * C + j] = static_cast<float>(p);
+    if (dlogits)
+      dlogits[static_cast<size_t>(warp) * C + j] =
+          static_cast<float>(p * scale - (j == y ? scale : 0.0));
+  }
+  if (lane == 0) row_loss[warp] = -((static_cast<double>(row[y]) - mx) - log(sum));
+}
+
+// Fixed-order reduction of the per-row losses: loss = sum / n * loss_weight.
+__global__ void loss_reduce_k(const double* __restrict__ row_loss, int n, double lw,
+                              double* __restrict__ loss, int* __restrict__ flag) {
+  __shared__ double part[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += row_loss[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double l = part[0] / n * lw;
+    *loss = l;
+    if (!isfinite(l)) *flag = 1;
+  }
+}
+
+// tensor.hpp:187-201 argmax (lowest index wins) + model.hpp:129-133 count.
+__global__ void argmax_count_k(const float* __restrict__ probs, const int32_t* __restrict__ labels,
+                               int n, int C, unsigned long long* correct) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* p = probs + static_cast<size_t>(i) * C;
+  int best = 0;
+  for (int j = 1; j < C; ++j)
+    if (p[j] > p[best]) best = j;
+  if (best == labels[i]) atomicAdd(correct, 1ULL);
+}
+
+// ---------------------------------------------------------------- gather ---
+// data.hpp:292-304 gather_batch from the HBM-resident shard (NHWC rows).
+__global__ void gather_k(const float* __restrict__ ds, const int32_t* __restrict__ ds_labels,
+                         const uint32_t* __restrict__ idx, const int* __restrict__ cursor, int b,
+                         int pixels, int C, int cs, float* __restrict__ out,
+                         int32_t* __restrict__ labels) {
+  const int i = blockIdx.y;
+  const uint32_t row = idx[static_cast<size_t>(cursor ? *cursor : 0) * b + i];
+  const float* src = ds + static_cast<size_t>(row) * pixels * C;
+  float* dst = out + static_cast<size_t>(i) * pixels * cs;
+  if (blockIdx.x == 0 && threadIdx.x == 0) labels[i] = ds_labels[row];
+  if (cs == C) {
+    const size_t n = static_cast<size_t>(pixels) * C;
+    if ((n % 4) == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      for (size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; j < n / 4;
+           j += static_cast<size_t>(gridDim.x) * blockDim.x)
+        d4[j] = __ldg(s4 + j);
+    } else {
+      for (size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; j < n;
+           j += static_cast<size_t>(gridDim.x) * blockDim.x)
+        dst[j] = __ldg(src + j);
+    }
+  } else {
+    const size_t n = static_cast<size_t>(pixels) * cs;
+    for (size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<size_t>(gridDim.x) * blockDim.x) {
+      const int c = static_cast<int>(j % cs);
+      const size_t p = j / cs;
+      dst[j] = c < C ? __ldg(src + p * C + c) : 0.f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- update ---
+// model.hpp:90-107 + tensor.hpp:60-71 fused into one pass over the flat
+// buffer: g' = g + wd*w; v = mu*v + g'; w += -lr*v  (mu = 0: w += -lr*g').
+// A sticky flag replaces ensure_finite; block 0 also advances the per-step
+// device counters (batch cursor, dropout step) for the next graph replay.
+__global__ void sgd_update_k(const UpdateChunk* __restrict__ chunks, float* __restrict__ w,
+                             float* __restrict__ v, const float* __restrict__ g, float mu,
+                             int* __restrict__ flag, int* __restrict__ cursor,
+                             uint64_t* __restrict__ step) {
+  const UpdateChunk ch = chunks[blockIdx.x];
+  bool bad = false;
+  const uint32_t vec_end = ch.begin + ((ch.end - ch.begin) / 4) * 4;
+  for (uint32_t i = ch.begin + threadIdx.x * 4; i < vec_end; i += blockDim.x * 4) {
+    float4 wv = *reinterpret_cast<float4*>(w + i);
+    const float4 gv = *reinterpret_cast<const float4*>(g + i);
+    float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+    float ww[4] = {wv.x, wv.y, wv.z, wv.w};
+    if (ch.wd != 0.f)
+      for (int q = 0; q < 4; ++q) gg[q] = fmaf(ch.wd, ww[q], gg[q]);
+    if (mu > 0.f) {
+      float4 vv = *reinterpret_cast<float4*>(v + i);
+      float vq[4] = {vv.x, vv.y, vv.z, vv.w};
+      for (int q = 0; q < 4; ++q) {
+        vq[q] = fmaf(mu, vq[q], gg[q]);
+        ww[q] = fmaf(-ch.lr, vq[q], ww[q]);
+        bad |= !isfinite(vq[q]) || !isfinite(ww[q]);
+      }
+      *reinterpret_cast<float4*>(v + i) = make_float4(vq[0], vq[1], vq[2], vq[3]);
+    } else {
+      for (int q = 0; q < 4; ++q) {
+        ww[q] = fmaf(-ch.lr, gg[q], ww[q]);
+        bad |= !isfinite(ww[q]);
+      }
+    }
+    *reinterpret_cast<float4*>(w + i) = make_float4(ww[0], ww[1], ww[2], ww[3]);
+  }
+  for (uint32_t i = vec_end + threadIdx.x; i < ch.end; i += blockDim.x) {
+    float gi = g[i];
+    if (ch.wd != 0.f) gi = fmaf(ch.wd, w[i], gi);
+    if (mu > 0.f) {
+      v[i] = fmaf(mu, v[i], gi);
+      w[i] = fmaf(-ch.lr, v[i], w[i]);
+      bad |= !isfinite(v[i]);
+    } else {
+      w[i] = fmaf(-ch.lr, gi, w[i]);
+    }
+    bad |= !isfinite(w[i]);
+  }
+  if (bad) *flag = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (cursor) *cursor += 1;
+    if (step) *step += 1;
+  }
+}
+
+// weights.hpp:90-107: acc = 0; acc += w_k for k ascending; acc /= K (fp64, one rounding).
+struct PtrPack {
+  float* p[64];
+};
+
+// out == nullptr: write the mean back into every input; else into out only.
+__global__ void average_ordered_k(PtrPack bufs, int K, size_t n, float* out, int* flag) {
+  const size_t n4 = n / 4;
+  GRID_STRIDE(i, n4) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const float4 t = reinterpret_cast<const float4*>(bufs.p[k])[i];
+      a0 += t.x;
+      a1 += t.y;
+      a2 += t.z;
+      a3 += t.w;
+    }
+    const double kk = K;
+    const float4 r = make_float4(static_cast<float>(a0 / kk), static_cast<float>(a1 / kk),
+                                 static_cast<float>(a2 / kk), static_cast<float>(a3 / kk));
+    if (!isfinite(r.x) || !isfinite(r.y) || !isfinite(r.z) || !isfinite(r.w)) *flag = 1;
+    if (out)
+      reinterpret_cast<float4*>(out)[i] = r;
+    else
+      for (int k = 0; k < K; ++k) reinterpret_cast<float4*>(bufs.p[k])[i] = r;
+  }
+  GRID_STRIDE(j, n - n4 * 4) {
+    const size_t i = n4 * 4 + j;
+    double a = 0.0;
+    for (int k = 0; k < K; ++k) a += bufs.p[k][i];
+    const float r = static_cast<float>(a / K);
+    if (!isfinite(r)) *flag = 1;
+    if (out)
+      out[i] = r;
+    else
+      for (int k = 0; k < K; ++k) bufs.p[k][i] = r;
+  }
+}
+
+__global__ void scale_k(float* x, size_t n, float a, int* flag) {
+  GRID_STRIDE(i, n) {
+    const float r = x[i] * a;
+    if (!isfinite(r)) *flag = 1;
+    x[i] = r;
+  }
+}
+
+__global__ void fill_uniform_k(float* x, size_t n, uint64_t seed, double lo, double hi) {
+  GRID_STRIDE(i, n) {
+    const double u = static_cast<double>(mix64(seed + i) >> 11) * 0x1.0p-53;
+    x[i] = static_cast<float>(lo + (hi - lo) * u);
+  }
+}
+
+}  // namespace
+
+void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaStream_t s) {
+  const size_t n = static_cast<size_t>(g.n) * g.OH * g.OW * g.C;
+  pool_fwd_k<<<grid_for(n), 256, 0, s>>>(g, x, y, route);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
+              bool accumulate, cudaStream_t s) {
+  const size_t n = static_cast<size_t>(g.n) * g.H * g.W * g.C;
+  pool_bwd_k<<<grid_for(n), 256, 0, s>>>(g, dy, route, dx, accumulate);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s) {
+  relu_fwd_k<<<grid_for(n / 4 + 1), 256, 0, s>>>(x, y, n);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumulate,
+              cudaStream_t s) {
+  relu_bwd_k<<<grid_for(n), 256, 0, s>>>(x, dy, dx, n, accumulate);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void lrn_fwd(const LrnGeom& g, const float* x, float* y, float* scale, cudaStream_t s) {
+  lrn_fwd_k<<<grid_for(static_cast<size_t>(g.pixels) * g.C), 256, 0, s>>>(g, x, y, scale);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void lrn_bwd(const LrnGeom& g, const float* x, const float* y, const float* scale,
+             const float* dy, float* dx, bool accumulate, cudaStream_t s) {
+  lrn_bwd_k<<<grid_for(static_cast<size_t>(g.pixels) * g.C), 256, 0, s>>>(g, x, y, scale, dy,
+                                                                          dx, accumulate);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void dropout_fwd(const DropGeom& g, const float* x, float* y, const uint64_t* d_step, bool train,
+                 cudaStream_t s) {
+  const size_t n = static_cast<size_t>(g.n) * g.C * g.H * g.W;
+  dropout_fwd_k<<<grid_for(n), 256, 0, s>>>(g, x, y, d_step, train);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void dropout_bwd(const DropGeom& g, const float* dy, float* dx, const uint64_t* d_step,
+                 bool accumulate, cudaStream_t s) {
+  const size_t n = static_cast<size_t>(g.n) * g.C * g.H * g.W;
+  dropout_bwd_k<<<grid_for(n), 256, 0, s>>>(g, dy, dx, d_step, accumulate);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void softmax_loss(const float* logits, const int32_t* labels, int n, int C, double loss_weight,
+                  float* probs, float* dlogits, double* row_loss, double* loss, int* flag,
+                  cudaStream_t s) {
+  const double scale = loss_weight * (1.0 / static_cast<double>(n));
+  softmax_loss_k<<<(n * 32 + 255) / 256, 256, 0, s>>>(logits, labels, n, C, scale, probs, dlogits,
+                                                      row_loss);
+  PSG_CUDA(cudaGetLastError());
+  loss_reduce_k<<<1, 256, 0, s>>>(row_loss, n, loss_weight, loss, flag);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void argmax_count(const float* probs, const int32_t* labels, int n, int C,
+                  unsigned long long* correct, cudaStream_t s) {
+  argmax_count_k<<<(n + 255) / 256, 256, 0, s>>>(probs, labels, n, C, correct);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void gather_batch(const float* ds_images, const int32_t* ds_labels, const uint32_t* idx,
+                  const int* cursor, int b, int pixels, int C, int cs, float* out,
+                  int32_t* labels, cudaStream_t s) {
+  const size_t per_row = static_cast<size_t>(pixels) * cs;
+  const int bx = static_cast<int>(std::max<size_t>(1, std::min<size_t>((per_row / 4 + 255) / 256, 64)));
+  gather_k<<<dim3(bx, b), 256, 0, s>>>(ds_images, ds_labels, idx, cursor, b, pixels, C, cs, out,
+                                       labels);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void sgd_update(const UpdateChunk* chunks, int nchunks, float* w, float* v, const float* g,
+                float momentum, int* flag, int* cursor, uint64_t* step, cudaStream_t s) {
+  sgd_update_k<<<nchunks, 256, 0, s>>>(chunks, w, v, g, momentum, flag, cursor, step);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void average_ordered_into(float* const* bufs, int K, size_t n, float* out, int* flag,
+                          cudaStream_t s) {
+  if (K > 64) throw std::invalid_argument("average: at most 64 buffers");
+  PtrPack pp{};
+  for (int k = 0; k < K; ++k) pp.p[k] = bufs[k];
+  average_ordered_k<<<grid_for(n / 4 + 1), 256, 0, s>>>(pp, K, n, out, flag);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void average_ordered(float* const* bufs, int K, size_t n, int* flag, cudaStream_t s) {
+  average_ordered_into(bufs, K, n, nullptr, flag, s);
+}
+
+void scale_inplace(float* x, size_t n, float a, int* flag, cudaStream_t s) {
+  scale_k<<<grid_for(n), 256, 0, s>>>(x, n, a, flag);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void fill_uniform(float* x, size_t n, uint64_t seed, double lo, double hi, cudaStream_t s) {
+  fill_uniform_k<<<grid_for(n), 256, 0, s>>>(x, n, seed, lo, hi);
+  PSG_CUDA(cudaGetLastError());
+}
+
+}  // namespace psg

@@ -1,0 +1,868 @@
+// class Net (model.hpp:50-597) on one B200: shape inference and init on the host
+// (bit-exact with the reference RNG), flat fp32 parameter / gradient / velocity
+// buffers in HBM, NHWC activations, and one CUDA graph per training step
+// (gather -> forward -> loss -> backward -> fused SGD update).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "runtime.h"
+
+namespace psg {
+
+namespace {
+
+constexpr size_t kAlign = 32;  // tensor offsets in floats (128 B)
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool is_param_layer(int kind) { return kind == PSG_LAYER_CONV || kind == PSG_LAYER_LINEAR; }
+
+int pool_out(int in, int k, int s, int p, int ceil_mode) {
+  int o;
+  if (ceil_mode) {
+    o = (in + 2 * p - k + s - 1) / s + 1;
+    if (p > 0 && (o - 1) * s >= in + p) --o;
+  } else {
+    o = (in + 2 * p - k) / s + 1;  // model.hpp:244-245
+  }
+  return o;
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (n) PSG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+std::string lname(const psg_layer_desc& d) { return std::string(d.name); }
+
+// NetSpec::validate (net_spec.hpp:112-169) on the C descriptors.
+void validate(const psg_layer_desc* layers, int n) {
+  int n_data = 0, n_label = 0, n_loss = 0;
+  for (int li = 0; li < n; ++li) {
+    const psg_layer_desc& d = layers[li];
+    if (d.name[0] == 0) throw std::invalid_argument("net: layer with empty name");
+    for (int j = 0; j < li; ++j)
+      if (std::strncmp(layers[j].name, d.name, sizeof d.name) == 0)
+        throw std::invalid_argument("net: duplicate layer name '" + lname(d) + "'");
+    if (d.n_inputs < 0 || d.n_inputs > 8) throw std::invalid_argument("net: bad input count");
+    for (int i = 0; i < d.n_inputs; ++i)
+      if (d.inputs[i] < 0 || d.inputs[i] >= li)
+        throw std::invalid_argument("net: layer '" + lname(d) +
+                                    "' references a layer which is not declared earlier");
+    switch (d.kind) {
+      case PSG_LAYER_DATA:
+        ++n_data;
+        if (d.batch < 1 || d.channels < 1 || d.height < 1 || d.width < 1)
+          throw std::invalid_argument("net: data layer needs [b,c,h,w]");
+        break;
+      case PSG_LAYER_LABEL:
+        ++n_label;
+        break;
+      case PSG_LAYER_CONV:
+        if (d.n_inputs != 1) throw std::invalid_argument("net: conv takes one input");
+        if (d.kernel_h < 1 || d.kernel_w < 1 || d.num_output < 1 || d.stride_h < 1 ||
+            d.stride_w < 1 || d.pad_h < 0 || d.pad_w < 0 || d.group < 1)
+          throw std::invalid_argument("net: conv '" + lname(d) + "' has non-positive geometry");
+        break;
+      case PSG_LAYER_POOL:
+        if (d.n_inputs != 1) throw std::invalid_argument("net: pool takes one input");
+        if (d.kernel_h < 1 || d.kernel_w < 1 || d.stride_h < 1 || d.stride_w < 1 ||
+            d.kernel_h * d.kernel_w > 255)
+          throw std::invalid_argument("net: pool '" + lname(d) + "' has non-positive geometry");
+        break;
+      case PSG_LAYER_LINEAR:
+        if (d.n_inputs != 1) throw std::invalid_argument("net: linear takes one input");
+        if (d.num_output < 1)
+          throw std::invalid_argument("net: linear '" + lname(d) + "' needs positive outputs");
+        break;
+      case PSG_LAYER_RELU:
+      case PSG_LAYER_LRN:
+      case PSG_LAYER_DROPOUT:
+        if (d.n_inputs != 1) throw std::invalid_argument("net: layer takes one input");
+        if (d.kind == PSG_LAYER_LRN && (d.local_size < 1 || d.local_size % 2 == 0))
+          throw std::invalid_argument("net: lrn local_size must be odd");
+        if (d.kind == PSG_LAYER_DROPOUT && !(d.dropout_ratio >= 0.0 && d.dropout_ratio < 1.0))
+          throw std::invalid_argument("net: dropout ratio must be in [0,1)");
+        break;
+      case PSG_LAYER_SOFTMAX_LOSS:
+        ++n_loss;
+        if (d.n_inputs != 2) throw std::invalid_argument("net: softmax loss takes [logits, label]");
+        break;
+      default:
+        throw std::invalid_argument("net: unsupported layer kind");
+    }
+  }
+  if (n_data != 1) throw std::invalid_argument("net: exactly one data layer required");
+  if (n_label != 1) throw std::invalid_argument("net: exactly one label layer required");
+  if (n_loss != 1) throw std::invalid_argument("net: exactly one softmax loss layer required");
+}
+
+void free_batch_buffers(psg_net* net) {
+  for (LayerRt& l : net->L) {
+    dfree(l.out);
+    dfree(l.grad);
+    dfree(l.aux);
+    dfree(l.route);
+    l.out = l.grad = l.aux = nullptr;
+    l.route = nullptr;
+  }
+  dfree(net->row_loss);
+  dfree(net->labels);
+  dfree(net->ws.ptr);
+  net->row_loss = nullptr;
+  net->labels = nullptr;
+  net->ws = Workspace{};
+  net->cap = 0;
+}
+
+ConvGeom geom_for(const LayerRt& l, size_t n) {
+  ConvGeom g = l.cg;
+  g.n = static_cast<int>(n);
+  return g;
+}
+
+void invalidate_graph(psg_net* net) {
+  if (net->graph) cudaGraphExecDestroy(net->graph);
+  net->graph = nullptr;
+  net->graph_batch = 0;
+}
+
+// Activation / gradient buffers for a batch of n rows.
+void ensure_capacity(psg_net* net, size_t n) {
+  if (net->cap >= n) return;
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  invalidate_graph(net);
+  free_batch_buffers(net);
+  size_t ws = 0;
+  for (LayerRt& l : net->L) {
+    if (l.kind == PSG_LAYER_LABEL) continue;
+    const size_t elems = n * l.vol();
+    l.out = dalloc<float>(elems);
+    if (l.kind != PSG_LAYER_DATA) l.grad = dalloc<float>(elems);
+    if (l.kind == PSG_LAYER_LRN) l.aux = dalloc<float>(elems);
+    if (l.kind == PSG_LAYER_POOL && l.d.pool == PSG_POOL_MAX) l.route = dalloc<uint8_t>(elems);
+    if (is_param_layer(l.kind)) {
+      for (Mode m : {Mode::Strict, Mode::Tf32})
+        ws = std::max(ws, wgrad_workspace_elems(geom_for(l, n), m));
+    }
+  }
+  // the data layer's grad is never produced (first-layer dgrad is skipped)
+  net->row_loss = dalloc<double>(n);
+  net->labels = dalloc<int32_t>(n);
+  net->ws.ptr = dalloc<float>(ws);
+  net->ws.elems = ws;
+  net->cap = n;
+}
+
+void ensure_stage(psg_net* net, size_t floats, size_t rows) {
+  if (net->h_stage_cap >= floats && net->h_lab) return;
+  if (net->h_stage) cudaFreeHost(net->h_stage);
+  if (net->h_lab) cudaFreeHost(net->h_lab);
+  PSG_CUDA(cudaMallocHost(&net->h_stage, std::max<size_t>(floats, 1) * sizeof(float)));
+  PSG_CUDA(cudaMallocHost(&net->h_lab, std::max<size_t>(rows, 1024) * sizeof(int32_t)));
+  net->h_stage_cap = floats;
+}
+
+void build_chunks(psg_net* net) {
+  std::vector<UpdateChunk> ch;
+  constexpr uint32_t piece = 8192;
+  for (const TensorRec& t : net->tensors) {
+    const float lr = static_cast<float>(net->lr * t.lr_mult);
+    const float wd = static_cast<float>(net->wd * t.decay_mult);
+    for (size_t b = t.int_off; b < t.int_off + t.int_count; b += piece) {
+      const size_t e = std::min(t.int_off + t.int_count, b + piece);
+      ch.push_back(UpdateChunk{static_cast<uint32_t>(b), static_cast<uint32_t>(e), lr, wd});
+    }
+  }
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  if (static_cast<int>(ch.size()) != net->nchunks) {
+    dfree(net->d_chunks);
+    net->d_chunks = dalloc<UpdateChunk>(ch.size());
+    net->nchunks = static_cast<int>(ch.size());
+    invalidate_graph(net);
+  }
+  if (!ch.empty())
+    PSG_CUDA(cudaMemcpy(net->d_chunks, ch.data(), ch.size() * sizeof(UpdateChunk),
+                        cudaMemcpyHostToDevice));
+}
+
+// ---- forward / backward launch sequences (eager or under stream capture) ----
+int run_forward(psg_net* net, size_t n, bool train, bool seed_grad) {
+  cudaStream_t s = net->stream;
+  int launches = 0;
+  for (size_t li = 0; li < net->L.size(); ++li) {
+    LayerRt& l = net->L[li];
+    switch (l.kind) {
+      case PSG_LAYER_DATA:
+      case PSG_LAYER_LABEL:
+        break;
+      case PSG_LAYER_CONV:
+      case PSG_LAYER_LINEAR: {
+        const LayerRt& src = net->L[l.inputs[0]];
+        const TensorRec& k = net->tensors[l.kern_t];
+        const TensorRec& b = net->tensors[l.bias_t];
+        conv_fprop(geom_for(l, n), src.out, net->w + k.int_off, net->w + b.int_off, l.out, false,
+                   net->mode, s);
+        launches += conv_launches(geom_for(l, n), 0, net->mode);
+        break;
+      }
+      case PSG_LAYER_POOL: {
+        PoolGeom g = l.pg;
+        g.n = static_cast<int>(n);
+        pool_fwd(g, net->L[l.inputs[0]].out, l.out, l.route, s);
+        ++launches;
+        break;
+      }
+      case PSG_LAYER_RELU:
+        relu_fwd(net->L[l.inputs[0]].out, l.out, n * l.vol(), s);
+        ++launches;
+        break;
+      case PSG_LAYER_LRN: {
+        LrnGeom g = l.lg;
+        g.pixels = static_cast<int>(n) * l.H * l.W;
+        lrn_fwd(g, net->L[l.inputs[0]].out, l.out, l.aux, s);
+        ++launches;
+        break;
+      }
+      case PSG_LAYER_DROPOUT: {
+        DropGeom g = l.dg;
+        g.n = static_cast<int>(n);
+        dropout_fwd(g, net->L[l.inputs[0]].out, l.out, &net->dsc->step, train, s);
+        ++launches;
+        break;
+      }
+      case PSG_LAYER_SOFTMAX_LOSS: {
+        LayerRt& logits = net->L[l.inputs[0]];
+        softmax_loss(logits.out, net->labels, static_cast<int>(n), net->classes, l.d.loss_weight,
+                     l.out, seed_grad ? logits.grad : nullptr, net->row_loss, &net->dsc->loss,
+                     &net->dsc->flag, s);
+        launches += 2;
+        break;
+      }
+    }
+  }
+  return launches;
+}
+
+int run_backward(psg_net* net, size_t n) {
+  cudaStream_t s = net->stream;
+  int launches = 0;
+  std::vector<char> written(net->L.size(), 0);
+  written[net->L[net->loss_idx].inputs[0]] = 1;  // the loss seed writes the logits grad
+  for (int li = static_cast<int>(net->L.size()) - 1; li >= 0; --li) {
+    LayerRt& l = net->L[li];
+    if (l.kind == PSG_LAYER_DATA || l.kind == PSG_LAYER_LABEL || l.kind == PSG_LAYER_SOFTMAX_LOSS)
+      continue;
+    const int pi = l.inputs[0];
+    LayerRt& src = net->L[pi];
+    const bool need_dx = src.kind != PSG_LAYER_DATA;
+    const bool acc = written[pi] != 0;
+    if (need_dx) written[pi] = 1;
+    switch (l.kind) {
+      case PSG_LAYER_CONV:
+      case PSG_LAYER_LINEAR: {
+        const TensorRec& k = net->tensors[l.kern_t];
+        const TensorRec& b = net->tensors[l.bias_t];
+        const ConvGeom g = geom_for(l, n);
+        conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off, net->ws, net->mode,
+                   s);
+        launches += conv_launches(g, 2, net->mode);
+        if (need_dx) {
+          conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->mode, s);
+          launches += conv_launches(g, 1, net->mode);
+        }
+        break;
+      }
+      case PSG_LAYER_POOL:
+        if (need_dx) {
+          PoolGeom g = l.pg;
+          g.n = static_cast<int>(n);
+          pool_bwd(g, l.grad, l.route, src.grad, acc, s);
+          ++launches;
+        }
+        break;
+      case PSG_LAYER_RELU:
+        if (need_dx) {
+          relu_bwd(src.out, l.grad, src.grad, n * l.vol(), acc, s);
+          ++launches;
+        }
+        break;
+      case PSG_LAYER_LRN:
+        if (need_dx) {
+          LrnGeom g = l.lg;
+          g.pixels = static_cast<int>(n) * l.H * l.W;
+          lrn_bwd(g, src.out, l.out, l.aux, l.grad, src.grad, acc, s);
+          ++launches;
+        }
+        break;
+      case PSG_LAYER_DROPOUT:
+        if (need_dx) {
+          DropGeom g = l.dg;
+          g.n = static_cast<int>(n);
+          dropout_bwd(g, l.grad, src.grad, &net->dsc->step, acc, s);
+          ++launches;
+        }
+        break;
+      default:
+        break;
+    }
+  }
+  return launches;
+}
+
+int run_update(psg_net* net, bool advance) {
+  if (net->nchunks == 0) return 0;
+  sgd_update(net->d_chunks, net->nchunks, net->w, net->v, net->g, static_cast<float>(net->mu),
+             &net->dsc->flag, advance ? &net->dsc->cursor : nullptr,
+             advance ? &net->dsc->step : nullptr, net->stream);
+  return 1;
+}
+
+// Host NCHW fp64 batch -> device NHWC (channel stride cs) into the data layer.
+void upload_batch(psg_net* net, const double* images, const int32_t* labels, size_t n) {
+  const LayerRt& d = net->L[net->data_idx];
+  if (n < 1) throw std::invalid_argument("forward: label count does not match batch");
+  for (size_t i = 0; i < n; ++i)
+    if (labels[i] < 0 || labels[i] >= net->classes)
+      throw std::invalid_argument("forward: label out of range");
+  ensure_capacity(net, n);
+  const size_t vol = d.vol();
+  ensure_stage(net, n * vol, n);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  const int C = d.C, H = d.H, W = d.W, cs = d.cs;
+  for (size_t b = 0; b < n; ++b)
+    for (int h = 0; h < H; ++h)
+      for (int w = 0; w < W; ++w)
+        for (int c = 0; c < cs; ++c)
+          net->h_stage[((b * H + h) * W + w) * cs + c] =
+              c < C ? static_cast<float>(images[((b * C + c) * H + h) * W + w]) : 0.f;
+  std::memcpy(net->h_lab, labels, n * sizeof(int32_t));
+  PSG_CUDA(cudaMemcpyAsync(d.out, net->h_stage, n * vol * sizeof(float), cudaMemcpyHostToDevice,
+                           net->stream));
+  PSG_CUDA(cudaMemcpyAsync(net->labels, net->h_lab, n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                           net->stream));
+}
+
+double read_loss(psg_net* net) {
+  PSG_CUDA(cudaMemcpyAsync(net->hsc, net->dsc, sizeof(DeviceScalars), cudaMemcpyDeviceToHost,
+                           net->stream));
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  if (net->hsc->flag) {
+    const int zero = 0;
+    PSG_CUDA(cudaMemcpy(&net->dsc->flag, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    throw std::runtime_error("softmax loss: non-finite loss");
+  }
+  return net->hsc->loss;
+}
+
+}  // namespace
+
+size_t TensorRec::to_int(size_t i) const {
+  switch (map) {
+    case 1: {  // ref [F][Cg][kh][kw] -> int [F][kh][kw][Cgs]
+      const size_t v = i % kw, u = (i / kw) % kh, c = (i / (kw * kh)) % Cg,
+                   f = i / (static_cast<size_t>(kw) * kh * Cg);
+      return ((f * kh + u) * kw + v) * Cgs + c;
+    }
+    case 2: {  // ref [O][c*h*w] (CHW flatten, model.hpp:409) -> int [O][h][w][pcs]
+      const size_t D = static_cast<size_t>(pc) * ph * pw;
+      const size_t o = i / D, d = i % D;
+      const size_t ww = d % pw, hh = (d / pw) % ph, c = d / (static_cast<size_t>(pw) * ph);
+      return o * (static_cast<size_t>(ph) * pw * pcs) + (hh * pw + ww) * pcs + c;
+    }
+    default:
+      return i;
+  }
+}
+
+void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed) {
+  validate(layers, n);
+  net->seed = seed;
+  net->L.resize(n);
+  size_t ref_off = 0, int_off = 0;
+  for (int li = 0; li < n; ++li) {
+    LayerRt& l = net->L[li];
+    l.d = layers[li];
+    l.kind = layers[li].kind;
+    for (int i = 0; i < l.d.n_inputs; ++i) {
+      l.inputs.push_back(l.d.inputs[i]);
+      net->L[l.d.inputs[i]].consumers.push_back(li);
+    }
+    const LayerRt* src = l.inputs.empty() ? nullptr : &net->L[l.inputs[0]];
+    switch (l.kind) {
+      case PSG_LAYER_DATA:
+        net->data_idx = li;
+        net->spec_batch = l.d.batch;
+        l.C = l.d.channels;
+        l.H = l.d.height;
+        l.W = l.d.width;
+        l.cs = l.C;
+        break;
+      case PSG_LAYER_LABEL:
+        net->label_idx = li;
+        l.C = l.H = l.W = l.cs = 1;
+        break;
+      case PSG_LAYER_CONV: {
+        const int C = src->C, G = l.d.group;
+        if (src->H + 2 * l.d.pad_h < l.d.kernel_h || src->W + 2 * l.d.pad_w < l.d.kernel_w)
+          throw std::invalid_argument("net: conv '" + lname(l.d) + "' kernel exceeds input");
+        if (C % G || l.d.num_output % G)
+          throw std::invalid_argument("net: conv '" + lname(l.d) +
+                                      "' group must divide channels and filters");
+        if (G > 1 && src->cs != C)
+          throw std::invalid_argument("net: grouped conv on a padded input");
+        l.C = l.cs = l.d.num_output;
+        l.H = (src->H + 2 * l.d.pad_h - l.d.kernel_h) / l.d.stride_h + 1;
+        l.W = (src->W + 2 * l.d.pad_w - l.d.kernel_w) / l.d.stride_w + 1;
+        ConvGeom& g = l.cg;
+        g.H = src->H;
+        g.W = src->W;
+        g.cs_in = src->cs;
+        g.OH = l.H;
+        g.OW = l.W;
+        g.F = l.C;
+        g.kh = l.d.kernel_h;
+        g.kw = l.d.kernel_w;
+        g.sh = l.d.stride_h;
+        g.sw = l.d.stride_w;
+        g.ph = l.d.pad_h;
+        g.pw = l.d.pad_w;
+        g.G = G;
+        TensorRec k;
+        k.layer = li;
+        k.slot = 0;
+        k.rank = 4;
+        k.shape[0] = l.C;
+        k.shape[1] = C / G;
+        k.shape[2] = g.kh;
+        k.shape[3] = g.kw;
+        k.ref_count = static_cast<size_t>(l.C) * (C / G) * g.kh * g.kw;
+        k.int_count = static_cast<size_t>(l.C) * g.Kf();
+        k.map = 1;
+        k.F = l.C;
+        k.Cg = C / G;
+        k.Cgs = g.Cgs();
+        k.kh = g.kh;
+        k.kw = g.kw;
+        k.lr_mult = static_cast<float>(l.d.lr_mult_w);
+        k.decay_mult = static_cast<float>(l.d.decay_mult_w);
+        net->tensors.push_back(k);
+        break;
+      }
+      case PSG_LAYER_POOL:
+        if (src->H + 2 * l.d.pad_h < l.d.kernel_h || src->W + 2 * l.d.pad_w < l.d.kernel_w)
+          throw std::invalid_argument("net: pool '" + lname(l.d) + "' kernel exceeds input");
+        l.C = src->C;
+        l.cs = src->cs;
+        l.H = pool_out(src->H, l.d.kernel_h, l.d.stride_h, l.d.pad_h, l.d.ceil_mode);
+        l.W = pool_out(src->W, l.d.kernel_w, l.d.stride_w, l.d.pad_w, l.d.ceil_mode);
+        l.pg = PoolGeom{0,         src->H,     src->W,     l.cs,        l.H,
+                        l.W,       l.d.kernel_h, l.d.kernel_w, l.d.stride_h, l.d.stride_w,
+                        l.d.pad_h, l.d.pad_w,  l.d.pool};
+        break;
+      case PSG_LAYER_LINEAR: {
+        l.C = l.cs = l.d.num_output;
+        l.H = l.W = 1;
+        const size_t Dint = src->vol();
+        ConvGeom& g = l.cg;
+        g.H = g.W = g.OH = g.OW = 1;
+        g.cs_in = static_cast<int>(Dint);
+        g.F = l.C;
+        TensorRec k;
+        k.layer = li;
+        k.slot = 0;
+        k.rank = 2;
+        k.shape[0] = l.C;
+        k.shape[1] = static_cast<int64_t>(src->C) * src->H * src->W;
+        k.ref_count = static_cast<size_t>(k.shape[0]) * k.shape[1];
+        k.int_count = static_cast<size_t>(l.C) * Dint;
+        k.map = (src->H == 1 && src->W == 1 && src->cs == src->C) ? 0 : 2;
+        k.O = l.C;
+        k.pc = src->C;
+        k.ph = src->H;
+        k.pw = src->W;
+        k.pcs = src->cs;
+        k.lr_mult = static_cast<float>(l.d.lr_mult_w);
+        k.decay_mult = static_cast<float>(l.d.decay_mult_w);
+        net->tensors.push_back(k);
+        break;
+      }
+      case PSG_LAYER_RELU:
+      case PSG_LAYER_LRN:
+      case PSG_LAYER_DROPOUT:
+        l.C = src->C;
+        l.H = src->H;
+        l.W = src->W;
+        l.cs = src->cs;
+        if (l.kind == PSG_LAYER_LRN) {
+          if (l.cs != l.C) throw std::invalid_argument("net: lrn on a padded input");
+          l.lg = LrnGeom{0, l.C, l.d.local_size, static_cast<float>(l.d.alpha),
+                         static_cast<float>(l.d.beta), static_cast<float>(l.d.k)};
+        }
+        if (l.kind == PSG_LAYER_DROPOUT) {
+          if (l.cs != l.C) throw std::invalid_argument("net: dropout on a padded input");
+          const uint64_t p[2] = {kStreamDropout, static_cast<uint64_t>(li)};
+          l.dg = DropGeom{0, l.C, l.H, l.W, static_cast<float>(l.d.dropout_ratio),
+                          derive_seed(seed, p, 2)};
+        }
+        break;
+      case PSG_LAYER_SOFTMAX_LOSS:
+        if (net->L[l.inputs[1]].kind != PSG_LAYER_LABEL)
+          throw std::invalid_argument("net: softmax loss second input must be the label layer");
+        if (src->H != 1 || src->W != 1 || src->cs != src->C)
+          throw std::invalid_argument("net: softmax logits must be [classes]");
+        net->loss_idx = li;
+        l.C = l.cs = src->C;
+        l.H = l.W = 1;
+        net->classes = l.C;
+        break;
+    }
+    if (is_param_layer(l.kind)) {
+      TensorRec& k = net->tensors.back();
+      k.ref_off = ref_off;
+      ref_off += k.ref_count;
+      k.int_off = int_off;
+      int_off = round_up(int_off + k.int_count, kAlign);
+      l.kern_t = static_cast<int>(net->tensors.size()) - 1;
+      TensorRec b;
+      b.layer = li;
+      b.slot = 1;
+      b.rank = 1;
+      b.shape[0] = l.C;
+      b.ref_count = b.int_count = static_cast<size_t>(l.C);
+      b.ref_off = ref_off;
+      ref_off += b.ref_count;
+      b.int_off = int_off;
+      int_off = round_up(int_off + b.int_count, kAlign);
+      b.lr_mult = static_cast<float>(l.d.lr_mult_b);
+      b.decay_mult = static_cast<float>(l.d.decay_mult_b);
+      net->tensors.push_back(b);
+      l.bias_t = static_cast<int>(net->tensors.size()) - 1;
+    }
+  }
+  if (net->classes < 1) throw std::invalid_argument("net: need at least one class");
+  net->P_ref = ref_off;
+  net->P_int = int_off;
+  // divisible into 4-aligned slices for up to 8 ranks (ordered reduce-scatter)
+  net->P_alloc = round_up(std::max<size_t>(int_off, 1), 4 * 840);
+
+  // model.hpp:200-283 initialisation, bit-exact fp64 then one rounding to fp32.
+  std::vector<float> host(net->P_alloc, 0.f);
+  for (int li = 0; li < n; ++li) {
+    LayerRt& l = net->L[li];
+    if (!is_param_layer(l.kind)) continue;
+    const TensorRec& k = net->tensors[l.kern_t];
+    Rng r(derive_seed2(seed, kStreamWeights, static_cast<uint64_t>(li)));
+    double s;
+    if (l.kind == PSG_LAYER_CONV) {
+      const double khw = static_cast<double>(l.d.kernel_h * l.d.kernel_w);
+      s = std::sqrt(6.0 / (static_cast<double>(k.Cg) * khw +
+                           static_cast<double>(l.C / l.d.group) * khw));
+    } else {
+      s = std::sqrt(6.0 / (static_cast<double>(k.shape[1]) + static_cast<double>(l.C)));
+    }
+    for (size_t i = 0; i < k.ref_count; ++i)
+      host[k.int_off + k.to_int(i)] = static_cast<float>(r.uniform(-s, s));
+  }
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaStreamCreateWithFlags(&net->stream, cudaStreamNonBlocking));
+  net->w = dalloc<float>(net->P_alloc);
+  net->g = dalloc<float>(net->P_alloc);
+  net->v = dalloc<float>(net->P_alloc);
+  PSG_CUDA(cudaMemcpy(net->w, host.data(), net->P_alloc * sizeof(float), cudaMemcpyHostToDevice));
+  PSG_CUDA(cudaMemset(net->g, 0, net->P_alloc * sizeof(float)));
+  PSG_CUDA(cudaMemset(net->v, 0, net->P_alloc * sizeof(float)));
+  PSG_CUDA(cudaMalloc(&net->dsc, sizeof(DeviceScalars)));
+  PSG_CUDA(cudaMemset(net->dsc, 0, sizeof(DeviceScalars)));
+  PSG_CUDA(cudaMallocHost(&net->hsc, sizeof(DeviceScalars)));
+  PSG_CUDA(cudaEventCreateWithFlags(&net->idx_ev, cudaEventDisableTiming));
+  PSG_CUDA(cudaEventCreate(&net->t0));
+  PSG_CUDA(cudaEventCreate(&net->t1));
+  build_chunks(net);
+}
+
+void net_free(psg_net* net) {
+  DeviceGuard dg(net->ctx->device);
+  if (net->stream) cudaStreamSynchronize(net->stream);
+  invalidate_graph(net);
+  free_batch_buffers(net);
+  dfree(net->w);
+  dfree(net->g);
+  dfree(net->v);
+  dfree(net->d_chunks);
+  dfree(net->dsc);
+  dfree(net->d_idx);
+  if (net->hsc) cudaFreeHost(net->hsc);
+  if (net->h_idx) cudaFreeHost(net->h_idx);
+  if (net->h_stage) cudaFreeHost(net->h_stage);
+  if (net->h_lab) cudaFreeHost(net->h_lab);
+  if (net->idx_ev) cudaEventDestroy(net->idx_ev);
+  if (net->t0) cudaEventDestroy(net->t0);
+  if (net->t1) cudaEventDestroy(net->t1);
+  if (net->stream) cudaStreamDestroy(net->stream);
+}
+
+void net_check_flag(psg_net* net) {
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  int flag = 0;
+  PSG_CUDA(cudaMemcpy(&flag, &net->dsc->flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    const int zero = 0;
+    PSG_CUDA(cudaMemcpy(&net->dsc->flag, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    throw std::runtime_error("train: produced a non-finite value");
+  }
+}
+
+void net_set_sgd(psg_net* net, double lr, double mu, double wd) {
+  if (!(lr > 0.0)) throw std::invalid_argument("sgd: learning rate must be > 0");
+  if (mu < 0.0 || mu >= 1.0) throw std::invalid_argument("sgd: momentum must be in [0,1)");
+  if (wd < 0.0) throw std::invalid_argument("sgd: weight decay must be >= 0");
+  if (mu != net->mu) invalidate_graph(net);
+  net->lr = lr;
+  net->mu = mu;
+  net->wd = wd;
+  build_chunks(net);
+}
+
+void net_get_weights(psg_net* net, double* flat, size_t n, bool velocity) {
+  if (n != net->P_ref) throw std::invalid_argument("get_weights: size mismatch");
+  DeviceGuard dg(net->ctx->device);
+  std::vector<float> host(net->P_int);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  PSG_CUDA(cudaMemcpy(host.data(), velocity ? net->v : net->w, net->P_int * sizeof(float),
+                      cudaMemcpyDeviceToHost));
+  for (const TensorRec& t : net->tensors)
+    for (size_t i = 0; i < t.ref_count; ++i)
+      flat[t.ref_off + i] = static_cast<double>(host[t.int_off + t.to_int(i)]);
+}
+
+void net_set_weights(psg_net* net, const double* flat, size_t n) {
+  if (n != net->P_ref)
+    throw std::invalid_argument("set_weights: expected " + std::to_string(net->P_ref) +
+                                " values, got " + std::to_string(n));
+  std::vector<float> host(net->P_int, 0.f);
+  for (const TensorRec& t : net->tensors)
+    for (size_t i = 0; i < t.ref_count; ++i)
+      host[t.int_off + t.to_int(i)] = static_cast<float>(flat[t.ref_off + i]);
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  PSG_CUDA(cudaMemcpy(net->w, host.data(), net->P_int * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+void net_forward_host(psg_net* net, const double* images, const int32_t* labels, size_t n,
+                      double* loss, double* probs) {
+  DeviceGuard dg(net->ctx->device);
+  upload_batch(net, images, labels, n);
+  run_forward(net, n, /*train=*/false, /*seed_grad=*/false);
+  net->last_n = n;
+  const double l = read_loss(net);
+  if (loss) *loss = l;
+  if (probs) {
+    std::vector<float> p(n * net->classes);
+    PSG_CUDA(cudaMemcpy(p.data(), net->L[net->loss_idx].out, p.size() * sizeof(float),
+                        cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < p.size(); ++i) probs[i] = p[i];
+  }
+}
+
+void net_backward_host(psg_net* net, const double* images, const int32_t* labels, size_t n,
+                       double* loss, double* grads) {
+  DeviceGuard dg(net->ctx->device);
+  upload_batch(net, images, labels, n);
+  run_forward(net, n, /*train=*/true, /*seed_grad=*/true);
+  run_backward(net, n);
+  net->last_n = n;
+  const double l = read_loss(net);
+  if (loss) *loss = l;
+  if (grads) {
+    std::vector<float> host(net->P_int);
+    PSG_CUDA(cudaMemcpy(host.data(), net->g, net->P_int * sizeof(float), cudaMemcpyDeviceToHost));
+    for (const TensorRec& t : net->tensors)
+      for (size_t i = 0; i < t.ref_count; ++i)
+        grads[t.ref_off + i] = static_cast<double>(host[t.int_off + t.to_int(i)]);
+    for (size_t i = 0; i < net->P_ref; ++i)
+      if (!std::isfinite(grads[i])) throw std::runtime_error("backward: produced a non-finite value");
+  }
+}
+
+void net_apply_update_host(psg_net* net, const double* grads, size_t n) {
+  if (n != net->P_ref) throw std::invalid_argument("apply_update: gradient structure mismatch");
+  std::vector<float> host(net->P_int, 0.f);
+  for (const TensorRec& t : net->tensors)
+    for (size_t i = 0; i < t.ref_count; ++i)
+      host[t.int_off + t.to_int(i)] = static_cast<float>(grads[t.ref_off + i]);
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  PSG_CUDA(cudaMemcpy(net->g, host.data(), net->P_int * sizeof(float), cudaMemcpyHostToDevice));
+  run_update(net, /*advance=*/false);
+  net_check_flag(net);
+}
+
+void net_layer_readback(psg_net* net, int layer, bool grad, double* out, size_t n) {
+  if (layer < 0 || layer >= static_cast<int>(net->L.size()))
+    throw std::invalid_argument("layer index out of range");
+  const LayerRt& l = net->L[layer];
+  const size_t rows = net->last_n;
+  const size_t want = rows * static_cast<size_t>(l.C) * l.H * l.W;
+  if (n != want) throw std::invalid_argument("layer readback: size mismatch");
+  const float* src = grad ? l.grad : l.out;
+  if (!src || rows == 0) throw std::runtime_error("layer readback: no state for this layer");
+  DeviceGuard dg(net->ctx->device);
+  std::vector<float> host(rows * l.vol());
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  PSG_CUDA(cudaMemcpy(host.data(), src, host.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  for (size_t b = 0; b < rows; ++b)
+    for (int c = 0; c < l.C; ++c)
+      for (int h = 0; h < l.H; ++h)
+        for (int w = 0; w < l.W; ++w)
+          out[((b * l.C + c) * l.H + h) * l.W + w] = host[((b * l.H + h) * l.W + w) * l.cs + c];
+}
+
+void net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* idx, size_t count,
+                      size_t batch, uint64_t seed) {
+  if (batch < 1) throw std::invalid_argument("batch iterator: batch size must be >= 1");
+  if (batch > count) throw std::invalid_argument("batch iterator: batch size exceeds shard size");
+  const LayerRt& d = net->L[net->data_idx];
+  if (ds->c != d.C || ds->h != d.H || ds->w != d.W)
+    throw std::invalid_argument("forward: batch extents do not match the data layer");
+  if (ds->ctx->device != net->ctx->device)
+    throw std::invalid_argument("attach: dataset lives on another device");
+  for (size_t i = 0; i < count; ++i)
+    if (idx[i] >= ds->n) throw std::invalid_argument("attach: shard index out of range");
+  for (int32_t y : ds->host_labels)
+    if (y < 0 || y >= net->classes) throw std::invalid_argument("forward: label out of range");
+  net->train_ds = ds;
+  net->shard.assign(idx, idx + count);
+  net->it_batch = batch;
+  net->it_seed = seed;
+  net->it_epoch = 0;
+  net->order.resize(count);
+  epoch_order(net->shard.data(), count, seed, 0, net->order.data());  // ctor -> start_epoch
+  net->it_cursor = 0;
+}
+
+void net_train(psg_net* net, long steps) {
+  if (steps < 0) throw std::invalid_argument("train: negative step count");
+  if (steps == 0) return;
+  if (!net->train_ds) throw std::runtime_error("train: no training data attached");
+  DeviceGuard dg(net->ctx->device);
+  const size_t b = net->it_batch;
+  ensure_capacity(net, b);
+  const size_t need = static_cast<size_t>(steps) * b;
+  if (need > net->idx_cap) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    dfree(net->d_idx);
+    if (net->h_idx) cudaFreeHost(net->h_idx);
+    net->idx_cap = std::max(need, static_cast<size_t>(4096));
+    net->d_idx = dalloc<uint32_t>(net->idx_cap);
+    PSG_CUDA(cudaMallocHost(&net->h_idx, net->idx_cap * sizeof(uint32_t)));
+    invalidate_graph(net);
+  }
+  // ShardBatchIterator::next() x steps (data.hpp:323-331) -> one index upload.
+  PSG_CUDA(cudaEventSynchronize(net->idx_ev));
+  for (long s = 0; s < steps; ++s) {
+    if ((net->it_cursor + 1) * b > net->order.size()) {
+      ++net->it_epoch;
+      epoch_order(net->shard.data(), net->shard.size(), net->it_seed, net->it_epoch,
+                  net->order.data());
+      net->it_cursor = 0;
+    }
+    for (size_t i = 0; i < b; ++i)
+      net->h_idx[s * b + i] = static_cast<uint32_t>(net->order[net->it_cursor * b + i]);
+    ++net->it_cursor;
+  }
+  PSG_CUDA(cudaMemcpyAsync(net->d_idx, net->h_idx, need * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           net->stream));
+  PSG_CUDA(cudaEventRecord(net->idx_ev, net->stream));
+  PSG_CUDA(cudaMemsetAsync(&net->dsc->cursor, 0, sizeof(int), net->stream));
+  const LayerRt& d = net->L[net->data_idx];
+  psg_dataset* ds = net->train_ds;
+  if (!net->graph || net->graph_batch != b) {
+    invalidate_graph(net);
+    cudaGraph_t graph;
+    PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
+    int launches = 0;
+    try {
+      gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
+                   d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+      ++launches;
+      launches += run_forward(net, b, true, true);
+      launches += run_backward(net, b);
+      launches += run_update(net, true);
+    } catch (...) {
+      cudaStreamEndCapture(net->stream, &graph);
+      throw;
+    }
+    PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
+    PSG_CUDA(cudaGraphInstantiate(&net->graph, graph, 0));
+    cudaGraphDestroy(graph);
+    net->graph_batch = b;
+    net->launches_per_step = launches;
+  }
+  PSG_CUDA(cudaEventRecord(net->t0, net->stream));
+  for (long s = 0; s < steps; ++s) PSG_CUDA(cudaGraphLaunch(net->graph, net->stream));
+  PSG_CUDA(cudaEventRecord(net->t1, net->stream));
+  net->timed = true;
+  net->last_n = b;
+}
+
+void net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch) {
+  if (batch < 1 || batch > ds->n) throw std::invalid_argument("eval iterator: bad batch size");
+  const LayerRt& d = net->L[net->data_idx];
+  if (ds->c != d.C || ds->h != d.H || ds->w != d.W)
+    throw std::invalid_argument("forward: batch extents do not match the data layer");
+  if (ds->ctx->device != net->ctx->device)
+    throw std::invalid_argument("attach: dataset lives on another device");
+  for (int32_t y : ds->host_labels)
+    if (y < 0 || y >= net->classes) throw std::invalid_argument("forward: label out of range");
+  net->val_ds = ds;
+  net->val_batch = batch;
+  net->val_cursor = 0;
+}
+
+double net_test(psg_net* net, long steps) {
+  if (steps < 1) throw std::invalid_argument("test: step count must be >= 1");
+  if (!net->val_ds) throw std::runtime_error("test: no validation data attached");
+  DeviceGuard dg(net->ctx->device);
+  const size_t b = net->val_batch;
+  ensure_capacity(net, b);
+  std::vector<uint32_t> idx(static_cast<size_t>(steps) * b);
+  for (long s = 0; s < steps; ++s) {  // SequentialBatchIterator::next (data.hpp:366-371)
+    if ((net->val_cursor + 1) * b > net->val_ds->n) net->val_cursor = 0;
+    for (size_t i = 0; i < b; ++i) idx[s * b + i] = static_cast<uint32_t>(net->val_cursor * b + i);
+    ++net->val_cursor;
+  }
+  uint32_t* d_vidx = dalloc<uint32_t>(idx.size());
+  PSG_CUDA(cudaMemcpyAsync(d_vidx, idx.data(), idx.size() * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice, net->stream));
+  PSG_CUDA(cudaMemsetAsync(&net->dsc->correct, 0, sizeof(unsigned long long), net->stream));
+  const LayerRt& d = net->L[net->data_idx];
+  for (long s = 0; s < steps; ++s) {
+    gather_batch(net->val_ds->images, net->val_ds->labels, d_vidx + s * b, nullptr,
+                 static_cast<int>(b), d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+    run_forward(net, b, /*train=*/false, /*seed_grad=*/false);
+    argmax_count(net->L[net->loss_idx].out, net->labels, static_cast<int>(b), net->classes,
+                 &net->dsc->correct, net->stream);
+  }
+  unsigned long long correct = 0;
+  PSG_CUDA(cudaMemcpyAsync(&net->hsc->correct, &net->dsc->correct, sizeof(correct),
+                           cudaMemcpyDeviceToHost, net->stream));
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  correct = net->hsc->correct;
+  dfree(d_vidx);
+  net->last_n = b;
+  return static_cast<double>(correct) / static_cast<double>(steps * static_cast<long>(b));
+}
+
+}  // namespace psg

@@ -1,0 +1,165 @@
+// Internal declarations of libpsg (B200-native SparkNet hot path).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/psg.h"
+
+namespace psg {
+
+// Exceptions mapped 1:1 onto psg_status by the C ABI layer (api.cpp).
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define PSG_CUDA(x) ::psg::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Scoped device selection: every entry point sets the device of the object it
+// touches (SURVEY §8(b) "Every entry point sets the device itself").
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) PSG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------- host rng --
+uint64_t splitmix64(uint64_t x);
+uint64_t derive_seed(uint64_t base, const uint64_t* parts, int nparts);
+inline uint64_t derive_seed1(uint64_t base, uint64_t a) { return derive_seed(base, &a, 1); }
+inline uint64_t derive_seed2(uint64_t base, uint64_t a, uint64_t b) {
+  const uint64_t p[2] = {a, b};
+  return derive_seed(base, p, 2);
+}
+constexpr uint64_t kStreamWeights = 0x57454947ULL;
+constexpr uint64_t kStreamShard = 0x53484152ULL;
+constexpr uint64_t kStreamWorker = 0x574f524bULL;
+constexpr uint64_t kStreamData = 0x44415441ULL;
+constexpr uint64_t kStreamDropout = 0x44524f50ULL;
+
+struct Rng {
+  uint64_t state;
+  double spare = 0.0;
+  bool has_spare = false;
+  explicit Rng(uint64_t s) : state(s) {}
+  uint64_t next_u64();
+  double uniform();
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  double normal();
+  void shuffle(uint64_t* v, size_t n);
+};
+
+void shard_perm(size_t n, int workers, uint64_t seed, uint64_t* perm, uint64_t* offsets);
+uint64_t worker_stream_seed(uint64_t global_seed, int worker);
+void epoch_order(const uint64_t* shard, size_t n, uint64_t stream_seed, uint64_t epoch,
+                 uint64_t* order);
+void generate_synthetic(int classes, size_t c, size_t h, size_t w, size_t per_class,
+                        double separation, uint64_t seed, uint64_t variant, double* images,
+                        int32_t* labels);
+
+// ------------------------------------------------------------- kernel API ---
+// NHWC everywhere.  Conv kernels are stored [F][kh][kw][cs_in/G]; a linear
+// layer is a 1x1 conv over a 1x1 "image" whose channels are the producer's
+// flattened (h, w, c) features.
+struct ConvGeom {
+  int n = 0;             // batch
+  int H = 0, W = 0;      // input spatial
+  int cs_in = 0;         // input channel stride (>= logical channels; data layer may be padded)
+  int OH = 0, OW = 0;    // output spatial
+  int F = 0;             // output channels (= output channel stride)
+  int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
+  int G = 1;             // groups
+  int Cgs() const { return cs_in / G; }
+  int Fg() const { return F / G; }
+  int Kf() const { return kh * kw * Cgs(); }  // reduction length of fprop / row length of dW
+};
+
+enum class Mode { Strict = 0, Tf32 = 1 };
+
+struct Workspace {
+  float* ptr = nullptr;
+  size_t elems = 0;
+};
+
+void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
+                bool relu, Mode mode, cudaStream_t s);
+void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
+                Mode mode, cudaStream_t s);
+// dW [F][Kf] and db [F] (written, not accumulated).  Needs wgrad_workspace_elems().
+void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
+                const Workspace& ws, Mode mode, cudaStream_t s);
+size_t wgrad_workspace_elems(const ConvGeom& g, Mode mode);
+int conv_launches(const ConvGeom& g, int which, Mode mode);  // 0 fprop 1 dgrad 2 wgrad
+
+struct PoolGeom {
+  int n = 0, H = 0, W = 0, C = 0, OH = 0, OW = 0;
+  int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
+  int method = 0;
+};
+void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaStream_t s);
+void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
+              bool accumulate, cudaStream_t s);
+
+void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s);
+void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumulate,
+              cudaStream_t s);
+
+struct LrnGeom {
+  int pixels = 0, C = 0, size = 5;
+  float alpha = 1e-4f, beta = 0.75f, k = 1.f;
+};
+void lrn_fwd(const LrnGeom& g, const float* x, float* y, float* scale, cudaStream_t s);
+void lrn_bwd(const LrnGeom& g, const float* x, const float* y, const float* scale,
+             const float* dy, float* dx, bool accumulate, cudaStream_t s);
+
+struct DropGeom {
+  int n = 0, C = 0, H = 1, W = 1;  // logical NCHW dims for the counter index
+  float ratio = 0.5f;
+  uint64_t base_seed = 0;          // derive_seed(net_seed, kStreamDropout, layer)
+};
+void dropout_fwd(const DropGeom& g, const float* x, float* y, const uint64_t* d_step, bool train,
+                 cudaStream_t s);
+void dropout_bwd(const DropGeom& g, const float* dy, float* dx, const uint64_t* d_step,
+                 bool accumulate, cudaStream_t s);
+
+// Softmax + mean cross-entropy (x loss_weight) + the loss seed; per-row loss
+// terms in fp64, reduced in fixed order into *loss.
+void softmax_loss(const float* logits, const int32_t* labels, int n, int C, double loss_weight,
+                  float* probs, float* dlogits, double* row_loss, double* loss, int* flag,
+                  cudaStream_t s);
+void argmax_count(const float* probs, const int32_t* labels, int n, int C,
+                  unsigned long long* correct, cudaStream_t s);
+
+// Batch staging from the HBM-resident dataset: rows idx[cursor*b + i].
+void gather_batch(const float* ds_images, const int32_t* ds_labels, const uint32_t* idx,
+                  const int* cursor, int b, int pixels, int C, int cs, float* out,
+                  int32_t* labels, cudaStream_t s);
+
+struct UpdateChunk {
+  uint32_t begin, end;  // element range (multiples of 4 except tails)
+  float lr, wd;         // effective lr and weight decay for this tensor
+};
+void sgd_update(const UpdateChunk* chunks, int nchunks, float* w, float* v, const float* g,
+                float momentum, int* flag, int* cursor, uint64_t* step, cudaStream_t s);
+
+// Ordered mean of K same-device buffers: fp64 accumulation ascending k, /K, one rounding.
+void average_ordered(float* const* bufs, int K, size_t n, int* flag, cudaStream_t s);
+void average_ordered_into(float* const* bufs, int K, size_t n, float* out, int* flag,
+                          cudaStream_t s);
+void scale_inplace(float* x, size_t n, float a, int* flag, cudaStream_t s);
+void fill_uniform(float* x, size_t n, uint64_t seed, double lo, double hi, cudaStream_t s);
+
+}  // namespace psg

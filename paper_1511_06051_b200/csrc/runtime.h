@@ -1,0 +1,147 @@
+// Runtime objects behind the opaque C handles (psg_ctx / psg_dataset / psg_net /
+// psg_buffer / psg_comm).
+#pragma once
+
+#include <vector>
+
+#include "psg_internal.h"
+
+struct psg_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+};
+
+struct psg_dataset {
+  psg_ctx* ctx = nullptr;
+  size_t n = 0;
+  int c = 0, h = 0, w = 0, classes = 0;
+  float* images = nullptr;   // device NHWC [n][h][w][c]
+  int32_t* labels = nullptr; // device [n]
+  std::vector<int32_t> host_labels;
+};
+
+struct psg_buffer {
+  psg_ctx* ctx = nullptr;
+  float* ptr = nullptr;
+  size_t n = 0;
+};
+
+namespace psg {
+
+// One WeightCollection tensor: reference (NCHW-order) view <-> internal slot.
+struct TensorRec {
+  int layer = 0, slot = 0, rank = 1;
+  int64_t shape[4] = {0, 0, 0, 0};
+  size_t ref_off = 0, ref_count = 0;
+  size_t int_off = 0, int_count = 0;
+  int map = 0;  // 0 identity, 1 conv kernel, 2 linear weight
+  int F = 0, Cg = 0, Cgs = 0, kh = 0, kw = 0;    // conv kernel
+  int O = 0, pc = 0, ph = 0, pw = 0, pcs = 0;    // linear: producer logical dims + channel stride
+  float lr_mult = 1.f, decay_mult = 1.f;
+  // reference flat index i (within tensor) -> internal flat index
+  size_t to_int(size_t i) const;
+};
+
+struct LayerRt {
+  psg_layer_desc d{};
+  int kind = 0;
+  std::vector<int> inputs, consumers;
+  int C = 0, H = 1, W = 1;  // logical per-example dims
+  int cs = 0;               // internal channel stride (NHWC)
+  size_t vol() const { return static_cast<size_t>(H) * W * cs; }
+  float* out = nullptr;
+  float* grad = nullptr;
+  float* aux = nullptr;
+  uint8_t* route = nullptr;
+  int kern_t = -1, bias_t = -1;
+  ConvGeom cg;  // conv / linear (per-example; n filled per call)
+  PoolGeom pg;
+  LrnGeom lg;
+  DropGeom dg;
+};
+
+struct DeviceScalars {
+  double loss;
+  int flag;
+  int cursor;
+  uint64_t step;
+  unsigned long long correct;
+};
+
+}  // namespace psg
+
+struct psg_net {
+  psg_ctx* ctx = nullptr;
+  cudaStream_t stream = nullptr;
+  uint64_t seed = 0;
+  std::vector<psg::LayerRt> L;
+  int data_idx = -1, label_idx = -1, loss_idx = -1, classes = 0, spec_batch = 0;
+  std::vector<psg::TensorRec> tensors;
+  size_t P_ref = 0, P_int = 0, P_alloc = 0;
+  float* w = nullptr;
+  float* g = nullptr;
+  float* v = nullptr;
+  psg::UpdateChunk* d_chunks = nullptr;
+  int nchunks = 0;
+  double lr = 0.01, mu = 0.0, wd = 0.0;
+  psg::Mode mode = psg::Mode::Strict;
+  psg::DeviceScalars* dsc = nullptr;
+  psg::DeviceScalars* hsc = nullptr;  // pinned mirror
+  double* row_loss = nullptr;
+  int32_t* labels = nullptr;
+  psg::Workspace ws;
+  size_t cap = 0;       // batch capacity of the activation buffers
+  size_t last_n = 0;    // batch of the last forward
+  // training stream (ShardBatchIterator, data.hpp:312-351)
+  psg_dataset* train_ds = nullptr;
+  std::vector<uint64_t> shard, order;
+  size_t it_batch = 0, it_cursor = 0;
+  uint64_t it_seed = 0, it_epoch = 0;
+  uint32_t* d_idx = nullptr;
+  uint32_t* h_idx = nullptr;  // pinned staging
+  size_t idx_cap = 0;
+  cudaEvent_t idx_ev = nullptr;
+  // validation stream (SequentialBatchIterator, data.hpp:355-382)
+  psg_dataset* val_ds = nullptr;
+  size_t val_batch = 0, val_cursor = 0;
+  // explicit-batch staging
+  float* h_stage = nullptr;
+  size_t h_stage_cap = 0;
+  int32_t* h_lab = nullptr;
+  // graph of one training step
+  cudaGraphExec_t graph = nullptr;
+  size_t graph_batch = 0;
+  int launches_per_step = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  bool timed = false;
+};
+
+namespace psg {
+void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed);
+void net_free(psg_net* net);
+void net_check_flag(psg_net* net);  // throws std::runtime_error on the sticky flag
+void net_set_sgd(psg_net* net, double lr, double mu, double wd);
+void net_get_weights(psg_net* net, double* flat, size_t n, bool velocity);
+void net_set_weights(psg_net* net, const double* flat, size_t n);
+void net_forward_host(psg_net* net, const double* images, const int32_t* labels, size_t n,
+                      double* loss, double* probs);
+void net_backward_host(psg_net* net, const double* images, const int32_t* labels, size_t n,
+                       double* loss, double* grads);
+void net_apply_update_host(psg_net* net, const double* grads, size_t n);
+void net_layer_readback(psg_net* net, int layer, bool grad, double* out, size_t n);
+void net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* idx, size_t count,
+                      size_t batch, uint64_t seed);
+void net_train(psg_net* net, long steps);
+void net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch);
+double net_test(psg_net* net, long steps);
+
+void comm_unique_id(unsigned char id[128]);
+psg_comm* comm_create(psg_ctx* ctx, int nranks, int rank, const unsigned char id[128]);
+void comm_create_all(psg_ctx* const* ctxs, int ndev, psg_comm** out);
+void comm_destroy(psg_comm* c);
+void comm_average_nets(psg_comm* const* comms, psg_net* const* nets, int count, int mode);
+void comm_broadcast_nets(psg_comm* const* comms, psg_net* const* nets, int count, int root);
+void comm_average_buffers(psg_comm* const* comms, psg_buffer* const* bufs, int count, int mode,
+                          float* device_ms);
+}  // namespace psg
