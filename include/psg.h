@@ -195,6 +195,31 @@ int psg_net_test(psg_net* net, long steps, double* accuracy);
 /* Kernel launches of one training step (device-side work count). */
 int psg_net_kernels_per_step(const psg_net* net, int* launches);
 
+/* ---- measurement ------------------------------------------------------------ */
+/* One op of a training step: algorithmic work and its CUDA-event device time. */
+typedef struct psg_op_time {
+  char name[64];
+  int layer;
+  int phase;     /* 0 gather, 1 forward, 2 loss, 3 wgrad, 4 dgrad, 5 backward (other), 6 update */
+  double flops;  /* algorithmic FLOPs (GEMM-shaped ops), else 0 */
+  double bytes;  /* algorithmic HBM bytes (bandwidth ops), else 0 */
+  float ms;      /* mean device time over `repeats` eager replays */
+  int launches;
+} psg_op_time;
+/* Replays one training step eagerly `repeats` times on the attached stream's
+ * current batch with an event pair around every op (a real step: it updates). */
+int psg_net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, int* n_ops);
+/* train(steps) fed from HOST memory: per step, an H2D copy of that step's batch
+ * (NCHW fp32, labels int32) then the step, then a D2H read of its loss.  The
+ * end-to-end path of the C ABI (pinned memory from psg_host_alloc is fastest). */
+int psg_net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,
+                       double* losses);
+int psg_host_alloc(size_t bytes, void** ptr);
+int psg_host_free(void* ptr);
+/* Event slots (0..15) on the net's stream for device-side timing of regions. */
+int psg_net_event_record(psg_net* net, int slot);
+int psg_net_event_elapsed(psg_net* net, int start_slot, int end_slot, float* ms);
+
 /* ---- averaging: weights_mean (weights.hpp:90-107) ---------------------------- */
 /* K nets on one device: ordered mean written back into every net. */
 int psg_average_local(psg_net* const* nets, int count);

@@ -97,6 +97,14 @@ SIGNATURES = {
     "psg_net_attach_validation": (ctypes.c_int, [_VP, _VP, _SZ]),
     "psg_net_test": (ctypes.c_int, [_VP, ctypes.c_long, _D]),
     "psg_net_kernels_per_step": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int)]),
+    "psg_net_profile_step": (ctypes.c_int, [_VP, ctypes.c_int, _VP, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_int)]),
+    "psg_net_train_host": (ctypes.c_int, [_VP, _F, _I32, ctypes.c_long, _D]),
+    "psg_host_alloc": (ctypes.c_int, [_SZ, _PP]),
+    "psg_host_free": (ctypes.c_int, [_VP]),
+    "psg_net_event_record": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "psg_net_event_elapsed": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_float)]),
     "psg_average_local": (ctypes.c_int, [_PP, ctypes.c_int]),
     "psg_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "psg_comm_create": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _PP]),
@@ -114,6 +122,39 @@ SIGNATURES = {
     "psg_comm_average_buffer": (ctypes.c_int, [_PP, _PP, ctypes.c_int, ctypes.c_int,
                                                ctypes.POINTER(ctypes.c_float)]),
 }
+
+class OpTime(ctypes.Structure):
+    """psg_op_time (include/psg.h)."""
+    _fields_ = [("name", ctypes.c_char * 64), ("layer", ctypes.c_int), ("phase", ctypes.c_int),
+                ("flops", ctypes.c_double), ("bytes", ctypes.c_double), ("ms", ctypes.c_float),
+                ("launches", ctypes.c_int)]
+
+
+PHASES = ["gather", "forward", "loss", "wgrad", "dgrad", "backward", "update"]
+
+
+class PinnedArray:
+    """numpy view over page-locked host memory (psg_host_alloc)."""
+
+    def __init__(self, shape, dtype):
+        import numpy as np
+        self.dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * self.dtype.itemsize
+        p = ctypes.c_void_p()
+        call("psg_host_alloc", nbytes, ctypes.byref(p))
+        self._ptr = p
+        buf = (ctypes.c_char * nbytes).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=self.dtype).reshape(shape)
+
+    def __del__(self):
+        p = getattr(self, "_ptr", None)
+        if p:
+            try:
+                lib().psg_host_free(p)
+            except Exception:
+                pass
+            self._ptr = None
+
 
 _lib = None
 _lock = threading.Lock()

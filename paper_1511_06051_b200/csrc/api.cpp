@@ -464,6 +464,53 @@ int psg_net_kernels_per_step(const psg_net* net, int* launches) {
   });
 }
 
+int psg_net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, int* n_ops) {
+  return guarded([&] {
+    need(net, "profile_step");
+    psg::net_profile_step(net, repeats, out, max_ops, n_ops);
+  });
+}
+
+int psg_net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,
+                       double* losses) {
+  return guarded([&] {
+    need(net, "train_host");
+    psg::net_train_host(net, images, labels, steps, losses);
+  });
+}
+
+int psg_host_alloc(size_t bytes, void** ptr) {
+  return guarded([&] { PSG_CUDA(cudaMallocHost(ptr, std::max<size_t>(bytes, 1))); });
+}
+
+int psg_host_free(void* ptr) {
+  return guarded([&] {
+    if (ptr) PSG_CUDA(cudaFreeHost(ptr));
+  });
+}
+
+int psg_net_event_record(psg_net* net, int slot) {
+  return guarded([&] {
+    need(net, "event_record");
+    if (slot < 0 || slot >= 16) throw std::invalid_argument("event slot out of range");
+    psg::DeviceGuard dg(net->ctx->device);
+    if (!net->slots[slot]) PSG_CUDA(cudaEventCreate(&net->slots[slot]));
+    PSG_CUDA(cudaEventRecord(net->slots[slot], net->stream));
+  });
+}
+
+int psg_net_event_elapsed(psg_net* net, int start_slot, int end_slot, float* ms) {
+  return guarded([&] {
+    need(net, "event_elapsed");
+    if (start_slot < 0 || start_slot >= 16 || end_slot < 0 || end_slot >= 16 ||
+        !net->slots[start_slot] || !net->slots[end_slot])
+      throw std::invalid_argument("event slot not recorded");
+    psg::DeviceGuard dg(net->ctx->device);
+    PSG_CUDA(cudaEventSynchronize(net->slots[end_slot]));
+    PSG_CUDA(cudaEventElapsedTime(ms, net->slots[start_slot], net->slots[end_slot]));
+  });
+}
+
 int psg_average_local(psg_net* const* nets, int count) {
   return guarded([&] {
     if (count < 1) throw std::invalid_argument("weights_mean: empty input");

@@ -4,13 +4,13 @@
 namespace psg {
 
 void conv_fprop_simt(const ConvGeom& g, const float* x, const float* w, const float* bias,
-                     float* y, bool relu, cudaStream_t s);
+                     float* y, bool relu, const Workspace& ws, cudaStream_t s);
 void conv_dgrad_simt(const ConvGeom& g, const float* dy, const float* w, float* dx,
-                     bool accumulate, cudaStream_t s);
+                     bool accumulate, const Workspace& ws, cudaStream_t s);
 void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
                      const Workspace& ws, cudaStream_t s);
-size_t wgrad_workspace_elems_simt(const ConvGeom& g);
-int wgrad_launches_simt(const ConvGeom& g);
+size_t conv_workspace_elems_simt(const ConvGeom& g);
+int conv_launches_simt(const ConvGeom& g, int which);
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e != cudaSuccess)
@@ -19,13 +19,13 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
 }
 
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
-                bool relu, Mode, cudaStream_t s) {
-  conv_fprop_simt(g, x, w, bias, y, relu, s);
+                bool relu, const Workspace& ws, Mode, cudaStream_t s) {
+  conv_fprop_simt(g, x, w, bias, y, relu, ws, s);
 }
 
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-                Mode, cudaStream_t s) {
-  conv_dgrad_simt(g, dy, w, dx, accumulate, s);
+                const Workspace& ws, Mode, cudaStream_t s) {
+  conv_dgrad_simt(g, dy, w, dx, accumulate, ws, s);
 }
 
 void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
@@ -33,10 +33,8 @@ void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, f
   conv_wgrad_simt(g, x, dy, dw, db, ws, s);
 }
 
-size_t wgrad_workspace_elems(const ConvGeom& g, Mode) { return wgrad_workspace_elems_simt(g); }
+size_t conv_workspace_elems(const ConvGeom& g, Mode) { return conv_workspace_elems_simt(g); }
 
-int conv_launches(const ConvGeom& g, int which, Mode) {
-  return which == 2 ? wgrad_launches_simt(g) : 1;
-}
+int conv_launches(const ConvGeom& g, int which, Mode) { return conv_launches_simt(g, which); }
 
 }  // namespace psg

@@ -26,6 +26,7 @@ struct FpropProb {
   int H, W, cs_in, OH, OW, F, kh, kw, sh, sw, ph, pw, Cgs, Fg, G;
   int M, N, K;
   int relu;
+  float* ws;  // split-K partials [splits][G][M][N], or null for a direct store
   static constexpr bool A_KC = true;  // A contiguous along k (channels)
   static constexpr bool B_KC = true;
   struct ACtx {
@@ -76,7 +77,11 @@ struct FpropProb {
   __device__ float b(const BCtx& c, const BK_& k) const {
     return (c.row && k.ok) ? __ldg(c.row + k.k) : 0.f;
   }
-  __device__ void store(int g, int, int m, int n, float v) const {
+  __device__ void store(int g, int z, int m, int n, float v) const {
+    if (ws) {
+      ws[((static_cast<size_t>(z) * G + g) * M + m) * N + n] = v;
+      return;
+    }
     const int f = g * Fg + n;
     v += bias[f];
     if (relu) v = v > 0.f ? v : 0.f;
@@ -92,6 +97,7 @@ struct DgradProb {
   int H, W, cs_in, OH, OW, F, kh, kw, sh, sw, ph, pw, Cgs, Fg, G;
   int M, N, K;
   int accumulate;
+  float* ws;  // split-K partials, or null for a direct store
   static constexpr bool A_KC = true;   // dY contiguous along f (fastest part of k)
   static constexpr bool B_KC = false;  // W contiguous along c (= n)
   struct ACtx {
@@ -144,7 +150,11 @@ struct DgradProb {
   __device__ float b(const BCtx& c, const BK_& k) const {
     return (c.c >= 0 && k.wp) ? __ldg(k.wp + c.c) : 0.f;
   }
-  __device__ void store(int g, int, int m, int n, float v) const {
+  __device__ void store(int g, int z, int m, int n, float v) const {
+    if (ws) {
+      ws[((static_cast<size_t>(z) * G + g) * M + m) * N + n] = v;
+      return;
+    }
     float* p = dx + static_cast<size_t>(m) * cs_in + g * Cgs + n;
     *p = accumulate ? *p + v : v;
   }
@@ -357,6 +367,30 @@ __global__ void wgrad_reduce(const float* __restrict__ ws, int splits, int G, in
   }
 }
 
+// Fixed-order sum of fprop / dgrad split partials into the NHWC output:
+//   out[m * ld + g * gstride + n] = (accumulate ? out : 0) + sum_z ws[z] (+ bias, relu)
+__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int G, int M, int N,
+                              const float* __restrict__ bias, int relu, int accumulate, int ld,
+                              int gstride, float* __restrict__ out) {
+  const size_t total = static_cast<size_t>(G) * M * N;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(i % N);
+    const size_t gm = i / N;
+    const int m = static_cast<int>(gm % M), g = static_cast<int>(gm / M);
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += ws[static_cast<size_t>(z) * total + i];
+    float* o = out + static_cast<size_t>(m) * ld + g * gstride + n;
+    if (bias) {
+      s += bias[g * gstride + n];
+      if (relu) s = s > 0.f ? s : 0.f;
+      *o = s;
+    } else {
+      *o = accumulate ? *o + s : s;
+    }
+  }
+}
+
 struct TileCfg {
   int bm, bn;
 };
@@ -414,25 +448,54 @@ void fill_geom(P& p, const ConvGeom& g) {
   p.G = g.G;
 }
 
-// Split-K plan for wgrad: enough blocks to cover ~2 waves of 148 SMs, K chunks
-// of at least 128 pixels and at most 4096 (bounded sequential fp32 sums).
-void wgrad_split(const ConvGeom& g, int& splits, int& kchunk) {
-  const int M = g.Fg(), N = g.Kf() + 1, K = g.n * g.OH * g.OW;
+// Split-K plan: enough blocks to cover ~2 waves of 148 SMs, K chunks of at least
+// `min_chunk` and at most `max_chunk` (bounded sequential fp32 sums).
+struct Split {
+  int splits, kchunk;
+};
+
+Split plan_split(int M, int N, int K, int G, int min_chunk, int max_chunk) {
   const TileCfg t = pick_tiles(M, N);
-  const long tiles = static_cast<long>((M + t.bm - 1) / t.bm) * ((N + t.bn - 1) / t.bn) * g.G;
+  const long tiles = static_cast<long>((M + t.bm - 1) / t.bm) * ((N + t.bn - 1) / t.bn) * G;
   long want = std::max<long>(1, (296 + tiles - 1) / tiles);
-  const long min_chunks = (K + 4095) / 4096;
-  want = std::max(want, min_chunks);
-  want = std::min<long>(want, std::max(1, K / 128));
-  kchunk = static_cast<int>((K + want - 1) / want);
+  want = std::max<long>(want, (K + max_chunk - 1) / max_chunk);
+  want = std::min<long>(want, std::max(1, K / min_chunk));
+  int kchunk = static_cast<int>((K + want - 1) / want);
   kchunk = (kchunk + BK - 1) / BK * BK;
-  splits = (K + kchunk - 1) / kchunk;
+  return Split{(K + kchunk - 1) / kchunk, kchunk};
+}
+
+Split fprop_split(const ConvGeom& g) {
+  return plan_split(g.n * g.OH * g.OW, g.Fg(), g.Kf(), g.G, 64, 1 << 30);
+}
+Split dgrad_split(const ConvGeom& g) {
+  return plan_split(g.n * g.H * g.W, g.Cgs(), g.kh * g.kw * g.Fg(), g.G, 64, 1 << 30);
+}
+// wgrad reduces over every output pixel: cap the sequential chunk at 4096.
+Split wgrad_split(const ConvGeom& g) {
+  return plan_split(g.Fg(), g.Kf() + 1, g.n * g.OH * g.OW, g.G, 128, 4096);
+}
+
+void reduce_into(const Workspace& ws, int splits, int G, int M, int N, const float* bias,
+                 bool relu, bool accumulate, int ld, int gstride, float* out, cudaStream_t s) {
+  const size_t total = static_cast<size_t>(G) * M * N;
+  const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 8));
+  splitk_reduce<<<blocks, 256, 0, s>>>(ws.ptr, splits, G, M, N, bias, relu, accumulate, ld,
+                                       gstride, out);
+  PSG_CUDA(cudaGetLastError());
+}
+
+float* split_ws(const Workspace& ws, const Split& sp, int G, int M, int N) {
+  if (sp.splits == 1) return nullptr;
+  if (ws.elems < static_cast<size_t>(sp.splits) * G * M * N)
+    throw std::logic_error("conv: split-K workspace too small");
+  return ws.ptr;
 }
 
 }  // namespace
 
 void conv_fprop_simt(const ConvGeom& g, const float* x, const float* w, const float* bias,
-                     float* y, bool relu, cudaStream_t s) {
+                     float* y, bool relu, const Workspace& ws, cudaStream_t s) {
   FpropProb p{};
   fill_geom(p, g);
   p.x = x;
@@ -443,11 +506,14 @@ void conv_fprop_simt(const ConvGeom& g, const float* x, const float* w, const fl
   p.N = g.Fg();
   p.K = g.Kf();
   p.relu = relu;
-  launch(p, 1, p.K, s);
+  const Split sp = fprop_split(g);
+  p.ws = split_ws(ws, sp, g.G, p.M, p.N);
+  launch(p, sp.splits, sp.kchunk, s);
+  if (p.ws) reduce_into(ws, sp.splits, g.G, p.M, p.N, bias, relu, false, g.F, g.Fg(), y, s);
 }
 
 void conv_dgrad_simt(const ConvGeom& g, const float* dy, const float* w, float* dx,
-                     bool accumulate, cudaStream_t s) {
+                     bool accumulate, const Workspace& ws, cudaStream_t s) {
   DgradProb p{};
   fill_geom(p, g);
   p.dy = dy;
@@ -457,20 +523,26 @@ void conv_dgrad_simt(const ConvGeom& g, const float* dy, const float* w, float* 
   p.N = g.Cgs();
   p.K = g.kh * g.kw * g.Fg();
   p.accumulate = accumulate;
-  launch(p, 1, p.K, s);
+  const Split sp = dgrad_split(g);
+  p.ws = split_ws(ws, sp, g.G, p.M, p.N);
+  launch(p, sp.splits, sp.kchunk, s);
+  if (p.ws)
+    reduce_into(ws, sp.splits, g.G, p.M, p.N, nullptr, false, accumulate, g.cs_in, g.Cgs(), dx,
+                s);
 }
 
-size_t wgrad_workspace_elems_simt(const ConvGeom& g) {
-  int splits, kchunk;
-  wgrad_split(g, splits, kchunk);
-  if (splits == 1) return 0;
-  return static_cast<size_t>(splits) * g.G * g.Fg() * (g.Kf() + 1);
+size_t conv_workspace_elems_simt(const ConvGeom& g) {
+  const Split f = fprop_split(g), d = dgrad_split(g), w = wgrad_split(g);
+  size_t e = 0;
+  if (f.splits > 1) e = std::max(e, static_cast<size_t>(f.splits) * g.G * g.n * g.OH * g.OW * g.Fg());
+  if (d.splits > 1) e = std::max(e, static_cast<size_t>(d.splits) * g.G * g.n * g.H * g.W * g.Cgs());
+  if (w.splits > 1) e = std::max(e, static_cast<size_t>(w.splits) * g.G * g.Fg() * (g.Kf() + 1));
+  return e;
 }
 
-int wgrad_launches_simt(const ConvGeom& g) {
-  int splits, kchunk;
-  wgrad_split(g, splits, kchunk);
-  return splits == 1 ? 1 : 2;
+int conv_launches_simt(const ConvGeom& g, int which) {
+  const Split sp = which == 0 ? fprop_split(g) : which == 1 ? dgrad_split(g) : wgrad_split(g);
+  return sp.splits == 1 ? 1 : 2;
 }
 
 void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
@@ -485,19 +557,14 @@ void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* 
   p.M = g.Fg();
   p.N = p.Kf + 1;
   p.K = g.n * g.OH * g.OW;
-  int splits, kchunk;
-  wgrad_split(g, splits, kchunk);
-  p.direct = splits == 1;
-  if (!p.direct) {
-    const size_t need = static_cast<size_t>(splits) * g.G * p.M * p.N;
-    if (ws.elems < need) throw std::logic_error("conv_wgrad: workspace too small");
-    p.ws = ws.ptr;
-  }
-  launch(p, splits, kchunk, s);
+  const Split sp = wgrad_split(g);
+  p.direct = sp.splits == 1;
+  p.ws = split_ws(ws, sp, g.G, p.M, p.N);
+  launch(p, sp.splits, sp.kchunk, s);
   if (!p.direct) {
     const size_t total = static_cast<size_t>(g.G) * p.M * p.N;
     const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 8));
-    wgrad_reduce<<<blocks, 256, 0, s>>>(ws.ptr, splits, g.G, p.M, p.N, p.Kf, g.Fg(), dw, db);
+    wgrad_reduce<<<blocks, 256, 0, s>>>(ws.ptr, sp.splits, g.G, p.M, p.N, p.Kf, g.Fg(), dw, db);
     PSG_CUDA(cudaGetLastError());
   }
 }

@@ -299,6 +299,21 @@ __global__ void gather_k(const float* __restrict__ ds, const int32_t* __restrict
   }
 }
 
+// Host-fed batch (reference NCHW layout) -> data layer NHWC with channel stride cs.
+__global__ void stage_nchw_k(const float* __restrict__ src, int n, int C, int H, int W, int cs,
+                             float* __restrict__ dst) {
+  const size_t total = static_cast<size_t>(n) * H * W * cs;
+  GRID_STRIDE(i, total) {
+    const int c = static_cast<int>(i % cs);
+    size_t t = i / cs;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const size_t b = t / H;
+    dst[i] = c < C ? src[((b * C + c) * H + h) * W + w] : 0.f;
+  }
+}
+
 // ---------------------------------------------------------------- update ---
 // model.hpp:90-107 + tensor.hpp:60-71 fused into one pass over the flat
 // buffer: g' = g + wd*w; v = mu*v + g'; w += -lr*v  (mu = 0: w += -lr*g').
@@ -484,6 +499,13 @@ void gather_batch(const float* ds_images, const int32_t* ds_labels, const uint32
   const int bx = static_cast<int>(std::max<size_t>(1, std::min<size_t>((per_row / 4 + 255) / 256, 64)));
   gather_k<<<dim3(bx, b), 256, 0, s>>>(ds_images, ds_labels, idx, cursor, b, pixels, C, cs, out,
                                        labels);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void stage_batch_nchw(const float* src, int n, int C, int H, int W, int cs, float* dst,
+                      cudaStream_t s) {
+  stage_nchw_k<<<grid_for(static_cast<size_t>(n) * H * W * cs), 256, 0, s>>>(src, n, C, H, W, cs,
+                                                                             dst);
   PSG_CUDA(cudaGetLastError());
 }
 

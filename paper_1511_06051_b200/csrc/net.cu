@@ -129,9 +129,13 @@ ConvGeom geom_for(const LayerRt& l, size_t n) {
   return g;
 }
 
+}  // namespace
+
 void invalidate_graph(psg_net* net) {
   if (net->graph) cudaGraphExecDestroy(net->graph);
+  if (net->host_graph) cudaGraphExecDestroy(net->host_graph);
   net->graph = nullptr;
+  net->host_graph = nullptr;
   net->graph_batch = 0;
 }
 
@@ -152,7 +156,7 @@ void ensure_capacity(psg_net* net, size_t n) {
     if (l.kind == PSG_LAYER_POOL && l.d.pool == PSG_POOL_MAX) l.route = dalloc<uint8_t>(elems);
     if (is_param_layer(l.kind)) {
       for (Mode m : {Mode::Strict, Mode::Tf32})
-        ws = std::max(ws, wgrad_workspace_elems(geom_for(l, n), m));
+        ws = std::max(ws, conv_workspace_elems(geom_for(l, n), m));
     }
   }
   // the data layer's grad is never produced (first-layer dgrad is skipped)
@@ -162,6 +166,8 @@ void ensure_capacity(psg_net* net, size_t n) {
   net->ws.elems = ws;
   net->cap = n;
 }
+
+namespace {
 
 void ensure_stage(psg_net* net, size_t floats, size_t rows) {
   if (net->h_stage_cap >= floats && net->h_lab) return;
@@ -194,138 +200,6 @@ void build_chunks(psg_net* net) {
   if (!ch.empty())
     PSG_CUDA(cudaMemcpy(net->d_chunks, ch.data(), ch.size() * sizeof(UpdateChunk),
                         cudaMemcpyHostToDevice));
-}
-
-// ---- forward / backward launch sequences (eager or under stream capture) ----
-int run_forward(psg_net* net, size_t n, bool train, bool seed_grad) {
-  cudaStream_t s = net->stream;
-  int launches = 0;
-  for (size_t li = 0; li < net->L.size(); ++li) {
-    LayerRt& l = net->L[li];
-    switch (l.kind) {
-      case PSG_LAYER_DATA:
-      case PSG_LAYER_LABEL:
-        break;
-      case PSG_LAYER_CONV:
-      case PSG_LAYER_LINEAR: {
-        const LayerRt& src = net->L[l.inputs[0]];
-        const TensorRec& k = net->tensors[l.kern_t];
-        const TensorRec& b = net->tensors[l.bias_t];
-        conv_fprop(geom_for(l, n), src.out, net->w + k.int_off, net->w + b.int_off, l.out, false,
-                   net->mode, s);
-        launches += conv_launches(geom_for(l, n), 0, net->mode);
-        break;
-      }
-      case PSG_LAYER_POOL: {
-        PoolGeom g = l.pg;
-        g.n = static_cast<int>(n);
-        pool_fwd(g, net->L[l.inputs[0]].out, l.out, l.route, s);
-        ++launches;
-        break;
-      }
-      case PSG_LAYER_RELU:
-        relu_fwd(net->L[l.inputs[0]].out, l.out, n * l.vol(), s);
-        ++launches;
-        break;
-      case PSG_LAYER_LRN: {
-        LrnGeom g = l.lg;
-        g.pixels = static_cast<int>(n) * l.H * l.W;
-        lrn_fwd(g, net->L[l.inputs[0]].out, l.out, l.aux, s);
-        ++launches;
-        break;
-      }
-      case PSG_LAYER_DROPOUT: {
-        DropGeom g = l.dg;
-        g.n = static_cast<int>(n);
-        dropout_fwd(g, net->L[l.inputs[0]].out, l.out, &net->dsc->step, train, s);
-        ++launches;
-        break;
-      }
-      case PSG_LAYER_SOFTMAX_LOSS: {
-        LayerRt& logits = net->L[l.inputs[0]];
-        softmax_loss(logits.out, net->labels, static_cast<int>(n), net->classes, l.d.loss_weight,
-                     l.out, seed_grad ? logits.grad : nullptr, net->row_loss, &net->dsc->loss,
-                     &net->dsc->flag, s);
-        launches += 2;
-        break;
-      }
-    }
-  }
-  return launches;
-}
-
-int run_backward(psg_net* net, size_t n) {
-  cudaStream_t s = net->stream;
-  int launches = 0;
-  std::vector<char> written(net->L.size(), 0);
-  written[net->L[net->loss_idx].inputs[0]] = 1;  // the loss seed writes the logits grad
-  for (int li = static_cast<int>(net->L.size()) - 1; li >= 0; --li) {
-    LayerRt& l = net->L[li];
-    if (l.kind == PSG_LAYER_DATA || l.kind == PSG_LAYER_LABEL || l.kind == PSG_LAYER_SOFTMAX_LOSS)
-      continue;
-    const int pi = l.inputs[0];
-    LayerRt& src = net->L[pi];
-    const bool need_dx = src.kind != PSG_LAYER_DATA;
-    const bool acc = written[pi] != 0;
-    if (need_dx) written[pi] = 1;
-    switch (l.kind) {
-      case PSG_LAYER_CONV:
-      case PSG_LAYER_LINEAR: {
-        const TensorRec& k = net->tensors[l.kern_t];
-        const TensorRec& b = net->tensors[l.bias_t];
-        const ConvGeom g = geom_for(l, n);
-        conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off, net->ws, net->mode,
-                   s);
-        launches += conv_launches(g, 2, net->mode);
-        if (need_dx) {
-          conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->mode, s);
-          launches += conv_launches(g, 1, net->mode);
-        }
-        break;
-      }
-      case PSG_LAYER_POOL:
-        if (need_dx) {
-          PoolGeom g = l.pg;
-          g.n = static_cast<int>(n);
-          pool_bwd(g, l.grad, l.route, src.grad, acc, s);
-          ++launches;
-        }
-        break;
-      case PSG_LAYER_RELU:
-        if (need_dx) {
-          relu_bwd(src.out, l.grad, src.grad, n * l.vol(), acc, s);
-          ++launches;
-        }
-        break;
-      case PSG_LAYER_LRN:
-        if (need_dx) {
-          LrnGeom g = l.lg;
-          g.pixels = static_cast<int>(n) * l.H * l.W;
-          lrn_bwd(g, src.out, l.out, l.aux, l.grad, src.grad, acc, s);
-          ++launches;
-        }
-        break;
-      case PSG_LAYER_DROPOUT:
-        if (need_dx) {
-          DropGeom g = l.dg;
-          g.n = static_cast<int>(n);
-          dropout_bwd(g, l.grad, src.grad, &net->dsc->step, acc, s);
-          ++launches;
-        }
-        break;
-      default:
-        break;
-    }
-  }
-  return launches;
-}
-
-int run_update(psg_net* net, bool advance) {
-  if (net->nchunks == 0) return 0;
-  sgd_update(net->d_chunks, net->nchunks, net->w, net->v, net->g, static_cast<float>(net->mu),
-             &net->dsc->flag, advance ? &net->dsc->cursor : nullptr,
-             advance ? &net->dsc->step : nullptr, net->stream);
-  return 1;
 }
 
 // Host NCHW fp64 batch -> device NHWC (channel stride cs) into the data layer.
@@ -606,6 +480,10 @@ void net_free(psg_net* net) {
   if (net->h_idx) cudaFreeHost(net->h_idx);
   if (net->h_stage) cudaFreeHost(net->h_stage);
   if (net->h_lab) cudaFreeHost(net->h_lab);
+  dfree(net->d_stage);
+  if (net->h_losses) cudaFreeHost(net->h_losses);
+  for (cudaEvent_t e : net->slots)
+    if (e) cudaEventDestroy(e);
   if (net->idx_ev) cudaEventDestroy(net->idx_ev);
   if (net->t0) cudaEventDestroy(net->t0);
   if (net->t1) cudaEventDestroy(net->t1);

@@ -1,0 +1,240 @@
+// Launch sequences of one training step (eager, under stream capture, or with a
+// per-op CUDA-event timer for bench.py's roofline numbers).
+#include <cstring>
+
+#include "runtime.h"
+
+namespace psg {
+
+void OpTimer::begin(const char* name, int layer, int phase, double flops, double bytes) {
+  Rec r{};
+  std::strncpy(r.info.name, name, sizeof(r.info.name) - 1);
+  r.info.layer = layer;
+  r.info.phase = phase;
+  r.info.flops = flops;
+  r.info.bytes = bytes;
+  PSG_CUDA(cudaEventCreate(&r.a));
+  PSG_CUDA(cudaEventCreate(&r.b));
+  PSG_CUDA(cudaEventRecord(r.a, stream));
+  recs.push_back(r);
+}
+
+void OpTimer::end(int launches) {
+  recs.back().info.launches = launches;
+  PSG_CUDA(cudaEventRecord(recs.back().b, stream));
+}
+
+OpTimer::~OpTimer() {
+  for (Rec& r : recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+}
+
+namespace {
+
+ConvGeom geom_n(const LayerRt& l, size_t n) {
+  ConvGeom g = l.cg;
+  g.n = static_cast<int>(n);
+  return g;
+}
+
+// Algorithmic FLOPs of one GEMM-shaped pass of a conv / linear layer (logical
+// channels, not the padded internal ones).
+double conv_flops(const psg_net* net, const LayerRt& l, size_t n) {
+  const LayerRt& src = net->L[l.inputs[0]];
+  double macs;
+  if (l.kind == PSG_LAYER_CONV)
+    macs = static_cast<double>(n) * l.H * l.W * l.C * l.d.kernel_h * l.d.kernel_w *
+           (src.C / l.d.group);
+  else
+    macs = static_cast<double>(n) * l.C * src.C * src.H * src.W;
+  return 2.0 * macs;
+}
+
+double act_bytes(const LayerRt& l, size_t n) { return 4.0 * static_cast<double>(n) * l.vol(); }
+
+struct Scope {
+  OpTimer* t;
+  Scope(OpTimer* t_, const char* name, int layer, int phase, double flops, double bytes) : t(t_) {
+    if (t) t->begin(name, layer, phase, flops, bytes);
+  }
+  void done(int launches) {
+    if (t) t->end(launches);
+  }
+};
+
+}  // namespace
+
+int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer) {
+  cudaStream_t s = net->stream;
+  int launches = 0;
+  for (size_t li = 0; li < net->L.size(); ++li) {
+    LayerRt& l = net->L[li];
+    const int lid = static_cast<int>(li);
+    const std::string nm = std::string(l.d.name) + ".fwd";
+    switch (l.kind) {
+      case PSG_LAYER_DATA:
+      case PSG_LAYER_LABEL:
+        break;
+      case PSG_LAYER_CONV:
+      case PSG_LAYER_LINEAR: {
+        const LayerRt& src = net->L[l.inputs[0]];
+        const TensorRec& k = net->tensors[l.kern_t];
+        const TensorRec& b = net->tensors[l.bias_t];
+        const ConvGeom g = geom_n(l, n);
+        Scope sc(timer, nm.c_str(), lid, 1, conv_flops(net, l, n), 0.0);
+        conv_fprop(g, src.out, net->w + k.int_off, net->w + b.int_off, l.out, false, net->ws,
+                   net->mode, s);
+        const int c = conv_launches(g, 0, net->mode);
+        sc.done(c);
+        launches += c;
+        break;
+      }
+      case PSG_LAYER_POOL: {
+        PoolGeom g = l.pg;
+        g.n = static_cast<int>(n);
+        const LayerRt& src = net->L[l.inputs[0]];
+        Scope sc(timer, nm.c_str(), lid, 1, 0.0,
+                 act_bytes(src, n) + act_bytes(l, n) * (l.route ? 1.25 : 1.0));
+        pool_fwd(g, src.out, l.out, l.route, s);
+        sc.done(1);
+        ++launches;
+        break;
+      }
+      case PSG_LAYER_RELU: {
+        Scope sc(timer, nm.c_str(), lid, 1, 0.0, 2 * act_bytes(l, n));
+        relu_fwd(net->L[l.inputs[0]].out, l.out, n * l.vol(), s);
+        sc.done(1);
+        ++launches;
+        break;
+      }
+      case PSG_LAYER_LRN: {
+        LrnGeom g = l.lg;
+        g.pixels = static_cast<int>(n) * l.H * l.W;
+        Scope sc(timer, nm.c_str(), lid, 1, 0.0, 3 * act_bytes(l, n));
+        lrn_fwd(g, net->L[l.inputs[0]].out, l.out, l.aux, s);
+        sc.done(1);
+        ++launches;
+        break;
+      }
+      case PSG_LAYER_DROPOUT: {
+        DropGeom g = l.dg;
+        g.n = static_cast<int>(n);
+        Scope sc(timer, nm.c_str(), lid, 1, 0.0, 2 * act_bytes(l, n));
+        dropout_fwd(g, net->L[l.inputs[0]].out, l.out, &net->dsc->step, train, s);
+        sc.done(1);
+        ++launches;
+        break;
+      }
+      case PSG_LAYER_SOFTMAX_LOSS: {
+        LayerRt& logits = net->L[l.inputs[0]];
+        Scope sc(timer, nm.c_str(), lid, 2, 0.0, 3 * act_bytes(l, n));
+        softmax_loss(logits.out, net->labels, static_cast<int>(n), net->classes, l.d.loss_weight,
+                     l.out, seed_grad ? logits.grad : nullptr, net->row_loss, &net->dsc->loss,
+                     &net->dsc->flag, s);
+        sc.done(2);
+        launches += 2;
+        break;
+      }
+    }
+  }
+  return launches;
+}
+
+int run_backward(psg_net* net, size_t n, OpTimer* timer) {
+  cudaStream_t s = net->stream;
+  int launches = 0;
+  std::vector<char> written(net->L.size(), 0);
+  written[net->L[net->loss_idx].inputs[0]] = 1;  // the loss seed writes the logits grad
+  for (int li = static_cast<int>(net->L.size()) - 1; li >= 0; --li) {
+    LayerRt& l = net->L[li];
+    if (l.kind == PSG_LAYER_DATA || l.kind == PSG_LAYER_LABEL || l.kind == PSG_LAYER_SOFTMAX_LOSS)
+      continue;
+    const int pi = l.inputs[0];
+    LayerRt& src = net->L[pi];
+    const bool need_dx = src.kind != PSG_LAYER_DATA;
+    const bool acc = written[pi] != 0;
+    if (need_dx) written[pi] = 1;
+    const std::string nm = std::string(l.d.name);
+    switch (l.kind) {
+      case PSG_LAYER_CONV:
+      case PSG_LAYER_LINEAR: {
+        const TensorRec& k = net->tensors[l.kern_t];
+        const TensorRec& b = net->tensors[l.bias_t];
+        const ConvGeom g = geom_n(l, n);
+        {
+          Scope sc(timer, (nm + ".wgrad").c_str(), li, 3, conv_flops(net, l, n), 0.0);
+          conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off, net->ws,
+                     net->mode, s);
+          const int c = conv_launches(g, 2, net->mode);
+          sc.done(c);
+          launches += c;
+        }
+        if (need_dx) {
+          Scope sc(timer, (nm + ".dgrad").c_str(), li, 4, conv_flops(net, l, n), 0.0);
+          conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->ws, net->mode, s);
+          const int c = conv_launches(g, 1, net->mode);
+          sc.done(c);
+          launches += c;
+        }
+        break;
+      }
+      case PSG_LAYER_POOL:
+        if (need_dx) {
+          PoolGeom g = l.pg;
+          g.n = static_cast<int>(n);
+          Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0,
+                   act_bytes(src, n) + act_bytes(l, n) * (l.route ? 1.25 : 1.0));
+          pool_bwd(g, l.grad, l.route, src.grad, acc, s);
+          sc.done(1);
+          ++launches;
+        }
+        break;
+      case PSG_LAYER_RELU:
+        if (need_dx) {
+          Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
+          relu_bwd(src.out, l.grad, src.grad, n * l.vol(), acc, s);
+          sc.done(1);
+          ++launches;
+        }
+        break;
+      case PSG_LAYER_LRN:
+        if (need_dx) {
+          LrnGeom g = l.lg;
+          g.pixels = static_cast<int>(n) * l.H * l.W;
+          Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 5 * act_bytes(l, n));
+          lrn_bwd(g, src.out, l.out, l.aux, l.grad, src.grad, acc, s);
+          sc.done(1);
+          ++launches;
+        }
+        break;
+      case PSG_LAYER_DROPOUT:
+        if (need_dx) {
+          DropGeom g = l.dg;
+          g.n = static_cast<int>(n);
+          Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 2 * act_bytes(l, n));
+          dropout_bwd(g, l.grad, src.grad, &net->dsc->step, acc, s);
+          sc.done(1);
+          ++launches;
+        }
+        break;
+      default:
+        break;
+    }
+  }
+  return launches;
+}
+
+int run_update(psg_net* net, bool advance, OpTimer* timer) {
+  if (net->nchunks == 0) return 0;
+  const double bytes = 4.0 * static_cast<double>(net->P_int) * (net->mu > 0.0 ? 5.0 : 3.0);
+  Scope sc(timer, "sgd_update", -1, 6, 0.0, bytes);
+  sgd_update(net->d_chunks, net->nchunks, net->w, net->v, net->g, static_cast<float>(net->mu),
+             &net->dsc->flag, advance ? &net->dsc->cursor : nullptr,
+             advance ? &net->dsc->step : nullptr, net->stream);
+  sc.done(1);
+  return 1;
+}
+
+}  // namespace psg

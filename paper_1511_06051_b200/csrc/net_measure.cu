@@ -1,0 +1,115 @@
+// Measurement paths of a Net: per-op CUDA-event profile of one training step,
+// and the host-fed (end-to-end) training loop used for bench.py's `e2e` number.
+#include <algorithm>
+#include <cstring>
+
+#include "runtime.h"
+
+namespace psg {
+
+void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, int* n_ops) {
+  if (repeats < 1) throw std::invalid_argument("profile: repeats must be >= 1");
+  if (!net->train_ds || !net->d_idx)
+    throw std::runtime_error("profile: attach training data and train at least one step first");
+  DeviceGuard dg(net->ctx->device);
+  const size_t b = net->it_batch;
+  ensure_capacity(net, b);
+  const LayerRt& d = net->L[net->data_idx];
+  psg_dataset* ds = net->train_ds;
+  std::vector<psg_op_time> acc;
+  for (int r = 0; r <= repeats; ++r) {  // r = 0 is an untimed warm-up
+    OpTimer t(net->stream);
+    PSG_CUDA(cudaMemsetAsync(&net->dsc->cursor, 0, sizeof(int), net->stream));
+    t.begin("gather", net->data_idx, 0, 0.0, 2.0 * 4.0 * static_cast<double>(b) * d.vol());
+    gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
+                 d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+    t.end(1);
+    run_forward(net, b, true, true, &t);
+    run_backward(net, b, &t);
+    run_update(net, true, &t);
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    if (r == 0) {
+      acc.resize(t.recs.size());
+      for (size_t i = 0; i < t.recs.size(); ++i) {
+        acc[i] = t.recs[i].info;
+        acc[i].ms = 0.f;
+      }
+      continue;
+    }
+    for (size_t i = 0; i < t.recs.size(); ++i) {
+      float ms = 0.f;
+      PSG_CUDA(cudaEventElapsedTime(&ms, t.recs[i].a, t.recs[i].b));
+      acc[i].ms += ms / static_cast<float>(repeats);
+    }
+  }
+  net_check_flag(net);
+  const int n = std::min<int>(max_ops, static_cast<int>(acc.size()));
+  for (int i = 0; i < n; ++i) out[i] = acc[i];
+  *n_ops = static_cast<int>(acc.size());
+}
+
+void net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,
+                    double* losses) {
+  if (steps < 0) throw std::invalid_argument("train: negative step count");
+  if (steps == 0) return;
+  DeviceGuard dg(net->ctx->device);
+  const LayerRt& d = net->L[net->data_idx];
+  const size_t b = static_cast<size_t>(net->spec_batch);
+  const size_t chw = static_cast<size_t>(d.C) * d.H * d.W;
+  for (long s = 0; s < steps; ++s)
+    for (size_t i = 0; i < b; ++i) {
+      const int32_t y = labels[s * b + i];
+      if (y < 0 || y >= net->classes) throw std::invalid_argument("forward: label out of range");
+    }
+  ensure_capacity(net, b);
+  if (net->d_stage_cap < b * chw) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    if (net->d_stage) cudaFree(net->d_stage);
+    PSG_CUDA(cudaMalloc(&net->d_stage, b * chw * sizeof(float)));
+    net->d_stage_cap = b * chw;
+    invalidate_graph(net);
+  }
+  if (net->h_losses_cap < static_cast<size_t>(steps)) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    if (net->h_losses) cudaFreeHost(net->h_losses);
+    PSG_CUDA(cudaMallocHost(&net->h_losses, steps * sizeof(double)));
+    net->h_losses_cap = static_cast<size_t>(steps);
+  }
+  if (!net->host_graph || net->graph_batch != b) {
+    if (net->graph_batch != b) invalidate_graph(net);
+    if (net->host_graph) cudaGraphExecDestroy(net->host_graph);
+    cudaGraph_t graph;
+    PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      stage_batch_nchw(net->d_stage, static_cast<int>(b), d.C, d.H, d.W, d.cs, d.out,
+                       net->stream);
+      run_forward(net, b, true, true);
+      run_backward(net, b);
+      run_update(net, true);
+    } catch (...) {
+      cudaStreamEndCapture(net->stream, &graph);
+      throw;
+    }
+    PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
+    PSG_CUDA(cudaGraphInstantiate(&net->host_graph, graph, 0));
+    cudaGraphDestroy(graph);
+    net->graph_batch = b;
+  }
+  PSG_CUDA(cudaEventRecord(net->t0, net->stream));
+  for (long s = 0; s < steps; ++s) {
+    PSG_CUDA(cudaMemcpyAsync(net->d_stage, images + s * b * chw, b * chw * sizeof(float),
+                             cudaMemcpyHostToDevice, net->stream));
+    PSG_CUDA(cudaMemcpyAsync(net->labels, labels + s * b, b * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, net->stream));
+    PSG_CUDA(cudaGraphLaunch(net->host_graph, net->stream));
+    PSG_CUDA(cudaMemcpyAsync(net->h_losses + s, &net->dsc->loss, sizeof(double),
+                             cudaMemcpyDeviceToHost, net->stream));
+  }
+  PSG_CUDA(cudaEventRecord(net->t1, net->stream));
+  net->timed = true;
+  net->last_n = b;
+  net_check_flag(net);
+  if (losses) std::memcpy(losses, net->h_losses, steps * sizeof(double));
+}
+
+}  // namespace psg

@@ -94,14 +94,16 @@ struct Workspace {
   size_t elems = 0;
 };
 
+// All three passes may split K across blocks (fixed-order second-stage sums);
+// the shared workspace must hold conv_workspace_elems() floats.
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
-                bool relu, Mode mode, cudaStream_t s);
+                bool relu, const Workspace& ws, Mode mode, cudaStream_t s);
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-                Mode mode, cudaStream_t s);
-// dW [F][Kf] and db [F] (written, not accumulated).  Needs wgrad_workspace_elems().
+                const Workspace& ws, Mode mode, cudaStream_t s);
+// dW [F][Kf] and db [F] (written, not accumulated).
 void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
                 const Workspace& ws, Mode mode, cudaStream_t s);
-size_t wgrad_workspace_elems(const ConvGeom& g, Mode mode);
+size_t conv_workspace_elems(const ConvGeom& g, Mode mode);
 int conv_launches(const ConvGeom& g, int which, Mode mode);  // 0 fprop 1 dgrad 2 wgrad
 
 struct PoolGeom {
@@ -147,6 +149,9 @@ void argmax_count(const float* probs, const int32_t* labels, int n, int C,
 void gather_batch(const float* ds_images, const int32_t* ds_labels, const uint32_t* idx,
                   const int* cursor, int b, int pixels, int C, int cs, float* out,
                   int32_t* labels, cudaStream_t s);
+
+void stage_batch_nchw(const float* src, int n, int C, int H, int W, int cs, float* dst,
+                      cudaStream_t s);
 
 struct UpdateChunk {
   uint32_t begin, end;  // element range (multiples of 4 except tails)

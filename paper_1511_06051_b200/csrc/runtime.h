@@ -115,9 +115,41 @@ struct psg_net {
   int launches_per_step = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   bool timed = false;
+  // host-fed (e2e) training: NCHW staging buffer + its own step graph
+  float* d_stage = nullptr;
+  size_t d_stage_cap = 0;
+  cudaGraphExec_t host_graph = nullptr;
+  double* h_losses = nullptr;
+  size_t h_losses_cap = 0;
+  cudaEvent_t slots[16] = {};
 };
 
 namespace psg {
+
+// Per-op CUDA-event timer (psg_net_profile_step).
+struct OpTimer {
+  cudaStream_t stream = nullptr;
+  struct Rec {
+    psg_op_time info;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  explicit OpTimer(cudaStream_t s) : stream(s) {}
+  ~OpTimer();
+  void begin(const char* name, int layer, int phase, double flops, double bytes);
+  void end(int launches);
+};
+
+int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer = nullptr);
+int run_backward(psg_net* net, size_t n, OpTimer* timer = nullptr);
+int run_update(psg_net* net, bool advance, OpTimer* timer = nullptr);
+void ensure_capacity(psg_net* net, size_t n);
+void invalidate_graph(psg_net* net);
+
+void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, int* n_ops);
+void net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,
+                    double* losses);
+
 void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed);
 void net_free(psg_net* net);
 void net_check_flag(psg_net* net);  // throws std::runtime_error on the sticky flag

@@ -303,6 +303,36 @@ class Net:
         _lib.call("psg_net_last_loss", self.handle, ctypes.byref(v))
         return v.value
 
+    def train_host(self, images: np.ndarray, labels: np.ndarray) -> np.ndarray:
+        """End-to-end path: steps = images.shape[0]; per step an H2D copy of that step's
+        batch (NCHW fp32, pinned if allocated with _lib.PinnedArray), the step, and a D2H
+        read of its loss.  Returns the per-step losses."""
+        steps = images.shape[0]
+        assert images.dtype == np.float32 and images.flags.c_contiguous
+        assert labels.dtype == np.int32 and labels.flags.c_contiguous
+        losses = np.empty(steps, np.float64)
+        _lib.call("psg_net_train_host", self.handle, images.ctypes.data_as(_lib._F),
+                  labels.ctypes.data_as(_lib._I32), steps, losses.ctypes.data_as(_lib._D))
+        return losses
+
+    def profile_step(self, repeats: int = 5):
+        """Per-op CUDA-event times of one training step (list of dicts)."""
+        cap = 512
+        arr = (_lib.OpTime * cap)()
+        n = ctypes.c_int()
+        _lib.call("psg_net_profile_step", self.handle, repeats, arr, cap, ctypes.byref(n))
+        return [dict(name=a.name.decode(), layer=a.layer, phase=_lib.PHASES[a.phase],
+                     flops=a.flops, bytes=a.bytes, ms=a.ms, launches=a.launches)
+                for a in arr[:min(n.value, cap)]]
+
+    def event_record(self, slot: int) -> None:
+        _lib.call("psg_net_event_record", self.handle, slot)
+
+    def event_elapsed(self, a: int, b: int) -> float:
+        ms = ctypes.c_float()
+        _lib.call("psg_net_event_elapsed", self.handle, a, b, ctypes.byref(ms))
+        return ms.value
+
     def kernels_per_step(self) -> int:
         v = ctypes.c_int()
         _lib.call("psg_net_kernels_per_step", self.handle, ctypes.byref(v))
