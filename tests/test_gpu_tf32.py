@@ -1,0 +1,100 @@
+"""TF32 tensor-core mode (tcgen05) parity: per-layer outputs and gradients within the
+north star's 1e-2 relative bar (per-tensor max-normalised) against the fp64 oracle, and
+within 1e-2 of the strict fp32 path on the same state."""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import max_relative_deviation
+from paper_1511_06051_b200 import netspec as ns
+
+pytestmark = pytest.mark.gpu
+TF32 = 1e-2
+
+
+def f32(x):
+    return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+
+def tc_nets():
+    return {
+        # fprop/dgrad/wgrad rect paths: 32-channel blocks, pad 2, 16x16 and 8x8 images
+        "cq_body": ns.NetSpec([
+            ns.data_layer("data", 3, 32, 16, 16), ns.label_layer("label", 3),
+            ns.conv_layer("c1", "data", 5, 5, 32, pad=2), ns.relu_layer("r1", "c1"),
+            ns.pool_layer("p1", "r1", 3, 3, 2, 2, method=ns.POOL_AVE, ceil_mode=True),
+            ns.conv_layer("c2", "p1", 5, 5, 64, pad=2), ns.relu_layer("r2", "c2"),
+            ns.linear_layer("fc", "r2", 64), ns.linear_layer("out", "fc", 10),
+            ns.softmax_loss_layer("loss", "fc", "label") if False else
+            ns.softmax_loss_layer("loss", "out", "label")]),
+        # groups with 48 channels per group (16-float K blocks, SWIZZLE_64B), odd sizes
+        "grouped48": ns.NetSpec([
+            ns.data_layer("data", 2, 96, 13, 13), ns.label_layer("label", 2),
+            ns.conv_layer("c1", "data", 3, 3, 64, pad=1, group=2), ns.relu_layer("r1", "c1"),
+            ns.conv_layer("c2", "r1", 3, 3, 96, pad=1, group=2),
+            ns.pool_layer("p", "c2", 3, 3, 2, 2, ceil_mode=True),
+            ns.linear_layer("fc", "p", 32), ns.softmax_loss_layer("loss", "fc", "label")]),
+        "wide_linear": ns.NetSpec([
+            ns.data_layer("data", 130, 1, 1, 512), ns.label_layer("label", 130),
+            ns.linear_layer("fc1", "data", 320), ns.relu_layer("r", "fc1"),
+            ns.linear_layer("fc2", "r", 96), ns.softmax_loss_layer("loss", "fc2", "label")]),
+        "cifar10_quick": ns.make_cifar10_quick(8),
+    }
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    from paper_1511_06051_b200 import model
+    return model
+
+
+@pytest.mark.parametrize("name", list(tc_nets()))
+def test_tf32_per_layer_parity(gpu, oracle_lib, name):
+    spec = tc_nets()[name]
+    net = gpu.Net(spec, 31, precision="tf32")
+    orc = oracle_lib.net(spec, 31)
+    orc.set_weights(net.get_weights_flat())
+    rng = np.random.default_rng(11)
+    d = spec.data_spec().shape
+    x = f32(rng.uniform(-1, 1, size=tuple(d)))
+    y = rng.integers(0, net.num_classes(), size=d[0]).astype(np.int32)
+    loss, g = net.backward_flat(gpu.Batch(x, y))
+    lo, go = orc.backward(x, y)
+    assert abs(loss - lo) <= TF32 * max(1.0, abs(lo))
+    # End to end, TF32 rounding compounds through every layer below the loss; the
+    # north-star bar (1e-2) is per layer in isolation (checked below).
+    assert max_relative_deviation(g, go, net.segments()) <= 5 * TF32
+    n = d[0]
+    for li, l in enumerate(spec.layers):
+        if l.kind in (ns.DATA, ns.LABEL, ns.SOFTMAX_LOSS):
+            continue
+        inputs = [net.layer_output(spec.index_of(i)) for i in l.inputs]
+        want = orc.layer_forward(li, n, inputs)
+        assert max_relative_deviation(net.layer_output(li), want) <= TF32, f"forward {l.name}"
+        dy = net.layer_grad(li)
+        src = spec.layers[spec.index_of(l.inputs[0])]
+        dx_want, dp_want = orc.layer_backward(li, n, dy, want_dx=src.kind != ns.DATA)
+        if src.kind != ns.DATA:
+            got = net.layer_grad(spec.index_of(l.inputs[0]))
+            assert max_relative_deviation(got, dx_want) <= TF32, f"dgrad {l.name}"
+        off, cnt = orc.layer_params(li)
+        if cnt:
+            kc = cnt - (l.num_filters if l.kind == ns.CONV else l.num_outputs)
+            assert max_relative_deviation(g[off:off + cnt], dp_want,
+                                          [(0, kc), (kc, cnt - kc)]) <= TF32, f"wgrad {l.name}"
+
+
+def test_tf32_train_steps_track_strict(gpu, oracle_lib):
+    """A few graph-replayed TF32 steps stay within the TF32 bar of the strict path."""
+    from paper_1511_06051_b200 import data
+    spec = ns.make_cifar10_quick(20)
+    img, lab = oracle_lib.generate_synthetic(10, 3, 32, 32, 8, 2.0, 12345, 0)
+    ds = data.Dataset(f32(img), lab, 10)
+    nets = []
+    for prec in ("fp32", "tf32"):
+        net = gpu.Net(spec, 1, precision=prec)
+        net.set_sgd(gpu.SgdOptions(0.001, 0.9, 0.004))
+        net.set_training_data(data.make_worker_iterator(data.shard(ds, 1, 1), 0, 20, 1))
+        net.train(3)
+        nets.append(net)
+    assert max_relative_deviation(nets[1].get_weights_flat(), nets[0].get_weights_flat(),
+                                  nets[0].segments()) <= TF32
