@@ -24,231 +24,12 @@
 
 #include "psg_internal.h"
 #include "tc_gemm.cuh"
+#include "tc_kernel.cuh"
 
 namespace psg {
 namespace {
 
-enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3 };
-enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3 };
-enum RowMap { ROW_RECT = 0, ROW_LINEAR = 1 };
-
-constexpr int kThreads = 256;
-constexpr int kTileM = 128;
-
-struct TcArgs {
-  int a_mode, b_mode, row_map;
-  int n_tile;             // UMMA N (multiple of 16, <= 256)
-  int stage_bytes, a_bytes, stages;
-  int m_tiles, n_tiles;   // per (group, tap)
-  int G, taps;            // blockIdx.y = g * taps + tap
-  int kblocks, kb_per_split;
-  // coordinate helpers
-  int a_c_g;              // A channel / M offset per group
-  int b_r_g;              // B row (K or N) offset per group
-  int b_n_g;              // B N offset per group (rect MN)
-  int cb;                 // K blocks per tap (rect-K A, W^T B)
-  int kw, ph, pw, sign;   // tap shift: coord = origin + sign * (u - p)
-  // M rectangles (ROW_RECT)
-  int rm, wm, th, tw;
-  int out_h, out_w;
-  // K rectangles (A/B_RECT_MN)
-  int rk, wk, kth, ktw;
-  // epilogue
-  float* out;
-  float* ws;
-  long long ws_stride;
-  const float* bias;
-  int relu, accumulate;
-  int ldo;
-  int m_valid;            // rows valid in M (per group), ROW_LINEAR
-  int n_valid;            // columns valid in N (per group)
-  int col_g, col_tap, row_g;
-};
-
-template <int KBLK>
-__global__ void __launch_bounds__(kThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, const TcArgs p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tmem_full_bar;
-  __shared__ uint32_t tmem_base_sh;
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tile_m = blockIdx.x / p.n_tiles, tile_n = blockIdx.x % p.n_tiles;
-  const int g = blockIdx.y / p.taps, tap = blockIdx.y % p.taps;
-  const int split = blockIdx.z;
-  const int kb0 = split * p.kb_per_split;
-  const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
-
-  if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&map_a);
-    tc::tma_prefetch(&map_b);
-    for (int s = 0; s < p.stages; ++s) {
-      tc::mbar_init(tc::smem_u32(&full_bar[s]), 1);
-      tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
-    }
-    tc::mbar_init(tc::smem_u32(&tmem_full_bar), 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == 2) tc::tmem_alloc(tc::smem_u32(&tmem_base_sh), 256);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = tmem_base_sh;
-
-  // M-tile origin for pixel rectangles
-  int rb = 0, r_oh0 = 0, r_ow0 = 0;
-  if (p.row_map == ROW_RECT) {
-    rb = tile_m / (p.th * p.tw);
-    const int r = tile_m % (p.th * p.tw);
-    r_oh0 = (r / p.tw) * p.rm;
-    r_ow0 = (r % p.tw) * p.wm;
-  }
-
-  if (warp == 0 && lane == 0) {
-    // ------------------------------------------------------------ producer
-    const int u = tap / p.kw, v = tap % p.kw;
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % p.stages;
-      tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ((i / p.stages) & 1) ^ 1);
-      const uint32_t bar = tc::smem_u32(&full_bar[s]);
-      tc::mbar_arrive_expect_tx(bar, p.stage_bytes);
-      const uint32_t sa = tc::smem_u32(smem + static_cast<size_t>(s) * p.stage_bytes);
-      const uint32_t sb = sa + p.a_bytes;
-      const int kb = kb0 + i;
-      // K rectangle (pixels) for MN-major rect operands
-      int kbi = 0, koh = 0, kow = 0;
-      if (p.a_mode == A_RECT_MN || p.b_mode == B_RECT_MN) {
-        kbi = kb / (p.kth * p.ktw);
-        const int r = kb % (p.kth * p.ktw);
-        koh = (r / p.ktw) * p.rk;
-        kow = (r % p.ktw) * p.wk;
-      }
-      switch (p.a_mode) {
-        case A_RECT_K: {
-          const int t = kb / p.cb, cb = kb % p.cb;
-          const int tu = t / p.kw, tv = t % p.kw;
-          tc::tma_load_4d(sa, &map_a, bar, p.a_c_g * g + cb * KBLK,
-                          r_ow0 + p.sign * (tv - p.pw), r_oh0 + p.sign * (tu - p.ph), rb);
-          break;
-        }
-        case A_2D_K:
-          tc::tma_load_2d(sa, &map_a, bar, kb * KBLK, tile_m * kTileM);
-          break;
-        case A_RECT_MN:
-          for (int j = 0; j < kTileM / 32; ++j)
-            tc::tma_load_4d(sa + j * KBLK * 128, &map_a, bar,
-                            p.a_c_g * g + tile_m * kTileM + 32 * j, kow, koh, kbi);
-          break;
-        case A_2D_MN:
-          for (int j = 0; j < kTileM / 32; ++j)
-            tc::tma_load_2d(sa + j * KBLK * 128, &map_a, bar, tile_m * kTileM + 32 * j,
-                            kb * KBLK);
-          break;
-      }
-      const int nch = (p.n_tile + 31) / 32;
-      switch (p.b_mode) {
-        case B_2D_K:
-          tc::tma_load_2d(sb, &map_b, bar, kb * KBLK, p.b_r_g * g + tile_n * p.n_tile);
-          break;
-        case B_WT_MN: {
-          const int t = kb / p.cb, fb = kb % p.cb;
-          for (int j = 0; j < nch; ++j)
-            tc::tma_load_3d(sb + j * KBLK * 128, &map_b, bar, tile_n * p.n_tile + 32 * j, t,
-                            p.b_r_g * g + fb * KBLK);
-          break;
-        }
-        case B_RECT_MN:
-          for (int j = 0; j < nch; ++j)
-            tc::tma_load_4d(sb + j * KBLK * 128, &map_b, bar,
-                            p.b_n_g * g + tile_n * p.n_tile + 32 * j, kow + v - p.pw,
-                            koh + u - p.ph, kbi);
-          break;
-        case B_2D_MN:
-          for (int j = 0; j < nch; ++j)
-            tc::tma_load_2d(sb + j * KBLK * 128, &map_b, bar, tile_n * p.n_tile + 32 * j,
-                            kb * KBLK);
-          break;
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ------------------------------------------------------------ MMA issue
-    const bool a_mn = p.a_mode == A_RECT_MN || p.a_mode == A_2D_MN;
-    const bool b_mn = p.b_mode != B_2D_K;
-    const uint32_t idesc = tc::idesc_tf32(kTileM, p.n_tile, a_mn, b_mn);
-    const uint32_t k_sw = KBLK == 32 ? tc::kSw128 : tc::kSw64;
-    const uint32_t k_sbo = 8 * KBLK * 4;  // 8 rows of KBLK floats
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % p.stages;
-      tc::mbar_wait(tc::smem_u32(&full_bar[s]), (i / p.stages) & 1);
-      tc::fence_after_sync();
-      const uint32_t sa = tc::smem_u32(smem + static_cast<size_t>(s) * p.stage_bytes);
-      const uint32_t sb = sa + p.a_bytes;
-#pragma unroll
-      for (int j = 0; j < KBLK / 8; ++j) {
-        const uint64_t ad = a_mn ? tc::smem_desc(sa + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
-                                 : tc::smem_desc(sa + j * 32, 16, k_sbo, k_sw);
-        const uint64_t bd = b_mn ? tc::smem_desc(sb + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
-                                 : tc::smem_desc(sb + j * 32, 16, k_sbo, k_sw);
-        tc::mma_tf32(tmem, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
-      }
-      tc::mma_commit(tc::smem_u32(&empty_bar[s]));
-    }
-    tc::mma_commit(tc::smem_u32(&tmem_full_bar));
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;
-    const int m = ew * 32 + lane;
-    bool row_ok;
-    long long out_row;
-    if (p.row_map == ROW_RECT) {
-      const int oh = r_oh0 + m / p.wm, ow = r_ow0 + m % p.wm;
-      row_ok = oh < p.out_h && ow < p.out_w;
-      out_row = (static_cast<long long>(rb) * p.out_h + oh) * p.out_w + ow;
-    } else {
-      const int mm = tile_m * kTileM + m;
-      row_ok = mm < p.m_valid;
-      out_row = static_cast<long long>(p.row_g) * g + mm;
-    }
-    const int col0 = p.col_g * g + p.col_tap * tap + tile_n * p.n_tile;
-    const int nvalid = min(p.n_tile, p.n_valid - tile_n * p.n_tile);
-    tc::mbar_wait(tc::smem_u32(&tmem_full_bar), 0);
-    tc::fence_after_sync();
-    for (int c0 = 0; c0 < p.n_tile; c0 += 16) {
-      float vals[16];
-      tc::tmem_ld16(tmem + (static_cast<uint32_t>(ew * 32) << 16) + c0, vals);
-      if (!row_ok) continue;
-      const long long base = out_row * p.ldo + col0 + c0;
-      if (p.ws) {
-        float* dst = p.ws + split * p.ws_stride + base;
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (c0 + q < nvalid) dst[q] = vals[q];
-      } else {
-        float* dst = p.out + base;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          if (c0 + q >= nvalid) continue;
-          float y = vals[q];
-          if (p.bias) {
-            y += p.bias[col0 + c0 + q];
-            if (p.relu) y = y > 0.f ? y : 0.f;
-          }
-          if (p.accumulate) y += dst[q];
-          dst[q] = y;
-        }
-      }
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 2) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc(tmem, 256);
-  }
-}
+using namespace tck;
 
 // Fixed-order second stage: out[i] (+)= sum_z ws[z][i] (+ bias[i % ldo], relu).
 __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long long stride,
@@ -359,15 +140,27 @@ void finish_args(TcArgs& a, int kblk, int sms) {
   const int nb = b_mn ? (a.n_tile + 31) / 32 * 32 : a.n_tile;
   a.a_bytes = kTileM * kblk * 4;
   a.stage_bytes = a.a_bytes + nb * kblk * 4;
-  a.stages = std::min(8, (220 * 1024) / a.stage_bytes);
+  a.stages = std::min(8, (225 * 1024 - kEpiBytes) / a.stage_bytes);
   const long long tiles = static_cast<long long>(a.m_tiles) * a.n_tiles * a.G * a.taps;
   int splits = 1;
   if (tiles < sms) splits = static_cast<int>(std::min<long long>((sms + tiles - 1) / tiles,
                                                                  std::max(1, a.kblocks / 4)));
   a.kb_per_split = (a.kblocks + splits - 1) / splits;
+  a.splits = (a.kblocks + a.kb_per_split - 1) / a.kb_per_split;
+  a.total_tiles = tiles * a.splits;
 }
 
 int splits_of(const TcArgs& a) { return (a.kblocks + a.kb_per_split - 1) / a.kb_per_split; }
+
+int sm_count() {
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return sms;
+}
 
 void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int kblk,
             long long out_elems, float* ws, size_t ws_elems, cudaStream_t s) {
@@ -379,8 +172,8 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     a.ws = ws;
     a.ws_stride = out_elems;
   }
-  const dim3 grid(a.m_tiles * a.n_tiles, a.G * a.taps, splits);
-  const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + 1024;
+  const dim3 grid(static_cast<unsigned>(std::min<long long>(a.total_tiles, sm_count())));
+  const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + kEpiBytes + 1024;
   if (kblk == 32) {
     PSG_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
@@ -549,15 +342,6 @@ bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   return true;
 }
 
-int sm_count() {
-  static int sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return sms;
-}
 
 // MN-major tf32 operands: 128B rows swizzled in 32B chunks (UMMA SWIZZLE_128B_BASE32B).
 constexpr CUtensorMapSwizzle kMnSwizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;

@@ -4,6 +4,7 @@
 // (gather -> forward -> loss -> backward -> fused SGD update).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -666,6 +667,27 @@ void net_train(psg_net* net, long steps) {
   PSG_CUDA(cudaMemsetAsync(&net->dsc->cursor, 0, sizeof(int), net->stream));
   const LayerRt& d = net->L[net->data_idx];
   psg_dataset* ds = net->train_ds;
+  // PSG_EAGER=1: launch the step's kernels directly instead of replaying the CUDA
+  // graph (ncu cannot replay graph kernel nodes that take a __grid_constant__
+  // CUtensorMap).  Same kernels, same order.
+  static const bool eager = [] {
+    const char* e = std::getenv("PSG_EAGER");
+    return e && e[0] == '1';
+  }();
+  if (eager) {
+    PSG_CUDA(cudaEventRecord(net->t0, net->stream));
+    for (long s = 0; s < steps; ++s) {
+      gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
+                   d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+      run_forward(net, b, true, true);
+      run_backward(net, b);
+      run_update(net, true);
+    }
+    PSG_CUDA(cudaEventRecord(net->t1, net->stream));
+    net->timed = true;
+    net->last_n = b;
+    return;
+  }
   if (!net->graph || net->graph_batch != b) {
     invalidate_graph(net);
     cudaGraph_t graph;

@@ -1,0 +1,347 @@
+// Persistent warp-specialised tcgen05 TF32 GEMM kernel (see conv_tc.cu for the operand
+// modes and the host-side planners).
+//
+//   warps 0, 3  TMA producers (A / B operand): fill a `stages`-deep SMEM ring, one stage
+//               per K block, with division-free incremental coordinates
+//   warp 1      MMA issuer: tcgen05.mma.kind::tf32 into one of two TMEM accumulators
+//   warp 2      TMEM allocator (512 columns = 2 x 256 fp32 accumulators)
+//   warps 4..7  epilogue: TMEM -> registers -> padded SMEM transpose -> coalesced
+//               128-byte row stores (bias / ReLU / accumulate / split-K partials)
+// CTAs are persistent (grid = #SMs); tile t of a CTA uses accumulator t % 2, so the
+// epilogue of tile t overlaps the MMAs of tile t + 1.
+#pragma once
+
+#include "tc_gemm.cuh"
+
+namespace psg {
+namespace tck {
+
+enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3 };
+enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3 };
+enum RowMap { ROW_RECT = 0, ROW_LINEAR = 1 };
+
+constexpr int kThreads = 256;
+constexpr int kTileM = 128;
+constexpr int kAccCols = 256;                 // one accumulator: 128 lanes x 256 fp32
+constexpr int kStagePad = 33;                 // epilogue transpose row pitch (floats)
+constexpr int kEpiBytes = 4 * 32 * kStagePad * 4;
+
+struct TcArgs {
+  int a_mode, b_mode, row_map;
+  int n_tile;             // UMMA N (multiple of 16, <= 256)
+  int stage_bytes, a_bytes, stages;
+  int m_tiles, n_tiles;   // per (group, tap)
+  int G, taps;            // group / tap index g * taps + tap
+  int kblocks, kb_per_split, splits;
+  long long total_tiles;  // m_tiles * n_tiles * G * taps * splits
+  // coordinate helpers
+  int a_c_g;              // A channel / M offset per group
+  int b_r_g;              // B row (K or N) offset per group
+  int b_n_g;              // B N offset per group (rect MN)
+  int cb;                 // K blocks per tap (rect-K A, W^T B)
+  int kw, ph, pw, sign;   // tap shift: coord = origin + sign * (u - p)
+  // M rectangles (ROW_RECT)
+  int rm, wm, th, tw;
+  int out_h, out_w;
+  // K rectangles (A/B_RECT_MN)
+  int rk, wk, kth, ktw;
+  // epilogue
+  float* out;
+  float* ws;
+  long long ws_stride;
+  const float* bias;
+  int relu, accumulate;
+  int ldo;
+  int m_valid;            // rows valid in M (per group), ROW_LINEAR
+  int n_valid;            // columns valid in N (per group)
+  int col_g, col_tap, row_g;
+};
+
+struct Tile {
+  int m, n, g, tap, split;
+};
+
+__device__ __forceinline__ Tile decode_tile(const TcArgs& p, long long t) {
+  Tile r;
+  r.n = static_cast<int>(t % p.n_tiles);
+  t /= p.n_tiles;
+  r.m = static_cast<int>(t % p.m_tiles);
+  t /= p.m_tiles;
+  const int gt = static_cast<int>(t % (p.G * p.taps));
+  r.split = static_cast<int>(t / (p.G * p.taps));
+  r.g = gt / p.taps;
+  r.tap = gt % p.taps;
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Incremental K-block cursor: coordinates advance without divisions in the loop.
+struct KCursor {
+  int kb;
+  int t0, t1;      // rect-K A / W^T B: (channel-or-filter block, tap)
+  int tu, tv;      // tap coordinates
+  int kbi, koh, kow;  // K pixel rectangle (MN rect operands)
+  __device__ __forceinline__ void init(const TcArgs& p, int kb0) {
+    kb = kb0;
+    if (p.cb) {
+      t0 = kb0 % p.cb;
+      t1 = kb0 / p.cb;
+      tu = t1 / p.kw;
+      tv = t1 % p.kw;
+    }
+    if (p.kth) {
+      kbi = kb0 / (p.kth * p.ktw);
+      const int r = kb0 % (p.kth * p.ktw);
+      koh = (r / p.ktw) * p.rk;
+      kow = (r % p.ktw) * p.wk;
+    }
+  }
+  __device__ __forceinline__ void next(const TcArgs& p) {
+    ++kb;
+    if (p.cb && ++t0 == p.cb) {
+      t0 = 0;
+      ++t1;
+      if (++tv == p.kw) {
+        tv = 0;
+        ++tu;
+      }
+    }
+    if (p.kth) {
+      kow += p.wk;
+      if (kow >= p.ktw * p.wk) {
+        kow = 0;
+        koh += p.rk;
+        if (koh >= p.kth * p.rk) {
+          koh = 0;
+          ++kbi;
+        }
+      }
+    }
+  }
+};
+
+// A operand of one K block (producer thread A).
+template <int KBLK>
+__device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, const Tile& t,
+                                       const KCursor& c, int rb, int oh0, int ow0, uint32_t sa,
+                                       uint32_t bar) {
+  switch (p.a_mode) {
+    case A_RECT_K:
+      tc::tma_load_4d(sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0 + p.sign * (c.tv - p.pw),
+                      oh0 + p.sign * (c.tu - p.ph), rb);
+      break;
+    case A_2D_K:
+      tc::tma_load_2d(sa, map, bar, c.kb * KBLK, t.m * kTileM);
+      break;
+    case A_RECT_MN:
+#pragma unroll
+      for (int j = 0; j < kTileM / 32; ++j)
+        tc::tma_load_4d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
+                        c.kow, c.koh, c.kbi);
+      break;
+    case A_2D_MN:
+#pragma unroll
+      for (int j = 0; j < kTileM / 32; ++j)
+        tc::tma_load_2d(sa + j * KBLK * 128, map, bar, t.m * kTileM + 32 * j, c.kb * KBLK);
+      break;
+  }
+}
+
+// B operand of one K block (producer thread B).
+template <int KBLK>
+__device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, const Tile& t,
+                                       const KCursor& c, int u, int v, uint32_t sb,
+                                       uint32_t bar) {
+  const int nch = (p.n_tile + 31) / 32;
+  switch (p.b_mode) {
+    case B_2D_K:
+      tc::tma_load_2d(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + t.n * p.n_tile);
+      break;
+    case B_WT_MN:
+      for (int j = 0; j < nch; ++j)
+        tc::tma_load_3d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.t1,
+                        p.b_r_g * t.g + c.t0 * KBLK);
+      break;
+    case B_RECT_MN:
+      for (int j = 0; j < nch; ++j)
+        tc::tma_load_4d(sb + j * KBLK * 128, map, bar, p.b_n_g * t.g + t.n * p.n_tile + 32 * j,
+                        c.kow + v - p.pw, c.koh + u - p.ph, c.kbi);
+      break;
+    case B_2D_MN:
+      for (int j = 0; j < nch; ++j)
+        tc::tma_load_2d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.kb * KBLK);
+      break;
+  }
+}
+
+template <int KBLK>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, const TcArgs p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  float* epi = reinterpret_cast<float*>(smem + static_cast<size_t>(p.stages) * p.stage_bytes);
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&map_a);
+    tc::tma_prefetch(&map_b);
+    for (int s = 0; s < p.stages; ++s) {
+      tc::mbar_init(tc::smem_u32(&full_bar[s]), 2);  // A and B producers
+      tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(tc::smem_u32(&tfull_bar[b]), 1);
+      tc::mbar_init(tc::smem_u32(&tempty_bar[b]), 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc(tc::smem_u32(&tmem_base_sh), 2 * kAccCols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_base_sh;
+
+  if ((warp == 0 || warp == 3) && lane == 0) {
+    // ----------------------------------------- producers: warp 0 -> A, warp 3 -> B
+    const bool is_a = warp == 0;
+    const uint32_t bytes = is_a ? p.a_bytes : p.stage_bytes - p.a_bytes;
+    uint32_t it = 0;
+    for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x) {
+      const Tile t = decode_tile(p, tt);
+      const int kb0 = t.split * p.kb_per_split;
+      const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
+      int rb = 0, oh0 = 0, ow0 = 0;
+      if (p.a_mode == A_RECT_K) {
+        rb = t.m / (p.th * p.tw);
+        const int r = t.m % (p.th * p.tw);
+        oh0 = (r / p.tw) * p.rm;
+        ow0 = (r % p.tw) * p.wm;
+      }
+      const int u = t.tap / p.kw, v = t.tap % p.kw;
+      KCursor c;
+      c.init(p, kb0);
+      for (int kb = kb0; kb < kb1; ++kb, ++it, c.next(p)) {
+        const uint32_t s = it % p.stages;
+        tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ((it / p.stages) & 1) ^ 1);
+        const uint32_t bar = tc::smem_u32(&full_bar[s]);
+        tc::mbar_arrive_expect_tx(bar, bytes);
+        const uint32_t sa = tc::smem_u32(smem + s * p.stage_bytes);
+        if (is_a)
+          load_a<KBLK>(p, &map_a, t, c, rb, oh0, ow0, sa, bar);
+        else
+          load_b<KBLK>(p, &map_b, t, c, u, v, sa + p.a_bytes, bar);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------ MMA issue
+    const bool a_mn = p.a_mode == A_RECT_MN || p.a_mode == A_2D_MN;
+    const bool b_mn = p.b_mode != B_2D_K;
+    const uint32_t idesc = tc::idesc_tf32(kTileM, p.n_tile, a_mn, b_mn);
+    const uint32_t k_sw = KBLK == 32 ? tc::kSw128 : tc::kSw64;
+    const uint32_t k_sbo = 8 * KBLK * 4;  // 8 rows of KBLK floats
+    uint32_t it = 0, local = 0;
+    for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x, ++local) {
+      const Tile t = decode_tile(p, tt);
+      const int kb0 = t.split * p.kb_per_split;
+      const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+      const uint32_t acc = local & 1;
+      tc::mbar_wait(tc::smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
+      tc::fence_after_sync();
+      const uint32_t d = tmem + acc * kAccCols;
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const uint32_t s = it % p.stages;
+        tc::mbar_wait(tc::smem_u32(&full_bar[s]), (it / p.stages) & 1);
+        tc::fence_after_sync();
+        const uint32_t sa = tc::smem_u32(smem + s * p.stage_bytes);
+        const uint32_t sb = sa + p.a_bytes;
+#pragma unroll
+        for (int j = 0; j < KBLK / 8; ++j) {
+          const uint64_t ad = a_mn ? tc::smem_desc(sa + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
+                                   : tc::smem_desc(sa + j * 32, 16, k_sbo, k_sw);
+          const uint64_t bd = b_mn ? tc::smem_desc(sb + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
+                                   : tc::smem_desc(sb + j * 32, 16, k_sbo, k_sw);
+          tc::mma_tf32(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+        }
+        tc::mma_commit(tc::smem_u32(&empty_bar[s]));
+      }
+      tc::mma_commit(tc::smem_u32(&tfull_bar[acc]));
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    float* stg = epi + ew * 32 * kStagePad;
+    uint32_t local = 0;
+    for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x, ++local) {
+      const Tile t = decode_tile(p, tt);
+      const int m = ew * 32 + lane;
+      bool row_ok;
+      long long out_row;
+      if (p.row_map == ROW_RECT) {
+        const int rb = t.m / (p.th * p.tw);
+        const int r = t.m % (p.th * p.tw);
+        const int oh = (r / p.tw) * p.rm + m / p.wm, ow = (r % p.tw) * p.wm + m % p.wm;
+        row_ok = oh < p.out_h && ow < p.out_w;
+        out_row = (static_cast<long long>(rb) * p.out_h + oh) * p.out_w + ow;
+      } else {
+        const int mm = t.m * kTileM + m;
+        row_ok = mm < p.m_valid;
+        out_row = static_cast<long long>(p.row_g) * t.g + mm;
+      }
+      float* base = (p.ws ? p.ws + t.split * p.ws_stride : p.out);
+      const long long row_off = out_row * p.ldo;
+      const int col0 = p.col_g * t.g + p.col_tap * t.tap + t.n * p.n_tile;
+      const int nvalid = min(p.n_tile, p.n_valid - t.n * p.n_tile);
+      const uint32_t acc = local & 1;
+      tc::mbar_wait(tc::smem_u32(&tfull_bar[acc]), (local >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t taddr = tmem + acc * kAccCols + (static_cast<uint32_t>(ew * 32) << 16);
+      for (int c0 = 0; c0 < p.n_tile; c0 += 32) {
+        float v[32];
+        tc::tmem_ld16(taddr + c0, v);
+        if (c0 + 16 < p.n_tile) tc::tmem_ld16(taddr + c0 + 16, v + 16);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) stg[lane * kStagePad + q] = v[q];
+        __syncwarp();
+        const int col = c0 + lane;
+        const bool col_ok = col < nvalid;
+        float bv = 0.f;
+        if (col_ok && p.bias && !p.ws) bv = p.bias[col0 + col];
+        for (int i = 0; i < 32; ++i) {
+          const bool ok = __shfl_sync(0xffffffffu, row_ok, i);
+          const long long ro = __shfl_sync(0xffffffffu, row_off, i);
+          if (!ok || !col_ok) continue;
+          float y = stg[i * kStagePad + lane];
+          float* dst = base + ro + col0 + col;
+          if (!p.ws) {
+            if (p.bias) {
+              y += bv;
+              if (p.relu) y = y > 0.f ? y : 0.f;
+            }
+            if (p.accumulate) y += *dst;
+          }
+          *dst = y;
+        }
+        __syncwarp();
+      }
+      tc::fence_before_sync();
+      mbar_arrive(tc::smem_u32(&tempty_bar[acc]));
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, 2 * kAccCols);
+  }
+}
+
+}  // namespace tck
+}  // namespace psg
