@@ -75,6 +75,32 @@ void net_train_host(psg_net* net, const float* images, const int32_t* labels, lo
     PSG_CUDA(cudaMallocHost(&net->h_losses, steps * sizeof(double)));
     net->h_losses_cap = static_cast<size_t>(steps);
   }
+  static const bool eager = [] {  // PSG_EAGER=1: no graph replay (see net_train)
+    const char* e = std::getenv("PSG_EAGER");
+    return e && e[0] == '1';
+  }();
+  if (eager) {
+    PSG_CUDA(cudaEventRecord(net->t0, net->stream));
+    for (long s = 0; s < steps; ++s) {
+      PSG_CUDA(cudaMemcpyAsync(net->d_stage, images + s * b * chw, b * chw * sizeof(float),
+                               cudaMemcpyHostToDevice, net->stream));
+      PSG_CUDA(cudaMemcpyAsync(net->labels, labels + s * b, b * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, net->stream));
+      stage_batch_nchw(net->d_stage, static_cast<int>(b), d.C, d.H, d.W, d.cs, d.out,
+                       net->stream);
+      run_forward(net, b, true, true);
+      run_backward(net, b);
+      run_update(net, true);
+      PSG_CUDA(cudaMemcpyAsync(net->h_losses + s, &net->dsc->loss, sizeof(double),
+                               cudaMemcpyDeviceToHost, net->stream));
+    }
+    PSG_CUDA(cudaEventRecord(net->t1, net->stream));
+    net->timed = true;
+    net->last_n = b;
+    net_check_flag(net);
+    if (losses) std::memcpy(losses, net->h_losses, steps * sizeof(double));
+    return;
+  }
   if (!net->host_graph || net->graph_batch != b) {
     if (net->graph_batch != b) invalidate_graph(net);
     if (net->host_graph) cudaGraphExecDestroy(net->host_graph);
