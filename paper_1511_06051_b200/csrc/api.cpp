@@ -282,10 +282,8 @@ int psg_net_set_precision(psg_net* net, int precision) {
     if (m != net->mode) {
       psg::DeviceGuard dg(net->ctx->device);
       PSG_CUDA(cudaStreamSynchronize(net->stream));
-      if (net->graph) cudaGraphExecDestroy(net->graph);
-      net->graph = nullptr;
-      net->graph_batch = 0;
       net->mode = m;
+      psg::release_batch_buffers(net);  // TF32 may need im2col buffers; realloc on next use
     }
   });
 }

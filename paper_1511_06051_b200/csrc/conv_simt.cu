@@ -26,6 +26,7 @@ struct FpropProb {
   int H, W, cs_in, OH, OW, F, kh, kw, sh, sw, ph, pw, Cgs, Fg, G;
   int M, N, K;
   int relu;
+  int Kp;     // weight row stride
   float* ws;  // split-K partials [splits][G][M][N], or null for a direct store
   static constexpr bool A_KC = true;  // A contiguous along k (channels)
   static constexpr bool B_KC = true;
@@ -71,7 +72,7 @@ struct FpropProb {
     return __ldg(c.base + (static_cast<size_t>(ih) * W + iw) * cs_in + k.off);
   }
   __device__ BCtx bctx(int g, int n) const {
-    return BCtx{n < N ? w + static_cast<size_t>(g * Fg + n) * K : nullptr};
+    return BCtx{n < N ? w + static_cast<size_t>(g * Fg + n) * Kp : nullptr};
   }
   __device__ BK_ bkey(int, int k, int ke) const { return BK_{k, k < ke}; }
   __device__ float b(const BCtx& c, const BK_& k) const {
@@ -97,6 +98,7 @@ struct DgradProb {
   int H, W, cs_in, OH, OW, F, kh, kw, sh, sw, ph, pw, Cgs, Fg, G;
   int M, N, K;
   int accumulate;
+  int Kp;     // weight row stride
   float* ws;  // split-K partials, or null for a direct store
   static constexpr bool A_KC = true;   // dY contiguous along f (fastest part of k)
   static constexpr bool B_KC = false;  // W contiguous along c (= n)
@@ -145,7 +147,7 @@ struct DgradProb {
   __device__ BK_ bkey(int g, int k, int ke) const {
     if (k >= ke) return BK_{nullptr};
     const int f = k % Fg, t = k / Fg, v = t % kw, u = t / kw;
-    return BK_{w + (static_cast<size_t>(g * Fg + f) * kh * kw + u * kw + v) * Cgs};
+    return BK_{w + static_cast<size_t>(g * Fg + f) * Kp + static_cast<size_t>(u * kw + v) * Cgs};
   }
   __device__ float b(const BCtx& c, const BK_& k) const {
     return (c.c >= 0 && k.wp) ? __ldg(k.wp + c.c) : 0.f;
@@ -170,6 +172,7 @@ struct WgradProb {
   int H, W, cs_in, OH, OW, F, kh, kw, sh, sw, ph, pw, Cgs, Fg, G;
   int M, N, K;  // M = Fg, N = Kf + 1, K = n*OH*OW
   int Kf;
+  int Kp;      // dW row stride
   int direct;  // one split: write dW / db directly
   static constexpr bool A_KC = false;  // dY contiguous along f (= m)
   static constexpr bool B_KC = false;  // X contiguous along c (part of n)
@@ -226,7 +229,7 @@ struct WgradProb {
   __device__ void store(int g, int z, int m, int n, float v) const {
     if (direct) {
       if (n < Kf)
-        dw[static_cast<size_t>(g * Fg + m) * Kf + n] = v;
+        dw[static_cast<size_t>(g * Fg + m) * Kp + n] = v;
       else
         db[g * Fg + m] = v;
     } else {
@@ -351,7 +354,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 
 // Fixed-order sum of the split partials into dW / db.
 __global__ void wgrad_reduce(const float* __restrict__ ws, int splits, int G, int M, int N,
-                             int Kf, int Fg, float* __restrict__ dw, float* __restrict__ db) {
+                             int Kf, int Kp, int Fg, float* __restrict__ dw,
+                             float* __restrict__ db) {
   const size_t total = static_cast<size_t>(G) * M * N;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -361,7 +365,7 @@ __global__ void wgrad_reduce(const float* __restrict__ ws, int splits, int G, in
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += ws[static_cast<size_t>(z) * total + i];
     if (n < Kf)
-      dw[static_cast<size_t>(g * Fg + m) * Kf + n] = s;
+      dw[static_cast<size_t>(g * Fg + m) * Kp + n] = s;
     else
       db[g * Fg + m] = s;
   }
@@ -505,6 +509,7 @@ void conv_fprop_simt(const ConvGeom& g, const float* x, const float* w, const fl
   p.M = g.n * g.OH * g.OW;
   p.N = g.Fg();
   p.K = g.Kf();
+  p.Kp = g.Kp();
   p.relu = relu;
   const Split sp = fprop_split(g);
   p.ws = split_ws(ws, sp, g.G, p.M, p.N);
@@ -522,6 +527,7 @@ void conv_dgrad_simt(const ConvGeom& g, const float* dy, const float* w, float* 
   p.M = g.n * g.H * g.W;
   p.N = g.Cgs();
   p.K = g.kh * g.kw * g.Fg();
+  p.Kp = g.Kp();
   p.accumulate = accumulate;
   const Split sp = dgrad_split(g);
   p.ws = split_ws(ws, sp, g.G, p.M, p.N);
@@ -554,6 +560,7 @@ void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* 
   p.dw = dw;
   p.db = db;
   p.Kf = g.Kf();
+  p.Kp = g.Kp();
   p.M = g.Fg();
   p.N = p.Kf + 1;
   p.K = g.n * g.OH * g.OW;
@@ -564,7 +571,8 @@ void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* 
   if (!p.direct) {
     const size_t total = static_cast<size_t>(g.G) * p.M * p.N;
     const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 8));
-    wgrad_reduce<<<blocks, 256, 0, s>>>(ws.ptr, sp.splits, g.G, p.M, p.N, p.Kf, g.Fg(), dw, db);
+    wgrad_reduce<<<blocks, 256, 0, s>>>(ws.ptr, sp.splits, g.G, p.M, p.N, p.Kf, p.Kp, g.Fg(), dw,
+                                        db);
     PSG_CUDA(cudaGetLastError());
   }
 }

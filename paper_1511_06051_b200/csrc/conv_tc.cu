@@ -338,7 +338,7 @@ bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.n_valid = g.Cgs();
   a.row_g = g.Fg();
   a.col_tap = g.Cgs();
-  a.ldo = g.Kf();
+  a.ldo = g.Kp();
   return true;
 }
 
@@ -357,7 +357,7 @@ size_t tc_wgrad_ws_elems(const ConvGeom& g) {
   if (!plan_wgrad(g, a, kblk)) return 0;
   finish_args(a, kblk, sm_count());
   const int splits = splits_of(a);
-  return (splits > 1 ? static_cast<size_t>(splits) * g.F * g.Kf() : 0) +
+  return (splits > 1 ? static_cast<size_t>(splits) * g.F * g.Kp() : 0) +
          64 * static_cast<size_t>(g.F);
 }
 
@@ -422,7 +422,7 @@ void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bi
     mb = map_2d(w, g.F, g.cs_in, kblk, a.n_tile, k_swizzle(kblk));
   } else {
     ma = map_nhwc(x, g.n, g.H, g.W, g.cs_in, kblk, a.wm, a.rm, k_swizzle(kblk));
-    mb = map_2d(w, g.F, g.Kf(), kblk, a.n_tile, k_swizzle(kblk));
+    mb = map_2d(w, g.F, g.Kp(), kblk, a.n_tile, k_swizzle(kblk));
   }
   launch(a, ma, mb, kblk, static_cast<long long>(g.n) * g.OH * g.OW * g.F, ws.ptr, ws.elems, s);
 }
@@ -444,7 +444,7 @@ void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, boo
     const uint64_t dims[3] = {static_cast<uint64_t>(g.Cgs()),
                               static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.F)};
     const uint64_t str[2] = {static_cast<uint64_t>(g.Cgs()) * 4,
-                             static_cast<uint64_t>(g.Kf()) * 4};
+                             static_cast<uint64_t>(g.Kp()) * 4};
     const uint32_t box[3] = {32, 1, static_cast<uint32_t>(kblk)};
     mb = make_map(w, 3, dims, str, box, kMnSwizzle);
   }
@@ -467,7 +467,7 @@ void tc_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, flo
     ma = map_nhwc(dy, g.n, g.OH, g.OW, g.F, 32, a.wk, a.rk, kMnSwizzle);
     mb = map_nhwc(x, g.n, g.H, g.W, g.cs_in, 32, a.wk, a.rk, kMnSwizzle);
   }
-  const long long dw_elems = static_cast<long long>(g.F) * g.Kf();
+  const long long dw_elems = static_cast<long long>(g.F) * g.Kp();
   // the split-K workspace holds dW partials; bias partials go after them
   const int splits = splits_of(a);
   float* part = ws.ptr + (splits > 1 ? splits * dw_elems : 0);

@@ -1,5 +1,6 @@
-// HBM-bound kernels of the training step (NHWC, fp32).  Every reduction is a
-// fixed-order gather (no float atomics), so a step is bitwise reproducible.
+// Elementwise / reduction kernels of the training step: ReLU, softmax-loss, argmax,
+// the fused SGD update, the ordered weight average.  Every reduction is fixed-order
+// (no float atomics), so a step is bitwise reproducible.
 #include <algorithm>
 #include <cfloat>
 
@@ -24,87 +25,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:11-16
   return x ^ (x >> 31);
 }
 
-// ------------------------------------------------------------------ pool ---
-// model.hpp:369-406 (max, strict '>' so the first maximum in (u, v) scan order
-// wins) with Caffe padding / ceil windows; AVE divides by the window clipped to
-// the padded extent.  route = (u * kw + v) relative to the unclipped window.
-__global__ void pool_fwd_k(PoolGeom g, const float* __restrict__ x, float* __restrict__ y,
-                           uint8_t* __restrict__ route) {
-  const size_t total = static_cast<size_t>(g.n) * g.OH * g.OW * g.C;
-  GRID_STRIDE(i, total) {
-    const int c = static_cast<int>(i % g.C);
-    size_t t = i / g.C;
-    const int ow = static_cast<int>(t % g.OW);
-    t /= g.OW;
-    const int oh = static_cast<int>(t % g.OH);
-    const int b = static_cast<int>(t / g.OH);
-    const int hs0 = oh * g.sh - g.ph, ws0 = ow * g.sw - g.pw;
-    const int he0 = hs0 + g.kh, we0 = ws0 + g.kw;
-    const int hs = max(hs0, 0), ws = max(ws0, 0), he = min(he0, g.H), we = min(we0, g.W);
-    const float* xb = x + static_cast<size_t>(b) * g.H * g.W * g.C + c;
-    if (g.method == PSG_POOL_AVE) {
-      const int size = (min(he0, g.H + g.ph) - hs0) * (min(we0, g.W + g.pw) - ws0);
-      float acc = 0.f;
-      for (int r = hs; r < he; ++r)
-        for (int s = ws; s < we; ++s) acc += xb[(static_cast<size_t>(r) * g.W + s) * g.C];
-      y[i] = acc / static_cast<float>(size);
-    } else {
-      float best = xb[(static_cast<size_t>(hs) * g.W + ws) * g.C];
-      int arg = (hs - hs0) * g.kw + (ws - ws0);
-      for (int r = hs; r < he; ++r) {
-        for (int s = ws; s < we; ++s) {
-          const float v = xb[(static_cast<size_t>(r) * g.W + s) * g.C];
-          if (v > best) {
-            best = v;
-            arg = (r - hs0) * g.kw + (s - ws0);
-          }
-        }
-      }
-      y[i] = best;
-      route[i] = static_cast<uint8_t>(arg);
-    }
-  }
-}
-
-// model.hpp:492-498 as a deterministic gather: each input sums, in ascending
-// output order, the dy of the covering windows that routed to it.
-__global__ void pool_bwd_k(PoolGeom g, const float* __restrict__ dy,
-                           const uint8_t* __restrict__ route, float* __restrict__ dx,
-                           int accumulate) {
-  const size_t total = static_cast<size_t>(g.n) * g.H * g.W * g.C;
-  GRID_STRIDE(i, total) {
-    const int c = static_cast<int>(i % g.C);
-    size_t t = i / g.C;
-    const int w = static_cast<int>(t % g.W);
-    t /= g.W;
-    const int h = static_cast<int>(t % g.H);
-    const int b = static_cast<int>(t / g.H);
-    // windows with oh*sh - ph <= h < oh*sh - ph + kh
-    const int ohl = max(0, (h + g.ph - g.kh + g.sh) / g.sh), ohh = min(g.OH - 1, (h + g.ph) / g.sh);
-    const int owl = max(0, (w + g.pw - g.kw + g.sw) / g.sw), owh = min(g.OW - 1, (w + g.pw) / g.sw);
-    const size_t obase = static_cast<size_t>(b) * g.OH * g.OW;
-    float acc = 0.f;
-    for (int oh = ohl; oh <= ohh; ++oh) {
-      const int hs0 = oh * g.sh - g.ph;
-      if (h < hs0 || h >= hs0 + g.kh) continue;
-      for (int ow = owl; ow <= owh; ++ow) {
-        const int ws0 = ow * g.sw - g.pw;
-        if (w < ws0 || w >= ws0 + g.kw) continue;
-        const size_t o = (obase + static_cast<size_t>(oh) * g.OW + ow) * g.C + c;
-        if (g.method == PSG_POOL_AVE) {
-          const int size =
-              (min(hs0 + g.kh, g.H + g.ph) - hs0) * (min(ws0 + g.kw, g.W + g.pw) - ws0);
-          acc += dy[o] / static_cast<float>(size);
-        } else if (route[o] == (h - hs0) * g.kw + (w - ws0)) {
-          acc += dy[o];
-        }
-      }
-    }
-    dx[i] = accumulate ? dx[i] + acc : acc;
-  }
-}
-
 // ------------------------------------------------------------------ relu ---
+// model.hpp:319-326 (y = x > 0 ? x : 0) and :484-491 (dx += x > 0 ? dy : 0).
 __global__ void relu_fwd_k(const float* __restrict__ x, float* __restrict__ y, size_t n) {
   const size_t n4 = n / 4;
   const float4* x4 = reinterpret_cast<const float4*>(x);
@@ -125,85 +47,27 @@ __global__ void relu_fwd_k(const float* __restrict__ x, float* __restrict__ y, s
 
 __global__ void relu_bwd_k(const float* __restrict__ x, const float* __restrict__ dy,
                            float* __restrict__ dx, size_t n, int accumulate) {
-  GRID_STRIDE(i, n) {
-    const float g = x[i] > 0.f ? dy[i] : 0.f;  // model.hpp:489
+  const size_t n4 = n / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* g4 = reinterpret_cast<const float4*>(dy);
+  float4* d4 = reinterpret_cast<float4*>(dx);
+  GRID_STRIDE(i, n4) {
+    const float4 xv = x4[i], gv = g4[i];
+    float4 r = make_float4(xv.x > 0.f ? gv.x : 0.f, xv.y > 0.f ? gv.y : 0.f,
+                           xv.z > 0.f ? gv.z : 0.f, xv.w > 0.f ? gv.w : 0.f);
+    if (accumulate) {
+      const float4 o = d4[i];
+      r.x += o.x;
+      r.y += o.y;
+      r.z += o.z;
+      r.w += o.w;
+    }
+    d4[i] = r;
+  }
+  GRID_STRIDE(j, n - n4 * 4) {
+    const size_t i = n4 * 4 + j;
+    const float g = x[i] > 0.f ? dy[i] : 0.f;
     dx[i] = accumulate ? dx[i] + g : g;
-  }
-}
-
-// ------------------------------------------------------------------- lrn ---
-// Caffe LRN ACROSS_CHANNELS on NHWC: the channel window is contiguous.
-__global__ void lrn_fwd_k(LrnGeom g, const float* __restrict__ x, float* __restrict__ y,
-                          float* __restrict__ scale) {
-  const size_t total = static_cast<size_t>(g.pixels) * g.C;
-  const int pre = (g.size - 1) / 2, post = g.size - pre - 1;
-  const float a = g.alpha / g.size;
-  GRID_STRIDE(i, total) {
-    const int c = static_cast<int>(i % g.C);
-    const float* row = x + (i - c);
-    const int lo = max(0, c - pre), hi = min(g.C - 1, c + post);
-    float acc = 0.f;
-    for (int q = lo; q <= hi; ++q) acc += row[q] * row[q];
-    const float s = g.k + a * acc;
-    scale[i] = s;
-    y[i] = x[i] * powf(s, -g.beta);
-  }
-}
-
-__global__ void lrn_bwd_k(LrnGeom g, const float* __restrict__ x, const float* __restrict__ y,
-                          const float* __restrict__ scale, const float* __restrict__ dy,
-                          float* __restrict__ dx, int accumulate) {
-  const size_t total = static_cast<size_t>(g.pixels) * g.C;
-  const int pre = (g.size - 1) / 2, post = g.size - pre - 1;
-  const float ratio = 2.f * g.alpha * g.beta / g.size;
-  GRID_STRIDE(i, total) {
-    const int c = static_cast<int>(i % g.C);
-    const size_t base = i - c;
-    const int lo = max(0, c - post), hi = min(g.C - 1, c + pre);
-    float acc = 0.f;
-    for (int q = lo; q <= hi; ++q) acc += dy[base + q] * y[base + q] / scale[base + q];
-    const float v = dy[i] * powf(scale[i], -g.beta) - ratio * x[i] * acc;
-    dx[i] = accumulate ? dx[i] + v : v;
-  }
-}
-
-// --------------------------------------------------------------- dropout ---
-// Keep-mask = splitmix64(mix(base ^ step) + nchw_index) >> 40 >= ratio * 2^24.
-__device__ __forceinline__ float drop_mask(const DropGeom& g, uint64_t base, size_t i,
-                                           uint32_t thresh, float keep) {
-  const int c = static_cast<int>(i % g.C);
-  size_t t = i / g.C;
-  const int w = static_cast<int>(t % g.W);
-  t /= g.W;
-  const int h = static_cast<int>(t % g.H);
-  const size_t b = t / g.H;
-  const uint64_t nchw = ((b * g.C + c) * g.H + h) * g.W + w;
-  const uint32_t u = static_cast<uint32_t>(mix64(base + nchw) >> 40);
-  return u >= thresh ? keep : 0.f;
-}
-
-__global__ void dropout_fwd_k(DropGeom g, const float* __restrict__ x, float* __restrict__ y,
-                              const uint64_t* __restrict__ d_step, int train) {
-  const size_t total = static_cast<size_t>(g.n) * g.C * g.H * g.W;
-  if (!train) {
-    GRID_STRIDE(i, total) y[i] = x[i];
-    return;
-  }
-  const uint64_t base = mix64(g.base_seed ^ *d_step);
-  const uint32_t thresh = static_cast<uint32_t>(static_cast<double>(g.ratio) * 16777216.0);
-  const float keep = static_cast<float>(1.0 / (1.0 - static_cast<double>(g.ratio)));
-  GRID_STRIDE(i, total) y[i] = x[i] * drop_mask(g, base, i, thresh, keep);
-}
-
-__global__ void dropout_bwd_k(DropGeom g, const float* __restrict__ dy, float* __restrict__ dx,
-                              const uint64_t* __restrict__ d_step, int accumulate) {
-  const size_t total = static_cast<size_t>(g.n) * g.C * g.H * g.W;
-  const uint64_t base = mix64(g.base_seed ^ *d_step);
-  const uint32_t thresh = static_cast<uint32_t>(static_cast<double>(g.ratio) * 16777216.0);
-  const float keep = static_cast<float>(1.0 / (1.0 - static_cast<double>(g.ratio)));
-  GRID_STRIDE(i, total) {
-    const float v = dy[i] * drop_mask(g, base, i, thresh, keep);
-    dx[i] = accumulate ? dx[i] + v : v;
   }
 }
 
@@ -261,57 +125,7 @@ __global__ void argmax_count_k(const float* __restrict__ probs, const int32_t* _
   int best = 0;
   for (int j = 1; j < C; ++j)
     if (p[j] > p[best]) best = j;
-  if (best == labels[i]) atomicAdd(correct, 1ULL);
-}
-
-// ---------------------------------------------------------------- gather ---
-// data.hpp:292-304 gather_batch from the HBM-resident shard (NHWC rows).
-__global__ void gather_k(const float* __restrict__ ds, const int32_t* __restrict__ ds_labels,
-                         const uint32_t* __restrict__ idx, const int* __restrict__ cursor, int b,
-                         int pixels, int C, int cs, float* __restrict__ out,
-                         int32_t* __restrict__ labels) {
-  const int i = blockIdx.y;
-  const uint32_t row = idx[static_cast<size_t>(cursor ? *cursor : 0) * b + i];
-  const float* src = ds + static_cast<size_t>(row) * pixels * C;
-  float* dst = out + static_cast<size_t>(i) * pixels * cs;
-  if (blockIdx.x == 0 && threadIdx.x == 0) labels[i] = ds_labels[row];
-  if (cs == C) {
-    const size_t n = static_cast<size_t>(pixels) * C;
-    if ((n % 4) == 0) {
-      const float4* s4 = reinterpret_cast<const float4*>(src);
-      float4* d4 = reinterpret_cast<float4*>(dst);
-      for (size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; j < n / 4;
-           j += static_cast<size_t>(gridDim.x) * blockDim.x)
-        d4[j] = __ldg(s4 + j);
-    } else {
-      for (size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; j < n;
-           j += static_cast<size_t>(gridDim.x) * blockDim.x)
-        dst[j] = __ldg(src + j);
-    }
-  } else {
-    const size_t n = static_cast<size_t>(pixels) * cs;
-    for (size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; j < n;
-         j += static_cast<size_t>(gridDim.x) * blockDim.x) {
-      const int c = static_cast<int>(j % cs);
-      const size_t p = j / cs;
-      dst[j] = c < C ? __ldg(src + p * C + c) : 0.f;
-    }
-  }
-}
-
-// Host-fed batch (reference NCHW layout) -> data layer NHWC with channel stride cs.
-__global__ void stage_nchw_k(const float* __restrict__ src, int n, int C, int H, int W, int cs,
-                             float* __restrict__ dst) {
-  const size_t total = static_cast<size_t>(n) * H * W * cs;
-  GRID_STRIDE(i, total) {
-    const int c = static_cast<int>(i % cs);
-    size_t t = i / cs;
-    const int w = static_cast<int>(t % W);
-    t /= W;
-    const int h = static_cast<int>(t % H);
-    const size_t b = t / H;
-    dst[i] = c < C ? src[((b * C + c) * H + h) * W + w] : 0.f;
-  }
+  if (best == labels[i]) atomicAdd(correct, 1ULL);  // integer count: order-independent
 }
 
 // ---------------------------------------------------------------- update ---
@@ -425,19 +239,6 @@ __global__ void fill_uniform_k(float* x, size_t n, uint64_t seed, double lo, dou
 
 }  // namespace
 
-void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaStream_t s) {
-  const size_t n = static_cast<size_t>(g.n) * g.OH * g.OW * g.C;
-  pool_fwd_k<<<grid_for(n), 256, 0, s>>>(g, x, y, route);
-  PSG_CUDA(cudaGetLastError());
-}
-
-void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
-              bool accumulate, cudaStream_t s) {
-  const size_t n = static_cast<size_t>(g.n) * g.H * g.W * g.C;
-  pool_bwd_k<<<grid_for(n), 256, 0, s>>>(g, dy, route, dx, accumulate);
-  PSG_CUDA(cudaGetLastError());
-}
-
 void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s) {
   relu_fwd_k<<<grid_for(n / 4 + 1), 256, 0, s>>>(x, y, n);
   PSG_CUDA(cudaGetLastError());
@@ -445,33 +246,7 @@ void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s) {
 
 void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumulate,
               cudaStream_t s) {
-  relu_bwd_k<<<grid_for(n), 256, 0, s>>>(x, dy, dx, n, accumulate);
-  PSG_CUDA(cudaGetLastError());
-}
-
-void lrn_fwd(const LrnGeom& g, const float* x, float* y, float* scale, cudaStream_t s) {
-  lrn_fwd_k<<<grid_for(static_cast<size_t>(g.pixels) * g.C), 256, 0, s>>>(g, x, y, scale);
-  PSG_CUDA(cudaGetLastError());
-}
-
-void lrn_bwd(const LrnGeom& g, const float* x, const float* y, const float* scale,
-             const float* dy, float* dx, bool accumulate, cudaStream_t s) {
-  lrn_bwd_k<<<grid_for(static_cast<size_t>(g.pixels) * g.C), 256, 0, s>>>(g, x, y, scale, dy,
-                                                                          dx, accumulate);
-  PSG_CUDA(cudaGetLastError());
-}
-
-void dropout_fwd(const DropGeom& g, const float* x, float* y, const uint64_t* d_step, bool train,
-                 cudaStream_t s) {
-  const size_t n = static_cast<size_t>(g.n) * g.C * g.H * g.W;
-  dropout_fwd_k<<<grid_for(n), 256, 0, s>>>(g, x, y, d_step, train);
-  PSG_CUDA(cudaGetLastError());
-}
-
-void dropout_bwd(const DropGeom& g, const float* dy, float* dx, const uint64_t* d_step,
-                 bool accumulate, cudaStream_t s) {
-  const size_t n = static_cast<size_t>(g.n) * g.C * g.H * g.W;
-  dropout_bwd_k<<<grid_for(n), 256, 0, s>>>(g, dy, dx, d_step, accumulate);
+  relu_bwd_k<<<grid_for(n / 4 + 1), 256, 0, s>>>(x, dy, dx, n, accumulate);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -489,23 +264,6 @@ void softmax_loss(const float* logits, const int32_t* labels, int n, int C, doub
 void argmax_count(const float* probs, const int32_t* labels, int n, int C,
                   unsigned long long* correct, cudaStream_t s) {
   argmax_count_k<<<(n + 255) / 256, 256, 0, s>>>(probs, labels, n, C, correct);
-  PSG_CUDA(cudaGetLastError());
-}
-
-void gather_batch(const float* ds_images, const int32_t* ds_labels, const uint32_t* idx,
-                  const int* cursor, int b, int pixels, int C, int cs, float* out,
-                  int32_t* labels, cudaStream_t s) {
-  const size_t per_row = static_cast<size_t>(pixels) * cs;
-  const int bx = static_cast<int>(std::max<size_t>(1, std::min<size_t>((per_row / 4 + 255) / 256, 64)));
-  gather_k<<<dim3(bx, b), 256, 0, s>>>(ds_images, ds_labels, idx, cursor, b, pixels, C, cs, out,
-                                       labels);
-  PSG_CUDA(cudaGetLastError());
-}
-
-void stage_batch_nchw(const float* src, int n, int C, int H, int W, int cs, float* dst,
-                      cudaStream_t s) {
-  stage_nchw_k<<<grid_for(static_cast<size_t>(n) * H * W * cs), 256, 0, s>>>(src, n, C, H, W, cs,
-                                                                             dst);
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -110,9 +110,9 @@ void free_batch_buffers(psg_net* net) {
   for (LayerRt& l : net->L) {
     dfree(l.out);
     dfree(l.grad);
-    dfree(l.aux);
     dfree(l.route);
-    l.out = l.grad = l.aux = nullptr;
+    dfree(l.col);
+    l.out = l.grad = l.col = nullptr;
     l.route = nullptr;
   }
   dfree(net->row_loss);
@@ -140,6 +140,13 @@ void invalidate_graph(psg_net* net) {
   net->graph_batch = 0;
 }
 
+void release_batch_buffers(psg_net* net) {
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+  invalidate_graph(net);
+  free_batch_buffers(net);
+}
+
 // Activation / gradient buffers for a batch of n rows.
 void ensure_capacity(psg_net* net, size_t n) {
   if (net->cap >= n) return;
@@ -153,8 +160,8 @@ void ensure_capacity(psg_net* net, size_t n) {
     const size_t elems = n * l.vol();
     l.out = dalloc<float>(elems);
     if (l.kind != PSG_LAYER_DATA) l.grad = dalloc<float>(elems);
-    if (l.kind == PSG_LAYER_LRN) l.aux = dalloc<float>(elems);
     if (l.kind == PSG_LAYER_POOL && l.d.pool == PSG_POOL_MAX) l.route = dalloc<uint8_t>(elems);
+    if (l.kind == PSG_LAYER_CONV) l.col = dalloc<float>(conv_col_elems(geom_for(l, n), net->mode));
     if (is_param_layer(l.kind)) {
       for (Mode m : {Mode::Strict, Mode::Tf32})
         ws = std::max(ws, conv_workspace_elems(geom_for(l, n), m));
@@ -247,7 +254,7 @@ size_t TensorRec::to_int(size_t i) const {
     case 1: {  // ref [F][Cg][kh][kw] -> int [F][kh][kw][Cgs]
       const size_t v = i % kw, u = (i / kw) % kh, c = (i / (kw * kh)) % Cg,
                    f = i / (static_cast<size_t>(kw) * kh * Cg);
-      return ((f * kh + u) * kw + v) * Cgs + c;
+      return f * Kp + (u * kw + v) * Cgs + c;
     }
     case 2: {  // ref [O][c*h*w] (CHW flatten, model.hpp:409) -> int [O][h][w][pcs]
       const size_t D = static_cast<size_t>(pc) * ph * pw;
@@ -313,6 +320,7 @@ void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed)
         g.ph = l.d.pad_h;
         g.pw = l.d.pad_w;
         g.G = G;
+        g.kp = static_cast<int>(round_up(static_cast<size_t>(g.Kf()), 4));  // 16-byte rows
         TensorRec k;
         k.layer = li;
         k.slot = 0;
@@ -322,13 +330,14 @@ void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed)
         k.shape[2] = g.kh;
         k.shape[3] = g.kw;
         k.ref_count = static_cast<size_t>(l.C) * (C / G) * g.kh * g.kw;
-        k.int_count = static_cast<size_t>(l.C) * g.Kf();
+        k.int_count = static_cast<size_t>(l.C) * g.Kp();
         k.map = 1;
         k.F = l.C;
         k.Cg = C / G;
         k.Cgs = g.Cgs();
         k.kh = g.kh;
         k.kw = g.kw;
+        k.Kp = g.Kp();
         k.lr_mult = static_cast<float>(l.d.lr_mult_w);
         k.decay_mult = static_cast<float>(l.d.decay_mult_w);
         net->tensors.push_back(k);

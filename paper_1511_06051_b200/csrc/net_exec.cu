@@ -85,7 +85,7 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         const ConvGeom g = geom_n(l, n);
         Scope sc(timer, nm.c_str(), lid, 1, conv_flops(net, l, n), 0.0);
         conv_fprop(g, src.out, net->w + k.int_off, net->w + b.int_off, l.out, false, net->ws,
-                   net->mode, s);
+                   l.col, net->mode, s);
         const int c = conv_launches(g, 0, net->mode);
         sc.done(c);
         launches += c;
@@ -112,8 +112,8 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
       case PSG_LAYER_LRN: {
         LrnGeom g = l.lg;
         g.pixels = static_cast<int>(n) * l.H * l.W;
-        Scope sc(timer, nm.c_str(), lid, 1, 0.0, 3 * act_bytes(l, n));
-        lrn_fwd(g, net->L[l.inputs[0]].out, l.out, l.aux, s);
+        Scope sc(timer, nm.c_str(), lid, 1, 0.0, 2 * act_bytes(l, n));
+        lrn_fwd(g, net->L[l.inputs[0]].out, l.out, s);
         sc.done(1);
         ++launches;
         break;
@@ -165,7 +165,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
         const ConvGeom g = geom_n(l, n);
         {
           Scope sc(timer, (nm + ".wgrad").c_str(), li, 3, conv_flops(net, l, n), 0.0);
-          conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off, net->ws,
+          conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off, net->ws, l.col,
                      net->mode, s);
           const int c = conv_launches(g, 2, net->mode);
           sc.done(c);
@@ -203,8 +203,8 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
         if (need_dx) {
           LrnGeom g = l.lg;
           g.pixels = static_cast<int>(n) * l.H * l.W;
-          Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 5 * act_bytes(l, n));
-          lrn_bwd(g, src.out, l.out, l.aux, l.grad, src.grad, acc, s);
+          Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
+          lrn_bwd(g, src.out, l.grad, src.grad, acc, s);
           sc.done(1);
           ++launches;
         }

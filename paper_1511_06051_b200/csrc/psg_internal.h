@@ -82,9 +82,13 @@ struct ConvGeom {
   int F = 0;             // output channels (= output channel stride)
   int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
   int G = 1;             // groups
-  int Cgs() const { return cs_in / G; }
-  int Fg() const { return F / G; }
-  int Kf() const { return kh * kw * Cgs(); }  // reduction length of fprop / row length of dW
+  int kp = 0;            // row stride of the weight matrix (>= Kf, 16-byte multiple); 0 = Kf
+  __host__ __device__ int Cgs() const { return cs_in / G; }
+  __host__ __device__ int Fg() const { return F / G; }
+  // reduction length of fprop / row length of dW
+  __host__ __device__ int Kf() const { return kh * kw * Cgs(); }
+  // weight row stride: W[f][Kp], dW[f][Kp]
+  __host__ __device__ int Kp() const { return kp ? kp : Kf(); }
 };
 
 enum class Mode { Strict = 0, Tf32 = 1 };
@@ -96,14 +100,17 @@ struct Workspace {
 
 // All three passes may split K across blocks (fixed-order second-stage sums);
 // the shared workspace must hold conv_workspace_elems() floats.
+// `col` (conv_col_elems floats, may be null) holds an im2col matrix written by fprop and
+// read by the same step's wgrad when a TF32 layer takes the im2col route.
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
-                bool relu, const Workspace& ws, Mode mode, cudaStream_t s);
+                bool relu, const Workspace& ws, float* col, Mode mode, cudaStream_t s);
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
                 const Workspace& ws, Mode mode, cudaStream_t s);
-// dW [F][Kf] and db [F] (written, not accumulated).
+// dW [F][Kp] and db [F] (written, not accumulated).
 void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
-                const Workspace& ws, Mode mode, cudaStream_t s);
+                const Workspace& ws, const float* col, Mode mode, cudaStream_t s);
 size_t conv_workspace_elems(const ConvGeom& g, Mode mode);
+size_t conv_col_elems(const ConvGeom& g, Mode mode);
 int conv_launches(const ConvGeom& g, int which, Mode mode);  // 0 fprop 1 dgrad 2 wgrad
 
 struct PoolGeom {
@@ -123,9 +130,10 @@ struct LrnGeom {
   int pixels = 0, C = 0, size = 5;
   float alpha = 1e-4f, beta = 0.75f, k = 1.f;
 };
-void lrn_fwd(const LrnGeom& g, const float* x, float* y, float* scale, cudaStream_t s);
-void lrn_bwd(const LrnGeom& g, const float* x, const float* y, const float* scale,
-             const float* dy, float* dx, bool accumulate, cudaStream_t s);
+// The LRN scale is recomputed in backward from x (not stored).
+void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s);
+void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool accumulate,
+             cudaStream_t s);
 
 struct DropGeom {
   int n = 0, C = 0, H = 1, W = 1;  // logical NCHW dims for the counter index

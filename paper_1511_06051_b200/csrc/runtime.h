@@ -36,7 +36,7 @@ struct TensorRec {
   size_t ref_off = 0, ref_count = 0;
   size_t int_off = 0, int_count = 0;
   int map = 0;  // 0 identity, 1 conv kernel, 2 linear weight
-  int F = 0, Cg = 0, Cgs = 0, kh = 0, kw = 0;    // conv kernel
+  int F = 0, Cg = 0, Cgs = 0, kh = 0, kw = 0, Kp = 0;  // conv kernel (Kp: row stride)
   int O = 0, pc = 0, ph = 0, pw = 0, pcs = 0;    // linear: producer logical dims + channel stride
   float lr_mult = 1.f, decay_mult = 1.f;
   // reference flat index i (within tensor) -> internal flat index
@@ -52,8 +52,8 @@ struct LayerRt {
   size_t vol() const { return static_cast<size_t>(H) * W * cs; }
   float* out = nullptr;
   float* grad = nullptr;
-  float* aux = nullptr;
   uint8_t* route = nullptr;
+  float* col = nullptr;  // im2col matrix (TF32 im2col route only)
   int kern_t = -1, bias_t = -1;
   ConvGeom cg;  // conv / linear (per-example; n filled per call)
   PoolGeom pg;
@@ -144,6 +144,7 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
 int run_backward(psg_net* net, size_t n, OpTimer* timer = nullptr);
 int run_update(psg_net* net, bool advance, OpTimer* timer = nullptr);
 void ensure_capacity(psg_net* net, size_t n);
+void release_batch_buffers(psg_net* net);  // drops activations + graphs; realloc on demand
 void invalidate_graph(psg_net* net);
 
 void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, int* n_ops);
