@@ -43,7 +43,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cifar10_quick", choices=list(WORKLOADS))
     p.add_argument("--tau", type=int, default=10)
-    p.add_argument("--precision", default="fp32", choices=["fp32", "tf32"])
+    # tf32 = tcgen05 tensor cores (north star's fast mode, per-layer parity 1e-2);
+    # fp32 = strict SIMT mode (parity 1e-5)
+    p.add_argument("--precision", default="tf32", choices=["fp32", "tf32"])
     p.add_argument("--average", default="fast", choices=["fast", "ordered"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-json", default=None, help="write the per-op profile here")
@@ -90,7 +92,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None

@@ -31,12 +31,18 @@ namespace {
 
 using namespace tck;
 
-// Fixed-order second stage: out[i] (+)= sum_z ws[z][i] (+ bias[i % ldo], relu).
+// Fixed-order second stage: out[i] (+)= sum_z ws[z][i] (+ bias[i % ldo], relu); columns
+// i % ldo >= valid_cols (row padding the GEMM never writes) are set to 0.
 __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long long stride,
                                 long long total, const float* __restrict__ bias, int ldo,
-                                int relu, int accumulate, float* __restrict__ out) {
+                                int valid_cols, int relu, int accumulate,
+                                float* __restrict__ out) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (valid_cols < ldo && i % ldo >= valid_cols) {
+      out[i] = 0.f;
+      continue;
+    }
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += ws[z * stride + i];
     if (bias) {
@@ -47,25 +53,51 @@ __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long l
   }
 }
 
-// db[c] = sum over rows of dy[r][c] in a fixed order: row chunks per block, then chunks.
-__global__ void bias_grad_partial(const float* __restrict__ dy, long long rows, int cols,
-                                  long long rows_per_chunk, float* __restrict__ part) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const long long r0 = blockIdx.y * rows_per_chunk;
-  if (c >= cols) return;
-  const long long r1 = min(rows, r0 + rows_per_chunk);
-  float s = 0.f;
-  for (long long r = r0; r < r1; ++r) s += dy[r * cols + c];
-  part[static_cast<long long>(blockIdx.y) * cols + c] = s;
+// db[c] = sum over rows of dy[r][c] in a fixed order.  Stage 1: block (cb, chunk) owns a
+// contiguous row chunk and up to 256 column units (float4 when cols % 4 == 0); thread
+// (ty, tx) sums rows r0 + ty, r0 + ty + rpi, ... of unit tx, then row-lanes combine in
+// order.  Stage 2: one warp per column sums the chunk partials (lane-strided, then a
+// fixed xor tree).  The order depends only on the geometry: deterministic.
+constexpr int kBiasChunksMax = 512;
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float add4(float a, float b) { return a + b; }
+__device__ __forceinline__ float4 zero4(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ float zero4(float) { return 0.f; }
+
+template <typename V>
+__global__ void __launch_bounds__(256) bias_grad_partial(const V* __restrict__ dy, int rows,
+                                                         int units, int rows_per_chunk,
+                                                         V* __restrict__ part) {
+  __shared__ V red[256];
+  const int cpr = min(units, 256), rpi = 256 / cpr;
+  const int tx = threadIdx.x % cpr, ty = threadIdx.x / cpr;
+  const int u = blockIdx.x * cpr + tx;
+  const int r0 = blockIdx.y * rows_per_chunk, r1 = min(rows, r0 + rows_per_chunk);
+  V acc = zero4(V{});
+  if (ty < rpi && u < units) {
+#pragma unroll 4
+    for (int r = r0 + ty; r < r1; r += rpi) acc = add4(acc, dy[static_cast<size_t>(r) * units + u]);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (ty == 0 && u < units) {
+    for (int i = 1; i < rpi; ++i) acc = add4(acc, red[i * cpr + tx]);
+    part[static_cast<size_t>(blockIdx.y) * units + u] = acc;
+  }
 }
 
 __global__ void bias_grad_final(const float* __restrict__ part, int chunks, int cols,
                                 float* __restrict__ db) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (c >= cols) return;
   float s = 0.f;
-  for (int z = 0; z < chunks; ++z) s += part[static_cast<long long>(z) * cols + c];
-  db[c] = s;
+  for (int z = lane; z < chunks; z += 32) s += part[static_cast<size_t>(z) * cols + c];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) db[c] = s;
 }
 
 // ---------------------------------------------------------------- host side
@@ -139,6 +171,10 @@ void finish_args(TcArgs& a, int kblk, int sms) {
   const bool b_mn = a.b_mode != B_2D_K;
   const int nb = b_mn ? (a.n_tile + 31) / 32 * 32 : a.n_tile;
   a.a_bytes = kTileM * kblk * 4;
+  const bool a_mn = a.a_mode == A_RECT_MN || a.a_mode == A_2D_MN;
+  a.a_chunks = a_mn && a.m_tiles == 1 ? std::min(kTileM / 32, (a.m_valid + 31) / 32)
+                                      : kTileM / 32;
+  a.a_tx = a_mn ? a.a_chunks * 32 * kblk * 4 : a.a_bytes;
   a.stage_bytes = a.a_bytes + nb * kblk * 4;
   a.stages = std::min(8, (225 * 1024 - kEpiBytes) / a.stage_bytes);
   const long long tiles = static_cast<long long>(a.m_tiles) * a.n_tiles * a.G * a.taps;
@@ -187,7 +223,8 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   if (splits > 1) {
     const int blocks = static_cast<int>(std::min<long long>((out_elems + 255) / 256, 148 * 8));
     tc_split_reduce<<<blocks, 256, 0, s>>>(ws, splits, out_elems, out_elems, a0.bias, a0.ldo,
-                                           a0.relu, a0.accumulate, a0.out);
+                                           a0.valid_cols ? a0.valid_cols : a0.ldo, a0.relu,
+                                           a0.accumulate, a0.out);
     PSG_CUDA(cudaGetLastError());
   }
 }
@@ -316,18 +353,25 @@ bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
     a.ldo = D;
     return true;
   }
-  if (g.sh != 1 || g.sw != 1 || g.Cgs() % 16 || g.Fg() % 4) return false;
-  a.a_mode = A_RECT_MN;  // dY: filters x pixels
-  a.b_mode = B_RECT_MN;  // X shifted by the tap: channels x pixels
+  // Multi-tap tiles: N spans several taps x (C/G rounded up to 32) channels, so one dY
+  // block (A) feeds up to 256 output columns; each 32-column chunk of B is X shifted by its
+  // own tap (channels past C/G are loaded but never stored).
+  if (g.sh != 1 || g.sw != 1 || g.cs_in % 4 || g.Cgs() < 16 || g.F % 4) return false;
+  a.a_mode = A_RECT_MN;  // dY: filters x pixel rectangle
+  a.b_mode = B_TAPS_MN;  // X shifted per chunk: (tap, channel) x pixel rectangle
   a.row_map = ROW_LINEAR;
   rect_shape(g.OW, kblk, a.rk, a.wk);
   a.kth = (g.OH + a.rk - 1) / a.rk;
   a.ktw = (g.OW + a.wk - 1) / a.wk;
-  a.n_tile = pick_n_tile(g.Cgs());
+  a.ntaps = g.kh * g.kw;
+  a.cpt = (g.Cgs() + 31) / 32 * 32;
+  a.cgs = g.Cgs();
+  const int chunks = a.ntaps * a.cpt / 32;
+  a.n_tiles = (chunks + 7) / 8;
+  a.n_tile = 32 * ((chunks + a.n_tiles - 1) / a.n_tiles);
   a.m_tiles = (g.Fg() + kTileM - 1) / kTileM;
-  a.n_tiles = (g.Cgs() + a.n_tile - 1) / a.n_tile;
   a.G = g.G;
-  a.taps = g.kh * g.kw;
+  a.taps = 1;
   a.kblocks = g.n * a.kth * a.ktw;
   a.a_c_g = g.Fg();
   a.b_n_g = g.Cgs();
@@ -335,10 +379,10 @@ bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.ph = g.ph;
   a.pw = g.pw;
   a.m_valid = g.Fg();
-  a.n_valid = g.Cgs();
+  a.n_valid = a.ntaps * a.cpt;
   a.row_g = g.Fg();
-  a.col_tap = g.Cgs();
   a.ldo = g.Kp();
+  a.valid_cols = g.Kf();
   return true;
 }
 
@@ -350,7 +394,51 @@ CUtensorMapSwizzle k_swizzle(int kblk) {
   return kblk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
 }
 
-// dW split partials followed by the bias-gradient partials (64 row chunks max).
+bool plan_wgrad_col(const ConvGeom& g, TcArgs& a) {
+  std::memset(&a, 0, sizeof a);
+  if (g.F % 4 || g.Fg() % 4 || g.Kp() % 4) return false;
+  a.a_mode = A_2D_MN;   // dY [pixels][F]
+  a.b_mode = B_COL_MN;  // col [G][pixels][Kp]
+  a.row_map = ROW_LINEAR;
+  a.n_tile = pick_n_tile(g.Kf());
+  a.m_tiles = (g.Fg() + kTileM - 1) / kTileM;
+  a.n_tiles = (g.Kf() + a.n_tile - 1) / a.n_tile;
+  a.G = g.G;
+  a.taps = 1;
+  a.kblocks = static_cast<int>((static_cast<long long>(g.n) * g.OH * g.OW + 31) / 32);
+  a.a_c_g = g.Fg();
+  a.m_valid = g.Fg();
+  a.n_valid = g.Kf();
+  a.row_g = g.Fg();
+  a.ldo = g.Kp();
+  a.valid_cols = g.Kf();  // dW's padding columns Kf..Kp: zero
+  return true;
+}
+
+// db[f] = sum over rows of dY[row][f], fixed order (row chunks, then chunks).
+void bias_grad(const float* dy, long long rows, int F, float* part, float* db, cudaStream_t s) {
+  if (rows >= (1LL << 31) || rows * F >= (1LL << 40)) throw std::invalid_argument("bias_grad: too large");
+  const bool vec = F % 4 == 0;
+  const int units = vec ? F / 4 : F;
+  const int cpr = std::min(units, 256), rpi = 256 / cpr;
+  const int cblocks = (units + cpr - 1) / cpr;
+  const long long want = std::max<long long>(1, std::min<long long>(
+      (rows + rpi * 8 - 1) / (rpi * 8), 4 * sm_count() / cblocks));
+  const int chunks = static_cast<int>(std::min<long long>(kBiasChunksMax, want));
+  const int per = static_cast<int>((rows + chunks - 1) / chunks);
+  const dim3 grid(cblocks, chunks);
+  if (vec)
+    bias_grad_partial<float4><<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(dy),
+                                                   static_cast<int>(rows), units, per,
+                                                   reinterpret_cast<float4*>(part));
+  else
+    bias_grad_partial<float><<<grid, 256, 0, s>>>(dy, static_cast<int>(rows), units, per, part);
+  PSG_CUDA(cudaGetLastError());
+  bias_grad_final<<<(F + 7) / 8, 256, 0, s>>>(part, chunks, F, db);
+  PSG_CUDA(cudaGetLastError());
+}
+
+// dW split partials followed by the bias-gradient partials (kBiasChunksMax row chunks max).
 size_t tc_wgrad_ws_elems(const ConvGeom& g) {
   TcArgs a;
   int kblk;
@@ -358,7 +446,7 @@ size_t tc_wgrad_ws_elems(const ConvGeom& g) {
   finish_args(a, kblk, sm_count());
   const int splits = splits_of(a);
   return (splits > 1 ? static_cast<size_t>(splits) * g.F * g.Kp() : 0) +
-         64 * static_cast<size_t>(g.F);
+         kBiasChunksMax * static_cast<size_t>(g.F);
 }
 
 }  // namespace
@@ -472,15 +560,53 @@ void tc_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, flo
   const int splits = splits_of(a);
   float* part = ws.ptr + (splits > 1 ? splits * dw_elems : 0);
   launch(a, ma, mb, kblk, dw_elems, ws.ptr, ws.elems, s);
-  // db[f] = sum over output pixels of dY[pix][f]
-  const long long rows = static_cast<long long>(g.n) * g.OH * g.OW;
-  const int chunks = static_cast<int>(std::min<long long>(64, (rows + 255) / 256));
-  const long long per = (rows + chunks - 1) / chunks;
-  const dim3 grid((g.F + 127) / 128, chunks);
-  bias_grad_partial<<<grid, 128, 0, s>>>(dy, rows, g.F, per, part);
-  PSG_CUDA(cudaGetLastError());
-  bias_grad_final<<<(g.F + 127) / 128, 128, 0, s>>>(part, chunks, g.F, db);
-  PSG_CUDA(cudaGetLastError());
+  bias_grad(dy, static_cast<long long>(g.n) * g.OH * g.OW, g.F, part, db, s);
+}
+
+// ---- wgrad of narrow layers against an im2col matrix col[G][n*OH*OW][Kp] ----
+// D_g[f][(u,v,c)] = sum_pix dY[pix][g*Fg + f] * col[g][pix][(u,v,c)]: M = Fg, N = Kf
+// (wide), K = pixels.  Used when the per-tap rectangles would give tiny tiles
+// (F/G < 128, C/G not a multiple of 32) or the layer takes the im2col route anyway.
+bool tc_wgrad_col_supported(const ConvGeom& g) {
+  TcArgs a;
+  return plan_wgrad_col(g, a);
+}
+
+size_t tc_wgrad_col_ws_elems(const ConvGeom& g) {
+  TcArgs a;
+  if (!plan_wgrad_col(g, a)) return 0;
+  finish_args(a, 32, sm_count());
+  const int splits = splits_of(a);
+  return (splits > 1 ? static_cast<size_t>(splits) * g.F * g.Kp() : 0) +
+         kBiasChunksMax * static_cast<size_t>(g.F);
+}
+
+int tc_wgrad_col_launches(const ConvGeom& g) {
+  TcArgs a;
+  if (!plan_wgrad_col(g, a)) return -1;
+  finish_args(a, 32, sm_count());
+  return (splits_of(a) > 1 ? 2 : 1) + 2;
+}
+
+void tc_wgrad_col(const ConvGeom& g, const float* col, const float* dy, float* dw, float* db,
+                  const Workspace& ws, cudaStream_t s) {
+  TcArgs a;
+  if (!plan_wgrad_col(g, a)) throw std::logic_error("tc_wgrad_col: unsupported geometry");
+  finish_args(a, 32, sm_count());
+  a.out = dw;
+  const long long pixels = static_cast<long long>(g.n) * g.OH * g.OW;
+  const CUtensorMap ma = map_2d(dy, pixels, g.F, 32, 32, kMnSwizzle);
+  const uint64_t dims[3] = {static_cast<uint64_t>(g.Kp()), static_cast<uint64_t>(pixels),
+                            static_cast<uint64_t>(g.G)};
+  const uint64_t str[2] = {static_cast<uint64_t>(g.Kp()) * 4,
+                           static_cast<uint64_t>(pixels) * g.Kp() * 4};
+  const uint32_t box[3] = {32, 32, 1};
+  const CUtensorMap mb = make_map(col, 3, dims, str, box, kMnSwizzle);
+  const long long dw_elems = static_cast<long long>(g.F) * g.Kp();
+  const int splits = splits_of(a);
+  float* part = ws.ptr + (splits > 1 ? splits * dw_elems : 0);
+  launch(a, ma, mb, 32, dw_elems, ws.ptr, ws.elems, s);
+  bias_grad(dy, pixels, g.F, part, db, s);
 }
 
 }  // namespace psg

@@ -34,47 +34,87 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:11-16
 // model.hpp:369-406 (max, strict '>' so the first maximum in (u, v) scan order
 // wins) with Caffe padding / ceil windows; AVE divides by the window clipped to
 // the padded extent.  route = (u * kw + v) relative to the unclipped window.
-__global__ void pool_fwd_k(PoolGeom g, const float* __restrict__ x, float* __restrict__ y,
-                           uint8_t* __restrict__ route, uint32_t total) {
+// V = float4 (4 channels per thread, C % 4 == 0) or float; index math per V.
+__device__ __forceinline__ float comp(const float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ float& comp(float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ float comp(const float& v, int) { return v; }
+__device__ __forceinline__ float& comp(float& v, int) { return v; }
+template <typename V> struct RouteOf;
+template <> struct RouteOf<float4> { using T = uchar4; static constexpr int n = 4; };
+template <> struct RouteOf<float> { using T = uint8_t; static constexpr int n = 1; };
+__device__ __forceinline__ uint8_t rcomp(const uchar4& r, int j) {
+  return j == 0 ? r.x : j == 1 ? r.y : j == 2 ? r.z : r.w;
+}
+__device__ __forceinline__ uint8_t& rcomp(uchar4& r, int j) {
+  return j == 0 ? r.x : j == 1 ? r.y : j == 2 ? r.z : r.w;
+}
+__device__ __forceinline__ uint8_t rcomp(const uint8_t& r, int) { return r; }
+__device__ __forceinline__ uint8_t& rcomp(uint8_t& r, int) { return r; }
+
+template <typename V>
+__global__ void pool_fwd_k(PoolGeom g, const V* __restrict__ x, V* __restrict__ y,
+                           typename RouteOf<V>::T* __restrict__ route, int cv, uint32_t total) {
+  constexpr int L = RouteOf<V>::n;
   GRID_STRIDE32(i, total) {
-    const uint32_t c = i % g.C, pix = i / g.C;
+    const uint32_t c = i % cv, pix = i / cv;
     const int ow = static_cast<int>(pix % g.OW), t = static_cast<int>(pix / g.OW);
     const int oh = t % g.OH, b = t / g.OH;
     const int hs0 = oh * g.sh - g.ph, ws0 = ow * g.sw - g.pw;
     const int he0 = hs0 + g.kh, we0 = ws0 + g.kw;
     const int hs = max(hs0, 0), ws = max(ws0, 0), he = min(he0, g.H), we = min(we0, g.W);
-    const float* xb = x + (static_cast<size_t>(b) * g.H * g.W) * g.C + c;
+    const V* xb = x + (static_cast<size_t>(b) * g.H * g.W) * cv + c;
     if (g.method == PSG_POOL_AVE) {
-      const int size = (min(he0, g.H + g.ph) - hs0) * (min(we0, g.W + g.pw) - ws0);
-      float acc = 0.f;
+      const float size = static_cast<float>((min(he0, g.H + g.ph) - hs0) *
+                                            (min(we0, g.W + g.pw) - ws0));
+      V acc;
+#pragma unroll
+      for (int j = 0; j < L; ++j) comp(acc, j) = 0.f;
       for (int r = hs; r < he; ++r)
-        for (int s = ws; s < we; ++s) acc += xb[(r * g.W + s) * g.C];
-      y[i] = acc / static_cast<float>(size);
+        for (int s = ws; s < we; ++s) {
+          const V v = __ldg(xb + (r * g.W + s) * cv);
+#pragma unroll
+          for (int j = 0; j < L; ++j) comp(acc, j) += comp(v, j);
+        }
+#pragma unroll
+      for (int j = 0; j < L; ++j) comp(acc, j) = comp(acc, j) / size;
+      y[i] = acc;
     } else {
-      float best = xb[(hs * g.W + ws) * g.C];
-      int arg = (hs - hs0) * g.kw + (ws - ws0);
+      V best = __ldg(xb + (hs * g.W + ws) * cv);
+      typename RouteOf<V>::T arg;
+      const uint8_t a0 = static_cast<uint8_t>((hs - hs0) * g.kw + (ws - ws0));
+#pragma unroll
+      for (int j = 0; j < L; ++j) rcomp(arg, j) = a0;
       for (int r = hs; r < he; ++r) {
         for (int s = ws; s < we; ++s) {
-          const float v = xb[(r * g.W + s) * g.C];
-          if (v > best) {
-            best = v;
-            arg = (r - hs0) * g.kw + (s - ws0);
-          }
+          const V v = __ldg(xb + (r * g.W + s) * cv);
+          const uint8_t a = static_cast<uint8_t>((r - hs0) * g.kw + (s - ws0));
+#pragma unroll
+          for (int j = 0; j < L; ++j)
+            if (comp(v, j) > comp(best, j)) {
+              comp(best, j) = comp(v, j);
+              rcomp(arg, j) = a;
+            }
         }
       }
       y[i] = best;
-      route[i] = static_cast<uint8_t>(arg);
+      route[i] = arg;
     }
   }
 }
 
 // model.hpp:492-498 as a deterministic gather: each input sums, in ascending
 // output order, the dy of the covering windows that routed to it.
-__global__ void pool_bwd_k(PoolGeom g, const float* __restrict__ dy,
-                           const uint8_t* __restrict__ route, float* __restrict__ dx,
-                           int accumulate, uint32_t total) {
+template <typename V>
+__global__ void pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
+                           const typename RouteOf<V>::T* __restrict__ route, V* __restrict__ dx,
+                           int accumulate, int cv, uint32_t total) {
+  constexpr int L = RouteOf<V>::n;
   GRID_STRIDE32(i, total) {
-    const uint32_t c = i % g.C, pix = i / g.C;
+    const uint32_t c = i % cv, pix = i / cv;
     const int w = static_cast<int>(pix % g.W), t = static_cast<int>(pix / g.W);
     const int h = t % g.H, b = t / g.H;
     // windows with oh*sh - ph <= h < oh*sh - ph + kh
@@ -83,94 +123,127 @@ __global__ void pool_bwd_k(PoolGeom g, const float* __restrict__ dy,
     const int owl = max(0, (w + g.pw - g.kw + g.sw) / g.sw);
     const int owh = min(g.OW - 1, (w + g.pw) / g.sw);
     const uint32_t obase = static_cast<uint32_t>(b) * g.OH * g.OW;
-    float acc = 0.f;
+    V acc;
+#pragma unroll
+    for (int j = 0; j < L; ++j) comp(acc, j) = 0.f;
     for (int oh = ohl; oh <= ohh; ++oh) {
       const int hs0 = oh * g.sh - g.ph;
       if (h < hs0 || h >= hs0 + g.kh) continue;
       for (int ow = owl; ow <= owh; ++ow) {
         const int ws0 = ow * g.sw - g.pw;
         if (w < ws0 || w >= ws0 + g.kw) continue;
-        const uint32_t o = (obase + oh * g.OW + ow) * g.C + c;
+        const uint32_t o = (obase + oh * g.OW + ow) * cv + c;
+        const V d = __ldg(dy + o);
         if (g.method == PSG_POOL_AVE) {
-          const int size =
-              (min(hs0 + g.kh, g.H + g.ph) - hs0) * (min(ws0 + g.kw, g.W + g.pw) - ws0);
-          acc += dy[o] / static_cast<float>(size);
-        } else if (route[o] == (h - hs0) * g.kw + (w - ws0)) {
-          acc += dy[o];
+          const float size = static_cast<float>((min(hs0 + g.kh, g.H + g.ph) - hs0) *
+                                                (min(ws0 + g.kw, g.W + g.pw) - ws0));
+#pragma unroll
+          for (int j = 0; j < L; ++j) comp(acc, j) += comp(d, j) / size;
+        } else {
+          const typename RouteOf<V>::T r = __ldg(route + o);
+          const uint8_t want = static_cast<uint8_t>((h - hs0) * g.kw + (w - ws0));
+#pragma unroll
+          for (int j = 0; j < L; ++j)
+            if (rcomp(r, j) == want) comp(acc, j) += comp(d, j);
         }
       }
     }
-    dx[i] = accumulate ? dx[i] + acc : acc;
+    if (accumulate) {
+      const V o = dx[i];
+#pragma unroll
+      for (int j = 0; j < L; ++j) comp(acc, j) += comp(o, j);
+    }
+    dx[i] = acc;
   }
 }
 
 // ------------------------------------------------------------------- lrn ---
-// Caffe LRN ACROSS_CHANNELS.  One warp per pixel: the pixel's C channels are staged
-// in shared memory, window sums read them from there (each value read once from HBM).
-// The scale is recomputed in backward instead of being stored.
-constexpr int kLrnWarps = 8;
+// Caffe LRN ACROSS_CHANNELS over NHWC.  A block stages a tile of whole pixels (a
+// contiguous run of tp*C floats) in shared memory with independent coalesced loads, then
+// every window sum reads shared memory; thread e's channel advances incrementally
+// (c += 256 % C) so there is no per-element division.  Window sums run in ascending
+// channel order; the scale is recomputed in backward instead of being stored.
+constexpr int kLrnThreads = 256;
+constexpr int kLrnTileElems = 2048;
 
-__global__ void lrn_fwd_k(LrnGeom g, const float* __restrict__ x, float* __restrict__ y) {
+__device__ __forceinline__ float lrn_pow(float s, float beta) {  // s^-beta, s >= k > 0
+  return exp2f(-beta * log2f(s));
+}
+
+__global__ void __launch_bounds__(kLrnThreads) lrn_fwd_k(LrnGeom g, const float* __restrict__ x,
+                                                         float* __restrict__ y, int tp) {
   extern __shared__ float sm[];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  float* sx = sm + warp * g.C;
-  const int pre = (g.size - 1) / 2, post = g.size - pre - 1;
+  float* sx = sm;
+  const int pre = (g.size - 1) / 2, post = g.size - pre - 1, C = g.C;
   const float a = g.alpha / g.size;
-  for (uint32_t p = blockIdx.x * kLrnWarps + warp; p < static_cast<uint32_t>(g.pixels);
-       p += gridDim.x * kLrnWarps) {
-    const float* xp = x + static_cast<size_t>(p) * g.C;
-    for (int c = lane; c < g.C; c += 32) {
-      const float v = xp[c];
-      sx[c] = v * v;
-    }
-    __syncwarp();
-    for (int c = lane; c < g.C; c += 32) {
-      const int lo = max(0, c - pre), hi = min(g.C - 1, c + post);
+  const int ntiles = (g.pixels + tp - 1) / tp, step = kLrnThreads % C;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const size_t e0 = static_cast<size_t>(tile) * tp * C;
+    const int ne = min(tp, g.pixels - tile * tp) * C;
+    for (int e = threadIdx.x; e < ne; e += kLrnThreads) sx[e] = __ldg(x + e0 + e);
+    __syncthreads();
+    int c = threadIdx.x % C;
+    for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
+      const int lo = max(0, c - pre), hi = min(C - 1, c + post);
+      const float* row = sx + (e - c);
       float acc = 0.f;
-      for (int q = lo; q <= hi; ++q) acc += sx[q];
-      const float s = g.k + a * acc;
-      y[static_cast<size_t>(p) * g.C + c] = xp[c] * powf(s, -g.beta);
+      for (int q = lo; q <= hi; ++q) acc += row[q] * row[q];
+      y[e0 + e] = sx[e] * lrn_pow(g.k + a * acc, g.beta);
+      c += step;
+      if (c >= C) c -= C;
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
-__global__ void lrn_bwd_k(LrnGeom g, const float* __restrict__ x, const float* __restrict__ dy,
-                          float* __restrict__ dx, int accumulate) {
+__global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float* __restrict__ x,
+                                                         const float* __restrict__ dy,
+                                                         float* __restrict__ dx, int accumulate,
+                                                         int tp) {
   extern __shared__ float sm[];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  float* sx = sm + warp * 3 * g.C;  // x^2
-  float* st = sx + g.C;             // dy * y / scale
-  float* ssp = st + g.C;            // scale^-beta
+  const int C = g.C, tile_elems = tp * C;
+  float* sx = sm;                   // x
+  float* sd = sx + tile_elems;      // dy
+  float* st = sd + tile_elems;      // dy * y / scale
+  float* ssp = st + tile_elems;     // scale^-beta
   const int pre = (g.size - 1) / 2, post = g.size - pre - 1;
   const float a = g.alpha / g.size, ratio = 2.f * g.alpha * g.beta / g.size;
-  for (uint32_t p = blockIdx.x * kLrnWarps + warp; p < static_cast<uint32_t>(g.pixels);
-       p += gridDim.x * kLrnWarps) {
-    const size_t base = static_cast<size_t>(p) * g.C;
-    for (int c = lane; c < g.C; c += 32) {
-      const float v = x[base + c];
-      sx[c] = v * v;
+  const int ntiles = (g.pixels + tp - 1) / tp, step = kLrnThreads % C;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const size_t e0 = static_cast<size_t>(tile) * tp * C;
+    const int ne = min(tp, g.pixels - tile * tp) * C;
+    for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
+      sx[e] = __ldg(x + e0 + e);
+      sd[e] = __ldg(dy + e0 + e);
     }
-    __syncwarp();
-    for (int c = lane; c < g.C; c += 32) {
-      const int lo = max(0, c - pre), hi = min(g.C - 1, c + post);
+    __syncthreads();
+    int c = threadIdx.x % C;
+    for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
+      const int lo = max(0, c - pre), hi = min(C - 1, c + post);
+      const float* row = sx + (e - c);
       float acc = 0.f;
-      for (int q = lo; q <= hi; ++q) acc += sx[q];
+      for (int q = lo; q <= hi; ++q) acc += row[q] * row[q];
       const float s = g.k + a * acc;
-      const float sp = powf(s, -g.beta);
-      ssp[c] = sp;
-      st[c] = dy[base + c] * x[base + c] * sp / s;
+      const float sp = lrn_pow(s, g.beta);
+      ssp[e] = sp;
+      st[e] = sd[e] * sx[e] * sp / s;
+      c += step;
+      if (c >= C) c -= C;
     }
-    __syncwarp();
-    for (int c = lane; c < g.C; c += 32) {
+    __syncthreads();
+    c = threadIdx.x % C;
+    for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
       // channels q whose window contains c: q in [c - post, c + pre]
-      const int lo = max(0, c - post), hi = min(g.C - 1, c + pre);
+      const int lo = max(0, c - post), hi = min(C - 1, c + pre);
+      const float* row = st + (e - c);
       float acc = 0.f;
-      for (int q = lo; q <= hi; ++q) acc += st[q];
-      const float v = dy[base + c] * ssp[c] - ratio * x[base + c] * acc;
-      dx[base + c] = accumulate ? dx[base + c] + v : v;
+      for (int q = lo; q <= hi; ++q) acc += row[q];
+      const float v = sd[e] * ssp[e] - ratio * sx[e] * acc;
+      dx[e0 + e] = accumulate ? dx[e0 + e] + v : v;
+      c += step;
+      if (c >= C) c -= C;
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -259,32 +332,54 @@ __global__ void stage_nchw_k(const float* __restrict__ src, int C, int H, int W,
 void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaStream_t s) {
   const uint32_t n = checked32(static_cast<size_t>(g.n) * g.OH * g.OW * g.C, "pool");
   checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
-  pool_fwd_k<<<grid_for(n), 256, 0, s>>>(g, x, y, route, n);
+  if (g.C % 4 == 0)
+    pool_fwd_k<float4><<<grid_for(n / 4), 256, 0, s>>>(
+        g, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+        reinterpret_cast<uchar4*>(route), g.C / 4, n / 4);
+  else
+    pool_fwd_k<float><<<grid_for(n), 256, 0, s>>>(g, x, y, route, g.C, n);
   PSG_CUDA(cudaGetLastError());
 }
 
 void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
               bool accumulate, cudaStream_t s) {
   const uint32_t n = checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
-  pool_bwd_k<<<grid_for(n), 256, 0, s>>>(g, dy, route, dx, accumulate, n);
+  if (g.C % 4 == 0)
+    pool_bwd_k<float4><<<grid_for(n / 4), 256, 0, s>>>(
+        g, reinterpret_cast<const float4*>(dy), reinterpret_cast<const uchar4*>(route),
+        reinterpret_cast<float4*>(dx), accumulate, g.C / 4, n / 4);
+  else
+    pool_bwd_k<float><<<grid_for(n), 256, 0, s>>>(g, dy, route, dx, accumulate, g.C, n);
   PSG_CUDA(cudaGetLastError());
 }
 
+namespace {
+int lrn_tile_pixels(const LrnGeom& g) { return std::max(1, kLrnTileElems / g.C); }
+int lrn_blocks(const LrnGeom& g, int tp) {
+  return static_cast<int>(std::min<long>((g.pixels + tp - 1) / tp, 148L * 16));
+}
+}  // namespace
+
 void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s) {
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
-  const int blocks = static_cast<int>(std::min<long>((g.pixels + kLrnWarps - 1) / kLrnWarps,
-                                                     148L * 8));
-  lrn_fwd_k<<<blocks, 32 * kLrnWarps, kLrnWarps * g.C * sizeof(float), s>>>(g, x, y);
+  const int tp = lrn_tile_pixels(g);
+  const size_t smem = static_cast<size_t>(tp) * g.C * sizeof(float);
+  if (smem > 48 * 1024)
+    PSG_CUDA(cudaFuncSetAttribute(lrn_fwd_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  lrn_fwd_k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, y, tp);
   PSG_CUDA(cudaGetLastError());
 }
 
 void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool accumulate,
              cudaStream_t s) {
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
-  const int blocks = static_cast<int>(std::min<long>((g.pixels + kLrnWarps - 1) / kLrnWarps,
-                                                     148L * 8));
-  lrn_bwd_k<<<blocks, 32 * kLrnWarps, 3 * kLrnWarps * g.C * sizeof(float), s>>>(g, x, dy, dx,
-                                                                               accumulate);
+  const int tp = lrn_tile_pixels(g);
+  const size_t smem = 4 * static_cast<size_t>(tp) * g.C * sizeof(float);
+  if (smem > 48 * 1024)
+    PSG_CUDA(cudaFuncSetAttribute(lrn_bwd_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  lrn_bwd_k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, dy, dx, accumulate, tp);
   PSG_CUDA(cudaGetLastError());
 }
 

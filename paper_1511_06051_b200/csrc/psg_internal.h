@@ -100,15 +100,15 @@ struct Workspace {
 
 // All three passes may split K across blocks (fixed-order second-stage sums);
 // the shared workspace must hold conv_workspace_elems() floats.
-// `col` (conv_col_elems floats, may be null) holds an im2col matrix written by fprop and
-// read by the same step's wgrad when a TF32 layer takes the im2col route.
+// `col` (conv_col_elems floats, may be null) holds an im2col matrix written by fprop (or by
+// wgrad itself) and read by the same step's wgrad when a TF32 layer takes an im2col route.
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
                 bool relu, const Workspace& ws, float* col, Mode mode, cudaStream_t s);
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
                 const Workspace& ws, Mode mode, cudaStream_t s);
 // dW [F][Kp] and db [F] (written, not accumulated).
 void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
-                const Workspace& ws, const float* col, Mode mode, cudaStream_t s);
+                const Workspace& ws, float* col, Mode mode, cudaStream_t s);
 size_t conv_workspace_elems(const ConvGeom& g, Mode mode);
 size_t conv_col_elems(const ConvGeom& g, Mode mode);
 int conv_launches(const ConvGeom& g, int which, Mode mode);  // 0 fprop 1 dgrad 2 wgrad

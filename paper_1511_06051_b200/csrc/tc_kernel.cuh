@@ -17,7 +17,7 @@ namespace psg {
 namespace tck {
 
 enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3 };
-enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3 };
+enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3, B_COL_MN = 4, B_TAPS_MN = 5 };
 enum RowMap { ROW_RECT = 0, ROW_LINEAR = 1 };
 
 constexpr int kThreads = 256;
@@ -30,6 +30,8 @@ struct TcArgs {
   int a_mode, b_mode, row_map;
   int n_tile;             // UMMA N (multiple of 16, <= 256)
   int stage_bytes, a_bytes, stages;
+  int a_chunks;           // MN-major A: 32-row chunks actually loaded (M tail skipped)
+  int a_tx;               // A bytes landing per stage (expect_tx)
   int m_tiles, n_tiles;   // per (group, tap)
   int G, taps;            // group / tap index g * taps + tap
   int kblocks, kb_per_split, splits;
@@ -55,6 +57,15 @@ struct TcArgs {
   int m_valid;            // rows valid in M (per group), ROW_LINEAR
   int n_valid;            // columns valid in N (per group)
   int col_g, col_tap, row_g;
+  // B_TAPS_MN (multi-tap wgrad): virtual N = ntaps x cpt columns (cpt = C/G rounded up to
+  // 32); column vc -> tap vc / cpt, channel vc % cpt (valid below cgs); dW column tap*cgs + c
+  int ntaps, cpt, cgs;
+  int valid_cols;         // split-K reduce: dW row padding columns (>= Kf) zeroed
+};
+
+// Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
+struct TapChunks {
+  int dx[8], dy[8], c[8];
 };
 
 struct Tile {
@@ -72,6 +83,17 @@ __device__ __forceinline__ Tile decode_tile(const TcArgs& p, long long t) {
   r.g = gt / p.taps;
   r.tap = gt % p.taps;
   return r;
+}
+
+__device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, TapChunks& k) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int vc = t.n * p.n_tile + 32 * j;
+    const int tap = min(vc / p.cpt, p.ntaps - 1);  // chunks past the last tap: harmless reloads
+    k.dy[j] = tap / p.kw - p.ph;
+    k.dx[j] = tap % p.kw - p.pw;
+    k.c[j] = p.b_n_g * t.g + vc % p.cpt;
+  }
 }
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -139,13 +161,16 @@ __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, 
     case A_RECT_MN:
 #pragma unroll
       for (int j = 0; j < kTileM / 32; ++j)
-        tc::tma_load_4d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
+        if (j < p.a_chunks)
+          tc::tma_load_4d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
                         c.kow, c.koh, c.kbi);
       break;
     case A_2D_MN:
 #pragma unroll
       for (int j = 0; j < kTileM / 32; ++j)
-        tc::tma_load_2d(sa + j * KBLK * 128, map, bar, t.m * kTileM + 32 * j, c.kb * KBLK);
+        if (j < p.a_chunks)
+          tc::tma_load_2d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
+                        c.kb * KBLK);
       break;
   }
 }
@@ -153,8 +178,8 @@ __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, 
 // B operand of one K block (producer thread B).
 template <int KBLK>
 __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, const Tile& t,
-                                       const KCursor& c, int u, int v, uint32_t sb,
-                                       uint32_t bar) {
+                                       const KCursor& c, int u, int v, const TapChunks& tk,
+                                       uint32_t sb, uint32_t bar) {
   const int nch = (p.n_tile + 31) / 32;
   switch (p.b_mode) {
     case B_2D_K:
@@ -173,6 +198,17 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
     case B_2D_MN:
       for (int j = 0; j < nch; ++j)
         tc::tma_load_2d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.kb * KBLK);
+      break;
+    case B_COL_MN:  // im2col matrix [G][rows][Kp]: group as the outer coordinate
+      for (int j = 0; j < nch; ++j)
+        tc::tma_load_3d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.kb * KBLK, t.g);
+      break;
+    case B_TAPS_MN:  // X shifted per 32-column chunk by that chunk's tap
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < nch)
+          tc::tma_load_4d(sb + j * KBLK * 128, map, bar, tk.c[j], c.kow + tk.dx[j],
+                          c.koh + tk.dy[j], c.kbi);
       break;
   }
 }
@@ -212,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((warp == 0 || warp == 3) && lane == 0) {
     // ----------------------------------------- producers: warp 0 -> A, warp 3 -> B
     const bool is_a = warp == 0;
-    const uint32_t bytes = is_a ? p.a_bytes : p.stage_bytes - p.a_bytes;
+    const uint32_t bytes = is_a ? p.a_tx : p.stage_bytes - p.a_bytes;
     uint32_t it = 0;
     for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x) {
       const Tile t = decode_tile(p, tt);
@@ -226,6 +262,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ow0 = (r % p.tw) * p.wm;
       }
       const int u = t.tap / p.kw, v = t.tap % p.kw;
+      TapChunks tk{};
+      if (!is_a && p.b_mode == B_TAPS_MN) tap_chunks(p, t, tk);
       KCursor c;
       c.init(p, kb0);
       for (int kb = kb0; kb < kb1; ++kb, ++it, c.next(p)) {
@@ -237,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (is_a)
           load_a<KBLK>(p, &map_a, t, c, rb, oh0, ow0, sa, bar);
         else
-          load_b<KBLK>(p, &map_b, t, c, u, v, sa + p.a_bytes, bar);
+          load_b<KBLK>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -303,23 +341,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(tc::smem_u32(&tfull_bar[acc]), (local >> 1) & 1);
       tc::fence_after_sync();
       const uint32_t taddr = tmem + acc * kAccCols + (static_cast<uint32_t>(ew * 32) << 16);
-      for (int c0 = 0; c0 < p.n_tile; c0 += 32) {
+      const int c_end = __any_sync(0xffffffffu, row_ok) ? p.n_tile : 0;  // idle rows: skip
+      for (int c0 = 0; c0 < c_end; c0 += 32) {
         float v[32];
         tc::tmem_ld16(taddr + c0, v);
         if (c0 + 16 < p.n_tile) tc::tmem_ld16(taddr + c0 + 16, v + 16);
 #pragma unroll
         for (int q = 0; q < 32; ++q) stg[lane * kStagePad + q] = v[q];
         __syncwarp();
-        const int col = c0 + lane;
-        const bool col_ok = col < nvalid;
+        int cidx;  // output column of this lane
+        bool col_ok;
+        if (p.cpt) {
+          const int vc = t.n * p.n_tile + c0, tap = vc / p.cpt, cc = vc % p.cpt + lane;
+          col_ok = c0 + lane < p.n_tile && tap < p.ntaps && cc < p.cgs;
+          cidx = tap * p.cgs + cc;
+        } else {
+          col_ok = c0 + lane < nvalid;
+          cidx = col0 + c0 + lane;
+        }
         float bv = 0.f;
-        if (col_ok && p.bias && !p.ws) bv = p.bias[col0 + col];
+        if (col_ok && p.bias && !p.ws) bv = p.bias[cidx];
         for (int i = 0; i < 32; ++i) {
           const bool ok = __shfl_sync(0xffffffffu, row_ok, i);
           const long long ro = __shfl_sync(0xffffffffu, row_off, i);
           if (!ok || !col_ok) continue;
           float y = stg[i * kStagePad + lane];
-          float* dst = base + ro + col0 + col;
+          float* dst = base + ro + cidx;
           if (!p.ws) {
             if (p.bias) {
               y += bv;

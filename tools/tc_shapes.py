@@ -12,8 +12,10 @@ from oracle.pyoracle import max_relative_deviation  # noqa: E402
 from paper_1511_06051_b200 import model  # noqa: E402
 from paper_1511_06051_b200 import netspec as ns  # noqa: E402
 
-# name: (batch, C, H, W, F, k, pad, group) ; C < 0 marks a linear layer (D = -C, O = F)
+# name: (batch, C, H, W, F, k, pad, group[, stride]) ; C < 0 marks a linear layer (D = -C, O = F)
 SHAPES = {
+    "ax_conv1": (2, 3, 227, 227, 96, 11, 0, 1, 4),
+    "cq_conv1": (8, 3, 32, 32, 32, 5, 2, 1),
     "ax_conv2": (4, 96, 27, 27, 256, 5, 2, 2),
     "ax_conv3": (4, 256, 13, 13, 384, 3, 1, 1),
     "ax_conv4": (4, 384, 13, 13, 384, 3, 1, 2),
@@ -26,14 +28,15 @@ SHAPES = {
 
 
 def spec_for(name):
-    b, c, h, w, f, k, p, g = SHAPES[name]
+    b, c, h, w, f, k, p, g = SHAPES[name][:8]
+    stride = SHAPES[name][8] if len(SHAPES[name]) > 8 else 1
     if c < 0:
         body = [ns.data_layer("data", b, 1, 1, -c), ns.label_layer("label", b),
                 ns.linear_layer("l", "data", f)]
     else:
         body = [ns.data_layer("data", b, c, h, w), ns.label_layer("label", b),
                 ns.conv_layer("pre", "data", 1, 1, c), ns.conv_layer("l", "pre", k, k, f, pad=p,
-                                                                    group=g)]
+                                                                    group=g, stride=stride)]
     body += [ns.linear_layer("cls", "l", 16), ns.softmax_loss_layer("loss", "cls", "label")]
     return ns.NetSpec(body)
 
