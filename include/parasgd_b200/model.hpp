@@ -301,6 +301,29 @@ class Net {
 
   /// Extension: accuracy over `num_steps` batches of a fresh SequentialBatchIterator on an
   /// HBM-resident copy of `ds` (schemes.hpp:134-139 evaluate, gather on device).
+  /// Extension (run_naive, schemes.hpp:233-247): this net consumes rows
+  /// [part*b/parts, (part+1)*b/parts) of every batch of the shard stream.
+  void set_training_part(const Shard& shard, std::size_t batch_size, std::uint64_t stream_seed,
+                         int part, int parts) {
+    psg_dataset* ds = upload(*shard.dataset);
+    std::vector<std::uint64_t> idx(shard.indices.begin(), shard.indices.end());
+    b200::check(psg_net_attach_shard_part(net_.get(), ds, idx.data(), idx.size(), batch_size,
+                                          stream_seed, part, parts));
+  }
+
+  /// Extension: queue sharded evaluation batches first, first+stride, ... < num_steps of a
+  /// fresh SequentialBatchIterator; test_shard_end returns (correct, total).
+  void test_shard_begin(const Dataset& ds, std::size_t batch, long num_steps, long first,
+                        long stride) {
+    b200::check(psg_net_attach_validation(net_.get(), upload(ds), batch));
+    b200::check(psg_net_test_begin(net_.get(), num_steps, first, stride));
+  }
+  std::pair<unsigned long long, unsigned long long> test_shard_end() {
+    unsigned long long c = 0, t = 0;
+    b200::check(psg_net_test_end(net_.get(), &c, &t));
+    return {c, t};
+  }
+
   double test_resident(const Dataset& ds, std::size_t batch, long num_steps) {
     b200::check(psg_net_attach_validation(net_.get(), upload(ds), batch));
     double acc = 0.0;

@@ -176,6 +176,16 @@ int psg_net_layer_grad(psg_net* net, int layer, double* out, size_t n);
  * ShardBatchIterator semantics (data.hpp:312-351). */
 int psg_net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* shard_indices,
                          size_t count, size_t batch, uint64_t stream_seed);
+/* run_naive (schemes.hpp:201-262): the net consumes rows [part*batch/parts, +batch/parts)
+ * of every batch of the stream (batch = the full minibatch; parts must divide it). */
+int psg_net_attach_shard_part(psg_net* net, psg_dataset* ds, const uint64_t* shard_indices,
+                              size_t count, size_t batch, uint64_t stream_seed, int part,
+                              int parts);
+/* One step of run_naive's per-part work (schemes.hpp:233-247): next batch part ->
+ * forward + backward; the gradient stays in the net's flat gradient buffer. */
+int psg_net_grad_step(psg_net* net);
+/* apply_update (model.hpp:90-107) with the resident (e.g. averaged) gradient. */
+int psg_net_apply_grads(psg_net* net);
 /* Iterator position (epoch, cursor) of the attached shard stream.  Lets a host
  * share one ShardBatchIterator between nets (the warm-start master consumes
  * worker 0's stream, schemes.hpp:314). */
@@ -192,6 +202,11 @@ int psg_net_last_loss(psg_net* net, double* loss);
 /* set_validation_data(SequentialBatchIterator) + test(steps) (model.hpp:122-136). */
 int psg_net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch);
 int psg_net_test(psg_net* net, long steps, double* accuracy);
+/* Sharded evaluation: queue batches first, first+stride, ... < steps of the iterator's
+ * next `steps` batches (the iterator advances by `steps`); test_end returns the counts.
+ * K nets with first = k, stride = K split one test(steps) exactly. */
+int psg_net_test_begin(psg_net* net, long steps, long first, long stride);
+int psg_net_test_end(psg_net* net, unsigned long long* correct, unsigned long long* total);
 /* Kernel launches of one training step (device-side work count). */
 int psg_net_kernels_per_step(const psg_net* net, int* launches);
 
@@ -223,6 +238,8 @@ int psg_net_event_elapsed(psg_net* net, int start_slot, int end_slot, float* ms)
 /* ---- averaging: weights_mean (weights.hpp:90-107) ---------------------------- */
 /* K nets on one device: ordered mean written back into every net. */
 int psg_average_local(psg_net* const* nets, int count);
+/* Same, over the nets' flat gradient buffers (run_naive's weights_mean of part gradients). */
+int psg_average_grads_local(psg_net* const* nets, int count);
 /* NCCL communicators (one per rank/device). */
 int psg_comm_unique_id(unsigned char id[128]);
 int psg_comm_create(psg_ctx* ctx, int nranks, int rank, const unsigned char id[128],
@@ -232,6 +249,8 @@ int psg_comm_destroy(psg_comm* comm);
 /* In-place average of every net's flat parameters across the communicator.
  * count = nets driven by this caller (1 per process, or ndev in one process). */
 int psg_comm_average(psg_comm* const* comms, psg_net* const* nets, int count, int mode);
+/* In-place average of every net's flat gradient buffer (run_naive, schemes.hpp:248). */
+int psg_comm_average_grads(psg_comm* const* comms, psg_net* const* nets, int count, int mode);
 int psg_comm_broadcast(psg_comm* const* comms, psg_net* const* nets, int count, int root);
 
 /* ---- raw flat buffers (averaging-only sweep) -------------------------------- */

@@ -1206,3 +1206,102 @@ long orc_run_sparknet(const orc_sparknet_args* a, orc_record* records, long max_
   free(offs);
   return rc ? -1 : nrec;
 }
+
+/* schemes.hpp:201-262 (run_naive), restated over the same stream / update helpers. */
+long orc_run_naive(const orc_sparknet_args* a, long iter_budget, long eval_every,
+                   orc_record* records, long max_records, double* step_weights) {
+  const int K = a->workers;
+  if (K < 1) {
+    set_err("run_naive: need at least one worker");
+    return -1;
+  }
+  if (a->batch % (size_t)K != 0) {
+    set_err("run_naive: worker count must divide the batch size");
+    return -1;
+  }
+  if (eval_every < 1) {
+    set_err("run_naive: eval_every must be >= 1");
+    return -1;
+  }
+  if (iter_budget < 0) {
+    set_err("run_naive: negative budget");
+    return -1;
+  }
+  uint64_t* perm = (uint64_t*)malloc((a->train_n ? a->train_n : 1) * sizeof(uint64_t));
+  uint64_t offs[2];
+  if (orc_shard(a->train_n, 1, a->seed, perm, offs)) { /* shard(*train, 1, seed) */
+    free(perm);
+    return -1;
+  }
+  if (offs[1] - offs[0] < a->batch) {
+    set_err("batch iterator: batch size exceeds shard size");
+    free(perm);
+    return -1;
+  }
+  const size_t dim = (size_t)a->c * a->h * a->w, part = a->batch / (size_t)K;
+  orc_net* net = orc_net_create(a->layers, a->n_layers, a->seed);
+  if (!net) {
+    free(perm);
+    return -1;
+  }
+  orc_net_set_sgd(net, a->lr, a->momentum, a->weight_decay);
+  const size_t P = net->P;
+  stream_state st;
+  memset(&st, 0, sizeof st);
+  st.shard = perm;
+  st.n = offs[1] - offs[0];
+  st.batch = a->batch;
+  st.seed = orc_worker_stream_seed(a->seed, 0); /* make_worker_iterator(shards, 0, ...) */
+  st.order = (uint64_t*)malloc(st.n * sizeof(uint64_t));
+  orc_epoch_order(st.shard, st.n, st.seed, 0, st.order);
+  double* bimg = (double*)malloc(a->batch * dim * sizeof(double));
+  int32_t* blab = (int32_t*)malloc(a->batch * sizeof(int32_t));
+  double* grads = (double*)malloc((size_t)K * (P ? P : 1) * sizeof(double));
+  const double** items = (const double**)malloc((size_t)K * sizeof(double*));
+  double* mean = (double*)malloc((P ? P : 1) * sizeof(double));
+  double* probs = (double*)malloc(a->batch * (size_t)net->classes * sizeof(double));
+  const double sub = a->sublinearity > 0.0 ? a->sublinearity : 1.0;
+  const double step_s = (sub == 1.0 ? a->compute_seconds / (double)K
+                                    : a->compute_seconds * pow(1.0 / (double)K, sub)) +
+                        a->sync_seconds; /* naive_step_seconds, schemes.hpp:56-61 */
+  long iters = 0, nrec = 0;
+  int rc = PSG_OK;
+  while (!rc && iters < iter_budget) {
+    const long chunk = eval_every < iter_budget - iters ? eval_every : iter_budget - iters;
+    for (long s = 0; !rc && s < chunk; ++s) {
+      stream_next(&st, a->train_images, a->train_labels, dim, bimg, blab);
+      for (int k = 0; !rc && k < K; ++k) { /* per-part gradients, schemes.hpp:235-246 */
+        items[k] = grads + (size_t)k * P;
+        rc = orc_net_backward(net, bimg + (size_t)k * part * dim, blab + (size_t)k * part, part,
+                              NULL, grads + (size_t)k * P);
+      }
+      if (rc) break;
+      orc_weights_mean(items, K, P, mean); /* schemes.hpp:248 */
+      rc = orc_net_apply_update(net, mean);
+      net->dropout_step++;
+      ++iters;
+      if (step_weights) orc_net_get_weights(net, step_weights + (size_t)(iters - 1) * P);
+    }
+    if (rc) break;
+    const double acc = evaluate(net, a, bimg, blab, probs);
+    if (nrec < max_records) {
+      records[nrec].serial_iters = iters;
+      records[nrec].parallel_iters = 0;
+      records[nrec].rounds = iters;
+      records[nrec].sim_time = (double)iters * step_s;
+      records[nrec].accuracy = acc;
+    }
+    ++nrec;
+    if (acc >= a->target_accuracy) break;
+  }
+  orc_net_destroy(net);
+  free(perm);
+  free(st.order);
+  free(bimg);
+  free(blab);
+  free(grads);
+  free(items);
+  free(mean);
+  free(probs);
+  return rc ? -1 : nrec;
+}

@@ -113,12 +113,19 @@ typedef struct orc_sparknet_args {
   long rounds, warm;
   int threads;
   int skip_eval; /* timing runs: skip the per-round evaluation */
+  double sublinearity; /* CostModel::sublinearity (run_naive clock); 0 reads as 1 */
 } orc_sparknet_args;
 /* Returns number of records written (<= max_records) or -1 on error.
  * round_weights (optional) receives rounds x P averaged weights. */
 long orc_run_sparknet(const orc_sparknet_args* args, orc_record* records, long max_records,
                       uint64_t* warm_digest, double* round_weights);
 uint64_t orc_weights_digest(const orc_net* net, const double* flat);
+/* schemes.hpp:201-262 run_naive: each batch of worker 0's single-shard stream is split
+ * into `workers` parts, the part gradients are averaged (weights_mean) and applied once.
+ * Uses args->workers / batch / lr / ...; evaluation every eval_every steps.  step_weights
+ * (optional) receives iter_budget x P weights after every step.  Returns records or -1. */
+long orc_run_naive(const orc_sparknet_args* args, long iter_budget, long eval_every,
+                   orc_record* records, long max_records, double* step_weights);
 
 #ifdef __cplusplus
 }

@@ -40,7 +40,7 @@ class SparknetArgs(ctypes.Structure):
         ("target_accuracy", ctypes.c_double), ("eval_steps", ctypes.c_long),
         ("workers", ctypes.c_int), ("tau", ctypes.c_int),
         ("rounds", ctypes.c_long), ("warm", ctypes.c_long), ("threads", ctypes.c_int),
-        ("skip_eval", ctypes.c_int),
+        ("skip_eval", ctypes.c_int), ("sublinearity", ctypes.c_double),
     ]
 
 
@@ -120,6 +120,9 @@ class OracleLib(_Lib):
         L.orc_run_sparknet.restype = ctypes.c_long
         L.orc_run_sparknet.argtypes = [ctypes.POINTER(SparknetArgs), ctypes.POINTER(Record),
                                        ctypes.c_long, _U64, _D]
+        L.orc_run_naive.restype = ctypes.c_long
+        L.orc_run_naive.argtypes = [ctypes.POINTER(SparknetArgs), ctypes.c_long, ctypes.c_long,
+                                    ctypes.POINTER(Record), ctypes.c_long, _D]
         L.orc_weights_digest.restype = ctypes.c_uint64
         L.orc_weights_digest.argtypes = [ctypes.c_void_p, _D]
 
@@ -182,6 +185,44 @@ class OracleLib(_Lib):
                              seed, workers, tau, rounds, warm, threads, weight_decay, target,
                              eval_steps, cost, want_weights, skip_eval,
                              lambda: self.error(), P=_param_count(self, spec, seed))
+
+    def run_naive(self, spec: NetSpec, train, evald, batch, lr, momentum, seed, workers, iters,
+                  eval_every, weight_decay=0.0, target=2.0, eval_steps=1, cost=(1.0, 0.0, 1.0),
+                  want_weights=False):
+        return _run_naive(self.lib.orc_run_naive, spec, train, evald, batch, lr, momentum, seed,
+                          workers, iters, eval_every, weight_decay, target, eval_steps, cost,
+                          want_weights, lambda: self.error(), P=_param_count(self, spec, seed))
+
+
+def _run_naive(fn, spec, train, evald, batch, lr, momentum, seed, workers, iters, eval_every,
+               weight_decay, target, eval_steps, cost, want_weights, err, P):
+    """Shared driver of orc_run_naive / ref_run_naive: returns (records, step_weights)."""
+    timg = np.ascontiguousarray(train[0], np.float64)
+    tlab = np.ascontiguousarray(train[1], np.int32)
+    eimg = np.ascontiguousarray(evald[0], np.float64)
+    elab = np.ascontiguousarray(evald[1], np.int32)
+    layers = spec.to_c()
+    a = SparknetArgs()
+    a.layers = layers
+    a.n_layers = len(spec.layers)
+    a.train_images, a.train_labels, a.train_n = _dp(timg), _ip(tlab), tlab.size
+    a.eval_images, a.eval_labels, a.eval_n = _dp(eimg), _ip(elab), elab.size
+    a.c, a.h, a.w = timg.shape[1], timg.shape[2], timg.shape[3]
+    a.batch, a.lr, a.momentum, a.weight_decay = batch, lr, momentum, weight_decay
+    a.seed = seed
+    a.compute_seconds, a.sync_seconds = cost[0], cost[1]
+    a.sublinearity = cost[2] if len(cost) > 2 else 1.0
+    a.target_accuracy, a.eval_steps = target, eval_steps
+    a.workers = workers
+    nmax = max(1, (iters + eval_every - 1) // eval_every)
+    recs = (Record * nmax)()
+    sw = np.zeros((max(iters, 1), P), np.float64) if want_weights else None
+    n = fn(ctypes.byref(a), iters, eval_every, recs, nmax, _dp(sw) if want_weights else None)
+    if n < 0:
+        raise RuntimeError(err())
+    out = [(r.serial_iters, r.parallel_iters, r.rounds, r.sim_time, r.accuracy)
+           for r in recs[:min(n, nmax)]]
+    return out, (sw[:iters] if want_weights else None)
 
 
 def _param_count(lib, spec, seed):
@@ -363,6 +404,9 @@ class RefLib(_Lib):
         L.ref_weights_mean.argtypes = [ctypes.POINTER(_D), ctypes.c_int, ctypes.c_size_t, _D]
         L.ref_net_digest.restype = ctypes.c_uint64
         L.ref_net_digest.argtypes = [ctypes.c_void_p]
+        L.ref_run_naive.restype = ctypes.c_long
+        L.ref_run_naive.argtypes = [ctypes.POINTER(SparknetArgs), ctypes.c_long, ctypes.c_long,
+                                    ctypes.POINTER(Record), ctypes.c_long, _D]
         L.ref_run_sparknet.restype = ctypes.c_long
         L.ref_run_sparknet.argtypes = [ctypes.POINTER(SparknetArgs), ctypes.POINTER(Record),
                                        ctypes.c_long, _U64, _D]
@@ -408,6 +452,13 @@ class RefLib(_Lib):
         return _run_sparknet(self.lib.ref_run_sparknet, spec, train, evald, batch, lr, momentum,
                              seed, workers, tau, rounds, warm, threads, 0.0, target, eval_steps,
                              cost, want_weights, False, lambda: self.error(), P=P)
+
+    def run_naive(self, spec, train, evald, batch, lr, momentum, seed, workers, iters, eval_every,
+                  target=2.0, eval_steps=1, cost=(1.0, 0.0, 1.0), want_weights=False):
+        P = RefNet(self, spec, seed).P
+        return _run_naive(self.lib.ref_run_naive, spec, train, evald, batch, lr, momentum, seed,
+                          workers, iters, eval_every, 0.0, target, eval_steps, cost, want_weights,
+                          lambda: self.error(), P=P)
 
 
 class RefNet:

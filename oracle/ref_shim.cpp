@@ -332,4 +332,46 @@ long ref_run_sparknet(const orc_sparknet_args* a, orc_record* records, long max_
   return nrec;
 }
 
+long ref_run_naive(const orc_sparknet_args* a, long iter_budget, long eval_every,
+                   orc_record* records, long max_records, double* step_weights) {
+  long nrec = -1;
+  guarded([&] {
+    const NetSpec spec = to_spec(a->layers, a->n_layers);
+    Net probe(spec, a->seed);
+    const int classes = probe.num_classes();
+    const Dataset train = make_dataset(a->train_images, a->train_labels, a->train_n, a->c, a->h,
+                                       a->w, classes);
+    const Dataset eval =
+        make_dataset(a->eval_images, a->eval_labels, a->eval_n, a->c, a->h, a->w, classes);
+    SchemeContext ctx;
+    ctx.net = spec;
+    ctx.train_data = &train;
+    ctx.eval_data = &eval;
+    ctx.batch = a->batch;
+    ctx.sgd = {a->lr, a->momentum};
+    ctx.seed = a->seed;
+    ctx.cost = {a->compute_seconds, a->sync_seconds,
+                a->sublinearity > 0.0 ? a->sublinearity : 1.0};
+    ctx.target_accuracy = a->target_accuracy;
+    ctx.eval_steps = a->eval_steps;
+    SchemeObserver obs;
+    obs.on_step = [&](long it, const Net& net) {
+      if (step_weights) {
+        const std::vector<double> v = flatten(net.get_weights());
+        std::copy(v.begin(), v.end(), step_weights + static_cast<std::size_t>(it - 1) * v.size());
+      }
+    };
+    const RunTrace t = run_naive(ctx, a->workers, iter_budget, eval_every, &obs);
+    for (std::size_t i = 0; i < t.records.size() && static_cast<long>(i) < max_records; ++i) {
+      records[i].serial_iters = t.records[i].serial_iters;
+      records[i].parallel_iters = t.records[i].parallel_iters;
+      records[i].rounds = t.records[i].rounds;
+      records[i].sim_time = t.records[i].sim_time;
+      records[i].accuracy = t.records[i].accuracy;
+    }
+    nrec = static_cast<long>(t.records.size());
+  });
+  return nrec;
+}
+
 }  // extern "C"

@@ -96,6 +96,15 @@ SIGNATURES = {
     "psg_net_last_loss": (ctypes.c_int, [_VP, _D]),
     "psg_net_attach_validation": (ctypes.c_int, [_VP, _VP, _SZ]),
     "psg_net_test": (ctypes.c_int, [_VP, ctypes.c_long, _D]),
+    "psg_net_test_begin": (ctypes.c_int, [_VP, ctypes.c_long, ctypes.c_long, ctypes.c_long]),
+    "psg_net_test_end": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_ulonglong),
+                                        ctypes.POINTER(ctypes.c_ulonglong)]),
+    "psg_net_attach_shard_part": (ctypes.c_int, [_VP, _VP, _U64, _SZ, _SZ, ctypes.c_uint64,
+                                                 ctypes.c_int, ctypes.c_int]),
+    "psg_net_grad_step": (ctypes.c_int, [_VP]),
+    "psg_net_apply_grads": (ctypes.c_int, [_VP]),
+    "psg_average_grads_local": (ctypes.c_int, [_PP, ctypes.c_int]),
+    "psg_comm_average_grads": (ctypes.c_int, [_PP, _PP, ctypes.c_int, ctypes.c_int]),
     "psg_net_kernels_per_step": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int)]),
     "psg_net_profile_step": (ctypes.c_int, [_VP, ctypes.c_int, _VP, ctypes.c_int,
                                             ctypes.POINTER(ctypes.c_int)]),

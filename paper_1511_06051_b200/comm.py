@@ -56,6 +56,13 @@ class Communicator:
         _lib.call("psg_comm_average", c, n, len(nets), MODES[mode])
 
     @staticmethod
+    def average_grads(comms: Sequence["Communicator"], nets: Sequence, mode: str = "fast") -> None:
+        """In-place mean of every net's flat gradient buffer (run_naive, schemes.hpp:248)."""
+        c = (ctypes.c_void_p * len(comms))(*[x.handle.value for x in comms])
+        n = (ctypes.c_void_p * len(nets))(*[x.handle.value for x in nets])
+        _lib.call("psg_comm_average_grads", c, n, len(nets), MODES[mode])
+
+    @staticmethod
     def broadcast(comms: Sequence["Communicator"], nets: Sequence, root: int = 0) -> None:
         c = (ctypes.c_void_p * len(comms))(*[x.handle.value for x in comms])
         n = (ctypes.c_void_p * len(nets))(*[x.handle.value for x in nets])

@@ -383,6 +383,30 @@ int psg_net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* shard_in
   });
 }
 
+int psg_net_attach_shard_part(psg_net* net, psg_dataset* ds, const uint64_t* shard_indices,
+                              size_t count, size_t batch, uint64_t stream_seed, int part,
+                              int parts) {
+  return guarded([&] {
+    need(net, "attach_shard_part");
+    need(ds, "attach_shard_part dataset");
+    psg::net_attach_shard(net, ds, shard_indices, count, batch, stream_seed, part, parts);
+  });
+}
+
+int psg_net_grad_step(psg_net* net) {
+  return guarded([&] {
+    need(net, "grad_step");
+    psg::net_grad_step(net);
+  });
+}
+
+int psg_net_apply_grads(psg_net* net) {
+  return guarded([&] {
+    need(net, "apply_grads");
+    psg::net_apply_grads(net);
+  });
+}
+
 int psg_net_get_stream_position(const psg_net* net, uint64_t* epoch, uint64_t* cursor) {
   return guarded([&] {
     need(net, "get_stream_position");
@@ -455,6 +479,20 @@ int psg_net_test(psg_net* net, long steps, double* accuracy) {
   });
 }
 
+int psg_net_test_begin(psg_net* net, long steps, long first, long stride) {
+  return guarded([&] {
+    need(net, "test_begin");
+    psg::net_test_begin(net, steps, first, stride);
+  });
+}
+
+int psg_net_test_end(psg_net* net, unsigned long long* correct, unsigned long long* total) {
+  return guarded([&] {
+    need(net, "test_end");
+    psg::net_test_end(net, correct, total);
+  });
+}
+
 int psg_net_kernels_per_step(const psg_net* net, int* launches) {
   return guarded([&] {
     need(net, "kernels_per_step");
@@ -509,8 +547,9 @@ int psg_net_event_elapsed(psg_net* net, int start_slot, int end_slot, float* ms)
   });
 }
 
-int psg_average_local(psg_net* const* nets, int count) {
-  return guarded([&] {
+namespace {
+void average_local_nets(psg_net* const* nets, int count, int which) {
+  {
     if (count < 1) throw std::invalid_argument("weights_mean: empty input");
     std::vector<float*> bufs(count);
     for (int i = 0; i < count; ++i) {
@@ -519,7 +558,7 @@ int psg_average_local(psg_net* const* nets, int count) {
         throw std::invalid_argument("average_local: nets on different devices");
       if (nets[i]->P_int != nets[0]->P_int)
         throw std::invalid_argument("weights_mean: structure mismatch");
-      bufs[i] = nets[i]->w;
+      bufs[i] = which ? nets[i]->g : nets[i]->w;
     }
     psg::DeviceGuard dg(nets[0]->ctx->device);
     // order the average after every net's queued work, and every net after it
@@ -535,7 +574,16 @@ int psg_average_local(psg_net* const* nets, int count) {
     for (int i = 1; i < count; ++i) PSG_CUDA(cudaStreamWaitEvent(nets[i]->stream, evs[0], 0));
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     psg::net_check_flag(nets[0]);
-  });
+  }
+}
+}  // namespace
+
+int psg_average_local(psg_net* const* nets, int count) {
+  return guarded([&] { average_local_nets(nets, count, 0); });
+}
+
+int psg_average_grads_local(psg_net* const* nets, int count) {
+  return guarded([&] { average_local_nets(nets, count, 1); });
 }
 
 int psg_comm_unique_id(unsigned char id[128]) {
@@ -565,6 +613,13 @@ int psg_comm_average(psg_comm* const* comms, psg_net* const* nets, int count, in
   return guarded([&] {
     if (count < 1) throw std::invalid_argument("weights_mean: empty input");
     psg::comm_average_nets(comms, nets, count, mode);
+  });
+}
+
+int psg_comm_average_grads(psg_comm* const* comms, psg_net* const* nets, int count, int mode) {
+  return guarded([&] {
+    if (count < 1) throw std::invalid_argument("weights_mean: empty input");
+    psg::comm_average_nets(comms, nets, count, mode, 1);
   });
 }
 

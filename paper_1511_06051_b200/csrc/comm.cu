@@ -196,7 +196,8 @@ void comm_destroy(psg_comm* c) {
   delete c;
 }
 
-void comm_average_nets(psg_comm* const* comms, psg_net* const* nets, int count, int mode) {
+void comm_average_nets(psg_comm* const* comms, psg_net* const* nets, int count, int mode,
+                       int which) {
   std::vector<float*> bufs(count);
   std::vector<size_t> counts(count);
   std::vector<cudaStream_t> streams(count);
@@ -204,7 +205,7 @@ void comm_average_nets(psg_comm* const* comms, psg_net* const* nets, int count, 
   for (int i = 0; i < count; ++i) {
     if (nets[i]->ctx->device != comms[i]->ctx->device)
       throw std::invalid_argument("average: net and communicator on different devices");
-    bufs[i] = nets[i]->w;
+    bufs[i] = which ? nets[i]->g : nets[i]->w;
     counts[i] = mode == PSG_AVERAGE_FAST ? nets[i]->P_int : nets[i]->P_alloc;
     streams[i] = nets[i]->stream;
     flags[i] = &nets[i]->dsc->flag;

@@ -178,9 +178,22 @@ void finish_args(TcArgs& a, int kblk, int sms) {
   a.stage_bytes = a.a_bytes + nb * kblk * 4;
   a.stages = std::min(8, (225 * 1024 - kEpiBytes) / a.stage_bytes);
   const long long tiles = static_cast<long long>(a.m_tiles) * a.n_tiles * a.G * a.taps;
+  // Split K so that the persistent grid's waves are full: minimise
+  // waves(tiles * s) * ceil(kblocks / s) (+ a small charge per extra split for the partials
+  // and the reduce pass); at least 4 K blocks per split.
   int splits = 1;
-  if (tiles < sms) splits = static_cast<int>(std::min<long long>((sms + tiles - 1) / tiles,
-                                                                 std::max(1, a.kblocks / 4)));
+  if (tiles < 2LL * sms) {
+    long long best = -1;
+    const int max_s = std::max(1, std::min(a.kblocks / 4, 64));
+    for (int sp = 1; sp <= max_s; ++sp) {
+      const long long waves = (tiles * sp + sms - 1) / sms;
+      const long long cost = waves * ((a.kblocks + sp - 1) / sp) + (sp > 1 ? 2 + sp / 4 : 0);
+      if (best < 0 || cost < best) {
+        best = cost;
+        splits = sp;
+      }
+    }
+  }
   a.kb_per_split = (a.kblocks + splits - 1) / splits;
   a.splits = (a.kblocks + a.kb_per_split - 1) / a.kb_per_split;
   a.total_tiles = tiles * a.splits;

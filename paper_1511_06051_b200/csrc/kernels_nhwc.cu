@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_fwd_k(LrnGeom g, const float*
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const size_t e0 = static_cast<size_t>(tile) * tp * C;
     const int ne = min(tp, g.pixels - tile * tp) * C;
+#pragma unroll 8
     for (int e = threadIdx.x; e < ne; e += kLrnThreads) sx[e] = __ldg(x + e0 + e);
     __syncthreads();
     int c = threadIdx.x % C;
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float*
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const size_t e0 = static_cast<size_t>(tile) * tp * C;
     const int ne = min(tp, g.pixels - tile * tp) * C;
+#pragma unroll 8
     for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
       sx[e] = __ldg(x + e0 + e);
       sd[e] = __ldg(dy + e0 + e);

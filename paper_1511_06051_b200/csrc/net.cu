@@ -135,9 +135,12 @@ ConvGeom geom_for(const LayerRt& l, size_t n) {
 void invalidate_graph(psg_net* net) {
   if (net->graph) cudaGraphExecDestroy(net->graph);
   if (net->host_graph) cudaGraphExecDestroy(net->host_graph);
+  if (net->grad_graph) cudaGraphExecDestroy(net->grad_graph);
   net->graph = nullptr;
   net->host_graph = nullptr;
+  net->grad_graph = nullptr;
   net->graph_batch = 0;
+  net->grad_graph_batch = 0;
 }
 
 void release_batch_buffers(psg_net* net) {
@@ -486,6 +489,7 @@ void net_free(psg_net* net) {
   dfree(net->d_chunks);
   dfree(net->dsc);
   dfree(net->d_idx);
+  dfree(net->d_vidx);
   if (net->hsc) cudaFreeHost(net->hsc);
   if (net->h_idx) cudaFreeHost(net->h_idx);
   if (net->h_stage) cudaFreeHost(net->h_stage);
@@ -618,8 +622,12 @@ void net_layer_readback(psg_net* net, int layer, bool grad, double* out, size_t 
 }
 
 void net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* idx, size_t count,
-                      size_t batch, uint64_t seed) {
+                      size_t batch, uint64_t seed, int part, int parts) {
   if (batch < 1) throw std::invalid_argument("batch iterator: batch size must be >= 1");
+  if (parts < 1 || part < 0 || part >= parts)
+    throw std::invalid_argument("attach: part index out of range");
+  if (batch % static_cast<size_t>(parts))
+    throw std::invalid_argument("run_naive: worker count must divide the batch size");
   if (batch > count) throw std::invalid_argument("batch iterator: batch size exceeds shard size");
   const LayerRt& d = net->L[net->data_idx];
   if (ds->c != d.C || ds->h != d.H || ds->w != d.W)
@@ -635,18 +643,20 @@ void net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* idx, size_t
   net->it_batch = batch;
   net->it_seed = seed;
   net->it_epoch = 0;
+  net->it_part = part;
+  net->it_parts = parts;
   net->order.resize(count);
   epoch_order(net->shard.data(), count, seed, 0, net->order.data());  // ctor -> start_epoch
   net->it_cursor = 0;
 }
 
-void net_train(psg_net* net, long steps) {
-  if (steps < 0) throw std::invalid_argument("train: negative step count");
-  if (steps == 0) return;
-  if (!net->train_ds) throw std::runtime_error("train: no training data attached");
-  DeviceGuard dg(net->ctx->device);
-  const size_t b = net->it_batch;
-  ensure_capacity(net, b);
+namespace {
+
+// ShardBatchIterator::next() x steps (data.hpp:323-331): this net's rows of each batch,
+// uploaded in one copy; the device cursor restarts at row block 0.  Returns rows per step.
+size_t upload_stream_indices(psg_net* net, long steps) {
+  const size_t B = net->it_batch, b = B / static_cast<size_t>(net->it_parts);
+  const size_t off = static_cast<size_t>(net->it_part) * b;
   const size_t need = static_cast<size_t>(steps) * b;
   if (need > net->idx_cap) {
     PSG_CUDA(cudaStreamSynchronize(net->stream));
@@ -657,25 +667,26 @@ void net_train(psg_net* net, long steps) {
     PSG_CUDA(cudaMallocHost(&net->h_idx, net->idx_cap * sizeof(uint32_t)));
     invalidate_graph(net);
   }
-  // ShardBatchIterator::next() x steps (data.hpp:323-331) -> one index upload.
   PSG_CUDA(cudaEventSynchronize(net->idx_ev));
   for (long s = 0; s < steps; ++s) {
-    if ((net->it_cursor + 1) * b > net->order.size()) {
+    if ((net->it_cursor + 1) * B > net->order.size()) {
       ++net->it_epoch;
       epoch_order(net->shard.data(), net->shard.size(), net->it_seed, net->it_epoch,
                   net->order.data());
       net->it_cursor = 0;
     }
     for (size_t i = 0; i < b; ++i)
-      net->h_idx[s * b + i] = static_cast<uint32_t>(net->order[net->it_cursor * b + i]);
+      net->h_idx[s * b + i] = static_cast<uint32_t>(net->order[net->it_cursor * B + off + i]);
     ++net->it_cursor;
   }
   PSG_CUDA(cudaMemcpyAsync(net->d_idx, net->h_idx, need * sizeof(uint32_t), cudaMemcpyHostToDevice,
                            net->stream));
   PSG_CUDA(cudaEventRecord(net->idx_ev, net->stream));
   PSG_CUDA(cudaMemsetAsync(&net->dsc->cursor, 0, sizeof(int), net->stream));
-  const LayerRt& d = net->L[net->data_idx];
-  psg_dataset* ds = net->train_ds;
+  return b;
+}
+
+bool eager_mode() {
   // PSG_EAGER=1: launch the step's kernels directly instead of replaying the CUDA
   // graph (ncu cannot replay graph kernel nodes that take a __grid_constant__
   // CUtensorMap).  Same kernels, same order.
@@ -683,7 +694,22 @@ void net_train(psg_net* net, long steps) {
     const char* e = std::getenv("PSG_EAGER");
     return e && e[0] == '1';
   }();
-  if (eager) {
+  return eager;
+}
+
+}  // namespace
+
+void net_train(psg_net* net, long steps) {
+  if (steps < 0) throw std::invalid_argument("train: negative step count");
+  if (steps == 0) return;
+  if (!net->train_ds) throw std::runtime_error("train: no training data attached");
+  DeviceGuard dg(net->ctx->device);
+  const size_t b = net->it_batch / static_cast<size_t>(net->it_parts);
+  ensure_capacity(net, b);
+  upload_stream_indices(net, steps);
+  const LayerRt& d = net->L[net->data_idx];
+  psg_dataset* ds = net->train_ds;
+  if (eager_mode()) {
     PSG_CUDA(cudaEventRecord(net->t0, net->stream));
     for (long s = 0; s < steps; ++s) {
       gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
@@ -726,6 +752,53 @@ void net_train(psg_net* net, long steps) {
   net->last_n = b;
 }
 
+// run_naive (schemes.hpp:233-250) on the device: one part of the next batch ->
+// forward + backward, gradient left in the flat buffer g (not applied).  The SGD
+// update runs separately after the K part gradients were averaged.
+void net_grad_step(psg_net* net) {
+  if (!net->train_ds) throw std::runtime_error("train: no training data attached");
+  DeviceGuard dg(net->ctx->device);
+  const size_t b = net->it_batch / static_cast<size_t>(net->it_parts);
+  ensure_capacity(net, b);
+  upload_stream_indices(net, 1);
+  const LayerRt& d = net->L[net->data_idx];
+  psg_dataset* ds = net->train_ds;
+  auto body = [&] {
+    gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
+                 d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+    run_forward(net, b, true, true);
+    run_backward(net, b);
+  };
+  if (eager_mode()) {
+    body();
+  } else {
+    if (!net->grad_graph || net->grad_graph_batch != b) {
+      if (net->grad_graph) cudaGraphExecDestroy(net->grad_graph);
+      net->grad_graph = nullptr;
+      cudaGraph_t graph;
+      PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        body();
+      } catch (...) {
+        cudaStreamEndCapture(net->stream, &graph);
+        throw;
+      }
+      PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
+      PSG_CUDA(cudaGraphInstantiate(&net->grad_graph, graph, 0));
+      cudaGraphDestroy(graph);
+      net->grad_graph_batch = b;
+    }
+    PSG_CUDA(cudaGraphLaunch(net->grad_graph, net->stream));
+  }
+  net->last_n = b;
+}
+
+// apply_update with the resident (averaged) gradient; advances the step counter.
+void net_apply_grads(psg_net* net) {
+  DeviceGuard dg(net->ctx->device);
+  run_update(net, true);
+}
+
 void net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch) {
   if (batch < 1 || batch > ds->n) throw std::invalid_argument("eval iterator: bad batch size");
   const LayerRt& d = net->L[net->data_idx];
@@ -740,38 +813,66 @@ void net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch) {
   net->val_cursor = 0;
 }
 
-double net_test(psg_net* net, long steps) {
+// Net::test (model.hpp:122-136) over a SequentialBatchIterator (data.hpp:355-382),
+// split for sharded evaluation: this call queues batches first, first + stride, ... < steps
+// of the iterator's next `steps` batches (forward-only, fused argmax/count) and advances
+// the iterator by `steps`, so K nets with first = k, stride = K cover one test(steps)
+// between them.  test_end collects (correct, total).
+void net_test_begin(psg_net* net, long steps, long first, long stride) {
   if (steps < 1) throw std::invalid_argument("test: step count must be >= 1");
+  if (first < 0 || stride < 1) throw std::invalid_argument("test: bad shard");
   if (!net->val_ds) throw std::runtime_error("test: no validation data attached");
+  if (net->val_pending) throw std::logic_error("test: previous evaluation not collected");
   DeviceGuard dg(net->ctx->device);
   const size_t b = net->val_batch;
-  ensure_capacity(net, b);
-  std::vector<uint32_t> idx(static_cast<size_t>(steps) * b);
-  for (long s = 0; s < steps; ++s) {  // SequentialBatchIterator::next (data.hpp:366-371)
-    if ((net->val_cursor + 1) * b > net->val_ds->n) net->val_cursor = 0;
-    for (size_t i = 0; i < b; ++i) idx[s * b + i] = static_cast<uint32_t>(net->val_cursor * b + i);
-    ++net->val_cursor;
+  const size_t nb = net->val_ds->n / b;  // batches before the iterator wraps
+  std::vector<uint32_t> idx;
+  long mine = 0;
+  for (long s = first; s < steps; s += stride, ++mine) {
+    const size_t cursor = (net->val_cursor + static_cast<size_t>(s)) % nb;
+    for (size_t i = 0; i < b; ++i) idx.push_back(static_cast<uint32_t>(cursor * b + i));
   }
-  uint32_t* d_vidx = dalloc<uint32_t>(idx.size());
-  PSG_CUDA(cudaMemcpyAsync(d_vidx, idx.data(), idx.size() * sizeof(uint32_t),
-                           cudaMemcpyHostToDevice, net->stream));
+  net->val_cursor = (net->val_cursor + static_cast<size_t>(steps)) % nb;
+  net->val_total = static_cast<unsigned long long>(mine) * b;
+  net->val_pending = true;
   PSG_CUDA(cudaMemsetAsync(&net->dsc->correct, 0, sizeof(unsigned long long), net->stream));
+  if (mine == 0) return;
+  ensure_capacity(net, b);
+  if (idx.size() > net->vidx_cap) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    dfree(net->d_vidx);
+    net->vidx_cap = idx.size();
+    net->d_vidx = dalloc<uint32_t>(net->vidx_cap);
+  }
+  PSG_CUDA(cudaMemcpyAsync(net->d_vidx, idx.data(), idx.size() * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice, net->stream));
   const LayerRt& d = net->L[net->data_idx];
-  for (long s = 0; s < steps; ++s) {
-    gather_batch(net->val_ds->images, net->val_ds->labels, d_vidx + s * b, nullptr,
+  for (long s = 0; s < mine; ++s) {
+    gather_batch(net->val_ds->images, net->val_ds->labels, net->d_vidx + s * b, nullptr,
                  static_cast<int>(b), d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
     run_forward(net, b, /*train=*/false, /*seed_grad=*/false);
     argmax_count(net->L[net->loss_idx].out, net->labels, static_cast<int>(b), net->classes,
                  &net->dsc->correct, net->stream);
   }
-  unsigned long long correct = 0;
-  PSG_CUDA(cudaMemcpyAsync(&net->hsc->correct, &net->dsc->correct, sizeof(correct),
+  net->last_n = b;  // (pageable idx: the async copy stages it before returning)
+}
+
+void net_test_end(psg_net* net, unsigned long long* correct, unsigned long long* total) {
+  if (!net->val_pending) throw std::logic_error("test: no evaluation in flight");
+  DeviceGuard dg(net->ctx->device);
+  PSG_CUDA(cudaMemcpyAsync(&net->hsc->correct, &net->dsc->correct, sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, net->stream));
   PSG_CUDA(cudaStreamSynchronize(net->stream));
-  correct = net->hsc->correct;
-  dfree(d_vidx);
-  net->last_n = b;
-  return static_cast<double>(correct) / static_cast<double>(steps * static_cast<long>(b));
+  net->val_pending = false;
+  *correct = net->hsc->correct;
+  *total = net->val_total;
+}
+
+double net_test(psg_net* net, long steps) {
+  net_test_begin(net, steps, 0, 1);
+  unsigned long long correct = 0, total = 0;
+  net_test_end(net, &correct, &total);
+  return static_cast<double>(correct) / static_cast<double>(total);
 }
 
 }  // namespace psg

@@ -98,6 +98,7 @@ struct psg_net {
   std::vector<uint64_t> shard, order;
   size_t it_batch = 0, it_cursor = 0;
   uint64_t it_seed = 0, it_epoch = 0;
+  int it_part = 0, it_parts = 1;  // this net consumes rows [part*b/parts, +b/parts) of a batch
   uint32_t* d_idx = nullptr;
   uint32_t* h_idx = nullptr;  // pinned staging
   size_t idx_cap = 0;
@@ -105,6 +106,10 @@ struct psg_net {
   // validation stream (SequentialBatchIterator, data.hpp:355-382)
   psg_dataset* val_ds = nullptr;
   size_t val_batch = 0, val_cursor = 0;
+  uint32_t* d_vidx = nullptr;  // queued evaluation batches (test_begin .. test_end)
+  size_t vidx_cap = 0;
+  unsigned long long val_total = 0;
+  bool val_pending = false;
   // explicit-batch staging
   float* h_stage = nullptr;
   size_t h_stage_cap = 0;
@@ -112,6 +117,8 @@ struct psg_net {
   // graph of one training step
   cudaGraphExec_t graph = nullptr;
   size_t graph_batch = 0;
+  cudaGraphExec_t grad_graph = nullptr;  // gather + forward + backward (run_naive parts)
+  size_t grad_graph_batch = 0;
   int launches_per_step = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   bool timed = false;
@@ -164,16 +171,22 @@ void net_backward_host(psg_net* net, const double* images, const int32_t* labels
 void net_apply_update_host(psg_net* net, const double* grads, size_t n);
 void net_layer_readback(psg_net* net, int layer, bool grad, double* out, size_t n);
 void net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* idx, size_t count,
-                      size_t batch, uint64_t seed);
+                      size_t batch, uint64_t seed, int part = 0, int parts = 1);
 void net_train(psg_net* net, long steps);
+void net_grad_step(psg_net* net);
+void net_apply_grads(psg_net* net);
 void net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch);
 double net_test(psg_net* net, long steps);
+void net_test_begin(psg_net* net, long steps, long first, long stride);
+void net_test_end(psg_net* net, unsigned long long* correct, unsigned long long* total);
 
 void comm_unique_id(unsigned char id[128]);
 psg_comm* comm_create(psg_ctx* ctx, int nranks, int rank, const unsigned char id[128]);
 void comm_create_all(psg_ctx* const* ctxs, int ndev, psg_comm** out);
 void comm_destroy(psg_comm* c);
-void comm_average_nets(psg_comm* const* comms, psg_net* const* nets, int count, int mode);
+// which: 0 = parameters (weights_mean), 1 = gradients (run_naive's per-step mean)
+void comm_average_nets(psg_comm* const* comms, psg_net* const* nets, int count, int mode,
+                       int which = 0);
 void comm_broadcast_nets(psg_comm* const* comms, psg_net* const* nets, int count, int root);
 void comm_average_buffers(psg_comm* const* comms, psg_buffer* const* bufs, int count, int mode,
                           float* device_ms);

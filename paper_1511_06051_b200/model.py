@@ -92,6 +92,7 @@ class Net:
         self._sgd = SgdOptions()
         self._train_it: Optional[ShardBatchIterator] = None
         self._attached = None
+        self._part = (0, 1)
         self._val_it: Optional[SequentialBatchIterator] = None
         self._structure = self._read_structure()
         self.set_precision(precision)
@@ -250,6 +251,19 @@ class Net:
     # --- data streams (model.hpp:68-69) -------------------------------------
     def set_training_data(self, it: ShardBatchIterator) -> None:
         self._train_it = it
+        self._part = (0, 1)
+        self._attached = None
+
+    def set_training_part(self, it: ShardBatchIterator, part: int, parts: int) -> None:
+        """run_naive (schemes.hpp:233-247): this net trains on rows
+        [part*b/parts, (part+1)*b/parts) of every batch the iterator yields."""
+        if parts < 1 or not 0 <= part < parts:
+            raise ValueError("attach: part index out of range")
+        if it.batch_size % parts:
+            raise ValueError("run_naive: worker count must divide the batch size")
+        self._train_it = it
+        self._part = (part, parts)
+        self._attached = None
 
     def set_validation_data(self, it: SequentialBatchIterator) -> None:
         self._val_it = it
@@ -260,8 +274,9 @@ class Net:
         it = self._train_it
         if self._attached is not it:
             idx = np.ascontiguousarray(it.shard.indices, np.uint64)
-            _lib.call("psg_net_attach_shard", self.handle, it.shard.dataset.handle(self.ctx),
-                      idx.ctypes.data_as(_lib._U64), idx.size, it.batch_size, it.seed)
+            _lib.call("psg_net_attach_shard_part", self.handle,
+                      it.shard.dataset.handle(self.ctx), idx.ctypes.data_as(_lib._U64),
+                      idx.size, it.batch_size, it.seed, self._part[0], self._part[1])
             self._attached = it
         _lib.call("psg_net_set_stream_position", self.handle, it._epoch, it._cursor)
 
@@ -288,6 +303,19 @@ class Net:
         self._sync_stream_out()
         if sync:
             self.sync()
+
+    def grad_step(self) -> None:
+        """One run_naive part (schemes.hpp:233-247): next batch (this net's rows) ->
+        forward + backward; the gradient stays on the device (enqueued, no sync)."""
+        if self._train_it is None:
+            raise RuntimeError("train: no training data attached")
+        self._sync_stream_in()
+        _lib.call("psg_net_grad_step", self.handle)
+        self._sync_stream_out()
+
+    def apply_grads(self) -> None:
+        """apply_update (model.hpp:90-107) with the device-resident gradient."""
+        _lib.call("psg_net_apply_grads", self.handle)
 
     def sync(self) -> None:
         """Wait for queued work; raises RuntimeError if a non-finite value appeared."""
@@ -347,6 +375,18 @@ class Net:
         acc = ctypes.c_double()
         _lib.call("psg_net_test", self.handle, num_steps, ctypes.byref(acc))
         return acc.value
+
+    def test_begin(self, num_steps: int, first: int, stride: int) -> None:
+        """Sharded test: queue batches first, first+stride, ... of the next num_steps."""
+        if self._val_it is None:
+            raise RuntimeError("test: no validation data attached")
+        _lib.call("psg_net_test_begin", self.handle, num_steps, first, stride)
+
+    def test_end(self):
+        """(correct, total) of the evaluation queued by test_begin."""
+        c, t = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+        _lib.call("psg_net_test_end", self.handle, ctypes.byref(c), ctypes.byref(t))
+        return c.value, t.value
 
     # SparkNet (Scala) spellings
     setTrainingData = set_training_data

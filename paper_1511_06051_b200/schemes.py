@@ -67,6 +67,11 @@ def naive_step_seconds(c: CostModel, workers: int) -> float:
     return part + c.sync_seconds
 
 
+def naive_sim_time(iters: int, c: CostModel, workers: int) -> float:
+    """schemes.hpp:62-64."""
+    return float(iters) * naive_step_seconds(c, workers)
+
+
 def sparknet_sim_time(rounds: int, tau: int, warm: int, c: CostModel) -> float:
     """schemes.hpp:69-73."""
     return float(warm) * c.compute_seconds + float(rounds) * (float(tau) * c.compute_seconds +
@@ -152,6 +157,137 @@ def evaluate(net: Net, ctx: SchemeContext) -> float:
     return net.test(ctx.eval_steps)
 
 
+def average_grads_local(nets: List[Net]) -> None:
+    """weights_mean of K same-GPU nets' gradient buffers, written back into every net."""
+    arr = (ctypes.c_void_p * len(nets))(*[n.handle.value for n in nets])
+    _lib.call("psg_average_grads_local", arr, len(nets))
+
+
+def evaluate_sharded(nets: List[Net], ctx: SchemeContext) -> float:
+    """evaluate() split across K nets that hold the same weights (one per GPU): net k
+    runs batches k, k+K, ... of the eval_steps; (correct, total) are summed on the host.
+    Integer counts, so the accuracy equals the single-net evaluate() exactly."""
+    if len(nets) == 1:
+        return evaluate(nets[0], ctx)
+    for n in nets:
+        n.set_validation_data(SequentialBatchIterator(ctx.eval_data, ctx.batch))
+    for k, n in enumerate(nets):
+        n.test_begin(ctx.eval_steps, k, len(nets))
+    correct = total = 0
+    for n in nets:
+        c, t = n.test_end()
+        correct += c
+        total += t
+    return correct / total
+
+
+def _make_serial_net(ctx: SchemeContext, device: int) -> Net:
+    """schemes.hpp:141-147: one net, worker 0's iterator over a single shard."""
+    net = Net(ctx.net, ctx.seed, device, ctx.precision)
+    net.set_sgd(ctx.sgd)
+    shards = shard(ctx.train_data, 1, ctx.seed)
+    net.set_training_data(make_worker_iterator(shards, 0, ctx.batch, ctx.seed))
+    return net
+
+
+def run_serial(ctx: SchemeContext, iter_budget: int, eval_every: int,
+               observer: Optional[SchemeObserver] = None) -> RunTrace:
+    """schemes.hpp:154-193: serial SGD, evaluation every eval_every steps."""
+    ctx.validate()
+    if eval_every < 1:
+        raise ValueError("run_serial: eval_every must be >= 1")
+    if iter_budget < 0:
+        raise ValueError("run_serial: negative budget")
+    net = _make_serial_net(ctx, (ctx.devices or [0])[0])
+    trace = RunTrace("serial", 1, 0, ctx.batch, ctx.sgd.learning_rate, ctx.seed,
+                     ctx.target_accuracy, ctx.cost)
+    clock = SimClock()
+    iters = 0
+    while iters < iter_budget:
+        chunk = min(eval_every, iter_budget - iters)
+        if observer is not None and observer.on_step is not None:
+            for s in range(chunk):
+                net.train(1)
+                observer.on_step(iters + s + 1, net)
+        else:
+            net.train(chunk)
+        iters += chunk
+        clock.advance_to(serial_sim_time(iters, ctx.cost))
+        acc = evaluate(net, ctx)
+        trace.records.append(EvalRecord(iters, 0, 0, clock.elapsed(), acc))
+        if acc >= ctx.target_accuracy:
+            trace.outcome = TARGET_REACHED
+            return trace
+    trace.outcome = BUDGET_EXHAUSTED
+    return trace
+
+
+def run_naive(ctx: SchemeContext, workers: int, iter_budget: int, eval_every: int,
+              observer: Optional[SchemeObserver] = None) -> RunTrace:
+    """schemes.hpp:201-262 on B200s: every size-b batch is split into K parts; part k's
+    forward/backward runs on worker k (GPU k, or K nets on one GPU), the K part gradients
+    are averaged (weights_mean: NCCL allreduce across GPUs, or the ordered device kernel),
+    and every replica applies the same SGD update, so all replicas stay identical to the
+    reference's single net.  trace.round_ms holds the measured device time per step."""
+    ctx.validate()
+    if workers < 1:
+        raise ValueError("run_naive: need at least one worker")
+    if ctx.batch % workers != 0:
+        raise ValueError("run_naive: worker count must divide the batch size")
+    if eval_every < 1:
+        raise ValueError("run_naive: eval_every must be >= 1")
+    if iter_budget < 0:
+        raise ValueError("run_naive: negative budget")
+    devices = ctx.devices or [0]
+    if len(devices) > 1 and len(devices) != workers:
+        raise ValueError("run_naive: use one device, or one device per worker")
+    shards = shard(ctx.train_data, 1, ctx.seed)
+    nets = []
+    for k in range(workers):
+        n = Net(ctx.net, ctx.seed, devices[k % len(devices)], ctx.precision)
+        n.set_sgd(ctx.sgd)
+        # every part net walks the same batch stream (worker 0's iterator over one shard)
+        n.set_training_part(make_worker_iterator(shards, 0, ctx.batch, ctx.seed), k, workers)
+        nets.append(n)
+    comms = None
+    if len(devices) > 1:
+        from .comm import Communicator
+        comms = Communicator.create_all([n.ctx for n in nets])
+    trace = RunTrace("naive", workers, 0, ctx.batch, ctx.sgd.learning_rate, ctx.seed,
+                     ctx.target_accuracy, ctx.cost)
+    clock = SimClock()
+    iters = 0
+    while iters < iter_budget:
+        chunk = min(eval_every, iter_budget - iters)
+        nets[0].event_record(0)
+        for _ in range(chunk):
+            for n in nets:
+                n.grad_step()
+            if comms is None:
+                average_grads_local(nets)
+            else:
+                Communicator.average_grads(comms, nets, ctx.average_mode)
+            for n in nets:
+                n.apply_grads()
+            iters += 1
+            if observer is not None and observer.on_step is not None:
+                for n in nets:
+                    n.sync()
+                observer.on_step(iters, nets[0])
+        nets[0].event_record(1)
+        for n in nets:
+            n.sync()
+        trace.round_ms.append(nets[0].event_elapsed(0, 1) / chunk)
+        clock.advance_to(naive_sim_time(iters, ctx.cost, workers))
+        acc = evaluate_sharded(nets, ctx) if comms is not None else evaluate(nets[0], ctx)
+        trace.records.append(EvalRecord(iters, 0, iters, clock.elapsed(), acc))
+        if acc >= ctx.target_accuracy:
+            trace.outcome = TARGET_REACHED
+            return trace
+    trace.outcome = BUDGET_EXHAUSTED
+    return trace
+
+
 def run_sparknet(ctx: SchemeContext, workers: int, tau: int, round_budget: int,
                  warm_start_iters: int, threads: int = 1,
                  observer: Optional[SchemeObserver] = None, evaluate_rounds: bool = True
@@ -213,7 +349,12 @@ def run_sparknet(ctx: SchemeContext, workers: int, tau: int, round_budget: int,
             n.sync()
         master.set_weights_flat(nets[0].get_weights_flat())
         clock.advance_to(sparknet_sim_time(rnd, tau, warm_start_iters, ctx.cost))
-        acc = evaluate(master, ctx) if evaluate_rounds else 0.0
+        if not evaluate_rounds:
+            acc = 0.0
+        elif comms is not None:  # every worker holds the average: shard the eval batches
+            acc = evaluate_sharded(nets, ctx)
+        else:
+            acc = evaluate(master, ctx)
         trace.records.append(EvalRecord(warm_start_iters, tau * rnd, rnd, clock.elapsed(), acc))
         if observer is not None and observer.on_round is not None:
             observer.on_round(rnd, master.get_weights())

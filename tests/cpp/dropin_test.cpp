@@ -128,6 +128,22 @@ int main() {
       },
       "shard smaller than batch");
 
+  // run_naive (schemes.hpp:201-262): K=2 parts of each batch, 4 steps, eval every 2
+  std::vector<std::vector<double>> naive_steps;
+  SchemeObserver nobs;
+  nobs.on_step = [&](long, const Net& net) {
+    std::vector<double> flat;
+    for (const auto& e : net.get_weights())
+      for (const NDArray& t : e.second) flat.insert(flat.end(), t.values().begin(), t.values().end());
+    naive_steps.push_back(std::move(flat));
+  };
+  const RunTrace nt = run_naive(ctx, 2, 4, 2, &nobs);
+  expect(nt.scheme == "naive" && nt.records.size() == 2, "naive records");
+  expect(nt.records.back().sim_time == 4.0 * (2.0 / 2.0 + 10.0), "naive closed-form clock");
+  expect_throw<std::invalid_argument>([&] { run_naive(ctx, 3, 1, 1); }, "K must divide b");
+  const RunTrace st = run_serial(ctx, 4, 2);
+  expect(st.scheme == "serial" && st.records.size() == 2, "serial records");
+
   std::printf("{\"failures\": %d, \"warm_digest\": %llu, \"records\": [", failures,
               static_cast<unsigned long long>(tr.warm_digest));
   for (std::size_t i = 0; i < tr.records.size(); ++i)
@@ -139,6 +155,13 @@ int main() {
     std::printf("%s[", r ? ", " : "");
     for (std::size_t i = 0; i < rounds[r].size(); ++i)
       std::printf("%s%.9g", i ? ", " : "", rounds[r][i]);
+    std::printf("]");
+  }
+  std::printf("], \"naive_weights\": [");
+  for (std::size_t r = 0; r < naive_steps.size(); ++r) {
+    std::printf("%s[", r ? ", " : "");
+    for (std::size_t i = 0; i < naive_steps[r].size(); ++i)
+      std::printf("%s%.9g", i ? ", " : "", naive_steps[r][i]);
     std::printf("]");
   }
   std::printf("]}\n");

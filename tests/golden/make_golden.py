@@ -149,6 +149,14 @@ def main() -> None:
         g[key + "_records"] = np.array(recs, np.float64)
         g[key + "_digest"] = np.array([digest], np.uint64)
         g[key + "_weights"] = rw
+    # schemes.hpp run_naive: the batch split into K part gradients, averaged, applied
+    for (K, iters, every, mu, sub) in [(1, 4, 2, 0.0, 1.0), (2, 5, 2, 0.9, 1.0),
+                                       (5, 3, 3, 0.5, 0.7)]:
+        recs, sw = ref.run_naive(spec, train, evald, 10, 0.05, mu, 1, K, iters, every,
+                                 eval_steps=2, cost=(2.0, 10.0, sub), want_weights=True)
+        key = f"naive_{K}_{iters}_{every}_{int(mu * 10)}"
+        g[key + "_records"] = np.array(recs, np.float64)
+        g[key + "_weights"] = sw
     path = os.path.join(OUT, "reference_golden.npz")
     np.savez_compressed(path, **compact(g))
     print(f"wrote {path}: {len(g)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

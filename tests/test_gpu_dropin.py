@@ -34,3 +34,9 @@ def test_cpp_dropin_run_sparknet_matches_oracle(oracle_lib):
     # 8 SGD steps of fp32 vs fp64 from the same (fp32-representable) data
     for r in range(3):
         assert max_relative_deviation(np.array(res["round_weights"][r]), rw[r]) <= 1e-4
+    # run_naive through the drop-in vs the oracle's (reference-pinned) run_naive
+    _, sw = oracle_lib.run_naive(spec, train, evald, 10, 0.05, 0.9, 1, 2, 4, 2, eval_steps=2,
+                                 cost=(2.0, 10.0, 1.0), want_weights=True)
+    assert len(res["naive_weights"]) == 4
+    for s in range(4):
+        assert max_relative_deviation(np.array(res["naive_weights"][s]), sw[s]) <= 2e-4

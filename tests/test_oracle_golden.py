@@ -128,3 +128,17 @@ def test_oracle_matches_live_reference_cq_valid(oracle_lib, ref_lib):
     la, ga = a.backward(x, y)
     lb, gb = b.backward(x, y)
     assert la == lb and np.array_equal(ga, gb)
+
+
+@pytest.mark.parametrize("K,iters,every,mu,sub", [(1, 4, 2, 0.0, 1.0), (2, 5, 2, 0.9, 1.0),
+                                                  (5, 3, 3, 0.5, 0.7)])
+def test_run_naive_bit_exact(oracle_lib, golden, K, iters, every, mu, sub):
+    """run_naive (schemes.hpp:201-262): per-step weights and the evaluation records."""
+    train = oracle_lib.generate_synthetic(10, 1, 16, 16, 24, 2.0, 12345, 0)
+    evald = oracle_lib.generate_synthetic(10, 1, 16, 16, 6, 2.0, 12345, 1)
+    spec = ns.make_lenet_small(10, 1, 16, 16, 10)
+    recs, sw = oracle_lib.run_naive(spec, train, evald, 10, 0.05, mu, 1, K, iters, every,
+                                    eval_steps=2, cost=(2.0, 10.0, sub), want_weights=True)
+    key = f"naive_{K}_{iters}_{every}_{int(mu * 10)}"
+    assert equal(golden, key + "_records", np.array(recs, np.float64))
+    assert equal(golden, key + "_weights", sw)
