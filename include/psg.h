@@ -135,6 +135,15 @@ int psg_dataset_upload_f32(psg_ctx* ctx, const float* images, const int32_t* lab
 /* Host generator (bit-exact with the reference) followed by upload. */
 int psg_dataset_synthetic(psg_ctx* ctx, int classes, int c, int h, int w, size_t per_class,
                           double separation, uint64_t seed, uint64_t variant, psg_dataset** out);
+/* generate_synthetic's distribution generated on the device: class
+ * means bit-exact with data.hpp:121-131, within-class noise from a counter-based RNG
+ * (same law, not the reference's serial stream).  For AX/GN-sized datasets. */
+int psg_dataset_synthetic_device(psg_ctx* ctx, int classes, int c, int h, int w,
+                                 size_t per_class, double separation, uint64_t seed,
+                                 uint64_t variant, psg_dataset** out);
+/* Read rows [first, first+count) back as NCHW fp32 + labels (tests, inspection). */
+int psg_dataset_read_f32(const psg_dataset* ds, size_t first, size_t count, float* images_nchw,
+                         int32_t* labels);
 int psg_dataset_size(const psg_dataset* ds, size_t* n);
 int psg_dataset_destroy(psg_dataset* ds);
 

@@ -60,6 +60,11 @@ SIGNATURES = {
                                               ctypes.c_int, ctypes.c_int, _PP]),
     "psg_dataset_upload_f32": (ctypes.c_int, [_VP, _F, _I32, _SZ, ctypes.c_int, ctypes.c_int,
                                               ctypes.c_int, ctypes.c_int, _PP]),
+    "psg_dataset_synthetic_device": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int,
+                                                    ctypes.c_int, ctypes.c_int, _SZ,
+                                                    ctypes.c_double, ctypes.c_uint64,
+                                                    ctypes.c_uint64, _PP]),
+    "psg_dataset_read_f32": (ctypes.c_int, [_VP, _SZ, _SZ, _F, _I32]),
     "psg_dataset_synthetic": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, _SZ, ctypes.c_double, ctypes.c_uint64,
                                              ctypes.c_uint64, _PP]),

@@ -193,6 +193,68 @@ int psg_dataset_synthetic(psg_ctx* ctx, int classes, int c, int h, int w, size_t
   });
 }
 
+int psg_dataset_synthetic_device(psg_ctx* ctx, int classes, int c, int h, int w,
+                                 size_t per_class, double separation, uint64_t seed,
+                                 uint64_t variant, psg_dataset** out) {
+  return guarded([&] {
+    need(ctx, "dataset_synthetic_device");
+    if (per_class < 1) throw std::invalid_argument("synthetic: need at least one example per class");
+    if (c < 1 || h < 1 || w < 1) throw std::invalid_argument("dataset: images/labels mismatch");
+    const size_t dim = static_cast<size_t>(c) * h * w, n = static_cast<size_t>(classes) * per_class;
+    std::vector<double> means(dim * static_cast<size_t>(std::max(classes, 1)));
+    psg::synthetic_means(classes, c, h, w, separation, seed, means.data());
+    std::vector<float> meansf(means.begin(), means.end());
+    psg::DeviceGuard dg(ctx->device);
+    auto* ds = new psg_dataset;
+    ds->ctx = ctx;
+    ds->n = n;
+    ds->c = c;
+    ds->h = h;
+    ds->w = w;
+    ds->classes = classes;
+    ds->host_labels.resize(n);
+    for (size_t r = 0; r < n; ++r) ds->host_labels[r] = static_cast<int32_t>(r / per_class);
+    float* d_means = nullptr;
+    try {
+      PSG_CUDA(cudaMalloc(&ds->images, n * dim * sizeof(float)));
+      PSG_CUDA(cudaMalloc(&ds->labels, n * sizeof(int32_t)));
+      PSG_CUDA(cudaMalloc(&d_means, meansf.size() * sizeof(float)));
+      PSG_CUDA(cudaMemcpy(d_means, meansf.data(), meansf.size() * sizeof(float),
+                          cudaMemcpyHostToDevice));
+      psg::synthetic_rows_device(d_means, classes, c, h, w, per_class,
+                                 psg::synthetic_noise_seed(seed, variant), ds->images, ds->labels,
+                                 ctx->stream);
+      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(d_means);
+    } catch (...) {
+      cudaFree(d_means);
+      cudaFree(ds->images);
+      cudaFree(ds->labels);
+      delete ds;
+      throw;
+    }
+    *out = ds;
+  });
+}
+
+int psg_dataset_read_f32(const psg_dataset* ds, size_t first, size_t count, float* images_nchw,
+                         int32_t* labels) {
+  return guarded([&] {
+    need(ds, "dataset_read");
+    if (first + count > ds->n) throw std::invalid_argument("dataset_read: rows out of range");
+    const size_t dim = static_cast<size_t>(ds->c) * ds->h * ds->w;
+    std::vector<float> nhwc(count * dim);
+    psg::DeviceGuard dg(ds->ctx->device);
+    PSG_CUDA(cudaMemcpy(nhwc.data(), ds->images + first * dim, nhwc.size() * sizeof(float),
+                        cudaMemcpyDeviceToHost));
+    for (size_t r = 0; r < count; ++r)
+      for (int ch = 0; ch < ds->c; ++ch)
+        for (int p = 0; p < ds->h * ds->w; ++p)
+          images_nchw[(r * ds->c + ch) * ds->h * ds->w + p] = nhwc[(r * ds->h * ds->w + p) * ds->c + ch];
+    for (size_t r = 0; r < count; ++r) labels[r] = ds->host_labels[first + r];
+  });
+}
+
 int psg_dataset_size(const psg_dataset* ds, size_t* n) {
   return guarded([&] {
     need(ds, "dataset_size");

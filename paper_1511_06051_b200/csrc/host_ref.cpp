@@ -125,6 +125,31 @@ void smooth_pattern(Rng& rng, size_t channels, size_t height, size_t width, bool
 }  // namespace
 
 // data.hpp:111-155
+// The class means of generate_synthetic (data.hpp:121-131), bit-exact: means [classes][c*h*w].
+void synthetic_means(int classes, size_t c, size_t h, size_t w, double separation, uint64_t seed,
+                     double* means) {
+  if (classes < 1) throw std::invalid_argument("synthetic: need at least one class");
+  if (separation < 0.0) throw std::invalid_argument("synthetic: negative separation");
+  const size_t dim = c * h * w;
+  Rng mean_stream(derive_seed2(seed, kStreamData, 0x4d45414eULL));
+  std::vector<double> nodes;
+  const double radius = separation / std::sqrt(2.0);
+  for (int cls = 0; cls < classes; ++cls) {
+    double* mu = means + static_cast<size_t>(cls) * dim;
+    smooth_pattern(mean_stream, c, h, w, false, mu, nodes);
+    double norm2 = 0.0;
+    for (size_t d = 0; d < dim; ++d) norm2 += mu[d] * mu[d];
+    const double inv = norm2 > 0.0 ? radius / std::sqrt(norm2) : 0.0;
+    for (size_t d = 0; d < dim; ++d) mu[d] *= inv;
+  }
+}
+
+// Seed of the within-class noise of (seed, variant) (data.hpp:120).
+uint64_t synthetic_noise_seed(uint64_t seed, uint64_t variant) {
+  const uint64_t np[3] = {kStreamData, 0x4e4f495345ULL, variant};
+  return derive_seed(seed, np, 3);
+}
+
 void generate_synthetic(int classes, size_t c, size_t h, size_t w, size_t per_class,
                         double separation, uint64_t seed, uint64_t variant, double* images,
                         int32_t* labels) {

@@ -69,6 +69,14 @@ void epoch_order(const uint64_t* shard, size_t n, uint64_t stream_seed, uint64_t
 void generate_synthetic(int classes, size_t c, size_t h, size_t w, size_t per_class,
                         double separation, uint64_t seed, uint64_t variant, double* images,
                         int32_t* labels);
+void synthetic_means(int classes, size_t c, size_t h, size_t w, double separation, uint64_t seed,
+                     double* means);
+uint64_t synthetic_noise_seed(uint64_t seed, uint64_t variant);
+// Device generator with generate_synthetic's distribution (exact class means; counter-based
+// within-class noise): writes NHWC fp32 rows [n][h][w][c] and labels.
+void synthetic_rows_device(const float* d_means, int classes, int c, int h, int w,
+                           size_t per_class, uint64_t noise_seed, float* images, int32_t* labels,
+                           cudaStream_t s);
 
 // ------------------------------------------------------------- kernel API ---
 // NHWC everywhere.  Conv kernels are stored [F][kh][kw][cs_in/G]; a linear

@@ -92,6 +92,53 @@ class Dataset:
             pass
 
 
+class DeviceSyntheticDataset(Dataset):
+    """generate_synthetic's distribution generated directly in HBM:
+    bit-exact class means, counter-based within-class noise (same law, not the reference's
+    serial stream).  Host-side only the labels exist (row // per_class)."""
+
+    def __init__(self, num_classes: int, c: int, h: int, w: int, per_class: int,
+                 separation: float, seed: int, variant: int = 0, label_classes: int = 0):
+        if num_classes < 1 or per_class < 1:
+            raise ValueError("synthetic: need at least one class and example")
+        self.gen = (num_classes, c, h, w, per_class, float(separation), seed, variant)
+        self.shape = (num_classes * per_class, c, h, w)
+        self.labels = (np.arange(self.shape[0]) // per_class).astype(np.int32)
+        self.num_classes = max(num_classes, label_classes)
+        self._device = {}
+
+    @property
+    def images(self):
+        raise AttributeError("DeviceSyntheticDataset: pixels live on the device; use read()")
+
+    def channels(self) -> int:
+        return self.shape[1]
+
+    def height(self) -> int:
+        return self.shape[2]
+
+    def width(self) -> int:
+        return self.shape[3]
+
+    def handle(self, ctx) -> ctypes.c_void_p:
+        if ctx.device not in self._device:
+            out = ctypes.c_void_p()
+            k, c, h, w, per, sep, seed, var = self.gen
+            _lib.call("psg_dataset_synthetic_device", ctx.handle, k, c, h, w, per, sep, seed, var,
+                      ctypes.byref(out))
+            self._device[ctx.device] = (out, ctx)
+        return self._device[ctx.device][0]
+
+    def read(self, ctx, first: int, count: int):
+        """Rows [first, first+count) as NCHW fp32 + labels."""
+        n, c, h, w = self.shape
+        img = np.empty((count, c, h, w), np.float32)
+        lab = np.empty(count, np.int32)
+        _lib.call("psg_dataset_read_f32", self.handle(ctx), first, count,
+                  img.ctypes.data_as(_lib._F), lab.ctypes.data_as(_lib._I32))
+        return img, lab
+
+
 @dataclass
 class Shard:
     """data.hpp:44-50: a contiguous slice of a shuffled permutation."""

@@ -1,0 +1,48 @@
+"""Device-side data generation and ingestion: the device synthetic
+generator has generate_synthetic's law (data.hpp:111-155): exact labels, class means
+equal to the reference generator's, unit within-class pixel variance."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_synthetic_distribution_matches_reference_generator():
+    from paper_1511_06051_b200.data import DeviceSyntheticDataset, generate_synthetic
+    from paper_1511_06051_b200.model import Context
+    ctx = Context.get(0)
+    k, c, h, w, per = 3, 3, 12, 10, 600
+    dev = DeviceSyntheticDataset(k, c, h, w, per, 2.0, 12345, 0)
+    img, lab = dev.read(ctx, 0, k * per)
+    ref_img, ref_lab = generate_synthetic(k, c, h, w, per, 2.0, 12345, 0)
+    np.testing.assert_array_equal(lab, ref_lab)
+    for cls in range(k):
+        a = img[lab == cls].astype(np.float64)
+        b = ref_img[ref_lab == cls]
+        # both are per-pixel means of 600 unit-variance rows around the same class mean
+        assert np.abs(a.mean(0) - b.mean(0)).max() < 6 * np.sqrt(2.0 / per)
+        var = a.var(0)
+        assert abs(var.mean() - 1.0) < 0.05 and var.min() > 0.7 and var.max() < 1.35
+        # spatially smooth structure: neighbouring pixels correlate like the reference's
+        def corr(x):
+            d = x - x.mean(0)
+            return float((d[:, :, :, 1:] * d[:, :, :, :-1]).mean() / d.var())
+        assert abs(corr(a) - corr(b)) < 0.05
+    # variants are independent noise streams around the same means
+    v1, _ = DeviceSyntheticDataset(k, c, h, w, per, 2.0, 12345, 1).read(ctx, 0, k * per)
+    assert not np.array_equal(v1, img)
+    assert np.abs(v1[lab == 0].mean(0) - img[lab == 0].mean(0)).max() < 6 * np.sqrt(2.0 / per)
+
+
+def test_device_synthetic_dataset_trains():
+    """A device-generated dataset drives the HBM-resident shard stream."""
+    from paper_1511_06051_b200 import data, netspec as ns
+    from paper_1511_06051_b200.model import Net, SgdOptions
+    ds = data.DeviceSyntheticDataset(10, 1, 16, 16, 20, 2.0, 7, 0)
+    spec = ns.make_lenet_small(10, 1, 16, 16, 10)
+    net = Net(spec, 1)
+    net.set_sgd(SgdOptions(0.05, 0.9))
+    shards = data.shard(ds, 2, 3)
+    net.set_training_data(data.make_worker_iterator(shards, 1, 10, 3))
+    net.train(12)
+    assert np.isfinite(net.last_loss())
