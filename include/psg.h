@@ -141,6 +141,18 @@ int psg_dataset_synthetic(psg_ctx* ctx, int classes, int c, int h, int w, size_t
 int psg_dataset_synthetic_device(psg_ctx* ctx, int classes, int c, int h, int w,
                                  size_t per_class, double separation, uint64_t seed,
                                  uint64_t variant, psg_dataset** out);
+/* load_idx / load_csv (data.hpp:163-255): same format checks and messages (runtime
+ * errors).  psg_read_* parse on the host only (images may be NULL to query n / extents;
+ * pixels p/255 in fp64 rounded to fp32); psg_dataset_load_* put the data in HBM, IDX
+ * bytes converted on the device. */
+int psg_read_idx(const char* images_path, const char* labels_path, size_t* n, int* h, int* w,
+                 int* num_classes, float* images, int32_t* labels);
+int psg_read_csv(const char* path, int c, int h, int w, int num_classes, size_t* n, float* images,
+                 int32_t* labels);
+int psg_dataset_load_idx(psg_ctx* ctx, const char* images_path, const char* labels_path,
+                         psg_dataset** out);
+int psg_dataset_load_csv(psg_ctx* ctx, const char* path, int c, int h, int w, int num_classes,
+                         psg_dataset** out);
 /* Read rows [first, first+count) back as NCHW fp32 + labels (tests, inspection). */
 int psg_dataset_read_f32(const psg_dataset* ds, size_t first, size_t count, float* images_nchw,
                          int32_t* labels);

@@ -65,6 +65,14 @@ SIGNATURES = {
                                                     ctypes.c_double, ctypes.c_uint64,
                                                     ctypes.c_uint64, _PP]),
     "psg_dataset_read_f32": (ctypes.c_int, [_VP, _SZ, _SZ, _F, _I32]),
+    "psg_read_idx": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(_SZ),
+                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                    ctypes.POINTER(ctypes.c_int), _F, _I32]),
+    "psg_read_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, ctypes.POINTER(_SZ), _F, _I32]),
+    "psg_dataset_load_idx": (ctypes.c_int, [_VP, ctypes.c_char_p, ctypes.c_char_p, _PP]),
+    "psg_dataset_load_csv": (ctypes.c_int, [_VP, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int, _PP]),
     "psg_dataset_synthetic": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, _SZ, ctypes.c_double, ctypes.c_uint64,
                                              ctypes.c_uint64, _PP]),

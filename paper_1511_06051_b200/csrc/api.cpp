@@ -255,6 +255,82 @@ int psg_dataset_read_f32(const psg_dataset* ds, size_t first, size_t count, floa
   });
 }
 
+int psg_read_idx(const char* images_path, const char* labels_path, size_t* n, int* h, int* w,
+                 int* num_classes, float* images, int32_t* labels) {
+  return guarded([&] {
+    if (!images_path || !labels_path) throw std::invalid_argument("idx: null path");
+    const psg::IdxData d = psg::read_idx(images_path, labels_path);
+    *n = d.n;
+    *h = static_cast<int>(d.h);
+    *w = static_cast<int>(d.w);
+    *num_classes = d.classes;
+    if (images)
+      for (size_t i = 0; i < d.pixels.size(); ++i)
+        images[i] = static_cast<float>(static_cast<double>(d.pixels[i]) / 255.0);
+    if (labels) std::memcpy(labels, d.labels.data(), d.labels.size() * sizeof(int32_t));
+  });
+}
+
+int psg_read_csv(const char* path, int c, int h, int w, int num_classes, size_t* n, float* images,
+                 int32_t* labels) {
+  return guarded([&] {
+    if (!path) throw std::invalid_argument("csv: null path");
+    if (c < 1 || h < 1 || w < 1) throw std::invalid_argument("csv: bad extents");
+    const psg::CsvData d = psg::read_csv(path, c, h, w, num_classes);
+    *n = d.labels.size();
+    if (images) std::memcpy(images, d.images.data(), d.images.size() * sizeof(float));
+    if (labels) std::memcpy(labels, d.labels.data(), d.labels.size() * sizeof(int32_t));
+  });
+}
+
+int psg_dataset_load_idx(psg_ctx* ctx, const char* images_path, const char* labels_path,
+                         psg_dataset** out) {
+  return guarded([&] {
+    need(ctx, "dataset_load_idx");
+    if (!images_path || !labels_path) throw std::invalid_argument("idx: null path");
+    const psg::IdxData d = psg::read_idx(images_path, labels_path);
+    psg::DeviceGuard dg(ctx->device);
+    auto* ds = new psg_dataset;
+    ds->ctx = ctx;
+    ds->n = d.n;
+    ds->c = 1;
+    ds->h = static_cast<int>(d.h);
+    ds->w = static_cast<int>(d.w);
+    ds->classes = d.classes;
+    ds->host_labels = d.labels;
+    unsigned char* d_px = nullptr;
+    try {
+      PSG_CUDA(cudaMalloc(&ds->images, d.pixels.size() * sizeof(float)));
+      PSG_CUDA(cudaMalloc(&ds->labels, d.n * sizeof(int32_t)));
+      PSG_CUDA(cudaMalloc(&d_px, d.pixels.size()));
+      PSG_CUDA(cudaMemcpy(d_px, d.pixels.data(), d.pixels.size(), cudaMemcpyHostToDevice));
+      PSG_CUDA(cudaMemcpy(ds->labels, d.labels.data(), d.n * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+      psg::ingest_u8_to_f32(d_px, d.pixels.size(), ds->images, ctx->stream);
+      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(d_px);
+    } catch (...) {
+      cudaFree(d_px);
+      cudaFree(ds->images);
+      cudaFree(ds->labels);
+      delete ds;
+      throw;
+    }
+    *out = ds;
+  });
+}
+
+int psg_dataset_load_csv(psg_ctx* ctx, const char* path, int c, int h, int w, int num_classes,
+                         psg_dataset** out) {
+  return guarded([&] {
+    need(ctx, "dataset_load_csv");
+    if (!path) throw std::invalid_argument("csv: null path");
+    const psg::CsvData d = psg::read_csv(path, c, h, w, num_classes);
+    *out = upload(ctx, nullptr, d.images.data(), d.labels.data(), d.labels.size(), c, h, w,
+                  num_classes);
+  });
+}
+
 int psg_dataset_size(const psg_dataset* ds, size_t* n) {
   return guarded([&] {
     need(ds, "dataset_size");

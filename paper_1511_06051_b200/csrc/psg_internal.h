@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -72,6 +73,22 @@ void generate_synthetic(int classes, size_t c, size_t h, size_t w, size_t per_cl
 void synthetic_means(int classes, size_t c, size_t h, size_t w, double separation, uint64_t seed,
                      double* means);
 uint64_t synthetic_noise_seed(uint64_t seed, uint64_t variant);
+// load_idx / load_csv (data.hpp:163-255): parsed on the host with the reference's checks.
+struct IdxData {
+  uint32_t n = 0, h = 0, w = 0;
+  int classes = 0;
+  std::vector<unsigned char> pixels;  // [n][h][w]
+  std::vector<int32_t> labels;
+};
+IdxData read_idx(const std::string& images_path, const std::string& labels_path);
+struct CsvData {
+  std::vector<float> images;  // NCHW, p / 255 rounded to fp32
+  std::vector<int32_t> labels;
+};
+CsvData read_csv(const std::string& path, size_t channels, size_t height, size_t width,
+                 int num_classes);
+// images[i] = (float)(pixels[i] / 255.0) on the device (single channel: NCHW == NHWC).
+void ingest_u8_to_f32(const unsigned char* pixels, size_t n, float* images, cudaStream_t s);
 // Device generator with generate_synthetic's distribution (exact class means; counter-based
 // within-class noise): writes NHWC fp32 rows [n][h][w][c] and labels.
 void synthetic_rows_device(const float* d_means, int classes, int c, int h, int w,

@@ -1,4 +1,4 @@
-// Device-side generate_synthetic (data.hpp:111-155) for AX/GN-sized datasets (SURVEY.md
+// Device-side generate_synthetic (and the IDX byte ingestion) (data.hpp:111-155) for AX/GN-sized datasets (SURVEY.md
 // §8(f) #3): the reference's noise stream is one serial RNG over every pixel of every row,
 // so the device generator keeps the DISTRIBUTION, not the bits:
 //   * class means: computed on the host with the reference's mean stream (bit-exact);
@@ -67,7 +67,20 @@ __global__ void synthetic_rows_k(const float* __restrict__ means, int c, int h, 
   }
 }
 
+__global__ void u8_to_f32_k(const unsigned char* __restrict__ px, size_t n,
+                            float* __restrict__ out) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(static_cast<double>(px[i]) / 255.0);
+}
+
 }  // namespace
+
+void ingest_u8_to_f32(const unsigned char* pixels, size_t n, float* images, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148 * 16));
+  u8_to_f32_k<<<std::max(1u, blocks), 256, 0, s>>>(pixels, n, images);
+  PSG_CUDA(cudaGetLastError());
+}
 
 void synthetic_rows_device(const float* d_means, int classes, int c, int h, int w,
                            size_t per_class, uint64_t noise_seed, float* images, int32_t* labels,

@@ -92,6 +92,30 @@ class Dataset:
             pass
 
 
+def load_idx(images_path: str, labels_path: str) -> Dataset:
+    """data.hpp:173-208: IDX pair (u8 payload, big-endian header), pixels p/255."""
+    n, h, w, k = ctypes.c_size_t(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    ip, lp = images_path.encode(), labels_path.encode()
+    _lib.call("psg_read_idx", ip, lp, ctypes.byref(n), ctypes.byref(h), ctypes.byref(w),
+              ctypes.byref(k), None, None)
+    img = np.empty((n.value, 1, h.value, w.value), np.float32)
+    lab = np.empty(n.value, np.int32)
+    _lib.call("psg_read_idx", ip, lp, ctypes.byref(n), ctypes.byref(h), ctypes.byref(w),
+              ctypes.byref(k), img.ctypes.data_as(_lib._F), lab.ctypes.data_as(_lib._I32))
+    return Dataset(img, lab, k.value)
+
+
+def load_csv(path: str, c: int, h: int, w: int, num_classes: int) -> Dataset:
+    """data.hpp:213-255: header-less `label,p0,p1,...` rows, pixels p/255."""
+    n = ctypes.c_size_t()
+    _lib.call("psg_read_csv", path.encode(), c, h, w, num_classes, ctypes.byref(n), None, None)
+    img = np.empty((n.value, c, h, w), np.float32)
+    lab = np.empty(n.value, np.int32)
+    _lib.call("psg_read_csv", path.encode(), c, h, w, num_classes, ctypes.byref(n),
+              img.ctypes.data_as(_lib._F), lab.ctypes.data_as(_lib._I32))
+    return Dataset(img, lab, num_classes)
+
+
 class DeviceSyntheticDataset(Dataset):
     """generate_synthetic's distribution generated directly in HBM:
     bit-exact class means, counter-based within-class noise (same law, not the reference's

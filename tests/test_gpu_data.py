@@ -46,3 +46,29 @@ def test_device_synthetic_dataset_trains():
     net.set_training_data(data.make_worker_iterator(shards, 1, 10, 3))
     net.train(12)
     assert np.isfinite(net.last_loss())
+
+
+def test_idx_device_ingestion_matches_host_parse(tmp_path):
+    """psg_dataset_load_idx: raw bytes uploaded, rescaled on the device == load_idx."""
+    import ctypes
+    import struct
+    from paper_1511_06051_b200 import _lib, data
+    from paper_1511_06051_b200.model import Context
+    rng = np.random.default_rng(4)
+    px = rng.integers(0, 256, size=(33, 9, 7)).astype(np.uint8)
+    labels = rng.integers(0, 6, size=33).astype(np.uint8)
+    ip, lp = tmp_path / "i.idx", tmp_path / "l.idx"
+    ip.write_bytes(struct.pack(">IIII", 0x803, 33, 9, 7) + px.tobytes())
+    lp.write_bytes(struct.pack(">II", 0x801, 33) + labels.tobytes())
+    host = data.load_idx(str(ip), str(lp))
+    ctx = Context.get(0)
+    h = ctypes.c_void_p()
+    _lib.call("psg_dataset_load_idx", ctx.handle, str(ip).encode(), str(lp).encode(),
+              ctypes.byref(h))
+    img = np.empty((33, 1, 9, 7), np.float32)
+    lab = np.empty(33, np.int32)
+    _lib.call("psg_dataset_read_f32", h, 0, 33, img.ctypes.data_as(_lib._F),
+              lab.ctypes.data_as(_lib._I32))
+    _lib.lib().psg_dataset_destroy(h)
+    np.testing.assert_array_equal(img, host.images)
+    np.testing.assert_array_equal(lab, host.labels)
