@@ -404,6 +404,12 @@ class RefLib(_Lib):
         L.ref_weights_mean.argtypes = [ctypes.POINTER(_D), ctypes.c_int, ctypes.c_size_t, _D]
         L.ref_net_digest.restype = ctypes.c_uint64
         L.ref_net_digest.argtypes = [ctypes.c_void_p]
+        L.ref_format_double.restype = ctypes.c_int
+        L.ref_format_double.argtypes = [ctypes.c_double, ctypes.c_char_p, ctypes.c_int]
+        L.ref_naive_speedup.restype = ctypes.c_double
+        L.ref_naive_speedup.argtypes = [ctypes.c_double, ctypes.c_int, ctypes.c_double]
+        L.ref_sparknet_speedup.restype = ctypes.c_double
+        L.ref_sparknet_speedup.argtypes = [ctypes.c_double] * 5
         L.ref_run_naive.restype = ctypes.c_long
         L.ref_run_naive.argtypes = [ctypes.POINTER(SparknetArgs), ctypes.c_long, ctypes.c_long,
                                     ctypes.POINTER(Record), ctypes.c_long, _D]
@@ -452,6 +458,18 @@ class RefLib(_Lib):
         return _run_sparknet(self.lib.ref_run_sparknet, spec, train, evald, batch, lr, momentum,
                              seed, workers, tau, rounds, warm, threads, 0.0, target, eval_steps,
                              cost, want_weights, False, lambda: self.error(), P=P)
+
+    def format_double(self, v: float) -> str:
+        buf = ctypes.create_string_buffer(64)
+        if self.lib.ref_format_double(v, buf, 64) < 0:
+            raise RuntimeError("format_double: buffer")
+        return buf.value.decode()
+
+    def naive_speedup(self, c, k, s):
+        return self.lib.ref_naive_speedup(c, k, s)
+
+    def sparknet_speedup(self, n, c, tau, s, m):
+        return self.lib.ref_sparknet_speedup(n, c, tau, s, m)
 
     def run_naive(self, spec, train, evald, batch, lr, momentum, seed, workers, iters, eval_every,
                   target=2.0, eval_steps=1, cost=(1.0, 0.0, 1.0), want_weights=False):

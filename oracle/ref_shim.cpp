@@ -43,6 +43,8 @@
 #include "parasgd/model.hpp"
 #undef private
 #include "parasgd/schemes.hpp"
+#include "parasgd/analysis.hpp"
+#include "parasgd/csv.hpp"
 
 #include "oracle.h"
 
@@ -372,6 +374,20 @@ long ref_run_naive(const orc_sparknet_args* a, long iter_budget, long eval_every
     nrec = static_cast<long>(t.records.size());
   });
   return nrec;
+}
+
+// csv::format_double (csv.hpp:22-33) for the CSV-schema pins.
+int ref_format_double(double v, char* out, int cap) {
+  const std::string s = csv::format_double(v);
+  if (static_cast<int>(s.size()) + 1 > cap) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
+// The analysis.hpp closed forms.
+double ref_naive_speedup(double c, int k, double s) { return naive_speedup(c, k, s); }
+double ref_sparknet_speedup(double n, double c, double tau, double s, double m) {
+  return sparknet_speedup(n, c, tau, s, m);
 }
 
 }  // extern "C"

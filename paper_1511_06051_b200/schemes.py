@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import time
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -107,6 +108,9 @@ class RunTrace:
     records: List[EvalRecord] = field(default_factory=list)
     outcome: str = BUDGET_EXHAUSTED
     round_ms: List[float] = field(default_factory=list)
+    # measured wall clock per round (sparknet): tau local steps on every worker / average
+    compute_ms: List[float] = field(default_factory=list)
+    sync_ms: List[float] = field(default_factory=list)
 
     def reached(self) -> bool:
         return self.outcome == TARGET_REACHED
@@ -337,16 +341,22 @@ def run_sparknet(ctx: SchemeContext, workers: int, tau: int, round_budget: int,
     for n in nets:  # round-1 broadcast of the warm-start weights
         n.set_weights_flat(current)
     for rnd in range(1, round_budget + 1):
+        t0 = time.perf_counter()
         for n in nets:
             n.train(tau, sync=False)
         for n in nets:
             n.sync()
+        t1 = time.perf_counter()
         if comms is None:
             average_local(nets)
         else:
             Communicator.average(comms, nets, ctx.average_mode)
         for n in nets:
             n.sync()
+        t2 = time.perf_counter()
+        trace.compute_ms.append((t1 - t0) * 1e3)
+        trace.sync_ms.append((t2 - t1) * 1e3)
+        trace.round_ms.append((t2 - t0) * 1e3)
         master.set_weights_flat(nets[0].get_weights_flat())
         clock.advance_to(sparknet_sim_time(rnd, tau, warm_start_iters, ctx.cost))
         if not evaluate_rounds:

@@ -157,6 +157,13 @@ def main() -> None:
         key = f"naive_{K}_{iters}_{every}_{int(mu * 10)}"
         g[key + "_records"] = np.array(recs, np.float64)
         g[key + "_weights"] = sw
+    # csv.hpp format_double: the shortest round-tripping '%.*g' (trace / heatmap schemas)
+    rng = np.random.default_rng(77)
+    vals = np.concatenate([[0.0, 1.0, 0.1, 1.0 / 3.0, 100.0, 1e-5, 2.5e-300, 123456789.0,
+                            -0.75, 1e300, 0.9, 4.0 * (2.0 * 2.0 + 10.0)],
+                           rng.uniform(-10, 10, 40), 10.0 ** rng.uniform(-20, 20, 40)])
+    g["fmt_values"] = vals
+    g["fmt_strings"] = np.array("|".join(ref.format_double(float(v)) for v in vals))
     path = os.path.join(OUT, "reference_golden.npz")
     np.savez_compressed(path, **compact(g))
     print(f"wrote {path}: {len(g)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")
