@@ -87,8 +87,8 @@ class SpeedupPoint:
     rounds_to_target: int = -1
     reached: bool = False
     speedup: float = 0.0
-    measured_step_ms: float = 0.0   # wall clock: tau local steps / tau, mean over rounds
-    measured_sync_ms: float = 0.0   # wall clock: one average (S), mean over rounds
+    measured_step_ms: float = 0.0   # wall clock: tau local steps / tau (median round)
+    measured_sync_ms: float = 0.0   # wall clock: one average, S (median round)
 
 
 @dataclass
@@ -168,8 +168,8 @@ def _for_workers(ctx: SchemeContext, k: int) -> SchemeContext:
 def _measured(trace: RunTrace, tau: int) -> Tuple[float, float]:
     if not trace.compute_ms:
         return 0.0, 0.0
-    n = len(trace.compute_ms)
-    return sum(trace.compute_ms) / n / tau, sum(trace.sync_ms) / n
+    # median over rounds: the first round also pays the one-time CUDA-graph capture
+    return lower_median(trace.compute_ms) / tau, lower_median(trace.sync_ms)
 
 
 def sweep_heatmap(base: SchemeContext, spec: HeatmapSpec) -> HeatmapResult:

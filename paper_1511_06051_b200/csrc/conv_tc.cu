@@ -187,7 +187,8 @@ void finish_args(TcArgs& a, int kblk, int sms) {
     const int max_s = std::max(1, std::min(a.kblocks / 4, 64));
     for (int sp = 1; sp <= max_s; ++sp) {
       const long long waves = (tiles * sp + sms - 1) / sms;
-      const long long cost = waves * ((a.kblocks + sp - 1) / sp) + (sp > 1 ? 2 + sp / 4 : 0);
+      // a split adds a reduce launch (~4 us ~ 8 K blocks) and sp partial tiles
+      const long long cost = waves * ((a.kblocks + sp - 1) / sp) + (sp > 1 ? 8 + sp / 4 : 0);
       if (best < 0 || cost < best) {
         best = cost;
         splits = sp;

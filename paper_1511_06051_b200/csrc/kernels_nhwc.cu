@@ -55,53 +55,66 @@ __device__ __forceinline__ uint8_t& rcomp(uchar4& r, int j) {
 __device__ __forceinline__ uint8_t rcomp(const uint8_t& r, int) { return r; }
 __device__ __forceinline__ uint8_t& rcomp(uint8_t& r, int) { return r; }
 
+// One block per output row (b, oh) in forward / input row (b, h) in backward: the row's
+// window ranges are decoded once per block; threads walk (column, channel-vector) pairs
+// with incremental indices (no per-element division).
 template <typename V>
-__global__ void pool_fwd_k(PoolGeom g, const V* __restrict__ x, V* __restrict__ y,
-                           typename RouteOf<V>::T* __restrict__ route, int cv, uint32_t total) {
+__global__ void __launch_bounds__(256) pool_fwd_k(PoolGeom g, const V* __restrict__ x,
+                                                  V* __restrict__ y,
+                                                  typename RouteOf<V>::T* __restrict__ route,
+                                                  int cv) {
   constexpr int L = RouteOf<V>::n;
-  GRID_STRIDE32(i, total) {
-    const uint32_t c = i % cv, pix = i / cv;
-    const int ow = static_cast<int>(pix % g.OW), t = static_cast<int>(pix / g.OW);
-    const int oh = t % g.OH, b = t / g.OH;
-    const int hs0 = oh * g.sh - g.ph, ws0 = ow * g.sw - g.pw;
-    const int he0 = hs0 + g.kh, we0 = ws0 + g.kw;
-    const int hs = max(hs0, 0), ws = max(ws0, 0), he = min(he0, g.H), we = min(we0, g.W);
-    const V* xb = x + (static_cast<size_t>(b) * g.H * g.W) * cv + c;
+  const int oh = blockIdx.x % g.OH, b = blockIdx.x / g.OH;
+  const int hs0 = oh * g.sh - g.ph, he0 = hs0 + g.kh;
+  const int hs = max(hs0, 0), he = min(he0, g.H);
+  const V* xb = x + static_cast<size_t>(b) * g.H * g.W * cv;
+  const size_t ybase = static_cast<size_t>(blockIdx.x) * g.OW * cv;
+  const int total = g.OW * cv, step_c = blockDim.x % cv, step_w = blockDim.x / cv;
+  int c = threadIdx.x % cv, ow = threadIdx.x / cv;
+  for (int j = threadIdx.x; j < total; j += blockDim.x) {
+    const int ws0 = ow * g.sw - g.pw, we0 = ws0 + g.kw;
+    const int ws = max(ws0, 0), we = min(we0, g.W);
     if (g.method == PSG_POOL_AVE) {
       const float size = static_cast<float>((min(he0, g.H + g.ph) - hs0) *
                                             (min(we0, g.W + g.pw) - ws0));
       V acc;
 #pragma unroll
-      for (int j = 0; j < L; ++j) comp(acc, j) = 0.f;
+      for (int q = 0; q < L; ++q) comp(acc, q) = 0.f;
       for (int r = hs; r < he; ++r)
-        for (int s = ws; s < we; ++s) {
-          const V v = __ldg(xb + (r * g.W + s) * cv);
+        for (int t = ws; t < we; ++t) {
+          const V v = __ldg(xb + (r * g.W + t) * cv + c);
 #pragma unroll
-          for (int j = 0; j < L; ++j) comp(acc, j) += comp(v, j);
+          for (int q = 0; q < L; ++q) comp(acc, q) += comp(v, q);
         }
 #pragma unroll
-      for (int j = 0; j < L; ++j) comp(acc, j) = comp(acc, j) / size;
-      y[i] = acc;
+      for (int q = 0; q < L; ++q) comp(acc, q) = comp(acc, q) / size;
+      y[ybase + j] = acc;
     } else {
-      V best = __ldg(xb + (hs * g.W + ws) * cv);
+      V best = __ldg(xb + (hs * g.W + ws) * cv + c);
       typename RouteOf<V>::T arg;
       const uint8_t a0 = static_cast<uint8_t>((hs - hs0) * g.kw + (ws - ws0));
 #pragma unroll
-      for (int j = 0; j < L; ++j) rcomp(arg, j) = a0;
+      for (int q = 0; q < L; ++q) rcomp(arg, q) = a0;
       for (int r = hs; r < he; ++r) {
-        for (int s = ws; s < we; ++s) {
-          const V v = __ldg(xb + (r * g.W + s) * cv);
-          const uint8_t a = static_cast<uint8_t>((r - hs0) * g.kw + (s - ws0));
+        for (int t = ws; t < we; ++t) {
+          const V v = __ldg(xb + (r * g.W + t) * cv + c);
+          const uint8_t a = static_cast<uint8_t>((r - hs0) * g.kw + (t - ws0));
 #pragma unroll
-          for (int j = 0; j < L; ++j)
-            if (comp(v, j) > comp(best, j)) {
-              comp(best, j) = comp(v, j);
-              rcomp(arg, j) = a;
+          for (int q = 0; q < L; ++q)
+            if (comp(v, q) > comp(best, q)) {
+              comp(best, q) = comp(v, q);
+              rcomp(arg, q) = a;
             }
         }
       }
-      y[i] = best;
-      route[i] = arg;
+      y[ybase + j] = best;
+      route[ybase + j] = arg;
+    }
+    c += step_c;
+    ow += step_w;
+    if (c >= cv) {
+      c -= cv;
+      ++ow;
     }
   }
 }
@@ -109,23 +122,24 @@ __global__ void pool_fwd_k(PoolGeom g, const V* __restrict__ x, V* __restrict__ 
 // model.hpp:492-498 as a deterministic gather: each input sums, in ascending
 // output order, the dy of the covering windows that routed to it.
 template <typename V>
-__global__ void pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
-                           const typename RouteOf<V>::T* __restrict__ route, V* __restrict__ dx,
-                           int accumulate, int cv, uint32_t total) {
+__global__ void __launch_bounds__(256) pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
+                                                  const typename RouteOf<V>::T* __restrict__ route,
+                                                  V* __restrict__ dx, int accumulate, int cv) {
   constexpr int L = RouteOf<V>::n;
-  GRID_STRIDE32(i, total) {
-    const uint32_t c = i % cv, pix = i / cv;
-    const int w = static_cast<int>(pix % g.W), t = static_cast<int>(pix / g.W);
-    const int h = t % g.H, b = t / g.H;
-    // windows with oh*sh - ph <= h < oh*sh - ph + kh
-    const int ohl = max(0, (h + g.ph - g.kh + g.sh) / g.sh);
-    const int ohh = min(g.OH - 1, (h + g.ph) / g.sh);
+  const int h = blockIdx.x % g.H, b = blockIdx.x / g.H;
+  // windows with oh*sh - ph <= h < oh*sh - ph + kh
+  const int ohl = max(0, (h + g.ph - g.kh + g.sh) / g.sh);
+  const int ohh = min(g.OH - 1, (h + g.ph) / g.sh);
+  const uint32_t obase = static_cast<uint32_t>(b) * g.OH * g.OW;
+  const size_t xbase = static_cast<size_t>(blockIdx.x) * g.W * cv;
+  const int total = g.W * cv, step_c = blockDim.x % cv, step_w = blockDim.x / cv;
+  int c = threadIdx.x % cv, w = threadIdx.x / cv;
+  for (int j = threadIdx.x; j < total; j += blockDim.x) {
     const int owl = max(0, (w + g.pw - g.kw + g.sw) / g.sw);
     const int owh = min(g.OW - 1, (w + g.pw) / g.sw);
-    const uint32_t obase = static_cast<uint32_t>(b) * g.OH * g.OW;
     V acc;
 #pragma unroll
-    for (int j = 0; j < L; ++j) comp(acc, j) = 0.f;
+    for (int q = 0; q < L; ++q) comp(acc, q) = 0.f;
     for (int oh = ohl; oh <= ohh; ++oh) {
       const int hs0 = oh * g.sh - g.ph;
       if (h < hs0 || h >= hs0 + g.kh) continue;
@@ -138,22 +152,28 @@ __global__ void pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
           const float size = static_cast<float>((min(hs0 + g.kh, g.H + g.ph) - hs0) *
                                                 (min(ws0 + g.kw, g.W + g.pw) - ws0));
 #pragma unroll
-          for (int j = 0; j < L; ++j) comp(acc, j) += comp(d, j) / size;
+          for (int q = 0; q < L; ++q) comp(acc, q) += comp(d, q) / size;
         } else {
           const typename RouteOf<V>::T r = __ldg(route + o);
           const uint8_t want = static_cast<uint8_t>((h - hs0) * g.kw + (w - ws0));
 #pragma unroll
-          for (int j = 0; j < L; ++j)
-            if (rcomp(r, j) == want) comp(acc, j) += comp(d, j);
+          for (int q = 0; q < L; ++q)
+            if (rcomp(r, q) == want) comp(acc, q) += comp(d, q);
         }
       }
     }
     if (accumulate) {
-      const V o = dx[i];
+      const V o = dx[xbase + j];
 #pragma unroll
-      for (int j = 0; j < L; ++j) comp(acc, j) += comp(o, j);
+      for (int q = 0; q < L; ++q) comp(acc, q) += comp(o, q);
     }
-    dx[i] = acc;
+    dx[xbase + j] = acc;
+    c += step_c;
+    w += step_w;
+    if (c >= cv) {
+      c -= cv;
+      ++w;
+    }
   }
 }
 
@@ -161,20 +181,51 @@ __global__ void pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
 // Caffe LRN ACROSS_CHANNELS over NHWC.  A block stages a tile of whole pixels (a
 // contiguous run of tp*C floats) in shared memory with independent coalesced loads, then
 // every window sum reads shared memory; thread e's channel advances incrementally
-// (c += 256 % C) so there is no per-element division.  Window sums run in ascending
-// channel order; the scale is recomputed in backward instead of being stored.
+// (c += 256 % C) so there is no per-element division.  The window (SIZE taps, a template
+// parameter for the common size 5) is unrolled with predicated taps, summed in ascending
+// channel order; s^-beta uses the SFU exp2/log2 (relative error ~1e-6, inside the 1e-5
+// strict bar).  The scale is recomputed in backward instead of being stored.
 constexpr int kLrnThreads = 256;
 constexpr int kLrnTileElems = 2048;
 
 __device__ __forceinline__ float lrn_pow(float s, float beta) {  // s^-beta, s >= k > 0
-  return exp2f(-beta * log2f(s));
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(s));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-beta * l));
+  return r;
 }
 
+// sum over q in [lo_off, hi_off] of f(row[c + q]) for taps inside [0, C), ascending q.
+template <int SIZE, bool SQUARE>
+__device__ __forceinline__ float lrn_window(const float* row, int c, int C, int lo_off, int n) {
+  float acc = 0.f;
+  if (SIZE > 0) {
+#pragma unroll
+    for (int q = 0; q < SIZE; ++q) {
+      const int ch = c + lo_off + q;
+      if (ch >= 0 && ch < C) {
+        const float v = row[ch];
+        acc += SQUARE ? v * v : v;
+      }
+    }
+  } else {
+    for (int q = 0; q < n; ++q) {
+      const int ch = c + lo_off + q;
+      if (ch >= 0 && ch < C) {
+        const float v = row[ch];
+        acc += SQUARE ? v * v : v;
+      }
+    }
+  }
+  return acc;
+}
+
+template <int SIZE>
 __global__ void __launch_bounds__(kLrnThreads) lrn_fwd_k(LrnGeom g, const float* __restrict__ x,
                                                          float* __restrict__ y, int tp) {
   extern __shared__ float sm[];
   float* sx = sm;
-  const int pre = (g.size - 1) / 2, post = g.size - pre - 1, C = g.C;
+  const int pre = (g.size - 1) / 2, C = g.C;
   const float a = g.alpha / g.size;
   const int ntiles = (g.pixels + tp - 1) / tp, step = kLrnThreads % C;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -185,10 +236,7 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_fwd_k(LrnGeom g, const float*
     __syncthreads();
     int c = threadIdx.x % C;
     for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
-      const int lo = max(0, c - pre), hi = min(C - 1, c + post);
-      const float* row = sx + (e - c);
-      float acc = 0.f;
-      for (int q = lo; q <= hi; ++q) acc += row[q] * row[q];
+      const float acc = lrn_window<SIZE, true>(sx + (e - c), c, C, -pre, g.size);
       y[e0 + e] = sx[e] * lrn_pow(g.k + a * acc, g.beta);
       c += step;
       if (c >= C) c -= C;
@@ -197,6 +245,7 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_fwd_k(LrnGeom g, const float*
   }
 }
 
+template <int SIZE>
 __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float* __restrict__ x,
                                                          const float* __restrict__ dy,
                                                          float* __restrict__ dx, int accumulate,
@@ -221,14 +270,10 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float*
     __syncthreads();
     int c = threadIdx.x % C;
     for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
-      const int lo = max(0, c - pre), hi = min(C - 1, c + post);
-      const float* row = sx + (e - c);
-      float acc = 0.f;
-      for (int q = lo; q <= hi; ++q) acc += row[q] * row[q];
-      const float s = g.k + a * acc;
+      const float s = g.k + a * lrn_window<SIZE, true>(sx + (e - c), c, C, -pre, g.size);
       const float sp = lrn_pow(s, g.beta);
       ssp[e] = sp;
-      st[e] = sd[e] * sx[e] * sp / s;
+      st[e] = sd[e] * sx[e] * sp * __frcp_rn(s);
       c += step;
       if (c >= C) c -= C;
     }
@@ -236,10 +281,7 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float*
     c = threadIdx.x % C;
     for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
       // channels q whose window contains c: q in [c - post, c + pre]
-      const int lo = max(0, c - post), hi = min(C - 1, c + pre);
-      const float* row = st + (e - c);
-      float acc = 0.f;
-      for (int q = lo; q <= hi; ++q) acc += row[q];
+      const float acc = lrn_window<SIZE, false>(st + (e - c), c, C, -post, g.size);
       const float v = sd[e] * ssp[e] - ratio * sx[e] * acc;
       dx[e0 + e] = accumulate ? dx[e0 + e] + v : v;
       c += step;
@@ -332,26 +374,28 @@ __global__ void stage_nchw_k(const float* __restrict__ src, int C, int H, int W,
 }  // namespace
 
 void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaStream_t s) {
-  const uint32_t n = checked32(static_cast<size_t>(g.n) * g.OH * g.OW * g.C, "pool");
+  checked32(static_cast<size_t>(g.n) * g.OH * g.OW * g.C, "pool");
   checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
+  const unsigned rows = static_cast<unsigned>(g.n) * g.OH;
   if (g.C % 4 == 0)
-    pool_fwd_k<float4><<<grid_for(n / 4), 256, 0, s>>>(
-        g, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
-        reinterpret_cast<uchar4*>(route), g.C / 4, n / 4);
+    pool_fwd_k<float4><<<rows, 256, 0, s>>>(g, reinterpret_cast<const float4*>(x),
+                                            reinterpret_cast<float4*>(y),
+                                            reinterpret_cast<uchar4*>(route), g.C / 4);
   else
-    pool_fwd_k<float><<<grid_for(n), 256, 0, s>>>(g, x, y, route, g.C, n);
+    pool_fwd_k<float><<<rows, 256, 0, s>>>(g, x, y, route, g.C);
   PSG_CUDA(cudaGetLastError());
 }
 
 void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
               bool accumulate, cudaStream_t s) {
-  const uint32_t n = checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
+  checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
+  const unsigned rows = static_cast<unsigned>(g.n) * g.H;
   if (g.C % 4 == 0)
-    pool_bwd_k<float4><<<grid_for(n / 4), 256, 0, s>>>(
-        g, reinterpret_cast<const float4*>(dy), reinterpret_cast<const uchar4*>(route),
-        reinterpret_cast<float4*>(dx), accumulate, g.C / 4, n / 4);
+    pool_bwd_k<float4><<<rows, 256, 0, s>>>(g, reinterpret_cast<const float4*>(dy),
+                                            reinterpret_cast<const uchar4*>(route),
+                                            reinterpret_cast<float4*>(dx), accumulate, g.C / 4);
   else
-    pool_bwd_k<float><<<grid_for(n), 256, 0, s>>>(g, dy, route, dx, accumulate, g.C, n);
+    pool_bwd_k<float><<<rows, 256, 0, s>>>(g, dy, route, dx, accumulate, g.C);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -362,14 +406,20 @@ int lrn_blocks(const LrnGeom& g, int tp) {
 }
 }  // namespace
 
+template <class K>
+void lrn_launch(K kernel, size_t smem) {
+  if (smem > 48 * 1024)
+    PSG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+}
+
 void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s) {
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
   const int tp = lrn_tile_pixels(g);
   const size_t smem = static_cast<size_t>(tp) * g.C * sizeof(float);
-  if (smem > 48 * 1024)
-    PSG_CUDA(cudaFuncSetAttribute(lrn_fwd_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-  lrn_fwd_k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, y, tp);
+  auto k = g.size == 5 ? lrn_fwd_k<5> : lrn_fwd_k<0>;
+  lrn_launch(k, smem);
+  k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, y, tp);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -378,10 +428,9 @@ void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool 
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
   const int tp = lrn_tile_pixels(g);
   const size_t smem = 4 * static_cast<size_t>(tp) * g.C * sizeof(float);
-  if (smem > 48 * 1024)
-    PSG_CUDA(cudaFuncSetAttribute(lrn_bwd_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-  lrn_bwd_k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, dy, dx, accumulate, tp);
+  auto k = g.size == 5 ? lrn_bwd_k<5> : lrn_bwd_k<0>;
+  lrn_launch(k, smem);
+  k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, dy, dx, accumulate, tp);
   PSG_CUDA(cudaGetLastError());
 }
 

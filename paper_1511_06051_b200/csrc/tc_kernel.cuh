@@ -20,7 +20,11 @@ enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3 };
 enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3, B_COL_MN = 4, B_TAPS_MN = 5 };
 enum RowMap { ROW_RECT = 0, ROW_LINEAR = 1 };
 
-constexpr int kThreads = 256;
+// Warp roles: 0..3 TMA producers (K block it -> warp it % 4), 4 MMA issuer, 5 TMEM
+// allocator, 8..11 epilogue (warp % 4 selects the TMEM lane quarter), 6-7 idle.
+constexpr int kProducers = 4;
+constexpr int kMmaWarp = 4, kAllocWarp = 5, kEpiWarp0 = 8;
+constexpr int kThreads = 384;
 constexpr int kTileM = 128;
 constexpr int kAccCols = 256;                 // one accumulator: 128 lanes x 256 fp32
 constexpr int kStagePad = 33;                 // epilogue transpose row pitch (floats)
@@ -65,7 +69,7 @@ struct TcArgs {
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
 struct TapChunks {
-  int dx[8], dy[8], c[8];
+  int dx[1], dy[1], c[1];
 };
 
 struct Tile {
@@ -85,15 +89,13 @@ __device__ __forceinline__ Tile decode_tile(const TcArgs& p, long long t) {
   return r;
 }
 
-__device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, TapChunks& k) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int vc = t.n * p.n_tile + 32 * j;
-    const int tap = min(vc / p.cpt, p.ntaps - 1);  // chunks past the last tap: harmless reloads
-    k.dy[j] = tap / p.kw - p.ph;
-    k.dx[j] = tap % p.kw - p.pw;
-    k.c[j] = p.b_n_g * t.g + vc % p.cpt;
-  }
+// B_TAPS_MN: tap shift and channel offset of this lane's 32-column chunk (slot 0).
+__device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, int j, TapChunks& k) {
+  const int vc = t.n * p.n_tile + 32 * max(j, 0);
+  const int tap = min(vc / p.cpt, p.ntaps - 1);  // chunks past the last tap: harmless reloads
+  k.dy[0] = tap / p.kw - p.ph;
+  k.dx[0] = tap % p.kw - p.pw;
+  k.c[0] = p.b_n_g * t.g + vc % p.cpt;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -145,70 +147,71 @@ struct KCursor {
   }
 };
 
-// A operand of one K block (producer thread A).
+// Operand loads of one K block.  A TMA issue occupies its thread for a few hundred
+// cycles whatever the box size (tools/tma_bench.cu: one issuing thread tops out near
+// 25-35 B/clk/SM with 16 KB boxes and ~7-12 with 4 KB boxes; 4-8 issuing warps reach
+// ~45).  So boxes stay as large as the layout allows (a whole K-major operand tile is one
+// box), the 32-float chunks of MN-major operands are issued by consecutive lanes in
+// parallel (lane l issues chunk l - base), and consecutive K blocks are issued by
+// different producer warps (kProducers of them, round robin).
 template <int KBLK>
 __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, const Tile& t,
                                        const KCursor& c, int rb, int oh0, int ow0, uint32_t sa,
-                                       uint32_t bar) {
+                                       uint32_t bar, int j) {
   switch (p.a_mode) {
     case A_RECT_K:
-      tc::tma_load_4d(sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0 + p.sign * (c.tv - p.pw),
-                      oh0 + p.sign * (c.tu - p.ph), rb);
+      if (j == 0)
+        tc::tma_load_4d(sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0 + p.sign * (c.tv - p.pw),
+                        oh0 + p.sign * (c.tu - p.ph), rb);
       break;
     case A_2D_K:
-      tc::tma_load_2d(sa, map, bar, c.kb * KBLK, t.m * kTileM);
+      if (j == 0) tc::tma_load_2d(sa, map, bar, c.kb * KBLK, t.m * kTileM);
       break;
     case A_RECT_MN:
-#pragma unroll
-      for (int j = 0; j < kTileM / 32; ++j)
-        if (j < p.a_chunks)
-          tc::tma_load_4d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
+      if (j >= 0 && j < p.a_chunks)
+        tc::tma_load_4d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
                         c.kow, c.koh, c.kbi);
       break;
     case A_2D_MN:
-#pragma unroll
-      for (int j = 0; j < kTileM / 32; ++j)
-        if (j < p.a_chunks)
-          tc::tma_load_2d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
+      if (j >= 0 && j < p.a_chunks)
+        tc::tma_load_2d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
                         c.kb * KBLK);
       break;
   }
 }
 
-// B operand of one K block (producer thread B).
 template <int KBLK>
 __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, const Tile& t,
                                        const KCursor& c, int u, int v, const TapChunks& tk,
-                                       uint32_t sb, uint32_t bar) {
+                                       uint32_t sb, uint32_t bar, int j) {
   const int nch = (p.n_tile + 31) / 32;
+  if (j < 0) return;
   switch (p.b_mode) {
     case B_2D_K:
-      tc::tma_load_2d(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + t.n * p.n_tile);
+      if (j == 0) tc::tma_load_2d(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + t.n * p.n_tile);
       break;
     case B_WT_MN:
-      for (int j = 0; j < nch; ++j)
+      if (j < nch)
         tc::tma_load_3d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.t1,
                         p.b_r_g * t.g + c.t0 * KBLK);
       break;
     case B_RECT_MN:
-      for (int j = 0; j < nch; ++j)
+      if (j < nch)
         tc::tma_load_4d(sb + j * KBLK * 128, map, bar, p.b_n_g * t.g + t.n * p.n_tile + 32 * j,
                         c.kow + v - p.pw, c.koh + u - p.ph, c.kbi);
       break;
     case B_2D_MN:
-      for (int j = 0; j < nch; ++j)
+      if (j < nch)
         tc::tma_load_2d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.kb * KBLK);
       break;
     case B_COL_MN:  // im2col matrix [G][rows][Kp]: group as the outer coordinate
-      for (int j = 0; j < nch; ++j)
+      if (j < nch)
         tc::tma_load_3d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.kb * KBLK, t.g);
       break;
     case B_TAPS_MN:  // X shifted per 32-column chunk by that chunk's tap
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nch)
-          tc::tma_load_4d(sb + j * KBLK * 128, map, bar, tk.c[j], c.kow + tk.dx[j],
-                          c.koh + tk.dy[j], c.kbi);
+      if (j < nch)
+        tc::tma_load_4d(sb + j * KBLK * 128, map, bar, tk.c[0], c.kow + tk.dx[0],
+                        c.koh + tk.dy[0], c.kbi);
       break;
   }
 }
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&map_a);
     tc::tma_prefetch(&map_b);
     for (int s = 0; s < p.stages; ++s) {
-      tc::mbar_init(tc::smem_u32(&full_bar[s]), 2);  // A and B producers
+      tc::mbar_init(tc::smem_u32(&full_bar[s]), 1);  // the stage's producer warp, lane 0
       tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -239,16 +242,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tc::smem_u32(&tmem_base_sh), 2 * kAccCols);
+  if (warp == kAllocWarp) tc::tmem_alloc(tc::smem_u32(&tmem_base_sh), 2 * kAccCols);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base_sh;
 
-  if ((warp == 0 || warp == 3) && lane == 0) {
-    // ----------------------------------------- producers: warp 0 -> A, warp 3 -> B
-    const bool is_a = warp == 0;
-    const uint32_t bytes = is_a ? p.a_tx : p.stage_bytes - p.a_bytes;
+  if (warp < kProducers) {
+    // ------------------------------------------------ producers: K block it -> warp it % 4
+    // lane 0 waits for the slot and posts the stage's bytes; lanes 0..15 issue A
+    // (chunk = lane), lanes 16..31 issue B (chunk = lane - 16)
+    const uint32_t bytes = p.a_tx + (p.stage_bytes - p.a_bytes);
+    const int ja = lane < 16 ? lane : -1, jb = lane >= 16 ? lane - 16 : -1;
     uint32_t it = 0;
     for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x) {
       const Tile t = decode_tile(p, tt);
@@ -263,22 +268,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int u = t.tap / p.kw, v = t.tap % p.kw;
       TapChunks tk{};
-      if (!is_a && p.b_mode == B_TAPS_MN) tap_chunks(p, t, tk);
+      if (p.b_mode == B_TAPS_MN) tap_chunks(p, t, jb, tk);
       KCursor c;
       c.init(p, kb0);
       for (int kb = kb0; kb < kb1; ++kb, ++it, c.next(p)) {
+        if (static_cast<int>(it % kProducers) != warp) continue;
         const uint32_t s = it % p.stages;
-        tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ((it / p.stages) & 1) ^ 1);
         const uint32_t bar = tc::smem_u32(&full_bar[s]);
-        tc::mbar_arrive_expect_tx(bar, bytes);
+        if (lane == 0) {
+          tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ((it / p.stages) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(bar, bytes);
+        }
+        __syncwarp();
         const uint32_t sa = tc::smem_u32(smem + s * p.stage_bytes);
-        if (is_a)
-          load_a<KBLK>(p, &map_a, t, c, rb, oh0, ow0, sa, bar);
-        else
-          load_b<KBLK>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar);
+        load_a<KBLK>(p, &map_a, t, c, rb, oh0, ow0, sa, bar, ja);
+        load_b<KBLK>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, jb);
       }
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == kMmaWarp && lane == 0) {
     // ------------------------------------------------------------ MMA issue
     const bool a_mn = p.a_mode == A_RECT_MN || p.a_mode == A_2D_MN;
     const bool b_mn = p.b_mode != B_2D_K;
@@ -312,9 +319,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc::mma_commit(tc::smem_u32(&tfull_bar[acc]));
     }
-  } else if (warp >= 4) {
+  } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;
+    const int ew = warp - kEpiWarp0;
     float* stg = epi + ew * 32 * kStagePad;
     uint32_t local = 0;
     for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x, ++local) {
@@ -384,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == kAllocWarp) {
     tc::fence_after_sync();
     tc::tmem_dealloc(tmem, 2 * kAccCols);
   }
