@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -177,6 +178,13 @@ void finish_args(TcArgs& a, int kblk, int sms) {
   a.a_tx = a_mn ? a.a_chunks * 32 * kblk * 4 : a.a_bytes;
   a.stage_bytes = a.a_bytes + nb * kblk * 4;
   a.stages = std::min(8, (225 * 1024 - kEpiBytes) / a.stage_bytes);
+  static const int producers = [] {
+    const char* e = std::getenv("PSG_TC_PRODUCERS");
+    const int v = e ? std::atoi(e) : kMaxProducers;
+    return std::max(1, std::min(kMaxProducers, v));
+  }();
+  // a producer may only run one ring ahead of the slot it refills (parity waits): <= stages
+  a.producers = std::min(producers, a.stages);
   const long long tiles = static_cast<long long>(a.m_tiles) * a.n_tiles * a.G * a.taps;
   // Split K so that the persistent grid's waves are full: minimise
   // waves(tiles * s) * ceil(kblocks / s) (+ a small charge per extra split for the partials

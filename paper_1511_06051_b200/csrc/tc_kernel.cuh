@@ -20,9 +20,9 @@ enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3 };
 enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3, B_COL_MN = 4, B_TAPS_MN = 5 };
 enum RowMap { ROW_RECT = 0, ROW_LINEAR = 1 };
 
-// Warp roles: 0..3 TMA producers (K block it -> warp it % 4), 4 MMA issuer, 5 TMEM
-// allocator, 8..11 epilogue (warp % 4 selects the TMEM lane quarter), 6-7 idle.
-constexpr int kProducers = 4;
+// Warp roles: 0..3 and 6..7 TMA producers (K block it -> producer it % p.producers),
+// 4 MMA issuer, 5 TMEM allocator, 8..11 epilogue (warp % 4 selects the TMEM lane quarter).
+constexpr int kMaxProducers = 6;
 constexpr int kMmaWarp = 4, kAllocWarp = 5, kEpiWarp0 = 8;
 constexpr int kThreads = 384;
 constexpr int kTileM = 128;
@@ -35,6 +35,7 @@ struct TcArgs {
   int n_tile;             // UMMA N (multiple of 16, <= 256)
   int stage_bytes, a_bytes, stages;
   int a_chunks;           // MN-major A: 32-row chunks actually loaded (M tail skipped)
+  int producers;          // TMA producer warps (<= kMaxProducers)
   int a_tx;               // A bytes landing per stage (expect_tx)
   int m_tiles, n_tiles;   // per (group, tap)
   int G, taps;            // group / tap index g * taps + tap
@@ -248,8 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base_sh;
 
-  if (warp < kProducers) {
-    // ------------------------------------------------ producers: K block it -> warp it % 4
+  const int pw = warp < 4 ? warp : (warp == 6 || warp == 7 ? warp - 2 : -1);
+  if (pw >= 0 && pw < p.producers) {
+    // ------------------------------------- producers: K block it -> producer it % producers
     // lane 0 waits for the slot and posts the stage's bytes; lanes 0..15 issue A
     // (chunk = lane), lanes 16..31 issue B (chunk = lane - 16)
     const uint32_t bytes = p.a_tx + (p.stage_bytes - p.a_bytes);
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       KCursor c;
       c.init(p, kb0);
       for (int kb = kb0; kb < kb1; ++kb, ++it, c.next(p)) {
-        if (static_cast<int>(it % kProducers) != warp) continue;
+        if (static_cast<int>(it % p.producers) != pw) continue;
         const uint32_t s = it % p.stages;
         const uint32_t bar = tc::smem_u32(&full_bar[s]);
         if (lane == 0) {
