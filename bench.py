@@ -6,7 +6,7 @@ replay of the worker's CUDA graph over its HBM-resident shard) followed by the K
 average (NCCL over NVLink for K > 1).  images/sec = K * tau * b / round time, whole job,
 device-timed with CUDA events on the worker stream, max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cifar10_quick|alexnet|cq-valid]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cifar10_quick|alexnet|googlenet|cq-valid]
                   [--tau T] [--precision fp32|tf32] [--average fast|ordered]
   python bench.py --impl reference ...   # the reference's CPU path (oracle port) on host cores
 Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
@@ -32,6 +32,7 @@ WORKLOADS = {
     "cifar10_quick": ("make_cifar10_quick", 100, (3, 32, 32), 5000, 0.001, 0.9, 0.004),
     "cq-valid": ("make_cq_valid", 100, (3, 32, 32), 5000, 0.001, 0.9, 0.0),
     "alexnet": ("make_alexnet", 256, (3, 227, 227), None, 0.01, 0.9, 0.0005),
+    "googlenet": ("make_googlenet", 32, (3, 224, 224), None, 0.01, 0.9, 0.0002),
 }
 
 
@@ -135,15 +136,21 @@ def make_spec(workload):
 
 
 def build_dataset(workload, K):
-    """Synthetic data of the workload's shape from the reference generator (data.hpp:111-155),
-    data.seed 12345, separation 2, 10 classes; AlexNet uses 1000 classes' label range."""
-    from paper_1511_06051_b200.data import Dataset, generate_synthetic
+    """Synthetic data of the workload's shape, data.seed 12345, separation 2, 10 classes:
+    the reference generator (data.hpp:111-155) for the 32x32 nets; for the ImageNet-shaped
+    nets (AlexNet, GoogLeNet; label range 1000 classes) the device generator with the same
+    law (SURVEY.md §8(f) #3), enough rows for K shards of 2 batches each."""
+    from paper_1511_06051_b200.data import Dataset, DeviceSyntheticDataset, generate_synthetic
     _, b, (c, h, w), per_class, *_ = WORKLOADS[workload]
-    if per_class is None:  # AlexNet: enough rows for K shards of 2 batches each
+    if per_class is None:
         per_class = max(1, (2 * b * K + 9) // 10)
+        return DeviceSyntheticDataset(10, c, h, w, per_class, 2.0, 12345, 0, label_classes=1000)
     img, lab = generate_synthetic(10, c, h, w, per_class, 2.0, 12345, 0)
-    classes = 1000 if workload == "alexnet" else 10
-    return Dataset(img.astype(np.float32), lab, classes)
+    return Dataset(img.astype(np.float32), lab, 10)
+
+
+# CPU-baseline sample batch per worker: ~10-30 s of fp64 work on the box's host cores
+CPU_SAMPLE_BATCH = {"cifar10_quick": None, "cq-valid": None, "alexnet": 16, "googlenet": 8}
 
 
 def cpu_baseline(workload, b, threads, steps=1):
@@ -152,7 +159,9 @@ def cpu_baseline(workload, b, threads, steps=1):
     reference (no pad / ave pool / LRN), so the C restatement is timed (kind "port");
     cq-valid runs the reference itself (kind "reference")."""
     from oracle import pyoracle
-    spec, _ = make_spec(workload)
+    b = CPU_SAMPLE_BATCH.get(workload) or b
+    spec = getattr(__import__("paper_1511_06051_b200.netspec", fromlist=["x"]),
+                   WORKLOADS[workload][0])(b)
     _, _, (c, h, w), *_ = WORKLOADS[workload]
     per_class = max(1, (b * threads + 9) // 10)
     orc = pyoracle.OracleLib()
@@ -278,7 +287,11 @@ def main():
     host_it = pdata.make_worker_iterator(shards, rank, b, 7)
     for s in range(args.tau):
         idx = host_it.next_indices().astype(np.int64)
-        pin_img.array[s] = ds.images[idx]
+        if isinstance(ds, pdata.DeviceSyntheticDataset):  # pixels only in HBM: fetch rows once
+            for i, r in enumerate(idx):
+                pin_img.array[s, i] = ds.read(net.ctx, int(r), 1)[0][0]
+        else:
+            pin_img.array[s] = ds.images[idx]
         pin_lab.array[s] = ds.labels[idx]
     net.train_host(pin_img.array, pin_lab.array)  # warm-up: capture the host-fed graph
     average()
@@ -332,7 +345,7 @@ def main():
                        "K": K, "tau": args.tau, "average": args.average,
                        "parallelism": f"sparknet-dp{K}",
                        "l2": "inputs larger than L2 (HBM-resident dataset "
-                             f"{ds.images.nbytes / 1e6:.0f} MB, random per-step gather)"},
+                             f"{ds.size() * c * h * w * 4 / 1e6:.0f} MB, random per-step gather)"},
             "e2e": {"value": e2e_value, "unit": "images/sec",
                     "h2d_bytes_per_step": args.tau * b * (chw * 4 + 4),
                     "d2h_bytes_per_step": args.tau * 8},

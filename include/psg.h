@@ -53,7 +53,7 @@ enum psg_layer_kind {
   PSG_LAYER_SOFTMAX_LOSS = 6,
   PSG_LAYER_LRN = 7,      /* extension: Caffe LRN ACROSS_CHANNELS */
   PSG_LAYER_DROPOUT = 8,  /* extension: Caffe dropout (counter-hash mask) */
-  PSG_LAYER_CONCAT = 9    /* extension: channel concat (reserved) */
+  PSG_LAYER_CONCAT = 9    /* extension: Caffe Concat along channels (GoogLeNet inception) */
 };
 
 enum psg_pool_method { PSG_POOL_MAX = 0, PSG_POOL_AVE = 1 };

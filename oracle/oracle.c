@@ -330,10 +330,31 @@ orc_net* orc_net_create(const psg_layer_desc* layers, int n_layers, uint64_t see
         l->w = l->iw;
         break;
       case PSG_LAYER_SOFTMAX_LOSS:
+        /* several weighted losses (GoogLeNet's auxiliary heads): they share the labels, so
+         * they must agree on the class count; probabilities / test use the last one */
+        if (net->classes && net->classes != (int)(l->ic * l->ih * l->iw)) {
+          set_err("net: loss layers disagree on the class count");
+          orc_net_destroy(net);
+          return NULL;
+        }
         net->loss_idx = li;
         l->c = l->ic * l->ih * l->iw;
         l->h = l->w = 1;
         net->classes = (int)l->c;
+        break;
+      case PSG_LAYER_CONCAT: /* Caffe Concat along channels: inputs share h, w */
+        l->c = 0;
+        for (int i = 0; i < l->d.n_inputs; ++i) {
+          const orc_layer* in = &net->L[l->d.inputs[i]];
+          if (in->h != l->ih || in->w != l->iw) {
+            set_err("net: concat inputs differ in height/width");
+            orc_net_destroy(net);
+            return NULL;
+          }
+          l->c += in->c;
+        }
+        l->h = l->ih;
+        l->w = l->iw;
         break;
       default:
         set_err("net: unsupported layer kind in oracle");
@@ -737,7 +758,7 @@ static int softmax_fwd(orc_net* net, const orc_layer* l, size_t n, const double*
     const int y = net->labels[b];
     loss -= (row[y] - mx) - log(sum);
   }
-  net->last_loss = loss / (double)n * l->d.loss_weight;
+  net->last_loss += loss / (double)n * l->d.loss_weight; /* sum of weighted losses */
   if (!isfinite(net->last_loss)) {
     set_err("softmax loss: non-finite loss");
     return PSG_ERUNTIME;
@@ -751,7 +772,7 @@ static void softmax_seed(const orc_net* net, const orc_layer* l, size_t n, const
   const int64_t C = l->c;
   const double inv_n = l->d.loss_weight * (1.0 / (double)n);
   for (size_t b = 0; b < n; ++b) {
-    for (int64_t j = 0; j < C; ++j) dlogits[(int64_t)b * C + j] = probs[(int64_t)b * C + j] * inv_n;
+    for (int64_t j = 0; j < C; ++j) dlogits[(int64_t)b * C + j] += probs[(int64_t)b * C + j] * inv_n;
     dlogits[(int64_t)b * C + net->labels[b]] -= inv_n;
   }
 }
@@ -793,6 +814,18 @@ static int layer_forward_impl(orc_net* net, int li, size_t n) {
       return PSG_OK;
     case PSG_LAYER_SOFTMAX_LOSS:
       return softmax_fwd(net, l, n, x, l->out);
+    case PSG_LAYER_CONCAT: { /* NCHW: input i fills channels [off_i, off_i + c_i) */
+      const int64_t hw = l->h * l->w;
+      int64_t off = 0;
+      for (int i = 0; i < l->d.n_inputs; ++i) {
+        const int64_t ci = net->L[l->d.inputs[i]].c;
+        for (size_t b = 0; b < n; ++b)
+          memcpy(l->out + ((int64_t)b * l->c + off) * hw, l->fin[i] + (int64_t)b * ci * hw,
+                 (size_t)(ci * hw) * sizeof(double));
+        off += ci;
+      }
+      return PSG_OK;
+    }
   }
   set_err("forward: unsupported layer");
   return PSG_EINVAL;
@@ -816,6 +849,7 @@ static int run_forward(orc_net* net, const double* images, const int32_t* labels
   }
   memcpy(net->labels, labels, n * sizeof(int32_t));
   net->batch = n;
+  net->last_loss = 0.0;
   for (int li = 0; li < net->n; ++li) {
     orc_layer* l = &net->L[li];
     if (l->kind == PSG_LAYER_DATA) {
@@ -884,13 +918,31 @@ int orc_net_backward(orc_net* net, const double* images, const int32_t* labels, 
     memset(l->grad, 0, n * (size_t)vol3(l) * sizeof(double));
   }
   memset(grads, 0, net->P * sizeof(double));
-  const orc_layer* ls = &net->L[net->loss_idx];
-  softmax_seed(net, ls, n, ls->out, net->L[ls->d.inputs[0]].grad);
+  for (int li = 0; li < net->n; ++li) { /* every loss seeds its logits (+=) */
+    const orc_layer* ls = &net->L[li];
+    if (ls->kind == PSG_LAYER_SOFTMAX_LOSS)
+      softmax_seed(net, ls, n, ls->out, net->L[ls->d.inputs[0]].grad);
+  }
   for (int li = net->n - 1; li >= 0; --li) {
     orc_layer* l = &net->L[li];
     if (l->kind == PSG_LAYER_DATA || l->kind == PSG_LAYER_LABEL ||
         l->kind == PSG_LAYER_SOFTMAX_LOSS)
       continue;
+    if (l->kind == PSG_LAYER_CONCAT) { /* dx_i += dy[:, off_i : off_i + c_i] */
+      const int64_t hw = l->h * l->w;
+      int64_t off = 0;
+      for (int i = 0; i < l->d.n_inputs; ++i) {
+        orc_layer* in = &net->L[l->d.inputs[i]];
+        const int64_t ci = in->c;
+        for (size_t b = 0; b < n; ++b) {
+          const double* src = l->grad + ((int64_t)b * l->c + off) * hw;
+          double* dst = in->grad + (int64_t)b * ci * hw;
+          for (int64_t e = 0; e < ci * hw; ++e) dst[e] += src[e];
+        }
+        off += ci;
+      }
+      continue;
+    }
     double* dx = net->L[l->d.inputs[0]].grad;
     if (net->L[l->d.inputs[0]].kind == PSG_LAYER_DATA && l->kind == PSG_LAYER_CONV) {
       /* the reference also computes the (unused) data-layer gradient; the

@@ -14,6 +14,7 @@
 //   A_2D_MN    linear wgrad A = dY: [K rows][M] (MN-major)
 //   B_2D_K     weights [N rows][K] (K-major)
 //   B_WT_MN    conv dgrad B = W^T: channels (N, contiguous) x (tap, filter block) (K)
+//   B_3D_K     conv fprop weights as [F][taps][C/G] (K-major, channel tail zero-filled)
 //   B_RECT_MN  conv wgrad B = X shifted by the CTA's tap (N = channels, K = pixels)
 //   B_2D_MN    [K rows][N] (MN-major): linear dgrad W, linear wgrad X
 #include <cudaTypedefs.h>
@@ -169,7 +170,7 @@ int pick_n_tile(int N) {
 }
 
 void finish_args(TcArgs& a, int kblk, int sms) {
-  const bool b_mn = a.b_mode != B_2D_K;
+  const bool b_mn = a.b_mode != B_2D_K && a.b_mode != B_3D_K;
   const int nb = b_mn ? (a.n_tile + 31) / 32 * 32 : a.n_tile;
   a.a_bytes = kTileM * kblk * 4;
   const bool a_mn = a.a_mode == A_RECT_MN || a.a_mode == A_2D_MN;
@@ -277,11 +278,18 @@ bool plan_fprop(const ConvGeom& g, TcArgs& a, int& kblk) {
     a.ldo = O;
     return true;
   }
-  if (g.sh != 1 || g.sw != 1) return false;
+  if (g.sh != 1 || g.sw != 1 || g.Fg() % 16) return false;
   kblk = kblk_for(g.Cgs());
-  if (!kblk || g.Fg() % 16) return false;
+  // C/G not a multiple of 16: 32-channel blocks per tap, the tail read as 0 (A: the NHWC
+  // input's channels past C read OOB, other groups' channels meet B's OOB zeros; B: W
+  // viewed as [F][taps][C/G])
+  const bool padded = kblk == 0;
+  if (padded) {
+    if (g.cs_in % 4 || g.Cgs() % 4) return false;
+    kblk = 32;
+  }
   a.a_mode = A_RECT_K;
-  a.b_mode = B_2D_K;
+  a.b_mode = padded ? B_3D_K : B_2D_K;
   a.row_map = ROW_RECT;
   rect_shape(g.OW, kTileM, a.rm, a.wm);
   a.th = (g.OH + a.rm - 1) / a.rm;
@@ -293,7 +301,7 @@ bool plan_fprop(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.n_tiles = (g.Fg() + a.n_tile - 1) / a.n_tile;
   a.G = g.G;
   a.taps = 1;
-  a.cb = g.Cgs() / kblk;
+  a.cb = (g.Cgs() + kblk - 1) / kblk;
   a.kblocks = g.kh * g.kw * a.cb;
   a.a_c_g = g.Cgs();
   a.b_r_g = g.Fg();
@@ -326,9 +334,12 @@ bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
     a.ldo = D;
     return true;
   }
-  if (g.sh != 1 || g.sw != 1) return false;
+  if (g.sh != 1 || g.sw != 1 || g.Cgs() % 4 || g.cs_in % 4) return false;
   kblk = kblk_for(g.Fg());
-  if (!kblk || g.Cgs() % 16) return false;
+  if (!kblk) {  // F/G not a multiple of 16: 32-filter blocks, the tail read as 0 (B's 4-D view)
+    if (g.Fg() % 4 || g.F % 4) return false;
+    kblk = 32;
+  }
   a.a_mode = A_RECT_K;   // dY rectangles, taps reversed
   a.b_mode = B_WT_MN;    // W^T
   a.row_map = ROW_RECT;
@@ -342,7 +353,7 @@ bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.n_tiles = (g.Cgs() + a.n_tile - 1) / a.n_tile;
   a.G = g.G;
   a.taps = 1;
-  a.cb = g.Fg() / kblk;
+  a.cb = (g.Fg() + kblk - 1) / kblk;
   a.kblocks = g.kh * g.kw * a.cb;
   a.a_c_g = g.Fg();
   a.b_r_g = g.Fg();
@@ -532,7 +543,16 @@ void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bi
     mb = map_2d(w, g.F, g.cs_in, kblk, a.n_tile, k_swizzle(kblk));
   } else {
     ma = map_nhwc(x, g.n, g.H, g.W, g.cs_in, kblk, a.wm, a.rm, k_swizzle(kblk));
-    mb = map_2d(w, g.F, g.Kp(), kblk, a.n_tile, k_swizzle(kblk));
+    if (a.b_mode == B_3D_K) {
+      const uint64_t dims[3] = {static_cast<uint64_t>(g.Cgs()),
+                                static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.F)};
+      const uint64_t str[2] = {static_cast<uint64_t>(g.Cgs()) * 4,
+                               static_cast<uint64_t>(g.Kp()) * 4};
+      const uint32_t box[3] = {static_cast<uint32_t>(kblk), 1, static_cast<uint32_t>(a.n_tile)};
+      mb = make_map(w, 3, dims, str, box, k_swizzle(kblk));
+    } else {
+      mb = map_2d(w, g.F, g.Kp(), kblk, a.n_tile, k_swizzle(kblk));
+    }
   }
   launch(a, ma, mb, kblk, static_cast<long long>(g.n) * g.OH * g.OW * g.F, ws.ptr, ws.elems, s);
 }
@@ -551,12 +571,14 @@ void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, boo
     mb = map_2d(w, g.F, g.cs_in, 32, kblk, kMnSwizzle);
   } else {
     ma = map_nhwc(dy, g.n, g.OH, g.OW, g.F, kblk, a.wm, a.rm, k_swizzle(kblk));
-    const uint64_t dims[3] = {static_cast<uint64_t>(g.Cgs()),
-                              static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.F)};
-    const uint64_t str[2] = {static_cast<uint64_t>(g.Cgs()) * 4,
-                             static_cast<uint64_t>(g.Kp()) * 4};
-    const uint32_t box[3] = {32, 1, static_cast<uint32_t>(kblk)};
-    mb = make_map(w, 3, dims, str, box, kMnSwizzle);
+    const uint64_t dims[4] = {static_cast<uint64_t>(g.Cgs()),
+                              static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.Fg()),
+                              static_cast<uint64_t>(g.G)};
+    const uint64_t str[3] = {static_cast<uint64_t>(g.Cgs()) * 4,
+                             static_cast<uint64_t>(g.Kp()) * 4,
+                             static_cast<uint64_t>(g.Fg()) * g.Kp() * 4};
+    const uint32_t box[4] = {32, 1, static_cast<uint32_t>(kblk), 1};
+    mb = make_map(w, 4, dims, str, box, kMnSwizzle);
   }
   launch(a, ma, mb, kblk, static_cast<long long>(g.n) * g.H * g.W * g.cs_in, ws.ptr, ws.elems,
          s);

@@ -99,7 +99,7 @@ __global__ void softmax_loss_k(const float* __restrict__ logits, const int32_t* 
 
 // Fixed-order reduction of the per-row losses: loss = sum / n * loss_weight.
 __global__ void loss_reduce_k(const double* __restrict__ row_loss, int n, double lw,
-                              double* __restrict__ loss, int* __restrict__ flag) {
+                              double* __restrict__ loss, int* __restrict__ flag, int accumulate) {
   __shared__ double part[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += row_loss[i];
@@ -110,7 +110,7 @@ __global__ void loss_reduce_k(const double* __restrict__ row_loss, int n, double
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const double l = part[0] / n * lw;
+    const double l = part[0] / n * lw + (accumulate ? *loss : 0.0);
     *loss = l;
     if (!isfinite(l)) *flag = 1;
   }
@@ -252,12 +252,50 @@ void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumul
 
 void softmax_loss(const float* logits, const int32_t* labels, int n, int C, double loss_weight,
                   float* probs, float* dlogits, double* row_loss, double* loss, int* flag,
-                  cudaStream_t s) {
+                  bool accumulate, cudaStream_t s) {
   const double scale = loss_weight * (1.0 / static_cast<double>(n));
   softmax_loss_k<<<(n * 32 + 255) / 256, 256, 0, s>>>(logits, labels, n, C, scale, probs, dlogits,
                                                       row_loss);
   PSG_CUDA(cudaGetLastError());
-  loss_reduce_k<<<1, 256, 0, s>>>(row_loss, n, loss_weight, loss, flag);
+  loss_reduce_k<<<1, 256, 0, s>>>(row_loss, n, loss_weight, loss, flag, accumulate ? 1 : 0);
+  PSG_CUDA(cudaGetLastError());
+}
+
+namespace {
+__global__ void concat_copy_k(const float* __restrict__ in, int ci, float* __restrict__ out,
+                              int ctot, int off, size_t total) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t p = i / ci, c = i % ci;
+    out[p * ctot + off + c] = in[i];
+  }
+}
+__global__ void concat_split_k(const float* __restrict__ dy, int ctot, int off,
+                               float* __restrict__ dx, int ci, size_t total, int accumulate) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t p = i / ci, c = i % ci;
+    const float v = dy[p * ctot + off + c];
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+unsigned concat_blocks(size_t total) {
+  return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((total + 255) / 256, 148 * 16)));
+}
+}  // namespace
+
+void concat_copy(const float* in, int ci, float* out, int ctot, int off, size_t pixels,
+                 cudaStream_t s) {
+  const size_t total = pixels * ci;
+  concat_copy_k<<<concat_blocks(total), 256, 0, s>>>(in, ci, out, ctot, off, total);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void concat_split(const float* dy, int ctot, int off, float* dx, int ci, size_t pixels,
+                  bool accumulate, cudaStream_t s) {
+  const size_t total = pixels * ci;
+  concat_split_k<<<concat_blocks(total), 256, 0, s>>>(dy, ctot, off, dx, ci, total,
+                                                       accumulate ? 1 : 0);
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -97,13 +97,16 @@ void validate(const psg_layer_desc* layers, int n) {
         ++n_loss;
         if (d.n_inputs != 2) throw std::invalid_argument("net: softmax loss takes [logits, label]");
         break;
+      case PSG_LAYER_CONCAT:
+        if (d.n_inputs < 1) throw std::invalid_argument("net: concat needs inputs");
+        break;
       default:
         throw std::invalid_argument("net: unsupported layer kind");
     }
   }
   if (n_data != 1) throw std::invalid_argument("net: exactly one data layer required");
   if (n_label != 1) throw std::invalid_argument("net: exactly one label layer required");
-  if (n_loss != 1) throw std::invalid_argument("net: exactly one softmax loss layer required");
+  if (n_loss < 1) throw std::invalid_argument("net: at least one softmax loss layer required");
 }
 
 void free_batch_buffers(psg_net* net) {
@@ -408,10 +411,28 @@ void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed)
           throw std::invalid_argument("net: softmax loss second input must be the label layer");
         if (src->H != 1 || src->W != 1 || src->cs != src->C)
           throw std::invalid_argument("net: softmax logits must be [classes]");
+        // several weighted losses (auxiliary heads) share the labels: same class count;
+        // probabilities and test() use the last loss layer
+        if (net->classes && net->classes != src->C)
+          throw std::invalid_argument("net: loss layers disagree on the class count");
         net->loss_idx = li;
         l.C = l.cs = src->C;
         l.H = l.W = 1;
         net->classes = l.C;
+        break;
+      case PSG_LAYER_CONCAT:  // Caffe Concat along channels
+        l.C = 0;
+        l.H = src->H;
+        l.W = src->W;
+        for (int in : l.inputs) {
+          const LayerRt& x = net->L[in];
+          if (x.H != l.H || x.W != l.W)
+            throw std::invalid_argument("net: concat inputs differ in height/width");
+          if (x.cs != x.C) throw std::invalid_argument("net: concat of a padded input");
+          l.coff.push_back(l.C);
+          l.C += x.C;
+        }
+        l.cs = l.C;
         break;
     }
     if (is_param_layer(l.kind)) {

@@ -69,6 +69,7 @@ struct Scope {
 int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer) {
   cudaStream_t s = net->stream;
   int launches = 0;
+  bool first_loss = true;  // the total loss sums every loss layer's weighted mean
   for (size_t li = 0; li < net->L.size(); ++li) {
     LayerRt& l = net->L[li];
     const int lid = static_cast<int>(li);
@@ -132,9 +133,21 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         Scope sc(timer, nm.c_str(), lid, 2, 0.0, 3 * act_bytes(l, n));
         softmax_loss(logits.out, net->labels, static_cast<int>(n), net->classes, l.d.loss_weight,
                      l.out, seed_grad ? logits.grad : nullptr, net->row_loss, &net->dsc->loss,
-                     &net->dsc->flag, s);
+                     &net->dsc->flag, !first_loss, s);
+        first_loss = false;
         sc.done(2);
         launches += 2;
+        break;
+      }
+      case PSG_LAYER_CONCAT: {
+        const size_t pixels = n * static_cast<size_t>(l.H) * l.W;
+        Scope sc(timer, nm.c_str(), lid, 1, 0.0, 2 * act_bytes(l, n));
+        for (size_t i = 0; i < l.inputs.size(); ++i) {
+          const LayerRt& x = net->L[l.inputs[i]];
+          concat_copy(x.out, x.C, l.out, l.C, l.coff[i], pixels, s);
+        }
+        sc.done(static_cast<int>(l.inputs.size()));
+        launches += static_cast<int>(l.inputs.size());
         break;
       }
     }
@@ -146,11 +159,28 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
   cudaStream_t s = net->stream;
   int launches = 0;
   std::vector<char> written(net->L.size(), 0);
-  written[net->L[net->loss_idx].inputs[0]] = 1;  // the loss seed writes the logits grad
+  for (const LayerRt& l : net->L)  // every loss seed writes its logits grad
+    if (l.kind == PSG_LAYER_SOFTMAX_LOSS) written[l.inputs[0]] = 1;
   for (int li = static_cast<int>(net->L.size()) - 1; li >= 0; --li) {
     LayerRt& l = net->L[li];
     if (l.kind == PSG_LAYER_DATA || l.kind == PSG_LAYER_LABEL || l.kind == PSG_LAYER_SOFTMAX_LOSS)
       continue;
+    if (l.kind == PSG_LAYER_CONCAT) {  // dx_i (+)= dy[:, off_i : off_i + C_i]
+      const size_t pixels = n * static_cast<size_t>(l.H) * l.W;
+      Scope sc(timer, (std::string(l.d.name) + ".bwd").c_str(), li, 5, 0.0, 2 * act_bytes(l, n));
+      int c = 0;
+      for (size_t i = 0; i < l.inputs.size(); ++i) {
+        const int in = l.inputs[i];
+        LayerRt& x = net->L[in];
+        if (x.kind == PSG_LAYER_DATA) continue;
+        concat_split(l.grad, l.C, l.coff[i], x.grad, x.C, pixels, written[in] != 0, s);
+        written[in] = 1;
+        ++c;
+      }
+      sc.done(c);
+      launches += c;
+      continue;
+    }
     const int pi = l.inputs[0];
     LayerRt& src = net->L[pi];
     const bool need_dx = src.kind != PSG_LAYER_DATA;

@@ -172,9 +172,16 @@ void dropout_bwd(const DropGeom& g, const float* dy, float* dx, const uint64_t* 
 
 // Softmax + mean cross-entropy (x loss_weight) + the loss seed; per-row loss
 // terms in fp64, reduced in fixed order into *loss.
+// loss (+)= loss_weight * mean CE (accumulate: add to *loss, for several loss layers)
 void softmax_loss(const float* logits, const int32_t* labels, int n, int C, double loss_weight,
                   float* probs, float* dlogits, double* row_loss, double* loss, int* flag,
-                  cudaStream_t s);
+                  bool accumulate, cudaStream_t s);
+// Caffe Concat along channels, NHWC: out[pix][off_i + c] = in_i[pix][c]; backward
+// dx_i[pix][c] (+)= dy[pix][off_i + c].
+void concat_copy(const float* in, int ci, float* out, int ctot, int off, size_t pixels,
+                 cudaStream_t s);
+void concat_split(const float* dy, int ctot, int off, float* dx, int ci, size_t pixels,
+                  bool accumulate, cudaStream_t s);
 void argmax_count(const float* probs, const int32_t* labels, int n, int C,
                   unsigned long long* correct, cudaStream_t s);
 

@@ -54,6 +54,7 @@ struct LayerRt {
   float* grad = nullptr;
   uint8_t* route = nullptr;
   float* col = nullptr;  // im2col matrix (TF32 im2col route only)
+  std::vector<int> coff;  // concat: channel offset of each input
   int kern_t = -1, bias_t = -1;
   ConvGeom cg;  // conv / linear (per-example; n filled per call)
   PoolGeom pg;

@@ -17,7 +17,8 @@ namespace psg {
 namespace tck {
 
 enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3 };
-enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3, B_COL_MN = 4, B_TAPS_MN = 5 };
+enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3, B_COL_MN = 4, B_TAPS_MN = 5,
+             B_3D_K = 6 };
 enum RowMap { ROW_RECT = 0, ROW_LINEAR = 1 };
 
 // Warp roles: 0..3 and 6..7 TMA producers (K block it -> producer it % p.producers),
@@ -191,10 +192,14 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
     case B_2D_K:
       if (j == 0) tc::tma_load_2d(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + t.n * p.n_tile);
       break;
-    case B_WT_MN:
+    case B_WT_MN:  // W viewed as [G][F/G][taps][C/G]: filter blocks past F/G read as 0
       if (j < nch)
-        tc::tma_load_3d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.t1,
-                        p.b_r_g * t.g + c.t0 * KBLK);
+        tc::tma_load_4d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.t1,
+                        c.t0 * KBLK, t.g);
+      break;
+    case B_3D_K:  // W viewed as [F][taps][C/G]: channel blocks past C/G read as 0
+      if (j == 0)
+        tc::tma_load_3d(sb, map, bar, c.t0 * KBLK, c.t1, p.b_r_g * t.g + t.n * p.n_tile);
       break;
     case B_RECT_MN:
       if (j < nch)
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp && lane == 0) {
     // ------------------------------------------------------------ MMA issue
     const bool a_mn = p.a_mode == A_RECT_MN || p.a_mode == A_2D_MN;
-    const bool b_mn = p.b_mode != B_2D_K;
+    const bool b_mn = p.b_mode != B_2D_K && p.b_mode != B_3D_K;
     const uint32_t idesc = tc::idesc_tf32(kTileM, p.n_tile, a_mn, b_mn);
     const uint32_t k_sw = KBLK == 32 ? tc::kSw128 : tc::kSw64;
     const uint32_t k_sbo = 8 * KBLK * 4;  // 8 rows of KBLK floats
@@ -370,20 +375,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float bv = 0.f;
         if (col_ok && p.bias && !p.ws) bv = p.bias[cidx];
+        const bool acc_out = p.accumulate && !p.ws;
+        float prev[32];  // accumulate: issue the 32 row loads before any store (ILP)
+        if (acc_out) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const bool ok = __shfl_sync(0xffffffffu, row_ok, i);
+            const long long ro = __shfl_sync(0xffffffffu, row_off, i);
+            prev[i] = ok && col_ok ? base[ro + cidx] : 0.f;
+          }
+        }
+#pragma unroll
         for (int i = 0; i < 32; ++i) {
           const bool ok = __shfl_sync(0xffffffffu, row_ok, i);
           const long long ro = __shfl_sync(0xffffffffu, row_off, i);
           if (!ok || !col_ok) continue;
           float y = stg[i * kStagePad + lane];
-          float* dst = base + ro + cidx;
           if (!p.ws) {
             if (p.bias) {
               y += bv;
               if (p.relu) y = y > 0.f ? y : 0.f;
             }
-            if (p.accumulate) y += *dst;
+            if (acc_out) y += prev[i];
           }
-          *dst = y;
+          base[ro + cidx] = y;
         }
         __syncwarp();
       }

@@ -122,6 +122,11 @@ def dropout_layer(name: str, input: str, ratio: float = 0.5) -> LayerSpec:
     return LayerSpec(kind=DROPOUT, name=name, inputs=[input], dropout_ratio=ratio)
 
 
+def concat_layer(name: str, inputs: Sequence[str]) -> LayerSpec:
+    """Caffe Concat along channels (extension; GoogLeNet inception outputs)."""
+    return LayerSpec(kind=CONCAT, name=name, inputs=list(inputs))
+
+
 def softmax_loss_layer(name: str, logits: str, label: str, loss_weight: float = 1.0) -> LayerSpec:
     return LayerSpec(kind=SOFTMAX_LOSS, name=name, inputs=[logits, label], loss_weight=loss_weight)
 
@@ -180,14 +185,17 @@ class NetSpec:
                 n_loss += 1
                 if len(l.inputs) != 2:
                     raise ValueError("net: softmax loss takes [logits, label]")
+            elif l.kind == CONCAT:
+                if not 1 <= len(l.inputs) <= 8:
+                    raise ValueError("net: concat takes 1..8 inputs")
             else:
                 raise ValueError(f"net: unknown layer kind {l.kind}")
         if n_data != 1:
             raise ValueError("net: exactly one data layer required")
         if n_label != 1:
             raise ValueError("net: exactly one label layer required")
-        if n_loss != 1:
-            raise ValueError("net: exactly one softmax loss layer required")
+        if n_loss < 1:  # several weighted losses: auxiliary heads (extension)
+            raise ValueError("net: at least one softmax loss layer required")
 
     def data_spec(self) -> LayerSpec:
         for l in self.layers:
@@ -243,6 +251,8 @@ class NetSpec:
                 return False
             if l.kind == SOFTMAX_LOSS and l.loss_weight != 1.0:
                 return False
+        if sum(l.kind == SOFTMAX_LOSS for l in self.layers) != 1:
+            return False
         return True
 
 
@@ -361,6 +371,79 @@ def make_alexnet(batch: int = 256, num_classes: int = 1000) -> NetSpec:
     return net
 
 
+def _inception(layers, name, inp, c1, c3r, c3, c5r, c5, cp, b):
+    """One GoogLeNet inception module (bvlc_googlenet): 1x1 | 1x1->3x3 | 1x1->5x5 |
+    maxpool 3/1 -> 1x1, each conv followed by ReLU, concatenated along channels."""
+    p = name + "/"
+    layers += [conv_layer(p + "1x1", inp, 1, 1, c1, **b), relu_layer(p + "relu_1x1", p + "1x1"),
+               conv_layer(p + "3x3_reduce", inp, 1, 1, c3r, **b),
+               relu_layer(p + "relu_3x3_reduce", p + "3x3_reduce"),
+               conv_layer(p + "3x3", p + "relu_3x3_reduce", 3, 3, c3, pad=1, **b),
+               relu_layer(p + "relu_3x3", p + "3x3"),
+               conv_layer(p + "5x5_reduce", inp, 1, 1, c5r, **b),
+               relu_layer(p + "relu_5x5_reduce", p + "5x5_reduce"),
+               conv_layer(p + "5x5", p + "relu_5x5_reduce", 5, 5, c5, pad=2, **b),
+               relu_layer(p + "relu_5x5", p + "5x5"),
+               pool_layer(p + "pool", inp, 3, 3, 1, 1, pad=1, ceil_mode=True),
+               conv_layer(p + "pool_proj", p + "pool", 1, 1, cp, **b),
+               relu_layer(p + "relu_pool_proj", p + "pool_proj"),
+               concat_layer(p + "output", [p + "relu_1x1", p + "relu_3x3", p + "relu_5x5",
+                                           p + "relu_pool_proj"])]
+    return p + "output"
+
+
+def _aux_head(layers, name, inp, num_classes, b):
+    """GoogLeNet auxiliary classifier (loss weight 0.3)."""
+    p = name + "/"
+    layers += [pool_layer(p + "ave_pool", inp, 5, 5, 3, 3, method=POOL_AVE, ceil_mode=True),
+               conv_layer(p + "conv", p + "ave_pool", 1, 1, 128, **b),
+               relu_layer(p + "relu_conv", p + "conv"),
+               linear_layer(p + "fc", p + "relu_conv", 1024, **b),
+               relu_layer(p + "relu_fc", p + "fc"),
+               dropout_layer(p + "drop_fc", p + "relu_fc", 0.7),
+               linear_layer(p + "classifier", p + "drop_fc", num_classes, **b),
+               softmax_loss_layer(p + "loss", p + "classifier", "label", loss_weight=0.3)]
+
+
+def make_googlenet(batch: int, num_classes: int = 1000, image: int = 224) -> NetSpec:
+    """GoogLeNet (Caffe bvlc_googlenet, with both auxiliary heads at loss weight 0.3):
+    conv 7x7/2 -> max 3/2 -> LRN -> 1x1 -> 3x3 -> LRN -> max 3/2 -> inception 3a,3b ->
+    max 3/2 -> 4a (aux1) 4b 4c 4d (aux2) 4e -> max 3/2 -> 5a 5b -> ave 7/1 -> drop 0.4 ->
+    classifier.  Bias lr_mult 2 / decay_mult 0 as in the prototxt."""
+    b = dict(lr_mult=(1.0, 2.0), decay_mult=(1.0, 0.0))
+    L = [data_layer("data", batch, 3, image, image), label_layer("label", batch),
+         conv_layer("conv1/7x7_s2", "data", 7, 7, 64, stride=2, pad=3, **b),
+         relu_layer("conv1/relu_7x7", "conv1/7x7_s2"),
+         pool_layer("pool1/3x3_s2", "conv1/relu_7x7", 3, 3, 2, 2, ceil_mode=True),
+         lrn_layer("pool1/norm1", "pool1/3x3_s2", 5, 1e-4, 0.75),
+         conv_layer("conv2/3x3_reduce", "pool1/norm1", 1, 1, 64, **b),
+         relu_layer("conv2/relu_3x3_reduce", "conv2/3x3_reduce"),
+         conv_layer("conv2/3x3", "conv2/relu_3x3_reduce", 3, 3, 192, pad=1, **b),
+         relu_layer("conv2/relu_3x3", "conv2/3x3"),
+         lrn_layer("conv2/norm2", "conv2/relu_3x3", 5, 1e-4, 0.75),
+         pool_layer("pool2/3x3_s2", "conv2/norm2", 3, 3, 2, 2, ceil_mode=True)]
+    x = _inception(L, "inception_3a", "pool2/3x3_s2", 64, 96, 128, 16, 32, 32, b)
+    x = _inception(L, "inception_3b", x, 128, 128, 192, 32, 96, 64, b)
+    L.append(pool_layer("pool3/3x3_s2", x, 3, 3, 2, 2, ceil_mode=True))
+    x = _inception(L, "inception_4a", "pool3/3x3_s2", 192, 96, 208, 16, 48, 64, b)
+    _aux_head(L, "loss1", x, num_classes, b)
+    x = _inception(L, "inception_4b", x, 160, 112, 224, 24, 64, 64, b)
+    x = _inception(L, "inception_4c", x, 128, 128, 256, 24, 64, 64, b)
+    x = _inception(L, "inception_4d", x, 112, 144, 288, 32, 64, 64, b)
+    _aux_head(L, "loss2", x, num_classes, b)
+    x = _inception(L, "inception_4e", x, 256, 160, 320, 32, 128, 128, b)
+    L.append(pool_layer("pool4/3x3_s2", x, 3, 3, 2, 2, ceil_mode=True))
+    x = _inception(L, "inception_5a", "pool4/3x3_s2", 256, 160, 320, 32, 128, 128, b)
+    x = _inception(L, "inception_5b", x, 384, 192, 384, 48, 128, 128, b)
+    L += [pool_layer("pool5/7x7_s1", x, 7, 7, 1, 1, method=POOL_AVE),
+          dropout_layer("pool5/drop_7x7_s1", "pool5/7x7_s1", 0.4),
+          linear_layer("loss3/classifier", "pool5/drop_7x7_s1", num_classes, **b),
+          softmax_loss_layer("loss3/loss3", "loss3/classifier", "label", loss_weight=1.0)]
+    net = NetSpec(L)
+    net.validate()
+    return net
+
+
 PRESETS = {
     "lenet-small": lambda b, c, h, w, k: make_lenet_small(b, c, h, w, k),
     "mlp": lambda b, c, h, w, k: make_mlp(b, c, h, w, k),
@@ -392,6 +475,8 @@ def param_count(spec: NetSpec) -> int:
             dims[l.name] = (l.num_outputs, 1, 1)
         elif l.kind == SOFTMAX_LOSS:
             dims[l.name] = (c * h * w, 1, 1)
+        elif l.kind == CONCAT:
+            dims[l.name] = (sum(dims[i][0] for i in l.inputs), h, w)
         else:
             dims[l.name] = (c, h, w)
     return total
@@ -431,6 +516,8 @@ def forward_macs(spec: NetSpec) -> dict:
             dims[l.name] = (l.num_outputs, 1, 1)
         elif l.kind == SOFTMAX_LOSS:
             dims[l.name] = (c * h * w, 1, 1)
+        elif l.kind == CONCAT:
+            dims[l.name] = (sum(dims[i][0] for i in l.inputs), h, w)
         else:
             dims[l.name] = (c, h, w)
     return macs

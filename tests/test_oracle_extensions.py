@@ -72,6 +72,18 @@ EXT_NETS = {
         ns.linear_layer("ip1", "data", 16), ns.relu_layer("r1", "ip1"),
         ns.dropout_layer("d1", "r1", 0.5), ns.linear_layer("ip2", "d1", 4),
         ns.softmax_loss_layer("loss", "ip2", "label", loss_weight=0.7)]),
+    # GoogLeNet-style branch + concat + an auxiliary weighted loss head
+    "inception_concat_aux": ns.NetSpec([
+        ns.data_layer("data", 2, 3, 6, 6), ns.label_layer("label", 2),
+        ns.conv_layer("a1", "data", 1, 1, 2), ns.relu_layer("ra", "a1"),
+        ns.conv_layer("b1", "data", 1, 1, 2), ns.conv_layer("b3", "b1", 3, 3, 3, pad=1),
+        ns.pool_layer("pp", "data", 3, 3, 1, 1, pad=1, ceil_mode=True),
+        ns.conv_layer("pj", "pp", 1, 1, 2),
+        ns.concat_layer("cat", ["ra", "b3", "pj"]),
+        ns.linear_layer("aux", "b1", 3),
+        ns.softmax_loss_layer("aux_loss", "aux", "label", loss_weight=0.3),
+        ns.pool_layer("gp", "cat", 6, 6, 1, 1, method=ns.POOL_AVE),
+        ns.linear_layer("fc", "gp", 3), ns.softmax_loss_layer("loss", "fc", "label")]),
 }
 
 
@@ -191,3 +203,41 @@ def test_weight_decay_and_multipliers(oracle_lib):
     want[:nk] = w[:nk] - 0.1 * (g[:nk] + 0.01 * w[:nk])
     want[nk:] = w[nk:] - 0.2 * g[nk:]
     np.testing.assert_allclose(net.get_weights(), want, rtol=1e-15, atol=1e-15)
+
+
+def test_concat_forward_is_channel_stacking(oracle_lib):
+    """concat output == the inputs stacked along channels (NCHW)."""
+    spec = ns.NetSpec([ns.data_layer("data", 2, 2, 3, 3), ns.label_layer("label", 2),
+                       ns.conv_layer("a", "data", 1, 1, 3), ns.conv_layer("b", "data", 3, 3, 2, pad=1),
+                       ns.concat_layer("cat", ["a", "b", "a"]), ns.linear_layer("fc", "cat", 2),
+                       ns.softmax_loss_layer("loss", "fc", "label")])
+    net = oracle_lib.net(spec, 4)
+    rng = np.random.default_rng(2)
+    x, y = _batch(rng, spec, 2)
+    net.forward(x, y)
+    a, b, cat = (net.layer_out(spec.index_of(k), 2) for k in ("a", "b", "cat"))
+    np.testing.assert_array_equal(cat, np.concatenate([a, b, a], axis=1))
+
+
+def test_multiple_losses_sum_weighted(oracle_lib):
+    """Total loss = sum of loss_weight x mean cross-entropy over the loss layers; the
+    gradient of a weighted aux head is that weight times its unit-weight gradient."""
+    def spec(w_aux):
+        return ns.NetSpec([ns.data_layer("data", 3, 1, 1, 5), ns.label_layer("label", 3),
+                           ns.linear_layer("h", "data", 4),
+                           ns.linear_layer("aux", "h", 3),
+                           ns.softmax_loss_layer("l1", "aux", "label", loss_weight=w_aux),
+                           ns.linear_layer("fc", "h", 3),
+                           ns.softmax_loss_layer("l2", "fc", "label")])
+    rng = np.random.default_rng(9)
+    x = rng.normal(size=(3, 1, 1, 5))
+    y = np.array([0, 2, 1], np.int32)
+    n0 = oracle_lib.net(spec(0.0), 3)
+    n1 = oracle_lib.net(spec(1.0), 3)
+    nw = oracle_lib.net(spec(0.3), 3)
+    l0, g0 = n0.backward(x, y)
+    l1, g1 = n1.backward(x, y)
+    lw, gw = nw.backward(x, y)
+    aux_only = l1 - l0
+    assert lw == pytest.approx(l0 + 0.3 * aux_only, rel=1e-12)
+    np.testing.assert_allclose(gw - g0, 0.3 * (g1 - g0), rtol=1e-9, atol=1e-12)

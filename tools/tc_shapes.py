@@ -22,6 +22,10 @@ SHAPES = {
     "ax_conv5": (4, 384, 13, 13, 256, 3, 1, 2),
     "cq_conv2": (8, 32, 16, 16, 32, 5, 2, 1),
     "cq_conv3": (8, 32, 8, 8, 64, 5, 2, 1),
+    "gn_4b_5x5": (4, 24, 14, 14, 64, 5, 2, 1),        # C/G = 24: padded channel blocks
+    "gn_4b_5x5_red": (4, 512, 14, 14, 24, 1, 0, 1),   # F = 24: padded filter blocks (dgrad)
+    "grp_c24": (4, 48, 13, 13, 96, 3, 1, 2),          # grouped, C/G = 24
+    "grp_f24": (4, 64, 9, 9, 48, 3, 1, 2),            # grouped, F/G = 24 (4-D W^T view)
     "ax_fc6": (64, -9216, 1, 1, 4096, 1, 0, 1),
     "ax_fc8": (64, -4096, 1, 1, 1000, 1, 0, 1),
 }
