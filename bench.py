@@ -326,6 +326,18 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": top["name"],
                 "share_of_step": top["ms"] / step_ms, "peak_source": peaks["source"]}
+    # traffic: DRAM bytes of the same op in the committed ncu capture of this workload
+    # (tools/op_traffic.py; cold-cache serialised replay, one training step)
+    tpath = os.path.join(ROOT, "profiles", "round1", f"{args.workload}_op_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f)
+        hit = [o for o in tr["ops"] if o["op"] == top["name"]]
+        if hit and tr.get("precision") == args.precision:
+            roof["traffic"] = hit[0]["dram_bytes"]
+            roof["traffic_unit"] = "bytes per op launch set (ncu dram__bytes_read+write)"
+            roof["ncu_share_of_step"] = hit[0]["ncu_share"]
+            roof["traffic_source"] = os.path.relpath(tpath, ROOT)
     if args.profile_json and rank == 0:
         with open(args.profile_json, "w") as f:
             json.dump({"ops": prof, "step_ms": step_ms}, f, indent=1)
