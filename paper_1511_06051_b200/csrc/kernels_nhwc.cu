@@ -291,6 +291,97 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float*
   }
 }
 
+// Streaming LRN for size 5 and C % 8 == 0 (AlexNet / GoogLeNet): thread = 8 consecutive
+// channels of one pixel, no shared memory and no barriers — each thread loads its run plus
+// the neighbouring channels it needs (float4, the neighbours mostly L1 hits) and keeps the
+// window sums in registers (same ascending 5-term sums as the tile kernels).  Channels
+// outside [0, C) read as zero.
+constexpr int kLrnRun = 8;
+
+__device__ __forceinline__ float4 lrn_ld4(const float* p, int c, int C) {
+  return (c >= 0 && c < C) ? __ldg(reinterpret_cast<const float4*>(p + c))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void lrn_put4(float* v, float4 q) {
+  v[0] = q.x;
+  v[1] = q.y;
+  v[2] = q.z;
+  v[3] = q.w;
+}
+
+__global__ void __launch_bounds__(256) lrn_fwd_run_k(LrnGeom g, const float* __restrict__ x,
+                                                     float* __restrict__ y, uint32_t total_runs) {
+  const int C = g.C, runs = C / kLrnRun;
+  const float a = g.alpha / g.size;
+  GRID_STRIDE32(r, total_runs) {
+    const uint32_t pix = r / runs;
+    const int c0 = static_cast<int>(r % runs) * kLrnRun;
+    const float* xp = x + static_cast<size_t>(pix) * C;
+    float v[16];  // channels c0-4 .. c0+11
+    lrn_put4(v, lrn_ld4(xp, c0 - 4, C));
+    lrn_put4(v + 4, lrn_ld4(xp, c0, C));
+    lrn_put4(v + 8, lrn_ld4(xp, c0 + 4, C));
+    lrn_put4(v + 12, lrn_ld4(xp, c0 + 8, C));
+    float out[kLrnRun];
+#pragma unroll
+    for (int i = 0; i < kLrnRun; ++i) {  // channel c0 + i = v[i + 4]; window v[i+2 .. i+6]
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc += v[i + 2 + q] * v[i + 2 + q];
+      out[i] = v[i + 4] * lrn_pow(g.k + a * acc, g.beta);
+    }
+    float4* dst = reinterpret_cast<float4*>(y + static_cast<size_t>(pix) * C + c0);
+    dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+    dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+  }
+}
+
+__global__ void __launch_bounds__(256) lrn_bwd_run_k(LrnGeom g, const float* __restrict__ x,
+                                                     const float* __restrict__ dy,
+                                                     float* __restrict__ dx, int accumulate,
+                                                     uint32_t total_runs) {
+  const int C = g.C, runs = C / kLrnRun;
+  const float a = g.alpha / g.size, ratio = 2.f * g.alpha * g.beta / g.size;
+  GRID_STRIDE32(r, total_runs) {
+    const uint32_t pix = r / runs;
+    const int c0 = static_cast<int>(r % runs) * kLrnRun;
+    const size_t base = static_cast<size_t>(pix) * C;
+    float v[16], d[16];  // channels c0-4 .. c0+11
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      lrn_put4(v + 4 * k, lrn_ld4(x + base, c0 - 4 + 4 * k, C));
+      lrn_put4(d + 4 * k, lrn_ld4(dy + base, c0 - 4 + 4 * k, C));
+    }
+    // st = dy * x * s^-beta / s and s^-beta for channels c0-2 .. c0+9 (index j = ch - c0 + 2)
+    float st[12], sp[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc += v[j + q] * v[j + q];  // window of channel j + c0 - 2
+      const float sc = g.k + a * acc;
+      sp[j] = lrn_pow(sc, g.beta);
+      st[j] = d[j + 2] * v[j + 2] * sp[j] * __frcp_rn(sc);  // zero outside [0, C): x = 0
+    }
+    float out[kLrnRun];
+#pragma unroll
+    for (int i = 0; i < kLrnRun; ++i) {  // channels q whose window holds c: [c-2, c+2]
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc += st[i + q];
+      out[i] = d[i + 4] * sp[i + 2] - ratio * v[i + 4] * acc;
+    }
+    float4* dst = reinterpret_cast<float4*>(dx + base + c0);
+    if (accumulate) {
+      const float4 o0 = dst[0], o1 = dst[1];
+      out[0] += o0.x; out[1] += o0.y; out[2] += o0.z; out[3] += o0.w;
+      out[4] += o1.x; out[5] += o1.y; out[6] += o1.z; out[7] += o1.w;
+    }
+    dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+    dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+  }
+}
+
 // --------------------------------------------------------------- dropout ---
 // Keep-mask = splitmix64(mix(base ^ step) + nchw_index) >> 40 >= ratio * 2^24.
 __device__ __forceinline__ float drop_mask(const DropGeom& g, uint64_t base, uint32_t i,
@@ -413,8 +504,16 @@ void lrn_launch(K kernel, size_t smem) {
                                   static_cast<int>(smem)));
 }
 
+bool lrn_run_ok(const LrnGeom& g) { return g.size == 5 && g.C % kLrnRun == 0; }
+
 void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s) {
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
+  if (lrn_run_ok(g)) {
+    const uint32_t runs = checked32(static_cast<size_t>(g.pixels) * (g.C / kLrnRun), "lrn");
+    lrn_fwd_run_k<<<grid_for(runs), 256, 0, s>>>(g, x, y, runs);
+    PSG_CUDA(cudaGetLastError());
+    return;
+  }
   const int tp = lrn_tile_pixels(g);
   const size_t smem = static_cast<size_t>(tp) * g.C * sizeof(float);
   auto k = g.size == 5 ? lrn_fwd_k<5> : lrn_fwd_k<0>;
@@ -426,6 +525,12 @@ void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s) {
 void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool accumulate,
              cudaStream_t s) {
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
+  if (lrn_run_ok(g)) {
+    const uint32_t runs = checked32(static_cast<size_t>(g.pixels) * (g.C / kLrnRun), "lrn");
+    lrn_bwd_run_k<<<grid_for(runs), 256, 0, s>>>(g, x, dy, dx, accumulate, runs);
+    PSG_CUDA(cudaGetLastError());
+    return;
+  }
   const int tp = lrn_tile_pixels(g);
   const size_t smem = 4 * static_cast<size_t>(tp) * g.C * sizeof(float);
   auto k = g.size == 5 ? lrn_bwd_k<5> : lrn_bwd_k<0>;
