@@ -228,6 +228,12 @@ int psg_net_test(psg_net* net, long steps, double* accuracy);
  * K nets with first = k, stride = K split one test(steps) exactly. */
 int psg_net_test_begin(psg_net* net, long steps, long first, long stride);
 int psg_net_test_end(psg_net* net, unsigned long long* correct, unsigned long long* total);
+/* ReLU fusion (default on): a conv / linear whose only consumer is a ReLU applies the ReLU
+ * in its GEMM epilogue (its stored output is then the post-ReLU value), and a ReLU feeding
+ * only an LRN has its backward folded into the LRN's (its own gradient buffer is not
+ * written).  Results are bitwise identical; turn it off to inspect every layer's state
+ * (per-layer parity tests). */
+int psg_net_set_fusion(psg_net* net, int on);
 /* Kernel launches of one training step (device-side work count). */
 int psg_net_kernels_per_step(const psg_net* net, int* launches);
 

@@ -115,6 +115,7 @@ SIGNATURES = {
     "psg_net_attach_shard_part": (ctypes.c_int, [_VP, _VP, _U64, _SZ, _SZ, ctypes.c_uint64,
                                                  ctypes.c_int, ctypes.c_int]),
     "psg_net_grad_step": (ctypes.c_int, [_VP]),
+    "psg_net_set_fusion": (ctypes.c_int, [_VP, ctypes.c_int]),
     "psg_net_apply_grads": (ctypes.c_int, [_VP]),
     "psg_average_grads_local": (ctypes.c_int, [_PP, ctypes.c_int]),
     "psg_comm_average_grads": (ctypes.c_int, [_PP, _PP, ctypes.c_int, ctypes.c_int]),

@@ -631,6 +631,16 @@ int psg_net_test_end(psg_net* net, unsigned long long* correct, unsigned long lo
   });
 }
 
+int psg_net_set_fusion(psg_net* net, int on) {
+  return guarded([&] {
+    need(net, "set_fusion");
+    if (net->fuse == (on != 0)) return;
+    psg::release_batch_buffers(net);
+    net->fuse = on != 0;
+    psg::plan_fusion(net);
+  });
+}
+
 int psg_net_kernels_per_step(const psg_net* net, int* launches) {
   return guarded([&] {
     need(net, "kernels_per_step");

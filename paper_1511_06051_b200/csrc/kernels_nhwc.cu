@@ -249,7 +249,7 @@ template <int SIZE>
 __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float* __restrict__ x,
                                                          const float* __restrict__ dy,
                                                          float* __restrict__ dx, int accumulate,
-                                                         int tp) {
+                                                         int relu_mask, int tp) {
   extern __shared__ float sm[];
   const int C = g.C, tile_elems = tp * C;
   float* sx = sm;                   // x
@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float*
     for (int e = threadIdx.x; e < ne; e += kLrnThreads) {
       // channels q whose window contains c: q in [c - post, c + pre]
       const float acc = lrn_window<SIZE, false>(st + (e - c), c, C, -post, g.size);
-      const float v = sd[e] * ssp[e] - ratio * sx[e] * acc;
+      float v = sd[e] * ssp[e] - ratio * sx[e] * acc;
+      if (relu_mask && !(sx[e] > 0.f)) v = 0.f;
       dx[e0 + e] = accumulate ? dx[e0 + e] + v : v;
       c += step;
       if (c >= C) c -= C;
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(256) lrn_fwd_run_k(LrnGeom g, const float* __r
 __global__ void __launch_bounds__(256) lrn_bwd_run_k(LrnGeom g, const float* __restrict__ x,
                                                      const float* __restrict__ dy,
                                                      float* __restrict__ dx, int accumulate,
-                                                     uint32_t total_runs) {
+                                                     int relu_mask, uint32_t total_runs) {
   const int C = g.C, runs = C / kLrnRun;
   const float a = g.alpha / g.size, ratio = 2.f * g.alpha * g.beta / g.size;
   GRID_STRIDE32(r, total_runs) {
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(256) lrn_bwd_run_k(LrnGeom g, const float* __r
 #pragma unroll
       for (int q = 0; q < 5; ++q) acc += st[i + q];
       out[i] = d[i + 4] * sp[i + 2] - ratio * v[i + 4] * acc;
+      if (relu_mask && !(v[i + 4] > 0.f)) out[i] = 0.f;
     }
     float4* dst = reinterpret_cast<float4*>(dx + base + c0);
     if (accumulate) {
@@ -523,11 +525,12 @@ void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s) {
 }
 
 void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool accumulate,
-             cudaStream_t s) {
+             cudaStream_t s, bool relu_mask) {
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
   if (lrn_run_ok(g)) {
     const uint32_t runs = checked32(static_cast<size_t>(g.pixels) * (g.C / kLrnRun), "lrn");
-    lrn_bwd_run_k<<<grid_for(runs), 256, 0, s>>>(g, x, dy, dx, accumulate, runs);
+    lrn_bwd_run_k<<<grid_for(runs), 256, 0, s>>>(g, x, dy, dx, accumulate, relu_mask ? 1 : 0,
+                                                 runs);
     PSG_CUDA(cudaGetLastError());
     return;
   }
@@ -535,7 +538,8 @@ void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool 
   const size_t smem = 4 * static_cast<size_t>(tp) * g.C * sizeof(float);
   auto k = g.size == 5 ? lrn_bwd_k<5> : lrn_bwd_k<0>;
   lrn_launch(k, smem);
-  k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, dy, dx, accumulate, tp);
+  k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, dy, dx, accumulate, relu_mask ? 1 : 0,
+                                                 tp);
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -110,6 +110,8 @@ void validate(const psg_layer_desc* layers, int n) {
 }
 
 void free_batch_buffers(psg_net* net) {
+  for (LayerRt& l : net->L)
+    if (l.fwd_relu >= 0) l.out = nullptr;  // aliases the ReLU's buffer
   for (LayerRt& l : net->L) {
     dfree(l.out);
     dfree(l.grad);
@@ -146,6 +148,27 @@ void invalidate_graph(psg_net* net) {
   net->grad_graph_batch = 0;
 }
 
+void plan_fusion(psg_net* net) {
+  for (LayerRt& l : net->L) l.fwd_relu = l.fused_from = l.bwd_by = l.bwd_relu = -1;
+  if (!net->fuse) return;
+  for (size_t ri = 0; ri < net->L.size(); ++ri) {
+    LayerRt& r = net->L[ri];
+    if (r.kind != PSG_LAYER_RELU) continue;
+    LayerRt& p = net->L[r.inputs[0]];
+    if ((p.kind == PSG_LAYER_CONV || p.kind == PSG_LAYER_LINEAR) && p.consumers.size() == 1) {
+      p.fwd_relu = static_cast<int>(ri);
+      r.fused_from = r.inputs[0];
+    }
+    if (p.kind != PSG_LAYER_DATA && p.consumers.size() == 1 && r.consumers.size() == 1) {
+      LayerRt& c = net->L[r.consumers[0]];
+      if (c.kind == PSG_LAYER_LRN) {
+        r.bwd_by = r.consumers[0];
+        c.bwd_relu = static_cast<int>(ri);
+      }
+    }
+  }
+}
+
 void release_batch_buffers(psg_net* net) {
   DeviceGuard dg(net->ctx->device);
   PSG_CUDA(cudaStreamSynchronize(net->stream));
@@ -164,7 +187,7 @@ void ensure_capacity(psg_net* net, size_t n) {
   for (LayerRt& l : net->L) {
     if (l.kind == PSG_LAYER_LABEL) continue;
     const size_t elems = n * l.vol();
-    l.out = dalloc<float>(elems);
+    if (l.fwd_relu < 0) l.out = dalloc<float>(elems);
     if (l.kind != PSG_LAYER_DATA) l.grad = dalloc<float>(elems);
     if (l.kind == PSG_LAYER_POOL && l.d.pool == PSG_POOL_MAX) l.route = dalloc<uint8_t>(elems);
     if (l.kind == PSG_LAYER_CONV) l.col = dalloc<float>(conv_col_elems(geom_for(l, n), net->mode));
@@ -173,6 +196,8 @@ void ensure_capacity(psg_net* net, size_t n) {
         ws = std::max(ws, conv_workspace_elems(geom_for(l, n), m));
     }
   }
+  for (LayerRt& l : net->L)
+    if (l.fwd_relu >= 0) l.out = net->L[l.fwd_relu].out;
   // the data layer's grad is never produced (first-layer dgrad is skipped)
   net->row_loss = dalloc<double>(n);
   net->labels = dalloc<int32_t>(n);
@@ -459,6 +484,7 @@ void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed)
     }
   }
   if (net->classes < 1) throw std::invalid_argument("net: need at least one class");
+  plan_fusion(net);
   net->P_ref = ref_off;
   net->P_int = int_off;
   // divisible into 4-aligned slices for up to 8 ranks (ordered reduce-scatter)

@@ -85,8 +85,9 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         const TensorRec& b = net->tensors[l.bias_t];
         const ConvGeom g = geom_n(l, n);
         Scope sc(timer, nm.c_str(), lid, 1, conv_flops(net, l, n), 0.0);
-        conv_fprop(g, src.out, net->w + k.int_off, net->w + b.int_off, l.out, false, net->ws,
-                   l.col, net->mode, s);
+        // fused ReLU: l.out aliases the ReLU's buffer and the epilogue applies max(0, .)
+        conv_fprop(g, src.out, net->w + k.int_off, net->w + b.int_off, l.out, l.fwd_relu >= 0,
+                   net->ws, l.col, net->mode, s);
         const int c = conv_launches(g, 0, net->mode);
         sc.done(c);
         launches += c;
@@ -104,6 +105,7 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         break;
       }
       case PSG_LAYER_RELU: {
+        if (l.fused_from >= 0) break;  // computed by the producer's epilogue
         Scope sc(timer, nm.c_str(), lid, 1, 0.0, 2 * act_bytes(l, n));
         relu_fwd(net->L[l.inputs[0]].out, l.out, n * l.vol(), s);
         sc.done(1);
@@ -222,6 +224,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
         }
         break;
       case PSG_LAYER_RELU:
+        if (l.bwd_by >= 0) break;  // done by the consuming LRN's backward
         if (need_dx) {
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
           relu_bwd(src.out, l.grad, src.grad, n * l.vol(), acc, s);
@@ -234,7 +237,13 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
           LrnGeom g = l.lg;
           g.pixels = static_cast<int>(n) * l.H * l.W;
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
-          lrn_bwd(g, src.out, l.grad, src.grad, acc, s);
+          if (l.bwd_relu >= 0) {  // fold the ReLU below: mask by x > 0, write its input grad
+            const int pi2 = net->L[l.bwd_relu].inputs[0];
+            lrn_bwd(g, src.out, l.grad, net->L[pi2].grad, written[pi2] != 0, s, true);
+            written[pi2] = 1;
+          } else {
+            lrn_bwd(g, src.out, l.grad, src.grad, acc, s);
+          }
           sc.done(1);
           ++launches;
         }

@@ -157,8 +157,10 @@ struct LrnGeom {
 };
 // The LRN scale is recomputed in backward from x (not stored).
 void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s);
+// relu_mask: the LRN's input is a ReLU output; write dx * (x > 0), i.e. the gradient at
+// the ReLU's input (the ReLU's own backward is folded in).
 void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool accumulate,
-             cudaStream_t s);
+             cudaStream_t s, bool relu_mask = false);
 
 struct DropGeom {
   int n = 0, C = 0, H = 1, W = 1;  // logical NCHW dims for the counter index

@@ -55,6 +55,11 @@ struct LayerRt {
   uint8_t* route = nullptr;
   float* col = nullptr;  // im2col matrix (TF32 im2col route only)
   std::vector<int> coff;  // concat: channel offset of each input
+  // ReLU fusion (psg_net_set_fusion): a conv / linear whose only consumer is a ReLU writes
+  // relu(out) into the ReLU's buffer from its epilogue (fwd_relu = that ReLU, out aliases
+  // it); a ReLU whose only consumer is an LRN has its backward folded into the LRN's
+  // (bwd_by = that LRN; the LRN masks with its input and writes the ReLU's input grad).
+  int fwd_relu = -1, fused_from = -1, bwd_by = -1, bwd_relu = -1;
   int kern_t = -1, bias_t = -1;
   ConvGeom cg;  // conv / linear (per-example; n filled per call)
   PoolGeom pg;
@@ -87,6 +92,7 @@ struct psg_net {
   int nchunks = 0;
   double lr = 0.01, mu = 0.0, wd = 0.0;
   psg::Mode mode = psg::Mode::Strict;
+  bool fuse = true;
   psg::DeviceScalars* dsc = nullptr;
   psg::DeviceScalars* hsc = nullptr;  // pinned mirror
   double* row_loss = nullptr;
@@ -154,6 +160,7 @@ int run_update(psg_net* net, bool advance, OpTimer* timer = nullptr);
 void ensure_capacity(psg_net* net, size_t n);
 void release_batch_buffers(psg_net* net);  // drops activations + graphs; realloc on demand
 void invalidate_graph(psg_net* net);
+void plan_fusion(psg_net* net);
 
 void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, int* n_ops);
 void net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,

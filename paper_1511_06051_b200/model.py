@@ -73,7 +73,10 @@ def device_count() -> int:
 class Net:
     """A trainable realisation of a NetSpec on one GPU (model.hpp:50)."""
 
-    def __init__(self, spec: NetSpec, seed: int, device: int = 0, precision: str = "fp32"):
+    def __init__(self, spec: NetSpec, seed: int, device: int = 0, precision: str = "fp32",
+                 fuse: bool = True):
+        """fuse: ReLU fusion (psg_net_set_fusion; bitwise-identical results).  Pass False
+        to read every layer's pre-activation output / gradient (per-layer parity tests)."""
         spec.validate()
         self._spec = spec
         self._seed = seed
@@ -96,6 +99,8 @@ class Net:
         self._val_it: Optional[SequentialBatchIterator] = None
         self._structure = self._read_structure()
         self.set_precision(precision)
+        if not fuse:
+            _lib.call("psg_net_set_fusion", h, 0)
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -36,7 +36,7 @@ def test_googlenet_structure(spec, oracle_lib):
 def test_googlenet_per_layer_parity(spec, oracle_lib, precision):
     from paper_1511_06051_b200.model import Batch, Net
     bar = BARS[precision]
-    net = Net(spec, 11, precision=precision)
+    net = Net(spec, 11, precision=precision, fuse=False)
     orc = oracle_lib.net(spec, 11)
     orc.set_weights(net.get_weights_flat())
     rng = np.random.default_rng(3)

@@ -47,7 +47,7 @@ def gpu():
 
 
 def _pair(gpu, oracle_lib, spec, seed):
-    net = gpu.Net(spec, seed)
+    net = gpu.Net(spec, seed, fuse=False)  # per-layer state is inspected
     orc = oracle_lib.net(spec, seed)
     return net, orc
 
@@ -296,3 +296,25 @@ def test_max_pool_tie_routes_to_lowest_index(gpu):
     p0, p1 = out.probabilities[0]
     dpool = (p0 - 1.0) - p1
     np.testing.assert_allclose(dk, [dpool * 1.0, dpool * 2.0], rtol=STRICT)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("name", ["cifar10_quick", "caffe_mix"])
+def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
+    """psg_net_set_fusion: the ReLU applied in the GEMM epilogue and the ReLU backward
+    folded into the LRN give bitwise-identical training to the unfused graph."""
+    from paper_1511_06051_b200 import data
+    spec = micro_nets()[name]
+    d = spec.data_spec().shape
+    img, lab = oracle_lib.generate_synthetic(10, d[1], d[2], d[3], 6, 2.0, 12345, 0)
+    ds = data.Dataset(f32(img), lab % 5 if name == "caffe_mix" else lab,
+                      5 if name == "caffe_mix" else 10)
+    out = []
+    for fuse in (True, False):
+        net = gpu.Net(spec, 3, precision=precision, fuse=fuse)
+        net.set_sgd(gpu.SgdOptions(0.01, 0.9, 0.001))
+        net.set_training_data(data.make_worker_iterator(data.shard(ds, 1, 1), 0, d[0], 1))
+        net.train(3)
+        out.append((net.get_weights_flat(), net.last_loss()))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]

@@ -50,7 +50,7 @@ def gpu():
 @pytest.mark.parametrize("name", list(tc_nets()))
 def test_tf32_per_layer_parity(gpu, oracle_lib, name):
     spec = tc_nets()[name]
-    net = gpu.Net(spec, 31, precision="tf32")
+    net = gpu.Net(spec, 31, precision="tf32", fuse=False)
     orc = oracle_lib.net(spec, 31)
     orc.set_weights(net.get_weights_flat())
     rng = np.random.default_rng(11)

@@ -22,7 +22,7 @@ def main(names):
     orc_lib = OracleLib()
     for name in names:
         spec = tc_nets()[name]
-        net = model.Net(spec, 31, precision="tf32")
+        net = model.Net(spec, 31, precision="tf32", fuse=False)
         orc = orc_lib.net(spec, 31)
         orc.set_weights(net.get_weights_flat())
         rng = np.random.default_rng(11)
