@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cifar10_quick", choices=list(WORKLOADS))
     p.add_argument("--tau", type=int, default=10)
+    p.add_argument("--batch", type=int, default=None,
+                   help="per-worker batch override (exploration; default: the config's)")
     # tf32 = tcgen05 tensor cores (north star's fast mode, per-layer parity 1e-2);
     # fp32 = strict SIMT mode (parity 1e-5)
     p.add_argument("--precision", default="tf32", choices=["fp32", "tf32"])
@@ -129,9 +131,10 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_spec(workload):
+def make_spec(workload, batch=None):
     from paper_1511_06051_b200 import netspec
     name, b, _, _, *_ = WORKLOADS[workload]
+    b = batch or b
     return getattr(netspec, name)(b), b
 
 
@@ -188,7 +191,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    spec, b = make_spec(args.workload)
+    spec, b = make_spec(args.workload, args.batch)
     threads = max(1, args.gpus)
     t = []
     for i in range(args.warmup + args.steps):
@@ -227,7 +230,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo")
     K = world
-    spec, b = make_spec(args.workload)
+    spec, b = make_spec(args.workload, args.batch)
     _, _, (c, h, w), _, lr, mu, wd = WORKLOADS[args.workload]
     ds = build_dataset(args.workload, K)
     shards = pdata.shard(ds, K, 1)
