@@ -140,6 +140,10 @@ ConvGeom geom_for(const LayerRt& l, size_t n) {
 void invalidate_graph(psg_net* net) {
   if (net->graph) cudaGraphExecDestroy(net->graph);
   if (net->host_graph) cudaGraphExecDestroy(net->host_graph);
+  for (auto& gx : net->host_graph2) {
+    if (gx) cudaGraphExecDestroy(gx);
+    gx = nullptr;
+  }
   if (net->grad_graph) cudaGraphExecDestroy(net->grad_graph);
   net->graph = nullptr;
   net->host_graph = nullptr;
@@ -542,6 +546,13 @@ void net_free(psg_net* net) {
   if (net->h_stage) cudaFreeHost(net->h_stage);
   if (net->h_lab) cudaFreeHost(net->h_lab);
   dfree(net->d_stage);
+  for (int k = 0; k < 2; ++k) {
+    dfree(net->d_stage2[k]);
+    dfree(net->d_lab2[k]);
+    if (net->copied[k]) cudaEventDestroy(net->copied[k]);
+    if (net->consumed[k]) cudaEventDestroy(net->consumed[k]);
+  }
+  if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
   if (net->h_losses) cudaFreeHost(net->h_losses);
   for (cudaEvent_t e : net->slots)
     if (e) cudaEventDestroy(e);

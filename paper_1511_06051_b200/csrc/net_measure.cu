@@ -101,13 +101,36 @@ void net_train_host(psg_net* net, const float* images, const int32_t* labels, lo
     if (losses) std::memcpy(losses, net->h_losses, steps * sizeof(double));
     return;
   }
-  if (!net->host_graph || net->graph_batch != b) {
-    if (net->graph_batch != b) invalidate_graph(net);
-    if (net->host_graph) cudaGraphExecDestroy(net->host_graph);
+  // Graph path: two staging buffers, the H2D copies on a copy stream.  Step s waits for
+  // its buffer's copy; the copy of step s+1 (other buffer) runs during step s.
+  if (net->d_stage2_cap < b * chw) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    for (int k = 0; k < 2; ++k) {
+      if (net->d_stage2[k]) cudaFree(net->d_stage2[k]);
+      if (net->d_lab2[k]) cudaFree(net->d_lab2[k]);
+      PSG_CUDA(cudaMalloc(&net->d_stage2[k], b * chw * sizeof(float)));
+      PSG_CUDA(cudaMalloc(&net->d_lab2[k], b * sizeof(int32_t)));
+      if (net->host_graph2[k]) cudaGraphExecDestroy(net->host_graph2[k]);
+      net->host_graph2[k] = nullptr;
+    }
+    net->d_stage2_cap = b * chw;
+  }
+  if (!net->copy_stream) {
+    PSG_CUDA(cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      PSG_CUDA(cudaEventCreateWithFlags(&net->copied[k], cudaEventDisableTiming));
+      PSG_CUDA(cudaEventCreateWithFlags(&net->consumed[k], cudaEventDisableTiming));
+    }
+  }
+  if (net->graph_batch != b) invalidate_graph(net);
+  for (int k = 0; k < 2; ++k) {
+    if (net->host_graph2[k]) continue;
     cudaGraph_t graph;
     PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
     try {
-      stage_batch_nchw(net->d_stage, static_cast<int>(b), d.C, d.H, d.W, d.cs, d.out,
+      PSG_CUDA(cudaMemcpyAsync(net->labels, net->d_lab2[k], b * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice, net->stream));
+      stage_batch_nchw(net->d_stage2[k], static_cast<int>(b), d.C, d.H, d.W, d.cs, d.out,
                        net->stream);
       run_forward(net, b, true, true);
       run_backward(net, b);
@@ -117,17 +140,26 @@ void net_train_host(psg_net* net, const float* images, const int32_t* labels, lo
       throw;
     }
     PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
-    PSG_CUDA(cudaGraphInstantiate(&net->host_graph, graph, 0));
+    PSG_CUDA(cudaGraphInstantiate(&net->host_graph2[k], graph, 0));
     cudaGraphDestroy(graph);
-    net->graph_batch = b;
   }
+  net->graph_batch = b;
   PSG_CUDA(cudaEventRecord(net->t0, net->stream));
+  PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->t0, 0));  // copies inside the timing
+  for (int k = 0; k < 2; ++k) {  // buffers are free once the stream's prior work is done
+    PSG_CUDA(cudaEventRecord(net->consumed[k], net->stream));
+  }
   for (long s = 0; s < steps; ++s) {
-    PSG_CUDA(cudaMemcpyAsync(net->d_stage, images + s * b * chw, b * chw * sizeof(float),
-                             cudaMemcpyHostToDevice, net->stream));
-    PSG_CUDA(cudaMemcpyAsync(net->labels, labels + s * b, b * sizeof(int32_t),
-                             cudaMemcpyHostToDevice, net->stream));
-    PSG_CUDA(cudaGraphLaunch(net->host_graph, net->stream));
+    const int k = static_cast<int>(s & 1);
+    PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->consumed[k], 0));
+    PSG_CUDA(cudaMemcpyAsync(net->d_stage2[k], images + s * b * chw, b * chw * sizeof(float),
+                             cudaMemcpyHostToDevice, net->copy_stream));
+    PSG_CUDA(cudaMemcpyAsync(net->d_lab2[k], labels + s * b, b * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, net->copy_stream));
+    PSG_CUDA(cudaEventRecord(net->copied[k], net->copy_stream));
+    PSG_CUDA(cudaStreamWaitEvent(net->stream, net->copied[k], 0));
+    PSG_CUDA(cudaGraphLaunch(net->host_graph2[k], net->stream));
+    PSG_CUDA(cudaEventRecord(net->consumed[k], net->stream));
     PSG_CUDA(cudaMemcpyAsync(net->h_losses + s, &net->dsc->loss, sizeof(double),
                              cudaMemcpyDeviceToHost, net->stream));
   }

@@ -130,9 +130,16 @@ struct psg_net {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   bool timed = false;
   // host-fed (e2e) training: NCHW staging buffer + its own step graph
-  float* d_stage = nullptr;
+  float* d_stage = nullptr;        // eager path (one buffer)
   size_t d_stage_cap = 0;
   cudaGraphExec_t host_graph = nullptr;
+  // graph path: double-buffered staging, H2D of step s+1 on copy_stream overlaps step s
+  float* d_stage2[2] = {nullptr, nullptr};
+  int32_t* d_lab2[2] = {nullptr, nullptr};
+  size_t d_stage2_cap = 0;
+  cudaGraphExec_t host_graph2[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
   double* h_losses = nullptr;
   size_t h_losses_cap = 0;
   cudaEvent_t slots[16] = {};

@@ -318,3 +318,29 @@ def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
         out.append((net.get_weights_flat(), net.last_loss()))
     np.testing.assert_array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+def test_train_host_matches_device_stream(gpu, oracle_lib):
+    """psg_net_train_host (host batches, double-buffered H2D overlapping the steps) ==
+    psg_net_train on the HBM-resident stream with the same batch order, bitwise."""
+    from paper_1511_06051_b200 import data
+    from paper_1511_06051_b200._lib import PinnedArray
+    spec = ns.make_cifar10_quick(10)
+    ds = _dataset(gpu, oracle_lib, spec, 6)
+    shards = data.shard(ds, 1, 4)
+    a = gpu.Net(spec, 2, precision="tf32")
+    b = gpu.Net(spec, 2, precision="tf32")
+    for n in (a, b):
+        n.set_sgd(gpu.SgdOptions(0.01, 0.9, 0.004))
+    a.set_training_data(data.make_worker_iterator(shards, 0, 10, 4))
+    a.train(5)
+    it = data.make_worker_iterator(shards, 0, 10, 4)
+    img = PinnedArray((5, 10, 3, 32, 32), np.float32)
+    lab = PinnedArray((5, 10), np.int32)
+    for s in range(5):
+        idx = it.next_indices().astype(np.int64)
+        img.array[s] = ds.images[idx]
+        lab.array[s] = ds.labels[idx]
+    losses = b.train_host(img.array, lab.array)
+    np.testing.assert_array_equal(a.get_weights_flat(), b.get_weights_flat())
+    assert losses[-1] == a.last_loss()
