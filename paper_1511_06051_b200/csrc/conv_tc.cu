@@ -178,7 +178,18 @@ void finish_args(TcArgs& a, int kblk, int sms) {
                                       : kTileM / 32;
   a.a_tx = a_mn ? a.a_chunks * 32 * kblk * 4 : a.a_bytes;
   a.stage_bytes = a.a_bytes + nb * kblk * 4;
-  a.stages = std::min(8, (225 * 1024 - kEpiBytes) / a.stage_bytes);
+  // narrow K blocks (small slots) are grouped kps per pipeline stage: fewer barrier round
+  // trips per MMA (PSG_TC_KPS overrides)
+  static const int kps_env = [] {
+    const char* e = std::getenv("PSG_TC_KPS");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  a.kps = kps_env ? kps_env : (a.stage_bytes <= 24 * 1024 ? 2 : 1);
+  a.stages = std::min(8, (225 * 1024 - kEpiBytes) / (a.kps * a.stage_bytes));
+  if (a.stages < 2) {
+    a.kps = 1;
+    a.stages = std::min(8, (225 * 1024 - kEpiBytes) / a.stage_bytes);
+  }
   static const int producers = [] {
     const char* e = std::getenv("PSG_TC_PRODUCERS");
     const int v = e ? std::atoi(e) : kMaxProducers;
@@ -232,7 +243,7 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     a.ws_stride = out_elems;
   }
   const dim3 grid(static_cast<unsigned>(std::min<long long>(a.total_tiles, sm_count())));
-  const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + kEpiBytes + 1024;
+  const size_t smem = static_cast<size_t>(a.stages) * a.kps * a.stage_bytes + kEpiBytes + 1024;
   if (kblk == 32) {
     PSG_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));

@@ -34,7 +34,8 @@ constexpr int kEpiBytes = 4 * 32 * kStagePad * 4;
 struct TcArgs {
   int a_mode, b_mode, row_map;
   int n_tile;             // UMMA N (multiple of 16, <= 256)
-  int stage_bytes, a_bytes, stages;
+  int stage_bytes, a_bytes, stages;  // stage_bytes: one K block's A + B (a "slot")
+  int kps;                // K blocks per pipeline stage (slots per stage)
   int a_chunks;           // MN-major A: 32-row chunks actually loaded (M tail skipped)
   int producers;          // TMA producer warps (<= kMaxProducers)
   int a_tx;               // A bytes landing per stage (expect_tx)
@@ -229,7 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  float* epi = reinterpret_cast<float*>(smem + static_cast<size_t>(p.stages) * p.stage_bytes);
+  float* epi = reinterpret_cast<float*>(smem + static_cast<size_t>(p.stages) * p.kps *
+                                        p.stage_bytes);
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
 
@@ -278,18 +280,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.b_mode == B_TAPS_MN) tap_chunks(p, t, jb, tk);
       KCursor c;
       c.init(p, kb0);
-      for (int kb = kb0; kb < kb1; ++kb, ++it, c.next(p)) {
-        if (static_cast<int>(it % p.producers) != pw) continue;
+      for (int kb = kb0; kb < kb1; ++it) {  // one pipeline stage = up to kps K blocks
+        const int cnt = min(p.kps, kb1 - kb);
+        if (static_cast<int>(it % p.producers) != pw) {
+          for (int j = 0; j < cnt; ++j, ++kb) c.next(p);
+          continue;
+        }
         const uint32_t s = it % p.stages;
         const uint32_t bar = tc::smem_u32(&full_bar[s]);
         if (lane == 0) {
           tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ((it / p.stages) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(bar, bytes);
+          tc::mbar_arrive_expect_tx(bar, bytes * cnt);
         }
         __syncwarp();
-        const uint32_t sa = tc::smem_u32(smem + s * p.stage_bytes);
-        load_a<KBLK>(p, &map_a, t, c, rb, oh0, ow0, sa, bar, ja);
-        load_b<KBLK>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, jb);
+        for (int j = 0; j < cnt; ++j, ++kb, c.next(p)) {
+          const uint32_t sa = tc::smem_u32(smem + (s * p.kps + j) * p.stage_bytes);
+          load_a<KBLK>(p, &map_a, t, c, rb, oh0, ow0, sa, bar, ja);
+          load_b<KBLK>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, jb);
+        }
       }
     }
   } else if (warp == kMmaWarp && lane == 0) {
@@ -308,19 +316,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(tc::smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
       tc::fence_after_sync();
       const uint32_t d = tmem + acc * kAccCols;
-      for (int i = 0; i < nkb; ++i, ++it) {
+      for (int i = 0; i < nkb; ++it) {
+        const int cnt = min(p.kps, nkb - i);
         const uint32_t s = it % p.stages;
         tc::mbar_wait(tc::smem_u32(&full_bar[s]), (it / p.stages) & 1);
         tc::fence_after_sync();
-        const uint32_t sa = tc::smem_u32(smem + s * p.stage_bytes);
-        const uint32_t sb = sa + p.a_bytes;
+        for (int q = 0; q < cnt; ++q, ++i) {
+          const uint32_t sa = tc::smem_u32(smem + (s * p.kps + q) * p.stage_bytes);
+          const uint32_t sb = sa + p.a_bytes;
 #pragma unroll
-        for (int j = 0; j < KBLK / 8; ++j) {
-          const uint64_t ad = a_mn ? tc::smem_desc(sa + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
-                                   : tc::smem_desc(sa + j * 32, 16, k_sbo, k_sw);
-          const uint64_t bd = b_mn ? tc::smem_desc(sb + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
-                                   : tc::smem_desc(sb + j * 32, 16, k_sbo, k_sw);
-          tc::mma_tf32(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+          for (int j = 0; j < KBLK / 8; ++j) {
+            const uint64_t ad = a_mn ? tc::smem_desc(sa + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
+                                     : tc::smem_desc(sa + j * 32, 16, k_sbo, k_sw);
+            const uint64_t bd = b_mn ? tc::smem_desc(sb + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
+                                     : tc::smem_desc(sb + j * 32, 16, k_sbo, k_sw);
+            tc::mma_tf32(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+          }
         }
         tc::mma_commit(tc::smem_u32(&empty_bar[s]));
       }
