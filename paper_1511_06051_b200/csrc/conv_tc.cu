@@ -178,13 +178,13 @@ void finish_args(TcArgs& a, int kblk, int sms) {
                                       : kTileM / 32;
   a.a_tx = a_mn ? a.a_chunks * 32 * kblk * 4 : a.a_bytes;
   a.stage_bytes = a.a_bytes + nb * kblk * 4;
-  // narrow K blocks (small slots) are grouped kps per pipeline stage: fewer barrier round
-  // trips per MMA (PSG_TC_KPS overrides)
+  // narrow K blocks (small slots) are grouped kps per pipeline stage, ~48 KB per stage:
+  // fewer barrier round trips per MMA (PSG_TC_KPS overrides)
   static const int kps_env = [] {
     const char* e = std::getenv("PSG_TC_KPS");
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
-  a.kps = kps_env ? kps_env : (a.stage_bytes <= 24 * 1024 ? 2 : 1);
+  a.kps = kps_env ? kps_env : std::max(1, std::min(4, 48 * 1024 / a.stage_bytes));  // ~48 KB
   a.stages = std::min(8, (225 * 1024 - kEpiBytes) / (a.kps * a.stage_bytes));
   if (a.stages < 2) {
     a.kps = 1;
