@@ -242,6 +242,9 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     a.ws = ws;
     a.ws_stride = out_elems;
   }
+  // float4 epilogue stores need 16-byte aligned rows and 4-column-aligned validity bounds
+  a.epi_vec = a.ldo % 4 == 0 && a.col_g % 4 == 0 && a.col_tap % 4 == 0 &&
+              (a.cpt ? a.cgs % 4 == 0 : a.n_valid % 4 == 0);
   const dim3 grid(static_cast<unsigned>(std::min<long long>(a.total_tiles, sm_count())));
   const size_t smem = static_cast<size_t>(a.stages) * a.kps * a.stage_bytes + kEpiBytes + 1024;
   if (kblk == 32) {

@@ -28,8 +28,7 @@ constexpr int kMmaWarp = 4, kAllocWarp = 5, kEpiWarp0 = 8;
 constexpr int kThreads = 384;
 constexpr int kTileM = 128;
 constexpr int kAccCols = 256;                 // one accumulator: 128 lanes x 256 fp32
-constexpr int kStagePad = 33;                 // epilogue transpose row pitch (floats)
-constexpr int kEpiBytes = 4 * 32 * kStagePad * 4;
+constexpr int kEpiBytes = 0;                  // the epilogue needs no shared memory
 
 struct TcArgs {
   int a_mode, b_mode, row_map;
@@ -68,6 +67,7 @@ struct TcArgs {
   // 32); column vc -> tap vc / cpt, channel vc % cpt (valid below cgs); dW column tap*cgs + c
   int ntaps, cpt, cgs;
   int valid_cols;         // split-K reduce: dW row padding columns (>= Kf) zeroed
+  int epi_vec;            // epilogue: float4 stores (16-byte aligned rows and column runs)
 };
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
@@ -230,8 +230,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  float* epi = reinterpret_cast<float*>(smem + static_cast<size_t>(p.stages) * p.kps *
-                                        p.stage_bytes);
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
 
@@ -340,7 +338,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - kEpiWarp0;
-    float* stg = epi + ew * 32 * kStagePad;
     uint32_t local = 0;
     for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x, ++local) {
       const Tile t = decode_tile(p, tt);
@@ -366,52 +363,90 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(tc::smem_u32(&tfull_bar[acc]), (local >> 1) & 1);
       tc::fence_after_sync();
       const uint32_t taddr = tmem + acc * kAccCols + (static_cast<uint32_t>(ew * 32) << 16);
+      // Thread = one accumulator row (its TMEM lane): the 32-column chunks stream out of
+      // TMEM double-buffered (the load of chunk c0+32 overlaps the stores of chunk c0) and
+      // go straight to global memory as float4 runs of the thread's row (no smem
+      // transpose); bias / ReLU / accumulate applied in registers.
       const int c_end = __any_sync(0xffffffffu, row_ok) ? p.n_tile : 0;  // idle rows: skip
+      const bool acc_out = p.accumulate && !p.ws;
+      float* rowp = base + row_off;
+      uint32_t va[32], vb[32];
+      if (c_end > 0) {
+        tc::tmem_ld32_async(taddr, va);
+        tc::tmem_wait_ld();
+      }
       for (int c0 = 0; c0 < c_end; c0 += 32) {
-        float v[32];
-        tc::tmem_ld16(taddr + c0, v);
-        if (c0 + 16 < p.n_tile) tc::tmem_ld16(taddr + c0 + 16, v + 16);
+        const bool more = c0 + 32 < c_end;
+        if (more) tc::tmem_ld32_async(taddr + c0 + 32, vb);
+        if (row_ok) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) stg[lane * kStagePad + q] = v[q];
-        __syncwarp();
-        int cidx;  // output column of this lane
-        bool col_ok;
-        if (p.cpt) {
-          const int vc = t.n * p.n_tile + c0, tap = vc / p.cpt, cc = vc % p.cpt + lane;
-          col_ok = c0 + lane < p.n_tile && tap < p.ntaps && cc < p.cgs;
-          cidx = tap * p.cgs + cc;
-        } else {
-          col_ok = c0 + lane < nvalid;
-          cidx = col0 + c0 + lane;
-        }
-        float bv = 0.f;
-        if (col_ok && p.bias && !p.ws) bv = p.bias[cidx];
-        const bool acc_out = p.accumulate && !p.ws;
-        float prev[32];  // accumulate: issue the 32 row loads before any store (ILP)
-        if (acc_out) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const bool ok = __shfl_sync(0xffffffffu, row_ok, i);
-            const long long ro = __shfl_sync(0xffffffffu, row_off, i);
-            prev[i] = ok && col_ok ? base[ro + cidx] : 0.f;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const bool ok = __shfl_sync(0xffffffffu, row_ok, i);
-          const long long ro = __shfl_sync(0xffffffffu, row_off, i);
-          if (!ok || !col_ok) continue;
-          float y = stg[i * kStagePad + lane];
-          if (!p.ws) {
-            if (p.bias) {
-              y += bv;
-              if (p.relu) y = y > 0.f ? y : 0.f;
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const int c = c0 + 4 * q4;  // column within the tile
+            int cidx;
+            bool ok;
+            if (p.cpt) {
+              const int vc = t.n * p.n_tile + c, tap = vc / p.cpt, cc = vc % p.cpt;
+              ok = c < p.n_tile && tap < p.ntaps && cc < p.cgs;
+              cidx = tap * p.cgs + cc;
+            } else {
+              ok = c < nvalid;
+              cidx = col0 + c;
             }
-            if (acc_out) y += prev[i];
+            if (!ok) continue;
+            float4 y = make_float4(__uint_as_float(va[4 * q4]), __uint_as_float(va[4 * q4 + 1]),
+                                   __uint_as_float(va[4 * q4 + 2]), __uint_as_float(va[4 * q4 + 3]));
+            if (p.epi_vec) {
+              float4* dst = reinterpret_cast<float4*>(rowp + cidx);
+              if (!p.ws) {
+                if (p.bias) {
+                  const float4 bb = *reinterpret_cast<const float4*>(p.bias + cidx);
+                  y.x += bb.x; y.y += bb.y; y.z += bb.z; y.w += bb.w;
+                  if (p.relu) {
+                    y.x = y.x > 0.f ? y.x : 0.f;
+                    y.y = y.y > 0.f ? y.y : 0.f;
+                    y.z = y.z > 0.f ? y.z : 0.f;
+                    y.w = y.w > 0.f ? y.w : 0.f;
+                  }
+                }
+                if (acc_out) {
+                  const float4 o = *dst;
+                  y.x += o.x; y.y += o.y; y.z += o.z; y.w += o.w;
+                }
+              }
+              *dst = y;
+            } else {  // unaligned outputs: element stores, each column checked
+              const float e4[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                int ce;
+                bool oke;
+                if (p.cpt) {
+                  const int vc = t.n * p.n_tile + c + e, tap = vc / p.cpt, cc = vc % p.cpt;
+                  oke = c + e < p.n_tile && tap < p.ntaps && cc < p.cgs;
+                  ce = tap * p.cgs + cc;
+                } else {
+                  oke = c + e < nvalid;
+                  ce = col0 + c + e;
+                }
+                if (!oke) continue;
+                float yv = e4[e];
+                if (!p.ws) {
+                  if (p.bias) {
+                    yv += p.bias[ce];
+                    if (p.relu) yv = yv > 0.f ? yv : 0.f;
+                  }
+                  if (acc_out) yv += rowp[ce];
+                }
+                rowp[ce] = yv;
+              }
+            }
           }
-          base[ro + cidx] = y;
         }
-        __syncwarp();
+        if (more) {
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 32; ++q) va[q] = vb[q];
+        }
       }
       tc::fence_before_sync();
       mbar_arrive(tc::smem_u32(&tempty_bar[acc]));
