@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -169,9 +170,31 @@ int pick_n_tile(int N) {
   return (per + 15) / 16 * 16;
 }
 
+// CTA pairs (cta_group::2, M = 256 per MMA): for K-major A (M = pixels / rows) with at
+// least two M tiles.  The pair halves each CTA's share of B and doubles the MMA's M, which
+// lifts the tensor-pipe ceiling (tools/tma_bench.cu: one CTA's M = 128 MMAs take a fixed
+// ~200 cycles each for N <= 256, a pair's M = 256 MMA reaches ~1.1 PFLOP/s at N >= 128).
+// MN-major B is loaded in 32-column chunks, so each half must be whole chunks (N % 64).
+bool want_pair(const TcArgs& a) {
+  static const int env = [] {
+    const char* e = std::getenv("PSG_TC_PAIR");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!env) return false;
+  if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K) return false;
+  return a.m_tiles >= 2;
+}
+
 void finish_args(TcArgs& a, int kblk, int sms) {
   const bool b_mn = a.b_mode != B_2D_K && a.b_mode != B_3D_K;
-  const int nb = b_mn ? (a.n_tile + 31) / 32 * 32 : a.n_tile;
+  a.pair = want_pair(a) ? 1 : 0;
+  if (a.pair && b_mn && a.n_tile % 64) {
+    a.n_tile = std::min(256, (a.n_tile + 63) / 64 * 64);  // pad: the extra columns read 0
+    a.n_tiles = (a.n_valid + a.n_tile - 1) / a.n_tile;
+  }
+  a.b_cols = a.pair ? a.n_tile / 2 : a.n_tile;
+  a.m_units = a.pair ? (a.m_tiles + 1) / 2 : a.m_tiles;
+  const int nb = b_mn ? (a.b_cols + 31) / 32 * 32 : a.b_cols;
   a.a_bytes = kTileM * kblk * 4;
   const bool a_mn = a.a_mode == A_RECT_MN || a.a_mode == A_2D_MN;
   a.a_chunks = a_mn && a.m_tiles == 1 ? std::min(kTileM / 32, (a.m_valid + 31) / 32)
@@ -197,7 +220,8 @@ void finish_args(TcArgs& a, int kblk, int sms) {
   }();
   // a producer may only run one ring ahead of the slot it refills (parity waits): <= stages
   a.producers = std::min(producers, a.stages);
-  const long long tiles = static_cast<long long>(a.m_tiles) * a.n_tiles * a.G * a.taps;
+  const long long tiles = static_cast<long long>(a.m_units) * a.n_tiles * a.G * a.taps;
+  if (a.pair) sms /= 2;  // one work unit per cluster
   // Split K so that the persistent grid's waves are full: minimise
   // waves(tiles * s) * ceil(kblocks / s) (+ a small charge per extra split for the partials
   // and the reduce pass); at least 4 K blocks per split.
@@ -245,17 +269,38 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   // float4 epilogue stores need 16-byte aligned rows and 4-column-aligned validity bounds
   a.epi_vec = a.ldo % 4 == 0 && a.col_g % 4 == 0 && a.col_tap % 4 == 0 &&
               (a.cpt ? a.cgs % 4 == 0 : a.n_valid % 4 == 0);
-  const dim3 grid(static_cast<unsigned>(std::min<long long>(a.total_tiles, sm_count())));
   const size_t smem = static_cast<size_t>(a.stages) * a.kps * a.stage_bytes + kEpiBytes + 1024;
-  if (kblk == 32) {
-    PSG_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int per = a.pair ? 2 : 1;
+  static const bool debug = std::getenv("PSG_TC_DEBUG") != nullptr;
+  if (debug)
+    std::fprintf(stderr,
+                 "tc: a%d b%d pair %d m_tiles %d m_units %d n_tile %d x%d G %d taps %d kblocks %d "
+                 "splits %d kps %d stages %d producers %d smem %zu\n",
+                 a.a_mode, a.b_mode, a.pair, a.m_tiles, a.m_units, a.n_tile, a.n_tiles, a.G,
+                 a.taps, a.kblocks, splits, a.kps, a.stages, a.producers, smem);
+  const unsigned units =
+      static_cast<unsigned>(std::min<long long>(a.total_tiles, sm_count() / per));
+  auto go = [&](auto kern) {
+    PSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    tc_gemm_kernel<32><<<grid, kThreads, smem, s>>>(ma, mb, a);
-  } else {
-    PSG_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    tc_gemm_kernel<16><<<grid, kThreads, smem, s>>>(ma, mb, a);
-  }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units * per);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = per;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.pair ? 1 : 0;
+    PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, a));
+  };
+  if (kblk == 32)
+    a.pair ? go(tc_gemm_kernel<32, true>) : go(tc_gemm_kernel<32, false>);
+  else
+    a.pair ? go(tc_gemm_kernel<16, true>) : go(tc_gemm_kernel<16, false>);
   PSG_CUDA(cudaGetLastError());
   if (splits > 1) {
     const int blocks = static_cast<int>(std::min<long long>((out_elems + 255) / 256, 148 * 8));
@@ -554,7 +599,7 @@ void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bi
   CUtensorMap ma, mb;
   if (a.a_mode == A_2D_K) {
     ma = map_2d(x, g.n, g.cs_in, kblk, kTileM, k_swizzle(kblk));
-    mb = map_2d(w, g.F, g.cs_in, kblk, a.n_tile, k_swizzle(kblk));
+    mb = map_2d(w, g.F, g.cs_in, kblk, a.b_cols, k_swizzle(kblk));
   } else {
     ma = map_nhwc(x, g.n, g.H, g.W, g.cs_in, kblk, a.wm, a.rm, k_swizzle(kblk));
     if (a.b_mode == B_3D_K) {
@@ -562,10 +607,10 @@ void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bi
                                 static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.F)};
       const uint64_t str[2] = {static_cast<uint64_t>(g.Cgs()) * 4,
                                static_cast<uint64_t>(g.Kp()) * 4};
-      const uint32_t box[3] = {static_cast<uint32_t>(kblk), 1, static_cast<uint32_t>(a.n_tile)};
+      const uint32_t box[3] = {static_cast<uint32_t>(kblk), 1, static_cast<uint32_t>(a.b_cols)};
       mb = make_map(w, 3, dims, str, box, k_swizzle(kblk));
     } else {
-      mb = map_2d(w, g.F, g.Kp(), kblk, a.n_tile, k_swizzle(kblk));
+      mb = map_2d(w, g.F, g.Kp(), kblk, a.b_cols, k_swizzle(kblk));
     }
   }
   launch(a, ma, mb, kblk, static_cast<long long>(g.n) * g.OH * g.OW * g.F, ws.ptr, ws.elems, s);

@@ -47,29 +47,66 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+#define PSG_TMA_ASM(DIM, GROUP, COORDS, BAR, ...)                                       \
+  asm volatile("cp.async.bulk.tensor." DIM GROUP                                       \
+               ".shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, " COORDS \
+               "], [" BAR "];" ::__VA_ARGS__                                           \
+               : "memory")
+template <bool PAIR = false>
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if constexpr (PAIR)
+    PSG_TMA_ASM("2d", ".cta_group::2", "{%2, %3}", "%4", "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(bar));
+  else
+    PSG_TMA_ASM("2d", "", "{%2, %3}", "%4", "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(bar));
 }
+template <bool PAIR = false>
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if constexpr (PAIR)
+    PSG_TMA_ASM("3d", ".cta_group::2", "{%2, %3, %4}", "%5", "r"(dst), "l"(m), "r"(c0), "r"(c1),
+                "r"(c2), "r"(bar));
+  else
+    PSG_TMA_ASM("3d", "", "{%2, %3, %4}", "%5", "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2),
+                "r"(bar));
 }
+template <bool PAIR = false>
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
-      : "memory");
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if constexpr (PAIR)
+    PSG_TMA_ASM("4d", ".cta_group::2", "{%2, %3, %4, %5}", "%6", "r"(dst), "l"(m), "r"(c0),
+                "r"(c1), "r"(c2), "r"(c3), "r"(bar));
+  else
+    PSG_TMA_ASM("4d", "", "{%2, %3, %4, %5}", "%6", "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2),
+                "r"(c3), "r"(bar));
+}
+#undef PSG_TMA_ASM
+
+// PAIR: cta_group::2 — `bar` may be the peer CTA's mbarrier (a shared::cluster address),
+// so both CTAs of a pair can report their bytes to the leader's barrier.
+
+// ------------------------------------------------------------------ cluster
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
 }
 
 // ------------------------------------------------------------------ tcgen05
@@ -81,6 +118,17 @@ __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
 }
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+// cta_group::2: both CTAs of the pair allocate (each gets the same columns of its own TMEM)
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
                : "memory");
 }
 __device__ __forceinline__ void fence_before_sync() {
@@ -97,6 +145,25 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// M = 256 over a CTA pair: A rows 0..127 / 128..255 and B columns [0, N/2) / [N/2, N)
+// come from the leader's / the peer's shared memory at the same offsets; each CTA's TMEM
+// receives its 128 rows.  Issued by the leader only.
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on the mbarrier at this offset in every CTA of `mask` once the pair's MMAs complete.
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar), "h"(mask)
       : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.

@@ -68,6 +68,12 @@ struct TcArgs {
   int ntaps, cpt, cgs;
   int valid_cols;         // split-K reduce: dW row padding columns (>= Kf) zeroed
   int epi_vec;            // epilogue: float4 stores (16-byte aligned rows and column runs)
+  // CTA pairs (cta_group::2, launched as 2-CTA clusters): a work unit is two vertically
+  // adjacent 128-row tiles (CTA rank r takes tile 2u + r) sharing one MMA of M = 256; each
+  // CTA loads its own A tile and half of the B tile (b_cols columns).
+  int pair;
+  int m_units;            // M work units: m_tiles, or ceil(m_tiles / 2) for pairs
+  int b_cols;             // B columns (N) loaded per CTA: n_tile, or n_tile / 2 for pairs
 };
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
@@ -83,8 +89,8 @@ __device__ __forceinline__ Tile decode_tile(const TcArgs& p, long long t) {
   Tile r;
   r.n = static_cast<int>(t % p.n_tiles);
   t /= p.n_tiles;
-  r.m = static_cast<int>(t % p.m_tiles);
-  t /= p.m_tiles;
+  r.m = static_cast<int>(t % p.m_units);
+  t /= p.m_units;
   const int gt = static_cast<int>(t % (p.G * p.taps));
   r.split = static_cast<int>(t / (p.G * p.taps));
   r.g = gt / p.taps;
@@ -93,8 +99,9 @@ __device__ __forceinline__ Tile decode_tile(const TcArgs& p, long long t) {
 }
 
 // B_TAPS_MN: tap shift and channel offset of this lane's 32-column chunk (slot 0).
-__device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, int j, TapChunks& k) {
-  const int vc = t.n * p.n_tile + 32 * max(j, 0);
+__device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, int j, TapChunks& k,
+                                           int rank) {
+  const int vc = t.n * p.n_tile + rank * p.b_cols + 32 * max(j, 0);
   const int tap = min(vc / p.cpt, p.ntaps - 1);  // chunks past the last tap: harmless reloads
   k.dy[0] = tap / p.kw - p.ph;
   k.dx[0] = tap % p.kw - p.pw;
@@ -157,73 +164,74 @@ struct KCursor {
 // box), the 32-float chunks of MN-major operands are issued by consecutive lanes in
 // parallel (lane l issues chunk l - base), and consecutive K blocks are issued by
 // different producer warps (kProducers of them, round robin).
-template <int KBLK>
+template <int KBLK, bool PAIR>
 __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, const Tile& t,
                                        const KCursor& c, int rb, int oh0, int ow0, uint32_t sa,
                                        uint32_t bar, int j) {
   switch (p.a_mode) {
     case A_RECT_K:
       if (j == 0)
-        tc::tma_load_4d(sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0 + p.sign * (c.tv - p.pw),
+        tc::tma_load_4d<PAIR>(sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0 + p.sign * (c.tv - p.pw),
                         oh0 + p.sign * (c.tu - p.ph), rb);
       break;
     case A_2D_K:
-      if (j == 0) tc::tma_load_2d(sa, map, bar, c.kb * KBLK, t.m * kTileM);
+      if (j == 0) tc::tma_load_2d<PAIR>(sa, map, bar, c.kb * KBLK, t.m * kTileM);
       break;
     case A_RECT_MN:
       if (j >= 0 && j < p.a_chunks)
-        tc::tma_load_4d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
+        tc::tma_load_4d<PAIR>(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
                         c.kow, c.koh, c.kbi);
       break;
     case A_2D_MN:
       if (j >= 0 && j < p.a_chunks)
-        tc::tma_load_2d(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
+        tc::tma_load_2d<PAIR>(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
                         c.kb * KBLK);
       break;
   }
 }
 
-template <int KBLK>
+template <int KBLK, bool PAIR>
 __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, const Tile& t,
                                        const KCursor& c, int u, int v, const TapChunks& tk,
-                                       uint32_t sb, uint32_t bar, int j) {
-  const int nch = (p.n_tile + 31) / 32;
+                                       uint32_t sb, uint32_t bar, int j, int rank) {
+  const int nch = (p.b_cols + 31) / 32;
+  const int n0 = t.n * p.n_tile + rank * p.b_cols;  // this CTA's first B column
   if (j < 0) return;
   switch (p.b_mode) {
     case B_2D_K:
-      if (j == 0) tc::tma_load_2d(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + t.n * p.n_tile);
+      if (j == 0) tc::tma_load_2d<PAIR>(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + n0);
       break;
     case B_WT_MN:  // W viewed as [G][F/G][taps][C/G]: filter blocks past F/G read as 0
       if (j < nch)
-        tc::tma_load_4d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.t1,
+        tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.t1,
                         c.t0 * KBLK, t.g);
       break;
     case B_3D_K:  // W viewed as [F][taps][C/G]: channel blocks past C/G read as 0
       if (j == 0)
-        tc::tma_load_3d(sb, map, bar, c.t0 * KBLK, c.t1, p.b_r_g * t.g + t.n * p.n_tile);
+        tc::tma_load_3d<PAIR>(sb, map, bar, c.t0 * KBLK, c.t1, p.b_r_g * t.g + n0);
       break;
     case B_RECT_MN:
       if (j < nch)
-        tc::tma_load_4d(sb + j * KBLK * 128, map, bar, p.b_n_g * t.g + t.n * p.n_tile + 32 * j,
+        tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, p.b_n_g * t.g + n0 + 32 * j,
                         c.kow + v - p.pw, c.koh + u - p.ph, c.kbi);
       break;
     case B_2D_MN:
       if (j < nch)
-        tc::tma_load_2d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.kb * KBLK);
+        tc::tma_load_2d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.kb * KBLK);
       break;
     case B_COL_MN:  // im2col matrix [G][rows][Kp]: group as the outer coordinate
       if (j < nch)
-        tc::tma_load_3d(sb + j * KBLK * 128, map, bar, t.n * p.n_tile + 32 * j, c.kb * KBLK, t.g);
+        tc::tma_load_3d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.kb * KBLK, t.g);
       break;
     case B_TAPS_MN:  // X shifted per 32-column chunk by that chunk's tap
       if (j < nch)
-        tc::tma_load_4d(sb + j * KBLK * 128, map, bar, tk.c[0], c.kow + tk.dx[0],
+        tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, tk.c[0], c.kow + tk.dx[0],
                         c.koh + tk.dy[0], c.kbi);
       break;
   }
 }
 
-template <int KBLK>
+template <int KBLK, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const TcArgs p) {
@@ -234,6 +242,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // pairs: the cluster is the unit of work; rank 0 (the leader) owns the MMA, the stage
+  // "full" barriers (both CTAs' TMA bytes land on them) and the TMEM "empty" barriers
+  const int rank = PAIR ? static_cast<int>(tc::cluster_rank()) : 0;
+  const long long unit0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const long long ustep = PAIR ? gridDim.x / 2 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&map_a);
@@ -244,13 +257,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(tc::smem_u32(&tfull_bar[b]), 1);
-      tc::mbar_init(tc::smem_u32(&tempty_bar[b]), 128);
+      tc::mbar_init(tc::smem_u32(&tempty_bar[b]), PAIR ? 256 : 128);
     }
     tc::fence_barrier_init();
   }
-  if (warp == kAllocWarp) tc::tmem_alloc(tc::smem_u32(&tmem_base_sh), 2 * kAccCols);
+  if (warp == kAllocWarp) {
+    if constexpr (PAIR)
+      tc::tmem_alloc_pair(tc::smem_u32(&tmem_base_sh), 2 * kAccCols);
+    else
+      tc::tmem_alloc(tc::smem_u32(&tmem_base_sh), 2 * kAccCols);
+  }
   tc::fence_before_sync();
-  __syncthreads();
+  if constexpr (PAIR)
+    tc::cluster_sync();  // the peer's barriers are initialised before anyone signals them
+  else
+    __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base_sh;
 
@@ -259,11 +280,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------- producers: K block it -> producer it % producers
     // lane 0 waits for the slot and posts the stage's bytes; lanes 0..15 issue A
     // (chunk = lane), lanes 16..31 issue B (chunk = lane - 16)
-    const uint32_t bytes = p.a_tx + (p.stage_bytes - p.a_bytes);
+    // pairs: the leader posts both CTAs' bytes (identical per CTA); the peer only loads
+    const uint32_t bytes = (p.a_tx + (p.stage_bytes - p.a_bytes)) * (PAIR ? 2 : 1);
     const int ja = lane < 16 ? lane : -1, jb = lane >= 16 ? lane - 16 : -1;
     uint32_t it = 0;
-    for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x) {
-      const Tile t = decode_tile(p, tt);
+    for (long long tt = unit0; tt < p.total_tiles; tt += ustep) {
+      Tile t = decode_tile(p, tt);
+      if (PAIR) t.m = 2 * t.m + rank;
       const int kb0 = t.split * p.kb_per_split;
       const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
       int rb = 0, oh0 = 0, ow0 = 0;
@@ -275,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int u = t.tap / p.kw, v = t.tap % p.kw;
       TapChunks tk{};
-      if (p.b_mode == B_TAPS_MN) tap_chunks(p, t, jb, tk);
+      if (p.b_mode == B_TAPS_MN) tap_chunks(p, t, jb, tk, rank);
       KCursor c;
       c.init(p, kb0);
       for (int kb = kb0; kb < kb1; ++it) {  // one pipeline stage = up to kps K blocks
@@ -285,28 +308,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         const uint32_t s = it % p.stages;
-        const uint32_t bar = tc::smem_u32(&full_bar[s]);
+        const uint32_t bar = PAIR ? tc::mapa(tc::smem_u32(&full_bar[s]), 0)
+                                  : tc::smem_u32(&full_bar[s]);
         if (lane == 0) {
           tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ((it / p.stages) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(bar, bytes * cnt);
+          if (rank == 0) tc::mbar_arrive_expect_tx(tc::smem_u32(&full_bar[s]), bytes * cnt);
         }
         __syncwarp();
         for (int j = 0; j < cnt; ++j, ++kb, c.next(p)) {
           const uint32_t sa = tc::smem_u32(smem + (s * p.kps + j) * p.stage_bytes);
-          load_a<KBLK>(p, &map_a, t, c, rb, oh0, ow0, sa, bar, ja);
-          load_b<KBLK>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, jb);
+          load_a<KBLK, PAIR>(p, &map_a, t, c, rb, oh0, ow0, sa, bar, ja);
+          load_b<KBLK, PAIR>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, jb, rank);
         }
       }
     }
-  } else if (warp == kMmaWarp && lane == 0) {
+  } else if (warp == kMmaWarp && lane == 0 && rank == 0) {
     // ------------------------------------------------------------ MMA issue
     const bool a_mn = p.a_mode == A_RECT_MN || p.a_mode == A_2D_MN;
     const bool b_mn = p.b_mode != B_2D_K && p.b_mode != B_3D_K;
-    const uint32_t idesc = tc::idesc_tf32(kTileM, p.n_tile, a_mn, b_mn);
+    const uint32_t idesc = tc::idesc_tf32(PAIR ? 2 * kTileM : kTileM, p.n_tile, a_mn, b_mn);
     const uint32_t k_sw = KBLK == 32 ? tc::kSw128 : tc::kSw64;
     const uint32_t k_sbo = 8 * KBLK * 4;  // 8 rows of KBLK floats
     uint32_t it = 0, local = 0;
-    for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x, ++local) {
+    for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {
       const Tile t = decode_tile(p, tt);
       const int kb0 = t.split * p.kb_per_split;
       const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
@@ -328,19 +352,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : tc::smem_desc(sa + j * 32, 16, k_sbo, k_sw);
             const uint64_t bd = b_mn ? tc::smem_desc(sb + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
                                      : tc::smem_desc(sb + j * 32, 16, k_sbo, k_sw);
-            tc::mma_tf32(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+            if constexpr (PAIR)
+              tc::mma_tf32_pair(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+            else
+              tc::mma_tf32(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
           }
         }
-        tc::mma_commit(tc::smem_u32(&empty_bar[s]));
+        if constexpr (PAIR)
+          tc::mma_commit_pair(tc::smem_u32(&empty_bar[s]), 3);
+        else
+          tc::mma_commit(tc::smem_u32(&empty_bar[s]));
       }
-      tc::mma_commit(tc::smem_u32(&tfull_bar[acc]));
+      if constexpr (PAIR)
+        tc::mma_commit_pair(tc::smem_u32(&tfull_bar[acc]), 3);
+      else
+        tc::mma_commit(tc::smem_u32(&tfull_bar[acc]));
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - kEpiWarp0;
     uint32_t local = 0;
-    for (long long tt = blockIdx.x; tt < p.total_tiles; tt += gridDim.x, ++local) {
-      const Tile t = decode_tile(p, tt);
+    for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {
+      Tile t = decode_tile(p, tt);
+      if (PAIR) t.m = 2 * t.m + rank;
       const int m = ew * 32 + lane;
       bool row_ok;
       long long out_row;
@@ -348,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rb = t.m / (p.th * p.tw);
         const int r = t.m % (p.th * p.tw);
         const int oh = (r / p.tw) * p.rm + m / p.wm, ow = (r % p.tw) * p.wm + m % p.wm;
-        row_ok = oh < p.out_h && ow < p.out_w;
+        row_ok = oh < p.out_h && ow < p.out_w && t.m < p.m_tiles;  // pairs: odd tail tile
         out_row = (static_cast<long long>(rb) * p.out_h + oh) * p.out_w + ow;
       } else {
         const int mm = t.m * kTileM + m;
@@ -449,14 +483,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc::fence_before_sync();
-      mbar_arrive(tc::smem_u32(&tempty_bar[acc]));
+      if constexpr (PAIR)
+        tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&tempty_bar[acc]), 0));
+      else
+        mbar_arrive(tc::smem_u32(&tempty_bar[acc]));
     }
   }
   tc::fence_before_sync();
-  __syncthreads();
+  if constexpr (PAIR)
+    tc::cluster_sync();  // the peer's remote arrivals / MMA reads of our smem are done
+  else
+    __syncthreads();
   if (warp == kAllocWarp) {
     tc::fence_after_sync();
-    tc::tmem_dealloc(tmem, 2 * kAccCols);
+    if constexpr (PAIR)
+      tc::tmem_dealloc_pair(tmem, 2 * kAccCols);
+    else
+      tc::tmem_dealloc(tmem, 2 * kAccCols);
   }
 }
 

@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(320, 1) tma_only(const __grid_constant__ CUten
 }
 
 // Back-to-back MMAs: KB K blocks of KBLK (8-column steps), commit per K block.
-__global__ void __launch_bounds__(128, 1) mma_only(int n, int kblk, int kblocks, int mn_major) {
+__global__ void __launch_bounds__(128, 1) mma_only(int n, int kblk, int kblocks, int mn_major,
+                                                   int nacc = 0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(128, 1) mma_only(int n, int kblk, int kblocks,
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // zero the operand tiles so the accumulators stay finite
-  for (int i = threadIdx.x; i < (128 + 256) * 32; i += blockDim.x)
+  for (int i = threadIdx.x; i < (128 + 256) * kblk; i += blockDim.x)
     reinterpret_cast<float*>(smem)[i] = 0.f;
   if (threadIdx.x == 0) {
     tc::mbar_init(tc::smem_u32(&done), 1);
@@ -129,7 +130,10 @@ __global__ void __launch_bounds__(128, 1) mma_only(int n, int kblk, int kblocks,
                                      : tc::smem_desc(sa + q * 32, 16, 8 * kblk * 4, sw);
         const uint64_t bd = mn_major ? tc::smem_desc(sb + q * 1024, kblk * 128, 512, tc::kSw128Base32)
                                      : tc::smem_desc(sb + q * 32, 16, 8 * kblk * 4, sw);
-        tc::mma_tf32(tbase + (kb & 1) * 256, ad, bd, idesc, q | (kb > 1));
+        if (nacc)  // independent accumulators round robin (each K block -> acc kb % nacc)
+          tc::mma_tf32(tbase + (kb % nacc) * n, ad, bd, idesc, q | (kb >= nacc));
+        else
+          tc::mma_tf32(tbase + (kb & 1) * 256, ad, bd, idesc, q | (kb > 1));
       }
       tc::mma_commit(tc::smem_u32(&done));  // per-K-block commit, as in the real kernel
     }
@@ -141,6 +145,58 @@ __global__ void __launch_bounds__(128, 1) mma_only(int n, int kblk, int kblocks,
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc(tbase, 512);
+  }
+}
+
+// Same loop with cta_group::2: a CTA pair computes M = 256 (128 rows of A per CTA) x N
+// (N/2 columns of B per CTA); only the leader issues, the commit multicasts to both.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma_pair(int n, int kblocks) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t fin;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = threadIdx.x; i < (128 + 128) * 32; i += blockDim.x)
+    reinterpret_cast<float*>(smem)[i] = 0.f;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(tc::smem_u32(&fin), 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(&tbase)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before_sync();
+  asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tc::fence_after_sync();
+  if (rank == 0 && warp == 0 && lane == 0) {
+    const uint32_t sa = tc::smem_u32(smem), sb = sa + 128 * 32 * 4;
+    const uint32_t idesc = tc::idesc_tf32(256, n, false, false);
+    for (int kb = 0; kb < kblocks; ++kb)
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t ad = tc::smem_desc(sa + q * 32, 16, 1024, tc::kSw128);
+        const uint64_t bd = tc::smem_desc(sb + q * 32, 16, 1024, tc::kSw128);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+                tbase + (kb & 1) * 256), "l"(ad), "l"(bd), "r"(idesc), "r"(uint32_t(q | (kb > 1)))
+            : "memory");
+      }
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(tc::smem_u32(&fin)), "h"(uint16_t(3)) : "memory");
+  }
+  if (threadIdx.x == 0) tc::mbar_wait(tc::smem_u32(&fin), 0);
+  tc::fence_before_sync();
+  asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 1) {
+    tc::fence_after_sync();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512) : "memory");
   }
 }
 
@@ -262,5 +318,39 @@ int main() {
                     n, kblk, mn ? "mn" : "k", 2 * macs / (ms * 1e-3) / 1e12,
                     macs / (ms * 1e-3) / (ghz * 1e9) / sms);
       }
+  for (int n : {64, 128, 256})
+    for (int nacc : {1, 2, 4, 8}) {
+      if (n * nacc > 512) continue;
+      const int kblocks = 4000;
+      const size_t smem = size_t(128 + 256) * 32 * 4 + 2048;
+      CK(cudaFuncSetAttribute(mma_only, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      mma_only<<<sms, 128, smem>>>(n, 32, 10, 0, nacc);
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0));
+      mma_only<<<sms, 128, smem>>>(n, 32, kblocks, 0, nacc);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double macs = double(sms) * kblocks * 128.0 * n * 32;
+      std::printf("{\"case\": \"mma_tf32_m128_n%d_k32_k_acc%d\", \"TFLOPs\": %.1f, \"MAC_per_clk_per_sm\": %.0f}\n",
+                  n, nacc, 2 * macs / (ms * 1e-3) / 1e12, macs / (ms * 1e-3) / (ghz * 1e9) / sms);
+    }
+  for (int n : {64, 128, 256}) {
+    const int kblocks = 4000, grid = sms / 2 * 2;
+    const size_t smem = size_t(256) * 32 * 4 + 2048;
+    CK(cudaFuncSetAttribute(mma_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    mma_pair<<<grid, 128, smem>>>(n, 10);
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0));
+    mma_pair<<<grid, 128, smem>>>(n, kblocks);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    const double macs = double(grid / 2) * kblocks * 256.0 * n * 32;
+    std::printf("{\"case\": \"mma_tf32_pair_m256_n%d_k32\", \"TFLOPs\": %.1f, \"MAC_per_clk_per_sm\": %.0f}\n",
+                n, 2 * macs / (ms * 1e-3) / 1e12, macs / (ms * 1e-3) / (ghz * 1e9) / grid);
+  }
   return 0;
 }
