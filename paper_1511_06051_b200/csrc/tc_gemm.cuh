@@ -88,6 +88,18 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
 // PAIR: cta_group::2 — `bar` may be the peer CTA's mbarrier (a shared::cluster address),
 // so both CTAs of a pair can report their bytes to the leader's barrier.
 
+// One lane of a converged warp (the lowest active lane: the same lane every call, so
+// tcgen05.commit sees the MMAs that lane issued).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ------------------------------------------------------------------ cluster
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;

@@ -322,14 +322,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kMmaWarp && lane == 0 && rank == 0) {
+  } else if (warp == kMmaWarp && rank == 0) {
     // ------------------------------------------------------------ MMA issue
+    // The whole warp runs the loop (warp-uniform control flow keeps the descriptors in
+    // uniform registers); one elected lane issues.  Descriptors are built once for slot 0
+    // and advanced by adding (byte offset >> 4) to the start-address field, so a K block
+    // costs a few integer adds per MMA instead of a descriptor build.
     const bool a_mn = p.a_mode == A_RECT_MN || p.a_mode == A_2D_MN;
     const bool b_mn = p.b_mode != B_2D_K && p.b_mode != B_3D_K;
     const uint32_t idesc = tc::idesc_tf32(PAIR ? 2 * kTileM : kTileM, p.n_tile, a_mn, b_mn);
     const uint32_t k_sw = KBLK == 32 ? tc::kSw128 : tc::kSw64;
     const uint32_t k_sbo = 8 * KBLK * 4;  // 8 rows of KBLK floats
-    uint32_t it = 0, local = 0;
+    const uint32_t s0 = tc::smem_u32(smem);
+    const uint64_t a_desc0 = a_mn ? tc::smem_desc(s0, KBLK * 128, 512, tc::kSw128Base32)
+                                  : tc::smem_desc(s0, 16, k_sbo, k_sw);
+    const uint64_t b_desc0 = b_mn ? tc::smem_desc(s0 + p.a_bytes, KBLK * 128, 512, tc::kSw128Base32)
+                                  : tc::smem_desc(s0 + p.a_bytes, 16, k_sbo, k_sw);
+    const uint32_t a_step = (a_mn ? 1024u : 32u) >> 4, b_step = (b_mn ? 1024u : 32u) >> 4;
+    const uint32_t slot_step = static_cast<uint32_t>(p.stage_bytes) >> 4;
+    const bool leader = tc::elect_one();
+    uint32_t st = 0, ph = 0, local = 0;  // ring slot and its parity
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {
       const Tile t = decode_tile(p, tt);
       const int kb0 = t.split * p.kb_per_split;
@@ -338,35 +350,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(tc::smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
       tc::fence_after_sync();
       const uint32_t d = tmem + acc * kAccCols;
-      for (int i = 0; i < nkb; ++it) {
+      for (int i = 0; i < nkb;) {
         const int cnt = min(p.kps, nkb - i);
-        const uint32_t s = it % p.stages;
-        tc::mbar_wait(tc::smem_u32(&full_bar[s]), (it / p.stages) & 1);
+        const uint32_t s = st;
+        tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
         tc::fence_after_sync();
-        for (int q = 0; q < cnt; ++q, ++i) {
-          const uint32_t sa = tc::smem_u32(smem + (s * p.kps + q) * p.stage_bytes);
-          const uint32_t sb = sa + p.a_bytes;
+        if (leader) {
+          uint32_t off = s * static_cast<uint32_t>(p.kps) * slot_step;
+          for (int q = 0; q < cnt; ++q, ++i, off += slot_step) {
 #pragma unroll
-          for (int j = 0; j < KBLK / 8; ++j) {
-            const uint64_t ad = a_mn ? tc::smem_desc(sa + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
-                                     : tc::smem_desc(sa + j * 32, 16, k_sbo, k_sw);
-            const uint64_t bd = b_mn ? tc::smem_desc(sb + j * 1024, KBLK * 128, 512, tc::kSw128Base32)
-                                     : tc::smem_desc(sb + j * 32, 16, k_sbo, k_sw);
-            if constexpr (PAIR)
-              tc::mma_tf32_pair(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
-            else
-              tc::mma_tf32(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+            for (int j = 0; j < KBLK / 8; ++j) {
+              const uint64_t ad = a_desc0 + off + j * a_step;
+              const uint64_t bd = b_desc0 + off + j * b_step;
+              if constexpr (PAIR)
+                tc::mma_tf32_pair(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+              else
+                tc::mma_tf32(d, ad, bd, idesc, (i | j) != 0 ? 1u : 0u);
+            }
           }
+          if constexpr (PAIR)
+            tc::mma_commit_pair(tc::smem_u32(&empty_bar[s]), 3);
+          else
+            tc::mma_commit(tc::smem_u32(&empty_bar[s]));
+        } else {
+          i += cnt;
         }
-        if constexpr (PAIR)
-          tc::mma_commit_pair(tc::smem_u32(&empty_bar[s]), 3);
-        else
-          tc::mma_commit(tc::smem_u32(&empty_bar[s]));
+        __syncwarp();
+        if (++st == static_cast<uint32_t>(p.stages)) {
+          st = 0;
+          ph ^= 1;
+        }
       }
-      if constexpr (PAIR)
-        tc::mma_commit_pair(tc::smem_u32(&tfull_bar[acc]), 3);
-      else
-        tc::mma_commit(tc::smem_u32(&tfull_bar[acc]));
+      if (leader) {
+        if constexpr (PAIR)
+          tc::mma_commit_pair(tc::smem_u32(&tfull_bar[acc]), 3);
+        else
+          tc::mma_commit(tc::smem_u32(&tfull_bar[acc]));
+      }
+      __syncwarp();
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
