@@ -220,6 +220,22 @@ void finish_args(TcArgs& a, int kblk, int sms) {
   }();
   // a producer may only run one ring ahead of the slot it refills (parity waits): <= stages
   a.producers = std::min(producers, a.stages);
+  // the producers' cursor jump over the other producers' stages, as mixed-radix digits
+  {
+    const int D = (a.producers - 1) * a.kps;
+    a.adv_kb = D;
+    if (a.cb) {
+      a.adv_c0 = D % a.cb;
+      a.adv_tap = D / a.cb;
+      a.adv_tv = a.adv_tap % a.kw;
+      a.adv_tu = a.adv_tap / a.kw;
+    }
+    if (a.kth) {
+      a.adv_w = D % a.ktw;
+      a.adv_h = (D / a.ktw) % a.kth;
+      a.adv_b = D / (a.ktw * a.kth);
+    }
+  }
   const long long tiles = static_cast<long long>(a.m_units) * a.n_tiles * a.G * a.taps;
   if (a.pair) sms /= 2;  // one work unit per cluster
   // Split K so that the persistent grid's waves are full: minimise

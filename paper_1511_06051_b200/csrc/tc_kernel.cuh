@@ -72,13 +72,17 @@ struct TcArgs {
   // adjacent 128-row tiles (CTA rank r takes tile 2u + r) sharing one MMA of M = 256; each
   // CTA loads its own A tile and half of the B tile (b_cols columns).
   int pair;
+  // producer cursor jump over the other producers' stages: D = (producers - 1) * kps K
+  // blocks split into the cursors' mixed-radix digits (host-computed, no divisions per stage)
+  int adv_kb, adv_c0, adv_tap, adv_tv, adv_tu, adv_w, adv_h, adv_b;
   int m_units;            // M work units: m_tiles, or ceil(m_tiles / 2) for pairs
   int b_cols;             // B columns (N) loaded per CTA: n_tile, or n_tile / 2 for pairs
 };
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
+constexpr int kMaxBChunks = 8;
 struct TapChunks {
-  int dx[1], dy[1], c[1];
+  int dx[kMaxBChunks], dy[kMaxBChunks], c[kMaxBChunks];
 };
 
 struct Tile {
@@ -98,14 +102,17 @@ __device__ __forceinline__ Tile decode_tile(const TcArgs& p, long long t) {
   return r;
 }
 
-// B_TAPS_MN: tap shift and channel offset of this lane's 32-column chunk (slot 0).
-__device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, int j, TapChunks& k,
+// B_TAPS_MN: tap shift and channel offset of every 32-column chunk of this CTA's B tile.
+__device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, TapChunks& k,
                                            int rank) {
-  const int vc = t.n * p.n_tile + rank * p.b_cols + 32 * max(j, 0);
-  const int tap = min(vc / p.cpt, p.ntaps - 1);  // chunks past the last tap: harmless reloads
-  k.dy[0] = tap / p.kw - p.ph;
-  k.dx[0] = tap % p.kw - p.pw;
-  k.c[0] = p.b_n_g * t.g + vc % p.cpt;
+#pragma unroll
+  for (int j = 0; j < kMaxBChunks; ++j) {
+    const int vc = t.n * p.n_tile + rank * p.b_cols + 32 * j;
+    const int tap = min(vc / p.cpt, p.ntaps - 1);  // chunks past the last tap: harmless reloads
+    k.dy[j] = tap / p.kw - p.ph;
+    k.dx[j] = tap % p.kw - p.pw;
+    k.c[j] = p.b_n_g * t.g + vc % p.cpt;
+  }
 }
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -133,6 +140,40 @@ struct KCursor {
       kow = (r % p.ktw) * p.wk;
     }
   }
+  // jump D = (producers - 1) * kps K blocks (digits precomputed in TcArgs::adv_*)
+  __device__ __forceinline__ void advance(const TcArgs& p) {
+    kb += p.adv_kb;
+    if (p.cb) {
+      int carry = 0;
+      t0 += p.adv_c0;
+      if (t0 >= p.cb) {
+        t0 -= p.cb;
+        carry = 1;
+      }
+      t1 += p.adv_tap + carry;
+      tv += p.adv_tv + carry;
+      tu += p.adv_tu;
+      if (tv >= p.kw) {
+        tv -= p.kw;
+        ++tu;
+      }
+    }
+    if (p.kth) {
+      int carry = 0;
+      kow += p.adv_w * p.wk;
+      if (kow >= p.ktw * p.wk) {
+        kow -= p.ktw * p.wk;
+        carry = 1;
+      }
+      koh += (p.adv_h + carry) * p.rk;
+      carry = 0;
+      if (koh >= p.kth * p.rk) {
+        koh -= p.kth * p.rk;
+        carry = 1;
+      }
+      kbi += p.adv_b + carry;
+    }
+  }
   __device__ __forceinline__ void next(const TcArgs& p) {
     ++kb;
     if (p.cb && ++t0 == p.cb) {
@@ -157,35 +198,33 @@ struct KCursor {
   }
 };
 
-// Operand loads of one K block.  A TMA issue occupies its thread for a few hundred
-// cycles whatever the box size (tools/tma_bench.cu: one issuing thread tops out near
-// 25-35 B/clk/SM with 16 KB boxes and ~7-12 with 4 KB boxes; 4-8 issuing warps reach
-// ~45).  So boxes stay as large as the layout allows (a whole K-major operand tile is one
-// box), the 32-float chunks of MN-major operands are issued by consecutive lanes in
-// parallel (lane l issues chunk l - base), and consecutive K blocks are issued by
-// different producer warps (kProducers of them, round robin).
+// Operand loads of one K block, all issued by the producer warp's elected lane.  A TMA
+// issue occupies its thread for a few hundred cycles whatever the box size
+// (tools/tma_bench.cu), and the lanes of one warp are serialised anyway (the tensor-map
+// operands must be warp-uniform), so throughput comes from several producer warps working
+// on different stages, and boxes stay as large as the layout allows (a whole K-major
+// operand tile is one box; MN-major operands are 32-float chunks).
 template <int KBLK, bool PAIR>
 __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, const Tile& t,
                                        const KCursor& c, int rb, int oh0, int ow0, uint32_t sa,
-                                       uint32_t bar, int j) {
+                                       uint32_t bar) {
   switch (p.a_mode) {
     case A_RECT_K:
-      if (j == 0)
-        tc::tma_load_4d<PAIR>(sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0 + p.sign * (c.tv - p.pw),
-                        oh0 + p.sign * (c.tu - p.ph), rb);
+      tc::tma_load_4d<PAIR>(sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0 + p.sign * (c.tv - p.pw),
+                            oh0 + p.sign * (c.tu - p.ph), rb);
       break;
     case A_2D_K:
-      if (j == 0) tc::tma_load_2d<PAIR>(sa, map, bar, c.kb * KBLK, t.m * kTileM);
+      tc::tma_load_2d<PAIR>(sa, map, bar, c.kb * KBLK, t.m * kTileM);
       break;
     case A_RECT_MN:
-      if (j >= 0 && j < p.a_chunks)
+      for (int j = 0; j < p.a_chunks; ++j)
         tc::tma_load_4d<PAIR>(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
-                        c.kow, c.koh, c.kbi);
+                              c.kow, c.koh, c.kbi);
       break;
     case A_2D_MN:
-      if (j >= 0 && j < p.a_chunks)
+      for (int j = 0; j < p.a_chunks; ++j)
         tc::tma_load_2d<PAIR>(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
-                        c.kb * KBLK);
+                              c.kb * KBLK);
       break;
   }
 }
@@ -193,40 +232,39 @@ __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, 
 template <int KBLK, bool PAIR>
 __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, const Tile& t,
                                        const KCursor& c, int u, int v, const TapChunks& tk,
-                                       uint32_t sb, uint32_t bar, int j, int rank) {
+                                       uint32_t sb, uint32_t bar, int rank) {
   const int nch = (p.b_cols + 31) / 32;
   const int n0 = t.n * p.n_tile + rank * p.b_cols;  // this CTA's first B column
-  if (j < 0) return;
   switch (p.b_mode) {
     case B_2D_K:
-      if (j == 0) tc::tma_load_2d<PAIR>(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + n0);
+      tc::tma_load_2d<PAIR>(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + n0);
       break;
     case B_WT_MN:  // W viewed as [G][F/G][taps][C/G]: filter blocks past F/G read as 0
-      if (j < nch)
-        tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.t1,
-                        c.t0 * KBLK, t.g);
+      for (int j = 0; j < nch; ++j)
+        tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.t1, c.t0 * KBLK, t.g);
       break;
     case B_3D_K:  // W viewed as [F][taps][C/G]: channel blocks past C/G read as 0
-      if (j == 0)
-        tc::tma_load_3d<PAIR>(sb, map, bar, c.t0 * KBLK, c.t1, p.b_r_g * t.g + n0);
+      tc::tma_load_3d<PAIR>(sb, map, bar, c.t0 * KBLK, c.t1, p.b_r_g * t.g + n0);
       break;
     case B_RECT_MN:
-      if (j < nch)
+      for (int j = 0; j < nch; ++j)
         tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, p.b_n_g * t.g + n0 + 32 * j,
-                        c.kow + v - p.pw, c.koh + u - p.ph, c.kbi);
+                              c.kow + v - p.pw, c.koh + u - p.ph, c.kbi);
       break;
     case B_2D_MN:
-      if (j < nch)
+      for (int j = 0; j < nch; ++j)
         tc::tma_load_2d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.kb * KBLK);
       break;
     case B_COL_MN:  // im2col matrix [G][rows][Kp]: group as the outer coordinate
-      if (j < nch)
+      for (int j = 0; j < nch; ++j)
         tc::tma_load_3d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.kb * KBLK, t.g);
       break;
     case B_TAPS_MN:  // X shifted per 32-column chunk by that chunk's tap
-      if (j < nch)
-        tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, tk.c[0], c.kow + tk.dx[0],
-                        c.koh + tk.dy[0], c.kbi);
+#pragma unroll
+      for (int j = 0; j < kMaxBChunks; ++j)
+        if (j < nch)
+          tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, tk.c[j], c.kow + tk.dx[j],
+                                c.koh + tk.dy[j], c.kbi);
       break;
   }
 }
@@ -276,51 +314,56 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_base_sh;
 
   const int pw = warp < 4 ? warp : (warp == 6 || warp == 7 ? warp - 2 : -1);
-  if (pw >= 0 && pw < p.producers) {
-    // ------------------------------------- producers: K block it -> producer it % producers
-    // lane 0 waits for the slot and posts the stage's bytes; lanes 0..15 issue A
-    // (chunk = lane), lanes 16..31 issue B (chunk = lane - 16)
+  if (pw >= 0 && pw < p.producers && lane == 0) {
+    // ----------------------- producers: pipeline stage it (kps K blocks) -> producer it % P
+    // Each producer walks only its own stages (the cursor jumps over the others' K blocks),
+    // waits for the slot, posts the stage's bytes and issues every box of the stage.
     // pairs: the leader posts both CTAs' bytes (identical per CTA); the peer only loads
     const uint32_t bytes = (p.a_tx + (p.stage_bytes - p.a_bytes)) * (PAIR ? 2 : 1);
-    const int ja = lane < 16 ? lane : -1, jb = lane >= 16 ? lane - 16 : -1;
-    uint32_t it = 0;
+    const int P = p.producers;
+    uint32_t it_tile = 0;  // global stage index of the tile's first stage
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep) {
       Tile t = decode_tile(p, tt);
       if (PAIR) t.m = 2 * t.m + rank;
       const int kb0 = t.split * p.kb_per_split;
       const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
-      int rb = 0, oh0 = 0, ow0 = 0;
-      if (p.a_mode == A_RECT_K) {
-        rb = t.m / (p.th * p.tw);
-        const int r = t.m % (p.th * p.tw);
-        oh0 = (r / p.tw) * p.rm;
-        ow0 = (r % p.tw) * p.wm;
-      }
-      const int u = t.tap / p.kw, v = t.tap % p.kw;
-      TapChunks tk{};
-      if (p.b_mode == B_TAPS_MN) tap_chunks(p, t, jb, tk, rank);
-      KCursor c;
-      c.init(p, kb0);
-      for (int kb = kb0; kb < kb1; ++it) {  // one pipeline stage = up to kps K blocks
-        const int cnt = min(p.kps, kb1 - kb);
-        if (static_cast<int>(it % p.producers) != pw) {
-          for (int j = 0; j < cnt; ++j, ++kb) c.next(p);
-          continue;
+      const int nst = (kb1 - kb0 + p.kps - 1) / p.kps;
+      const int first = static_cast<int>((static_cast<uint32_t>(pw + P) - it_tile % P) % P);
+      if (first < nst) {
+        int rb = 0, oh0 = 0, ow0 = 0;
+        if (p.a_mode == A_RECT_K) {
+          rb = t.m / (p.th * p.tw);
+          const int r = t.m % (p.th * p.tw);
+          oh0 = (r / p.tw) * p.rm;
+          ow0 = (r % p.tw) * p.wm;
         }
-        const uint32_t s = it % p.stages;
-        const uint32_t bar = PAIR ? tc::mapa(tc::smem_u32(&full_bar[s]), 0)
-                                  : tc::smem_u32(&full_bar[s]);
-        if (lane == 0) {
-          tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ((it / p.stages) & 1) ^ 1);
+        const int u = t.tap / p.kw, v = t.tap % p.kw;
+        TapChunks tk;
+        if (p.b_mode == B_TAPS_MN) tap_chunks(p, t, tk, rank);
+        const uint32_t it = it_tile + first;
+        uint32_t s = it % p.stages, ph = (it / p.stages) & 1;
+        KCursor c;
+        c.init(p, kb0 + first * p.kps);
+        for (int si = first; si < nst; si += P) {
+          const int cnt = min(p.kps, kb1 - (kb0 + si * p.kps));
+          const uint32_t bar = PAIR ? tc::mapa(tc::smem_u32(&full_bar[s]), 0)
+                                    : tc::smem_u32(&full_bar[s]);
+          tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
           if (rank == 0) tc::mbar_arrive_expect_tx(tc::smem_u32(&full_bar[s]), bytes * cnt);
-        }
-        __syncwarp();
-        for (int j = 0; j < cnt; ++j, ++kb, c.next(p)) {
-          const uint32_t sa = tc::smem_u32(smem + (s * p.kps + j) * p.stage_bytes);
-          load_a<KBLK, PAIR>(p, &map_a, t, c, rb, oh0, ow0, sa, bar, ja);
-          load_b<KBLK, PAIR>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, jb, rank);
+          for (int j = 0; j < cnt; ++j, c.next(p)) {
+            const uint32_t sa = tc::smem_u32(smem + (s * p.kps + j) * p.stage_bytes);
+            load_a<KBLK, PAIR>(p, &map_a, t, c, rb, oh0, ow0, sa, bar);
+            load_b<KBLK, PAIR>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, rank);
+          }
+          c.advance(p);
+          s += P;
+          if (s >= static_cast<uint32_t>(p.stages)) {
+            s -= p.stages;
+            ph ^= 1;
+          }
         }
       }
+      it_tile += nst;
     }
   } else if (warp == kMmaWarp && rank == 0) {
     // ------------------------------------------------------------ MMA issue

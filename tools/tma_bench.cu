@@ -233,10 +233,10 @@ int main() {
       {"4d_c32_16x8_C384", 1, 32, 16, 8, 384, CU_TENSOR_MAP_SWIZZLE_128B},
       {"2d_mn32_rows32_sw128b32", 0, 32, 32, 1, 4096, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B},
   };
-  for (int lanes : {0, 1})
-  for (int prod : {1, 4, 8})
-  for (int per : {8})
-  for (int stages : {4})
+  for (int lanes : {0})
+  for (int prod : {1, 2, 4, 8})
+  for (int per : {2, 4, 8})
+  for (int stages : {3, 6})
   for (const Case& c : cases) {
     CUtensorMap m;
     uint32_t estr[5] = {1, 1, 1, 1, 1};
