@@ -8,7 +8,14 @@
 //       (never needed for a first layer) stays on the SIMT kernel;
 //     wgrad runs multi-tap implicit GEMM tiles from the activations; only layers whose
 //       activations TMA cannot tile (stride > 1, C/G < 16) use the im2col matrix.
+//   Strided convolutions (AlexNet conv1 11x11/4, GoogLeNet conv1 7x7/2) instead take the
+//   space-to-depth route: x is rearranged once into s x s pixel blocks,
+//   x'[b][hs][ws][(dy*s + dx)*C + c] = x[b][s*hs + dy - p][s*ws + dx - p][c], which turns
+//   the layer into a stride-1 ceil(k/s) x ceil(k/s) convolution over s*s*C channels with
+//   zero-extended weights W'.  fprop and wgrad then run as ordinary TMA-tiled tcgen05
+//   convolutions (no im2col round trip through HBM); dW is folded back from dW'.
 #include <algorithm>
+#include <cstdlib>
 
 #include "psg_internal.h"
 
@@ -60,13 +67,121 @@ ConvGeom col_geom(const ConvGeom& g) {
   return l;
 }
 
+// ---- space-to-depth route ----
+int s2d_channels(const ConvGeom& g) { return (g.sh * g.sh * g.Cgs() + 15) / 16 * 16; }
+
+ConvGeom s2d_geom(const ConvGeom& g) {
+  const int s = g.sh, k = (g.kh + s - 1) / s;
+  ConvGeom q;
+  q.n = g.n;
+  q.OH = g.OH;
+  q.OW = g.OW;
+  q.H = g.OH + k - 1;
+  q.W = g.OW + k - 1;
+  q.cs_in = s2d_channels(g);
+  q.F = g.F;
+  q.kh = q.kw = k;
+  return q;
+}
+
+size_t s2d_x_elems(const ConvGeom& g) {
+  const ConvGeom q = s2d_geom(g);
+  return static_cast<size_t>(q.n) * q.H * q.W * q.cs_in;
+}
+size_t s2d_w_elems(const ConvGeom& g) {
+  const ConvGeom q = s2d_geom(g);
+  return (static_cast<size_t>(q.F) * q.Kf() + 31) / 32 * 32;  // keep the next buffer aligned
+}
+
+bool s2d_route(const ConvGeom& g) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("PSG_S2D");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (!enabled || is_linear(g) || g.G != 1 || g.sh < 2 || g.sh != g.sw || g.kh != g.kw ||
+      g.ph != g.pw || tc_supported(g, 0))
+    return false;
+  const ConvGeom q = s2d_geom(g);
+  // the s2d input must cover every output's receptive field
+  if ((q.H - 1) * g.sh + g.sh - 1 - g.ph < (g.OH - 1) * g.sh + g.kh - 1 - g.ph) return false;
+  return tc_supported(q, 0) && tc_supported(q, 2);
+}
+
+// x'[b][hs][ws][c'] for c' = (dy*s + dx)*C + c < s*s*C; 0 beyond (and outside x).
+// Block y = one x' row (b, hs); threads stride over its W' x C'/4 float4 cells (32-bit
+// index math), so every store is a coalesced float4 run.
+__global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, ConvGeom g,
+                                               ConvGeom q, float* __restrict__ xs) {
+  const int s = g.sh, C = g.Cgs(), c4n = q.cs_in / 4, row = blockIdx.x;
+  const int hs = row % q.H, b = row / q.H;
+  float4* out = reinterpret_cast<float4*>(xs) + static_cast<size_t>(row) * q.W * c4n;
+  const float* xb = x + static_cast<size_t>(b) * g.H * g.W * g.cs_in;
+  for (int j = threadIdx.x; j < q.W * c4n; j += blockDim.x) {
+    const int ws = j / c4n, c0 = (j - ws * c4n) * 4;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int cp = c0 + e;
+      v[e] = 0.f;
+      if (cp < s * s * C) {
+        const int blk = cp / C, c = cp - blk * C;
+        const int ih = s * hs + blk / s - g.ph, iw = s * ws + blk % s - g.pw;
+        if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
+          v[e] = __ldg(xb + (ih * g.W + iw) * g.cs_in + c);
+      }
+    }
+    out[j] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+// W'[f][tu][tv][c'] = W[f][s*tu + dy][s*tv + dx][c] (0 past the kernel / past s*s*C)
+__global__ void s2d_w_k(const float* __restrict__ w, ConvGeom g, ConvGeom q,
+                        float* __restrict__ ws, int total) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = g.sh, C = g.Cgs(), Cp = q.cs_in, Kf = q.Kf();
+  const int f = i / Kf, r = i % Kf;
+  const int cp = r % Cp, tap = r / Cp, tu = tap / q.kw, tv = tap % q.kw;
+  float v = 0.f;
+  if (cp < s * s * C) {
+    const int blk = cp / C, c = cp - blk * C;
+    const int u = s * tu + blk / s, vv = s * tv + blk % s;
+    if (u < g.kh && vv < g.kw) v = w[static_cast<size_t>(f) * g.Kp() + (u * g.kw + vv) * C + c];
+  }
+  ws[i] = v;
+}
+
+// dW[f][(u*kw + v)*C + c] = dW'[f][tu][tv][c'] (the inverse map; row padding stays 0)
+__global__ void s2d_dw_k(const float* __restrict__ dws, ConvGeom g, ConvGeom q,
+                         float* __restrict__ dw, int total) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int s = g.sh, C = g.Cgs(), Kp = g.Kp(), Kf = g.Kf();
+  const int f = i / Kp, k = i % Kp;
+  float v = 0.f;
+  if (k < Kf) {
+    const int c = k % C, t = k / C, u = t / g.kw, vv = t % g.kw;
+    const int cp = ((u % s) * s + vv % s) * C + c, tap = (u / s) * q.kw + vv / s;
+    v = dws[static_cast<size_t>(f) * q.Kf() + tap * q.cs_in + cp];
+  }
+  dw[i] = v;
+}
+
+void s2d_x(const ConvGeom& g, const float* x, float* xs, cudaStream_t st) {
+  const ConvGeom q = s2d_geom(g);
+  if (static_cast<size_t>(g.H) * g.W * g.cs_in >= (1ULL << 31))
+    throw std::invalid_argument("s2d: image too large");
+  s2d_x_k<<<q.n * q.H, 256, 0, st>>>(x, g, q, xs);
+  PSG_CUDA(cudaGetLastError());
+}
+
 bool fprop_col_route(const ConvGeom& g) {
-  return !is_linear(g) && g.G == 1 && !tc_supported(g, 0) && tc_supported(col_geom(g), 0) &&
-         tc_wgrad_col_supported(g);
+  return !is_linear(g) && g.G == 1 && !tc_supported(g, 0) && !s2d_route(g) &&
+         tc_supported(col_geom(g), 0) && tc_wgrad_col_supported(g);
 }
 
 bool wgrad_col_route(const ConvGeom& g) {
-  if (is_linear(g) || !tc_wgrad_col_supported(g)) return false;
+  if (is_linear(g) || s2d_route(g) || !tc_wgrad_col_supported(g)) return false;
   return fprop_col_route(g) || !tc_supported(g, 2);
 }
 
@@ -131,13 +246,23 @@ bool use_tc(const ConvGeom& g, int which, Mode m) {
 }  // namespace
 
 size_t conv_col_elems(const ConvGeom& g, Mode m) {
+  // s2d route: x' (written by fprop, read by wgrad), W', dW'
+  if (m == Mode::Tf32 && s2d_route(g)) return s2d_x_elems(g) + 2 * s2d_w_elems(g);
   if (m != Mode::Tf32 || !(fprop_col_route(g) || wgrad_col_route(g))) return 0;
   return static_cast<size_t>(g.G) * g.n * g.OH * g.OW * g.Kp();
 }
 
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
                 bool relu, const Workspace& ws, float* col, Mode m, cudaStream_t s) {
-  if (m == Mode::Tf32 && col && fprop_col_route(g)) {
+  if (m == Mode::Tf32 && col && s2d_route(g)) {
+    const ConvGeom q = s2d_geom(g);
+    float* wq = col + s2d_x_elems(g);
+    s2d_x(g, x, col, s);
+    const int wt = q.F * q.Kf();
+    s2d_w_k<<<(wt + 255) / 256, 256, 0, s>>>(w, g, q, wq, wt);
+    PSG_CUDA(cudaGetLastError());
+    tc_fprop(q, col, wq, bias, y, relu, ws, s);
+  } else if (m == Mode::Tf32 && col && fprop_col_route(g)) {
     im2col(g, x, col, s);
     tc_fprop(col_geom(g), col, w, bias, y, relu, ws, s);
   } else if (use_tc(g, 0, m)) {
@@ -157,7 +282,14 @@ void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, b
 
 void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
                 const Workspace& ws, float* col, Mode m, cudaStream_t s) {
-  if (m == Mode::Tf32 && col && wgrad_col_route(g)) {
+  if (m == Mode::Tf32 && col && s2d_route(g)) {  // x' written by this step's fprop
+    const ConvGeom q = s2d_geom(g);
+    float* dwq = col + s2d_x_elems(g) + s2d_w_elems(g);
+    tc_wgrad(q, col, dy, dwq, db, ws, s);
+    const int total = g.F * g.Kp();
+    s2d_dw_k<<<(total + 255) / 256, 256, 0, s>>>(dwq, g, q, dw, total);
+    PSG_CUDA(cudaGetLastError());
+  } else if (m == Mode::Tf32 && col && wgrad_col_route(g)) {
     if (!fprop_col_route(g)) im2col(g, x, col, s);  // else written by this step's fprop
     tc_wgrad_col(g, col, dy, dw, db, ws, s);
   } else if (use_tc(g, 2, m)) {
@@ -171,6 +303,7 @@ size_t conv_workspace_elems(const ConvGeom& g, Mode m) {
   size_t e = conv_workspace_elems_simt(g);
   if (m == Mode::Tf32) {
     e = std::max(e, tc_workspace_elems(g));
+    if (s2d_route(g)) e = std::max(e, tc_workspace_elems(s2d_geom(g)));
     if (fprop_col_route(g)) e = std::max(e, tc_workspace_elems(col_geom(g)));
     if (wgrad_col_route(g)) e = std::max(e, tc_wgrad_col_ws_elems(g));
   }
@@ -178,6 +311,8 @@ size_t conv_workspace_elems(const ConvGeom& g, Mode m) {
 }
 
 int conv_launches(const ConvGeom& g, int which, Mode m) {
+  if (m == Mode::Tf32 && which == 0 && s2d_route(g)) return 2 + tc_launches(s2d_geom(g), 0);
+  if (m == Mode::Tf32 && which == 2 && s2d_route(g)) return tc_launches(s2d_geom(g), 2) + 1;
   if (m == Mode::Tf32 && which == 0 && fprop_col_route(g))
     return 1 + tc_launches(col_geom(g), 0);
   if (m == Mode::Tf32 && which == 2 && wgrad_col_route(g))

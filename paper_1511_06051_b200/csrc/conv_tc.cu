@@ -175,6 +175,8 @@ int pick_n_tile(int N) {
 // lifts the tensor-pipe ceiling (tools/tma_bench.cu: one CTA's M = 128 MMAs take a fixed
 // ~200 cycles each for N <= 256, a pair's M = 256 MMA reaches ~1.1 PFLOP/s at N >= 128).
 // MN-major B is loaded in 32-column chunks, so each half must be whole chunks (N % 64).
+int sm_count();
+
 bool want_pair(const TcArgs& a) {
   static const int env = [] {
     const char* e = std::getenv("PSG_TC_PAIR");
@@ -182,7 +184,11 @@ bool want_pair(const TcArgs& a) {
   }();
   if (!env) return false;
   if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K) return false;
-  return a.m_tiles >= 2;
+  if (a.m_tiles < 2) return false;
+  // small GEMMs: halving the number of work units costs more in load balance than the
+  // pair gains (cifar10_quick); want >= 2 waves of clusters
+  const long long units = static_cast<long long>((a.m_tiles + 1) / 2) * a.n_tiles * a.G * a.taps;
+  return env > 1 || units >= sm_count();
 }
 
 void finish_args(TcArgs& a, int kblk, int sms) {
@@ -333,6 +339,16 @@ bool is_linear(const ConvGeom& g) {
 
 int kblk_for(int channels) { return channels % 32 == 0 ? 32 : (channels % 16 == 0 ? 16 : 0); }
 
+// 16-channel K blocks move 64-byte rows, which the TMA engine serves at about half the
+// bytes per clock of 128-byte rows (tools/tma_bench.cu): prefer zero-padded 32-blocks.
+bool prefer_k32() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_TC_K32");
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  return v;
+}
+
 // --- planners: fill TcArgs (out/bias/flags are set by the caller) -------------
 bool plan_fprop(const ConvGeom& g, TcArgs& a, int& kblk) {
   std::memset(&a, 0, sizeof a);
@@ -355,6 +371,7 @@ bool plan_fprop(const ConvGeom& g, TcArgs& a, int& kblk) {
   }
   if (g.sh != 1 || g.sw != 1 || g.Fg() % 16) return false;
   kblk = kblk_for(g.Cgs());
+  if (kblk == 16 && prefer_k32()) kblk = 0;
   // C/G not a multiple of 16: 32-channel blocks per tap, the tail read as 0 (A: the NHWC
   // input's channels past C read OOB, other groups' channels meet B's OOB zeros; B: W
   // viewed as [F][taps][C/G])
@@ -411,6 +428,7 @@ bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   }
   if (g.sh != 1 || g.sw != 1 || g.Cgs() % 4 || g.cs_in % 4) return false;
   kblk = kblk_for(g.Fg());
+  if (kblk == 16 && prefer_k32()) kblk = 0;
   if (!kblk) {  // F/G not a multiple of 16: 32-filter blocks, the tail read as 0 (B's 4-D view)
     if (g.Fg() % 4 || g.F % 4) return false;
     kblk = 32;

@@ -1,4 +1,7 @@
-for cfg in "PSG_TC_PAIR=1" "PSG_TC_KPS=1" "PSG_TC_KPS=1 PSG_TC_PRODUCERS=2" "PSG_TC_PRODUCERS=2" "PSG_TC_PRODUCERS=1" "PSG_TC_KPS=4"; do
-  name=$(echo $cfg | tr ' =' '__')
-  env $cfg timeout 300 python bench.py --workload alexnet --steps 3 --warmup 3 --profile-json gpurun_out/pr_$name.json > gpurun_out/pr_$name.log 2>&1
+# A/B the tcgen05 GEMM knobs on one workload: per-op profile per setting.
+#   bash tools/probe_env.sh <workload> "ENV=1 ..." "ENV=2" ...
+W=$1; shift
+for cfg in "$@"; do
+  name=$(echo "$W $cfg" | tr ' =' '__')
+  env $cfg timeout 300 python bench.py --workload $W --profile-json gpurun_out/pr_$name.json > gpurun_out/pr_$name.log 2>&1
 done
