@@ -291,7 +291,7 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   // float4 epilogue stores need 16-byte aligned rows and 4-column-aligned validity bounds
   a.epi_vec = a.ldo % 4 == 0 && a.col_g % 4 == 0 && a.col_tap % 4 == 0 &&
               (a.cpt ? a.cgs % 4 == 0 : a.n_valid % 4 == 0);
-  const size_t smem = static_cast<size_t>(a.stages) * a.kps * a.stage_bytes + kEpiBytes + 1024;
+  const size_t smem = static_cast<size_t>(a.stages) * a.kps * a.stage_bytes + 1024;  // + static
   const int per = a.pair ? 2 : 1;
   static const bool debug = std::getenv("PSG_TC_DEBUG") != nullptr;
   if (debug)

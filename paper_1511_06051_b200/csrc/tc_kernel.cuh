@@ -28,7 +28,7 @@ constexpr int kMmaWarp = 4, kAllocWarp = 5, kEpiWarp0 = 8;
 constexpr int kThreads = 384;
 constexpr int kTileM = 128;
 constexpr int kAccCols = 256;                 // one accumulator: 128 lanes x 256 fp32
-constexpr int kEpiBytes = 0;                  // the epilogue needs no shared memory
+constexpr int kEpiBytes = 2 * kAccCols * 4;  // static smem: the bias of each accumulator's tile
 
 struct TcArgs {
   int a_mode, b_mode, row_map;
@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(16) float bias_sh[2][kAccCols];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -458,6 +459,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int col0 = p.col_g * t.g + p.col_tap * t.tap + t.n * p.n_tile;
       const int nvalid = min(p.n_tile, p.n_valid - t.n * p.n_tile);
       const uint32_t acc = local & 1;
+      // the tile's bias to smem while its MMAs run (safe to overwrite: every epilogue thread
+      // passed tile local-1's barrier, so tile local-2's reads of this buffer are done)
+      const float* bsh = bias_sh[acc];
+      if (p.bias && !p.ws) {
+        for (int i = ew * 32 + lane; i < p.n_tile; i += 128)
+          bias_sh[acc][i] = i < nvalid ? p.bias[col0 + i] : 0.f;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
       tc::mbar_wait(tc::smem_u32(&tfull_bar[acc]), (local >> 1) & 1);
       tc::fence_after_sync();
       const uint32_t taddr = tmem + acc * kAccCols + (static_cast<uint32_t>(ew * 32) << 16);
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               float4* dst = reinterpret_cast<float4*>(rowp + cidx);
               if (!p.ws) {
                 if (p.bias) {
-                  const float4 bb = *reinterpret_cast<const float4*>(p.bias + cidx);
+                  const float4 bb = *reinterpret_cast<const float4*>(bsh + c);
                   y.x += bb.x; y.y += bb.y; y.z += bb.z; y.w += bb.w;
                   if (p.relu) {
                     y.x = y.x > 0.f ? y.x : 0.f;
@@ -530,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float yv = e4[e];
                 if (!p.ws) {
                   if (p.bias) {
-                    yv += p.bias[ce];
+                    yv += bsh[c + e];
                     if (p.relu) yv = yv > 0.f ? yv : 0.f;
                   }
                   if (acc_out) yv += rowp[ce];
