@@ -109,13 +109,26 @@ bool s2d_route(const ConvGeom& g) {
 
 // x'[b][hs][ws][c'] for c' = (dy*s + dx)*C + c < s*s*C; 0 beyond (and outside x).
 // Block y = one x' row (b, hs); threads stride over its W' x C'/4 float4 cells (32-bit
-// index math), so every store is a coalesced float4 run.
+// index math), so every store is a coalesced float4 run.  With `idx` the images come
+// straight from the HBM-resident dataset (row idx[cursor * batch + b], channel stride
+// src_cs) and the block of row hs = 0 also copies the label: the batch gather and the
+// space-to-depth rearrangement in one pass (data.hpp:292-304 gather_batch).
 __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, ConvGeom g,
-                                               ConvGeom q, float* __restrict__ xs) {
+                                               ConvGeom q, float* __restrict__ xs,
+                                               const uint32_t* __restrict__ idx,
+                                               const int* __restrict__ cursor, int batch,
+                                               int src_cs, const int32_t* __restrict__ ds_labels,
+                                               int32_t* __restrict__ labels) {
+  pdl_enter();
   const int s = g.sh, C = g.Cgs(), c4n = q.cs_in / 4, row = blockIdx.x;
   const int hs = row % q.H, b = row / q.H;
   float4* out = reinterpret_cast<float4*>(xs) + static_cast<size_t>(row) * q.W * c4n;
-  const float* xb = x + static_cast<size_t>(b) * g.H * g.W * g.cs_in;
+  size_t img = b;
+  if (idx) {
+    img = idx[static_cast<size_t>(cursor ? *cursor : 0) * batch + b];
+    if (hs == 0 && threadIdx.x == 0) labels[b] = ds_labels[img];
+  }
+  const float* xb = x + img * g.H * g.W * src_cs;
   for (int j = threadIdx.x; j < q.W * c4n; j += blockDim.x) {
     const int ws = j / c4n, c0 = (j - ws * c4n) * 4;
     float v[4];
@@ -127,7 +140,7 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
         const int blk = cp / C, c = cp - blk * C;
         const int ih = s * hs + blk / s - g.ph, iw = s * ws + blk % s - g.pw;
         if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
-          v[e] = __ldg(xb + (ih * g.W + iw) * g.cs_in + c);
+          v[e] = __ldg(xb + (ih * g.W + iw) * src_cs + c);
       }
     }
     out[j] = make_float4(v[0], v[1], v[2], v[3]);
@@ -137,6 +150,7 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
 // W'[f][tu][tv][c'] = W[f][s*tu + dy][s*tv + dx][c] (0 past the kernel / past s*s*C)
 __global__ void s2d_w_k(const float* __restrict__ w, ConvGeom g, ConvGeom q,
                         float* __restrict__ ws, int total) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const int s = g.sh, C = g.Cgs(), Cp = q.cs_in, Kf = q.Kf();
@@ -154,6 +168,7 @@ __global__ void s2d_w_k(const float* __restrict__ w, ConvGeom g, ConvGeom q,
 // dW[f][(u*kw + v)*C + c] = dW'[f][tu][tv][c'] (the inverse map; row padding stays 0)
 __global__ void s2d_dw_k(const float* __restrict__ dws, ConvGeom g, ConvGeom q,
                          float* __restrict__ dw, int total) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const int s = g.sh, C = g.Cgs(), Kp = g.Kp(), Kf = g.Kf();
@@ -171,7 +186,8 @@ void s2d_x(const ConvGeom& g, const float* x, float* xs, cudaStream_t st) {
   const ConvGeom q = s2d_geom(g);
   if (static_cast<size_t>(g.H) * g.W * g.cs_in >= (1ULL << 31))
     throw std::invalid_argument("s2d: image too large");
-  s2d_x_k<<<q.n * q.H, 256, 0, st>>>(x, g, q, xs);
+  launch_k(s2d_x_k, q.n * q.H, 256, 0, st, x, g, q, xs, nullptr, nullptr, 0, g.cs_in, nullptr,
+           nullptr);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -194,6 +210,7 @@ constexpr int kPixPerBlock = 16;
 
 __global__ void __launch_bounds__(128) im2col_k(const float* __restrict__ x, ConvGeom g,
                                                 float* __restrict__ col, uint32_t pixels) {
+  pdl_enter();
   __shared__ int s_ih[kPixPerBlock], s_iw[kPixPerBlock], s_base[kPixPerBlock];
   const int Kf = g.Kf(), Kp = g.Kp(), Cgs = g.Cgs(), grp = blockIdx.y;
   const uint32_t p0 = blockIdx.x * kPixPerBlock;
@@ -235,7 +252,7 @@ void im2col(const ConvGeom& g, const float* x, float* col, cudaStream_t s) {
   const size_t pixels = static_cast<size_t>(g.n) * g.OH * g.OW;
   if (pixels >= (1ULL << 31)) throw std::invalid_argument("im2col: too many pixels");
   const dim3 grid(static_cast<unsigned>((pixels + kPixPerBlock - 1) / kPixPerBlock), g.G);
-  im2col_k<<<grid, 128, 0, s>>>(x, g, col, static_cast<uint32_t>(pixels));
+  launch_k(im2col_k, grid, 128, 0, s, x, g, col, static_cast<uint32_t>(pixels));
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -245,6 +262,19 @@ bool use_tc(const ConvGeom& g, int which, Mode m) {
 
 }  // namespace
 
+bool conv_s2d_input(const ConvGeom& g, Mode m) { return m == Mode::Tf32 && s2d_route(g); }
+
+void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_labels,
+                const uint32_t* idx, const int* cursor, int src_cs, float* col, int32_t* labels,
+                cudaStream_t st) {
+  const ConvGeom q = s2d_geom(g);
+  if (static_cast<size_t>(g.H) * g.W * src_cs >= (1ULL << 31))
+    throw std::invalid_argument("s2d: image too large");
+  launch_k(s2d_x_k, q.n * q.H, 256, 0, st, ds_images, g, q, col, idx, cursor, g.n, src_cs,
+           ds_labels, labels);
+  PSG_CUDA(cudaGetLastError());
+}
+
 size_t conv_col_elems(const ConvGeom& g, Mode m) {
   // s2d route: x' (written by fprop, read by wgrad), W', dW'
   if (m == Mode::Tf32 && s2d_route(g)) return s2d_x_elems(g) + 2 * s2d_w_elems(g);
@@ -253,13 +283,13 @@ size_t conv_col_elems(const ConvGeom& g, Mode m) {
 }
 
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
-                bool relu, const Workspace& ws, float* col, Mode m, cudaStream_t s) {
+                bool relu, const Workspace& ws, float* col, Mode m, cudaStream_t s, bool x_s2d) {
   if (m == Mode::Tf32 && col && s2d_route(g)) {
     const ConvGeom q = s2d_geom(g);
     float* wq = col + s2d_x_elems(g);
-    s2d_x(g, x, col, s);
+    if (!x_s2d) s2d_x(g, x, col, s);
     const int wt = q.F * q.Kf();
-    s2d_w_k<<<(wt + 255) / 256, 256, 0, s>>>(w, g, q, wq, wt);
+    launch_k(s2d_w_k, (wt + 255) / 256, 256, 0, s, w, g, q, wq, wt);
     PSG_CUDA(cudaGetLastError());
     tc_fprop(q, col, wq, bias, y, relu, ws, s);
   } else if (m == Mode::Tf32 && col && fprop_col_route(g)) {
@@ -287,7 +317,7 @@ void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, f
     float* dwq = col + s2d_x_elems(g) + s2d_w_elems(g);
     tc_wgrad(q, col, dy, dwq, db, ws, s);
     const int total = g.F * g.Kp();
-    s2d_dw_k<<<(total + 255) / 256, 256, 0, s>>>(dwq, g, q, dw, total);
+    launch_k(s2d_dw_k, (total + 255) / 256, 256, 0, s, dwq, g, q, dw, total);
     PSG_CUDA(cudaGetLastError());
   } else if (m == Mode::Tf32 && col && wgrad_col_route(g)) {
     if (!fprop_col_route(g)) im2col(g, x, col, s);  // else written by this step's fprop

@@ -241,6 +241,7 @@ struct WgradProb {
 template <class P, int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     igemm_simt(const P p, int tiles_n, int kchunk) {
+  pdl_enter();
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int AL = BM * BK / NT, BL = BN * BK / NT;
   static_assert(AL >= 1 && BL >= 1 && NT % BK == 0, "tile config");
@@ -356,6 +357,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 __global__ void wgrad_reduce(const float* __restrict__ ws, int splits, int G, int M, int N,
                              int Kf, int Kp, int Fg, float* __restrict__ dw,
                              float* __restrict__ db) {
+  pdl_enter();
   const size_t total = static_cast<size_t>(G) * M * N;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -376,6 +378,7 @@ __global__ void wgrad_reduce(const float* __restrict__ ws, int splits, int G, in
 __global__ void splitk_reduce(const float* __restrict__ ws, int splits, int G, int M, int N,
                               const float* __restrict__ bias, int relu, int accumulate, int ld,
                               int gstride, float* __restrict__ out) {
+  pdl_enter();
   const size_t total = static_cast<size_t>(G) * M * N;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -421,15 +424,15 @@ void launch(const P& p, int splits, int kchunk, cudaStream_t s) {
   const int tiles_m = (p.M + t.bm - 1) / t.bm, tiles_n = (p.N + t.bn - 1) / t.bn;
   const dim3 grid(tiles_m * tiles_n, 1, p.G * splits);
   if (t.bm == 128 && t.bn == 128)
-    igemm_simt<P, 128, 128, 8, 8><<<grid, 256, 0, s>>>(p, tiles_n, kchunk);
+    launch_k(igemm_simt<P, 128, 128, 8, 8>, grid, 256, 0, s, p, tiles_n, kchunk);
   else if (t.bm == 128 && t.bn == 64)
-    igemm_simt<P, 128, 64, 8, 4><<<grid, 256, 0, s>>>(p, tiles_n, kchunk);
+    launch_k(igemm_simt<P, 128, 64, 8, 4>, grid, 256, 0, s, p, tiles_n, kchunk);
   else if (t.bm == 64 && t.bn == 128)
-    igemm_simt<P, 64, 128, 4, 8><<<grid, 256, 0, s>>>(p, tiles_n, kchunk);
+    launch_k(igemm_simt<P, 64, 128, 4, 8>, grid, 256, 0, s, p, tiles_n, kchunk);
   else if (t.bm == 128 && t.bn == 32)
-    igemm_simt<P, 128, 32, 4, 4><<<grid, 256, 0, s>>>(p, tiles_n, kchunk);
+    launch_k(igemm_simt<P, 128, 32, 4, 4>, grid, 256, 0, s, p, tiles_n, kchunk);
   else
-    igemm_simt<P, 64, 64, 4, 4><<<grid, 256, 0, s>>>(p, tiles_n, kchunk);
+    launch_k(igemm_simt<P, 64, 64, 4, 4>, grid, 256, 0, s, p, tiles_n, kchunk);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -484,7 +487,7 @@ void reduce_into(const Workspace& ws, int splits, int G, int M, int N, const flo
                  bool relu, bool accumulate, int ld, int gstride, float* out, cudaStream_t s) {
   const size_t total = static_cast<size_t>(G) * M * N;
   const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 8));
-  splitk_reduce<<<blocks, 256, 0, s>>>(ws.ptr, splits, G, M, N, bias, relu, accumulate, ld,
+  launch_k(splitk_reduce, blocks, 256, 0, s, ws.ptr, splits, G, M, N, bias, relu, accumulate, ld,
                                        gstride, out);
   PSG_CUDA(cudaGetLastError());
 }
@@ -571,7 +574,7 @@ void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* 
   if (!p.direct) {
     const size_t total = static_cast<size_t>(g.G) * p.M * p.N;
     const int blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 8));
-    wgrad_reduce<<<blocks, 256, 0, s>>>(ws.ptr, sp.splits, g.G, p.M, p.N, p.Kf, p.Kp, g.Fg(), dw,
+    launch_k(wgrad_reduce, blocks, 256, 0, s, ws.ptr, sp.splits, g.G, p.M, p.N, p.Kf, p.Kp, g.Fg(), dw,
                                         db);
     PSG_CUDA(cudaGetLastError());
   }

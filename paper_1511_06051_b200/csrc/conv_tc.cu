@@ -40,6 +40,7 @@ __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long l
                                 long long total, const float* __restrict__ bias, int ldo,
                                 int valid_cols, int relu, int accumulate,
                                 float* __restrict__ out) {
+  pdl_enter();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     if (valid_cols < ldo && i % ldo >= valid_cols) {
@@ -74,6 +75,7 @@ template <typename V>
 __global__ void __launch_bounds__(256) bias_grad_partial(const V* __restrict__ dy, int rows,
                                                          int units, int rows_per_chunk,
                                                          V* __restrict__ part) {
+  pdl_enter();
   __shared__ V red[256];
   const int cpr = min(units, 256), rpi = 256 / cpr;
   const int tx = threadIdx.x % cpr, ty = threadIdx.x / cpr;
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(256) bias_grad_partial(const V* __restrict__ d
 
 __global__ void bias_grad_final(const float* __restrict__ part, int chunks, int cols,
                                 float* __restrict__ db) {
+  pdl_enter();
   const int c = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (c >= cols) return;
   float s = 0.f;
@@ -143,6 +146,71 @@ CUtensorMap map_nhwc(const float* base, int n, int h, int w, int c, int box_c, i
   return make_map(base, 4, dims, str, box, sw);
 }
 
+// im2col-mode map over NHWC [n][h][w][c]: boxes of `pixels` consecutive traversal
+// positions x box_c channels.  The traversal grid is the (w + upper - lower) x
+// (h + upper - lower) positions starting at the lower corner (corners: [0] = W, [1] = H).
+CUtensorMap map_nhwc_im2col(const float* base, int n, int h, int w, int c, int box_c,
+                            int pixels, int lw, int lh, int uw, int uh, CUtensorMapSwizzle sw) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                          const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<Fn>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeIm2col unavailable");
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
+                              static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  const cuuint64_t str[3] = {static_cast<cuuint64_t>(c) * 4, static_cast<cuuint64_t>(w) * c * 4,
+                             static_cast<cuuint64_t>(h) * w * c * 4};
+  const int lower[2] = {lw, lh}, upper[2] = {uw, uh};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
+                        str, lower, upper, static_cast<cuuint32_t>(box_c),
+                        static_cast<cuuint32_t>(pixels), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeIm2col failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+// TMA im2col boxes over linear pixel tiles (no rectangle padding of M in fprop / dgrad,
+// of K in wgrad).  PSG_TC_IM2COL bit 0: fprop / dgrad, bit 1: wgrad (default 3; 0 keeps
+// the pixel rectangles).
+bool use_im2col(int bit = 1) {
+  static const int v = [] {
+    const char* e = std::getenv("PSG_TC_IM2COL");
+    return e ? std::atoi(e) : 3;
+  }();
+  return (v & bit) != 0;
+}
+
+// Switch a rect-K plan (fprop / dgrad) to linear pixel tiles over an out_h x out_w grid.
+void to_im2col(TcArgs& a, const ConvGeom& g, int out_h, int out_w, int sign) {
+  if (!use_im2col()) return;
+  // TMA im2col corners are signed 8-bit for 4-D maps
+  const int lw = sign > 0 ? -g.pw : -(g.kw - 1 - g.pw), lh = sign > 0 ? -g.ph : -(g.kh - 1 - g.ph);
+  if (lw < -128 || lh < -128 || g.kw > 128 || g.kh > 128) return;
+  a.a_mode = A_IM2COL_K;
+  a.row_map = ROW_LINEAR;
+  a.out_h = out_h;
+  a.out_w = out_w;
+  a.kh = g.kh;
+  a.im_lw = lw;
+  a.im_lh = lh;
+  a.m_valid = g.n * out_h * out_w;
+  a.m_tiles = (a.m_valid + kTileM - 1) / kTileM;
+  a.row_g = 0;
+}
+
 CUtensorMap map_2d(const float* base, long long rows, long long cols, int box_c, int box_r,
                    CUtensorMapSwizzle sw) {
   const uint64_t dims[2] = {static_cast<uint64_t>(cols), static_cast<uint64_t>(rows)};
@@ -183,7 +251,7 @@ bool want_pair(const TcArgs& a) {
     return e ? std::atoi(e) : 1;
   }();
   if (!env) return false;
-  if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K) return false;
+  if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K && a.a_mode != A_IM2COL_K) return false;
   if (a.m_tiles < 2) return false;
   // small GEMMs: halving the number of work units costs more in load balance than the
   // pair gains (cifar10_quick); want >= 2 waves of clusters
@@ -310,13 +378,20 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = per;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (a.pair) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = per;
+      attr[na].val.clusterDim.y = 1;
+      attr[na++].val.clusterDim.z = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = a.pair ? 1 : 0;
+    cfg.numAttrs = na;
     PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, a));
   };
   if (kblk == 32)
@@ -326,7 +401,7 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   PSG_CUDA(cudaGetLastError());
   if (splits > 1) {
     const int blocks = static_cast<int>(std::min<long long>((out_elems + 255) / 256, 148 * 8));
-    tc_split_reduce<<<blocks, 256, 0, s>>>(ws, splits, out_elems, out_elems, a0.bias, a0.ldo,
+    launch_k(tc_split_reduce, blocks, 256, 0, s, ws, splits, out_elems, out_elems, a0.bias, a0.ldo,
                                            a0.valid_cols ? a0.valid_cols : a0.ldo, a0.relu,
                                            a0.accumulate, a0.out);
     PSG_CUDA(cudaGetLastError());
@@ -404,6 +479,7 @@ bool plan_fprop(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.n_valid = g.Fg();
   a.col_g = g.Fg();
   a.ldo = g.F;
+  to_im2col(a, g, g.OH, g.OW, 1);
   return true;
 }
 
@@ -457,6 +533,7 @@ bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.n_valid = g.Cgs();
   a.col_g = g.Cgs();
   a.ldo = g.cs_in;
+  to_im2col(a, g, g.H, g.W, -1);
   return true;
 }
 
@@ -509,6 +586,19 @@ bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.row_g = g.Fg();
   a.ldo = g.Kp();
   a.valid_cols = g.Kf();
+  if (use_im2col(2) && g.pw <= 128 && g.ph <= 128 && g.kw <= 128 && g.kh <= 128) {
+    // K = linear output pixels (no rectangle padding): dY as a plain [pixels][F] matrix,
+    // X chunks as TMA im2col boxes shifted by each chunk's tap
+    a.a_mode = A_2D_MN;
+    a.b_mode = B_TAPS_IM2COL;
+    a.kth = a.ktw = 0;
+    a.out_h = g.OH;
+    a.out_w = g.OW;
+    a.im_lw = -g.pw;
+    a.im_lh = -g.ph;
+    a.kh = g.kh;
+    a.kblocks = (g.n * g.OH * g.OW + kblk - 1) / kblk;
+  }
   return true;
 }
 
@@ -554,13 +644,13 @@ void bias_grad(const float* dy, long long rows, int F, float* part, float* db, c
   const int per = static_cast<int>((rows + chunks - 1) / chunks);
   const dim3 grid(cblocks, chunks);
   if (vec)
-    bias_grad_partial<float4><<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(dy),
+    launch_k(bias_grad_partial<float4>, grid, 256, 0, s, reinterpret_cast<const float4*>(dy),
                                                    static_cast<int>(rows), units, per,
                                                    reinterpret_cast<float4*>(part));
   else
-    bias_grad_partial<float><<<grid, 256, 0, s>>>(dy, static_cast<int>(rows), units, per, part);
+    launch_k(bias_grad_partial<float>, grid, 256, 0, s, dy, static_cast<int>(rows), units, per, part);
   PSG_CUDA(cudaGetLastError());
-  bias_grad_final<<<(F + 7) / 8, 256, 0, s>>>(part, chunks, F, db);
+  launch_k(bias_grad_final, (F + 7) / 8, 256, 0, s, part, chunks, F, db);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -635,7 +725,11 @@ void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bi
     ma = map_2d(x, g.n, g.cs_in, kblk, kTileM, k_swizzle(kblk));
     mb = map_2d(w, g.F, g.cs_in, kblk, a.b_cols, k_swizzle(kblk));
   } else {
-    ma = map_nhwc(x, g.n, g.H, g.W, g.cs_in, kblk, a.wm, a.rm, k_swizzle(kblk));
+    if (a.a_mode == A_IM2COL_K)  // traversal grid OH x OW: upper = pad - (k - 1)
+      ma = map_nhwc_im2col(x, g.n, g.H, g.W, g.cs_in, kblk, kTileM, a.im_lw, a.im_lh,
+                           g.pw - (g.kw - 1), g.ph - (g.kh - 1), k_swizzle(kblk));
+    else
+      ma = map_nhwc(x, g.n, g.H, g.W, g.cs_in, kblk, a.wm, a.rm, k_swizzle(kblk));
     if (a.b_mode == B_3D_K) {
       const uint64_t dims[3] = {static_cast<uint64_t>(g.Cgs()),
                                 static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.F)};
@@ -663,7 +757,11 @@ void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, boo
     ma = map_2d(dy, g.n, g.F, kblk, kTileM, k_swizzle(kblk));
     mb = map_2d(w, g.F, g.cs_in, 32, kblk, kMnSwizzle);
   } else {
-    ma = map_nhwc(dy, g.n, g.OH, g.OW, g.F, kblk, a.wm, a.rm, k_swizzle(kblk));
+    if (a.a_mode == A_IM2COL_K)  // traversal grid H x W over dY: lower = -(k-1-p), upper = -p
+      ma = map_nhwc_im2col(dy, g.n, g.OH, g.OW, g.F, kblk, kTileM, a.im_lw, a.im_lh, -g.pw,
+                           -g.ph, k_swizzle(kblk));
+    else
+      ma = map_nhwc(dy, g.n, g.OH, g.OW, g.F, kblk, a.wm, a.rm, k_swizzle(kblk));
     const uint64_t dims[4] = {static_cast<uint64_t>(g.Cgs()),
                               static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.Fg()),
                               static_cast<uint64_t>(g.G)};
@@ -685,7 +783,11 @@ void tc_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, flo
   finish_args(a, kblk, sm_count());
   a.out = dw;
   CUtensorMap ma, mb;
-  if (a.a_mode == A_2D_MN) {
+  if (a.b_mode == B_TAPS_IM2COL) {
+    ma = map_2d(dy, static_cast<long long>(g.n) * g.OH * g.OW, g.F, 32, kblk, kMnSwizzle);
+    mb = map_nhwc_im2col(x, g.n, g.H, g.W, g.cs_in, 32, kblk, a.im_lw, a.im_lh,
+                         g.pw - (g.kw - 1), g.ph - (g.kh - 1), kMnSwizzle);
+  } else if (a.a_mode == A_2D_MN) {
     ma = map_2d(dy, g.n, g.F, 32, kblk, kMnSwizzle);
     mb = map_2d(x, g.n, g.cs_in, 32, kblk, kMnSwizzle);
   } else {

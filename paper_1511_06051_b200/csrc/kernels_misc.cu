@@ -3,10 +3,19 @@
 // (no float atomics), so a step is bitwise reproducible.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "psg_internal.h"
 
 namespace psg {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PSG_PDL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
 namespace {
 
 inline int grid_for(size_t n, int block = 256, int max_blocks = 148 * 16) {
@@ -28,6 +37,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:11-16
 // ------------------------------------------------------------------ relu ---
 // model.hpp:319-326 (y = x > 0 ? x : 0) and :484-491 (dx += x > 0 ? dy : 0).
 __global__ void relu_fwd_k(const float* __restrict__ x, float* __restrict__ y, size_t n) {
+  pdl_enter();
   const size_t n4 = n / 4;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4* y4 = reinterpret_cast<float4*>(y);
@@ -47,6 +57,7 @@ __global__ void relu_fwd_k(const float* __restrict__ x, float* __restrict__ y, s
 
 __global__ void relu_bwd_k(const float* __restrict__ x, const float* __restrict__ dy,
                            float* __restrict__ dx, size_t n, int accumulate) {
+  pdl_enter();
   const size_t n4 = n / 4;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   const float4* g4 = reinterpret_cast<const float4*>(dy);
@@ -77,6 +88,7 @@ __global__ void relu_bwd_k(const float* __restrict__ x, const float* __restrict_
 __global__ void softmax_loss_k(const float* __restrict__ logits, const int32_t* __restrict__ labels,
                                int n, int C, double scale, float* __restrict__ probs,
                                float* __restrict__ dlogits, double* __restrict__ row_loss) {
+  pdl_enter();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (warp >= n) return;
   const float* row = logits + static_cast<size_t>(warp) * C;
@@ -100,6 +112,7 @@ __global__ void softmax_loss_k(const float* __restrict__ logits, const int32_t* 
 // Fixed-order reduction of the per-row losses: loss = sum / n * loss_weight.
 __global__ void loss_reduce_k(const double* __restrict__ row_loss, int n, double lw,
                               double* __restrict__ loss, int* __restrict__ flag, int accumulate) {
+  pdl_enter();
   __shared__ double part[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += row_loss[i];
@@ -119,6 +132,7 @@ __global__ void loss_reduce_k(const double* __restrict__ row_loss, int n, double
 // tensor.hpp:187-201 argmax (lowest index wins) + model.hpp:129-133 count.
 __global__ void argmax_count_k(const float* __restrict__ probs, const int32_t* __restrict__ labels,
                                int n, int C, unsigned long long* correct) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float* p = probs + static_cast<size_t>(i) * C;
@@ -137,6 +151,7 @@ __global__ void sgd_update_k(const UpdateChunk* __restrict__ chunks, float* __re
                              float* __restrict__ v, const float* __restrict__ g, float mu,
                              int* __restrict__ flag, int* __restrict__ cursor,
                              uint64_t* __restrict__ step) {
+  pdl_enter();
   const UpdateChunk ch = chunks[blockIdx.x];
   bool bad = false;
   const uint32_t vec_end = ch.begin + ((ch.end - ch.begin) / 4) * 4;
@@ -190,6 +205,7 @@ struct PtrPack {
 
 // out == nullptr: write the mean back into every input; else into out only.
 __global__ void average_ordered_k(PtrPack bufs, int K, size_t n, float* out, int* flag) {
+  pdl_enter();
   const size_t n4 = n / 4;
   GRID_STRIDE(i, n4) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -223,6 +239,7 @@ __global__ void average_ordered_k(PtrPack bufs, int K, size_t n, float* out, int
 }
 
 __global__ void scale_k(float* x, size_t n, float a, int* flag) {
+  pdl_enter();
   GRID_STRIDE(i, n) {
     const float r = x[i] * a;
     if (!isfinite(r)) *flag = 1;
@@ -231,6 +248,7 @@ __global__ void scale_k(float* x, size_t n, float a, int* flag) {
 }
 
 __global__ void fill_uniform_k(float* x, size_t n, uint64_t seed, double lo, double hi) {
+  pdl_enter();
   GRID_STRIDE(i, n) {
     const double u = static_cast<double>(mix64(seed + i) >> 11) * 0x1.0p-53;
     x[i] = static_cast<float>(lo + (hi - lo) * u);
@@ -240,13 +258,13 @@ __global__ void fill_uniform_k(float* x, size_t n, uint64_t seed, double lo, dou
 }  // namespace
 
 void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s) {
-  relu_fwd_k<<<grid_for(n / 4 + 1), 256, 0, s>>>(x, y, n);
+  launch_k(relu_fwd_k, grid_for(n / 4 + 1), 256, 0, s, x, y, n);
   PSG_CUDA(cudaGetLastError());
 }
 
 void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumulate,
               cudaStream_t s) {
-  relu_bwd_k<<<grid_for(n / 4 + 1), 256, 0, s>>>(x, dy, dx, n, accumulate);
+  launch_k(relu_bwd_k, grid_for(n / 4 + 1), 256, 0, s, x, dy, dx, n, accumulate);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -254,16 +272,17 @@ void softmax_loss(const float* logits, const int32_t* labels, int n, int C, doub
                   float* probs, float* dlogits, double* row_loss, double* loss, int* flag,
                   bool accumulate, cudaStream_t s) {
   const double scale = loss_weight * (1.0 / static_cast<double>(n));
-  softmax_loss_k<<<(n * 32 + 255) / 256, 256, 0, s>>>(logits, labels, n, C, scale, probs, dlogits,
+  launch_k(softmax_loss_k, (n * 32 + 255) / 256, 256, 0, s, logits, labels, n, C, scale, probs, dlogits,
                                                       row_loss);
   PSG_CUDA(cudaGetLastError());
-  loss_reduce_k<<<1, 256, 0, s>>>(row_loss, n, loss_weight, loss, flag, accumulate ? 1 : 0);
+  launch_k(loss_reduce_k, 1, 256, 0, s, row_loss, n, loss_weight, loss, flag, accumulate ? 1 : 0);
   PSG_CUDA(cudaGetLastError());
 }
 
 namespace {
 __global__ void concat_copy_k(const float* __restrict__ in, int ci, float* __restrict__ out,
                               int ctot, int off, size_t total) {
+  pdl_enter();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t p = i / ci, c = i % ci;
@@ -272,6 +291,7 @@ __global__ void concat_copy_k(const float* __restrict__ in, int ci, float* __res
 }
 __global__ void concat_split_k(const float* __restrict__ dy, int ctot, int off,
                                float* __restrict__ dx, int ci, size_t total, int accumulate) {
+  pdl_enter();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t p = i / ci, c = i % ci;
@@ -287,27 +307,27 @@ unsigned concat_blocks(size_t total) {
 void concat_copy(const float* in, int ci, float* out, int ctot, int off, size_t pixels,
                  cudaStream_t s) {
   const size_t total = pixels * ci;
-  concat_copy_k<<<concat_blocks(total), 256, 0, s>>>(in, ci, out, ctot, off, total);
+  launch_k(concat_copy_k, concat_blocks(total), 256, 0, s, in, ci, out, ctot, off, total);
   PSG_CUDA(cudaGetLastError());
 }
 
 void concat_split(const float* dy, int ctot, int off, float* dx, int ci, size_t pixels,
                   bool accumulate, cudaStream_t s) {
   const size_t total = pixels * ci;
-  concat_split_k<<<concat_blocks(total), 256, 0, s>>>(dy, ctot, off, dx, ci, total,
+  launch_k(concat_split_k, concat_blocks(total), 256, 0, s, dy, ctot, off, dx, ci, total,
                                                        accumulate ? 1 : 0);
   PSG_CUDA(cudaGetLastError());
 }
 
 void argmax_count(const float* probs, const int32_t* labels, int n, int C,
                   unsigned long long* correct, cudaStream_t s) {
-  argmax_count_k<<<(n + 255) / 256, 256, 0, s>>>(probs, labels, n, C, correct);
+  launch_k(argmax_count_k, (n + 255) / 256, 256, 0, s, probs, labels, n, C, correct);
   PSG_CUDA(cudaGetLastError());
 }
 
 void sgd_update(const UpdateChunk* chunks, int nchunks, float* w, float* v, const float* g,
                 float momentum, int* flag, int* cursor, uint64_t* step, cudaStream_t s) {
-  sgd_update_k<<<nchunks, 256, 0, s>>>(chunks, w, v, g, momentum, flag, cursor, step);
+  launch_k(sgd_update_k, nchunks, 256, 0, s, chunks, w, v, g, momentum, flag, cursor, step);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -316,7 +336,7 @@ void average_ordered_into(float* const* bufs, int K, size_t n, float* out, int* 
   if (K > 64) throw std::invalid_argument("average: at most 64 buffers");
   PtrPack pp{};
   for (int k = 0; k < K; ++k) pp.p[k] = bufs[k];
-  average_ordered_k<<<grid_for(n / 4 + 1), 256, 0, s>>>(pp, K, n, out, flag);
+  launch_k(average_ordered_k, grid_for(n / 4 + 1), 256, 0, s, pp, K, n, out, flag);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -325,12 +345,12 @@ void average_ordered(float* const* bufs, int K, size_t n, int* flag, cudaStream_
 }
 
 void scale_inplace(float* x, size_t n, float a, int* flag, cudaStream_t s) {
-  scale_k<<<grid_for(n), 256, 0, s>>>(x, n, a, flag);
+  launch_k(scale_k, grid_for(n), 256, 0, s, x, n, a, flag);
   PSG_CUDA(cudaGetLastError());
 }
 
 void fill_uniform(float* x, size_t n, uint64_t seed, double lo, double hi, cudaStream_t s) {
-  fill_uniform_k<<<grid_for(n), 256, 0, s>>>(x, n, seed, lo, hi);
+  launch_k(fill_uniform_k, grid_for(n), 256, 0, s, x, n, seed, lo, hi);
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -58,11 +58,12 @@ __device__ __forceinline__ uint8_t& rcomp(uint8_t& r, int) { return r; }
 // One block per output row (b, oh) in forward / input row (b, h) in backward: the row's
 // window ranges are decoded once per block; threads walk (column, channel-vector) pairs
 // with incremental indices (no per-element division).
-template <typename V>
+template <typename V, int K>
 __global__ void __launch_bounds__(256) pool_fwd_k(PoolGeom g, const V* __restrict__ x,
                                                   V* __restrict__ y,
                                                   typename RouteOf<V>::T* __restrict__ route,
                                                   int cv) {
+  pdl_enter();
   constexpr int L = RouteOf<V>::n;
   const int oh = blockIdx.x % g.OH, b = blockIdx.x / g.OH;
   const int hs0 = oh * g.sh - g.ph, he0 = hs0 + g.kh;
@@ -74,7 +75,64 @@ __global__ void __launch_bounds__(256) pool_fwd_k(PoolGeom g, const V* __restric
   for (int j = threadIdx.x; j < total; j += blockDim.x) {
     const int ws0 = ow * g.sw - g.pw, we0 = ws0 + g.kw;
     const int ws = max(ws0, 0), we = min(we0, g.W);
-    if (g.method == PSG_POOL_AVE) {
+    if constexpr (K > 0) {
+      // K x K window (kh = kw = K): all taps loaded first (predicated), then reduced in
+      // (u, v) scan order — the same arithmetic as the runtime-bound loops below
+      V v[K > 0 ? K * K : 1];
+#pragma unroll
+      for (int u = 0; u < K; ++u)
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const int r = hs0 + u, t = ws0 + q;
+          if (r >= hs && r < he && t >= ws && t < we) v[u * K + q] = __ldg(xb + (r * g.W + t) * cv + c);
+        }
+      if (g.method == PSG_POOL_AVE) {
+        const float size = static_cast<float>((min(he0, g.H + g.ph) - hs0) *
+                                              (min(we0, g.W + g.pw) - ws0));
+        V acc;
+#pragma unroll
+        for (int q = 0; q < L; ++q) comp(acc, q) = 0.f;
+#pragma unroll
+        for (int u = 0; u < K; ++u)
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            const int r = hs0 + u, t = ws0 + q;
+            if (r >= hs && r < he && t >= ws && t < we)
+#pragma unroll
+              for (int e = 0; e < L; ++e) comp(acc, e) += comp(v[u * K + q], e);
+          }
+#pragma unroll
+        for (int q = 0; q < L; ++q) comp(acc, q) = comp(acc, q) / size;
+        y[ybase + j] = acc;
+      } else {
+        V best;  // the first valid tap, then strict '>' in scan order
+        typename RouteOf<V>::T arg;
+        bool have = false;
+#pragma unroll
+        for (int u = 0; u < K; ++u)
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            const int r = hs0 + u, t = ws0 + q;
+            if (r >= hs && r < he && t >= ws && t < we) {
+              if (!have) {
+                best = v[u * K + q];
+#pragma unroll
+                for (int e = 0; e < L; ++e) rcomp(arg, e) = static_cast<uint8_t>(u * K + q);
+                have = true;
+                continue;
+              }
+#pragma unroll
+              for (int e = 0; e < L; ++e)
+                if (comp(v[u * K + q], e) > comp(best, e)) {
+                  comp(best, e) = comp(v[u * K + q], e);
+                  rcomp(arg, e) = static_cast<uint8_t>(u * K + q);
+                }
+            }
+          }
+        y[ybase + j] = best;
+        route[ybase + j] = arg;
+      }
+    } else if (g.method == PSG_POOL_AVE) {
       const float size = static_cast<float>((min(he0, g.H + g.ph) - hs0) *
                                             (min(we0, g.W + g.pw) - ws0));
       V acc;
@@ -125,6 +183,7 @@ template <typename V>
 __global__ void __launch_bounds__(256) pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
                                                   const typename RouteOf<V>::T* __restrict__ route,
                                                   V* __restrict__ dx, int accumulate, int cv) {
+  pdl_enter();
   constexpr int L = RouteOf<V>::n;
   const int h = blockIdx.x % g.H, b = blockIdx.x / g.H;
   // windows with oh*sh - ph <= h < oh*sh - ph + kh
@@ -223,6 +282,7 @@ __device__ __forceinline__ float lrn_window(const float* row, int c, int C, int 
 template <int SIZE>
 __global__ void __launch_bounds__(kLrnThreads) lrn_fwd_k(LrnGeom g, const float* __restrict__ x,
                                                          float* __restrict__ y, int tp) {
+  pdl_enter();
   extern __shared__ float sm[];
   float* sx = sm;
   const int pre = (g.size - 1) / 2, C = g.C;
@@ -250,6 +310,7 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float*
                                                          const float* __restrict__ dy,
                                                          float* __restrict__ dx, int accumulate,
                                                          int relu_mask, int tp) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int C = g.C, tile_elems = tp * C;
   float* sx = sm;                   // x
@@ -312,6 +373,7 @@ __device__ __forceinline__ void lrn_put4(float* v, float4 q) {
 
 __global__ void __launch_bounds__(256) lrn_fwd_run_k(LrnGeom g, const float* __restrict__ x,
                                                      float* __restrict__ y, uint32_t total_runs) {
+  pdl_enter();
   const int C = g.C, runs = C / kLrnRun;
   const float a = g.alpha / g.size;
   GRID_STRIDE32(r, total_runs) {
@@ -341,6 +403,7 @@ __global__ void __launch_bounds__(256) lrn_bwd_run_k(LrnGeom g, const float* __r
                                                      const float* __restrict__ dy,
                                                      float* __restrict__ dx, int accumulate,
                                                      int relu_mask, uint32_t total_runs) {
+  pdl_enter();
   const int C = g.C, runs = C / kLrnRun;
   const float a = g.alpha / g.size, ratio = 2.f * g.alpha * g.beta / g.size;
   GRID_STRIDE32(r, total_runs) {
@@ -384,6 +447,75 @@ __global__ void __launch_bounds__(256) lrn_bwd_run_k(LrnGeom g, const float* __r
   }
 }
 
+// ------------------------------------------------------- LRN -> max pool ---
+// An LRN (size 5, C % 8 == 0) whose only consumer is a 3x3 max pool: the LRN output is
+// never stored.  Thread = (pool output pixel, 8-channel run); each valid window tap
+// recomputes the LRN of its 8 channels from x (the same ascending 5-term sums and lrn_pow
+// as lrn_fwd_run_k) and feeds the max / route scan of pool_fwd_k — bitwise the unfused
+// pair (each LRN value is recomputed by the <= 4 windows that hold it).
+__device__ __forceinline__ void lrn_run8(const float* xp, int c0, int C, float a, const LrnGeom& g,
+                                         float* out) {
+  float v[16];  // channels c0-4 .. c0+11
+  lrn_put4(v, lrn_ld4(xp, c0 - 4, C));
+  lrn_put4(v + 4, lrn_ld4(xp, c0, C));
+  lrn_put4(v + 8, lrn_ld4(xp, c0 + 4, C));
+  lrn_put4(v + 12, lrn_ld4(xp, c0 + 8, C));
+#pragma unroll
+  for (int i = 0; i < kLrnRun; ++i) {
+    float acc = 0.f;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) acc += v[i + 2 + q] * v[i + 2 + q];
+    out[i] = v[i + 4] * lrn_pow(g.k + a * acc, g.beta);
+  }
+}
+
+__global__ void __launch_bounds__(256) lrn_maxpool_fwd_k(LrnGeom lg, PoolGeom g,
+                                                         const float* __restrict__ x,
+                                                         float* __restrict__ y,
+                                                         uint8_t* __restrict__ route,
+                                                         uint32_t total_runs) {
+  pdl_enter();
+  constexpr int K = 3;
+  const int C = g.C, runs = C / kLrnRun;
+  const float a = lg.alpha / lg.size;
+  GRID_STRIDE32(r, total_runs) {
+    const uint32_t opix = r / runs;
+    const int c0 = static_cast<int>(r % runs) * kLrnRun;
+    const int ow = static_cast<int>(opix % g.OW);
+    const uint32_t t = opix / g.OW;
+    const int oh = static_cast<int>(t % g.OH), b = static_cast<int>(t / g.OH);
+    const int hs0 = oh * g.sh - g.ph, ws0 = ow * g.sw - g.pw;
+    const int hs = max(hs0, 0), he = min(hs0 + K, g.H), ws = max(ws0, 0), we = min(ws0 + K, g.W);
+    const float* xb = x + static_cast<size_t>(b) * g.H * g.W * C;
+    float best[kLrnRun];
+    uint8_t arg[kLrnRun];
+    bool have = false;
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const int rr = hs0 + u, tt = ws0 + q;
+        if (rr < hs || rr >= he || tt < ws || tt >= we) continue;
+        float o[kLrnRun];
+        lrn_run8(xb + static_cast<size_t>(rr * g.W + tt) * C, c0, C, a, lg, o);
+#pragma unroll
+        for (int e = 0; e < kLrnRun; ++e)
+          if (!have || o[e] > best[e]) {
+            best[e] = o[e];
+            arg[e] = static_cast<uint8_t>(u * K + q);
+          }
+        have = true;
+      }
+    const size_t ob = static_cast<size_t>(opix) * C + c0;
+    float4* dst = reinterpret_cast<float4*>(y + ob);
+    dst[0] = make_float4(best[0], best[1], best[2], best[3]);
+    dst[1] = make_float4(best[4], best[5], best[6], best[7]);
+    uchar4* rd = reinterpret_cast<uchar4*>(route + ob);
+    rd[0] = make_uchar4(arg[0], arg[1], arg[2], arg[3]);
+    rd[1] = make_uchar4(arg[4], arg[5], arg[6], arg[7]);
+  }
+}
+
 // --------------------------------------------------------------- dropout ---
 // Keep-mask = splitmix64(mix(base ^ step) + nchw_index) >> 40 >= ratio * 2^24.
 __device__ __forceinline__ float drop_mask(const DropGeom& g, uint64_t base, uint32_t i,
@@ -398,6 +530,7 @@ __device__ __forceinline__ float drop_mask(const DropGeom& g, uint64_t base, uin
 
 __global__ void dropout_fwd_k(DropGeom g, const float* __restrict__ x, float* __restrict__ y,
                               const uint64_t* __restrict__ d_step, int train, uint32_t total) {
+  pdl_enter();
   if (!train) {
     GRID_STRIDE32(i, total) y[i] = x[i];
     return;
@@ -411,6 +544,7 @@ __global__ void dropout_fwd_k(DropGeom g, const float* __restrict__ x, float* __
 __global__ void dropout_bwd_k(DropGeom g, const float* __restrict__ dy, float* __restrict__ dx,
                               const uint64_t* __restrict__ d_step, int accumulate,
                               uint32_t total) {
+  pdl_enter();
   const uint64_t base = mix64(g.base_seed ^ *d_step);
   const uint32_t thresh = static_cast<uint32_t>(static_cast<double>(g.ratio) * 16777216.0);
   const float keep = static_cast<float>(1.0 / (1.0 - static_cast<double>(g.ratio)));
@@ -426,6 +560,7 @@ __global__ void gather_k(const float* __restrict__ ds, const int32_t* __restrict
                          const uint32_t* __restrict__ idx, const int* __restrict__ cursor, int b,
                          int pixels, int C, int cs, float* __restrict__ out,
                          int32_t* __restrict__ labels) {
+  pdl_enter();
   const int i = blockIdx.y;
   const uint32_t row = idx[static_cast<size_t>(cursor ? *cursor : 0) * b + i];
   const float* src = ds + static_cast<size_t>(row) * pixels * C;
@@ -455,6 +590,7 @@ __global__ void gather_k(const float* __restrict__ ds, const int32_t* __restrict
 // Host-fed batch (reference NCHW layout) -> data layer NHWC with channel stride cs.
 __global__ void stage_nchw_k(const float* __restrict__ src, int C, int H, int W, int cs,
                              float* __restrict__ dst, uint32_t total) {
+  pdl_enter();
   GRID_STRIDE32(i, total) {
     const uint32_t c = i % cs, t = i / cs;
     const uint32_t w = t % W, t2 = t / W;
@@ -466,16 +602,27 @@ __global__ void stage_nchw_k(const float* __restrict__ src, int C, int H, int W,
 
 }  // namespace
 
+namespace {
+// compile-time window for the common square 3x3 / 2x2 pools (loads issued together)
+int pool_k(const PoolGeom& g) {
+  if (g.kh == g.kw && (g.kh == 2 || g.kh == 3)) return g.kh;
+  return 0;
+}
+}  // namespace
+
 void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaStream_t s) {
   checked32(static_cast<size_t>(g.n) * g.OH * g.OW * g.C, "pool");
   checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
   const unsigned rows = static_cast<unsigned>(g.n) * g.OH;
-  if (g.C % 4 == 0)
-    pool_fwd_k<float4><<<rows, 256, 0, s>>>(g, reinterpret_cast<const float4*>(x),
-                                            reinterpret_cast<float4*>(y),
-                                            reinterpret_cast<uchar4*>(route), g.C / 4);
-  else
-    pool_fwd_k<float><<<rows, 256, 0, s>>>(g, x, y, route, g.C);
+  const int k = pool_k(g);
+  if (g.C % 4 == 0) {
+    auto kern = k == 3 ? pool_fwd_k<float4, 3> : k == 2 ? pool_fwd_k<float4, 2> : pool_fwd_k<float4, 0>;
+    launch_k(kern, rows, 256, 0, s, g, reinterpret_cast<const float4*>(x),
+             reinterpret_cast<float4*>(y), reinterpret_cast<uchar4*>(route), g.C / 4);
+  } else {
+    auto kern = k == 3 ? pool_fwd_k<float, 3> : k == 2 ? pool_fwd_k<float, 2> : pool_fwd_k<float, 0>;
+    launch_k(kern, rows, 256, 0, s, g, x, y, route, g.C);
+  }
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -484,11 +631,11 @@ void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* d
   checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
   const unsigned rows = static_cast<unsigned>(g.n) * g.H;
   if (g.C % 4 == 0)
-    pool_bwd_k<float4><<<rows, 256, 0, s>>>(g, reinterpret_cast<const float4*>(dy),
-                                            reinterpret_cast<const uchar4*>(route),
-                                            reinterpret_cast<float4*>(dx), accumulate, g.C / 4);
+    launch_k(pool_bwd_k<float4>, rows, 256, 0, s, g, reinterpret_cast<const float4*>(dy),
+             reinterpret_cast<const uchar4*>(route), reinterpret_cast<float4*>(dx), accumulate,
+             g.C / 4);
   else
-    pool_bwd_k<float><<<rows, 256, 0, s>>>(g, dy, route, dx, accumulate, g.C);
+    launch_k(pool_bwd_k<float>, rows, 256, 0, s, g, dy, route, dx, accumulate, g.C);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -512,7 +659,7 @@ void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s) {
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
   if (lrn_run_ok(g)) {
     const uint32_t runs = checked32(static_cast<size_t>(g.pixels) * (g.C / kLrnRun), "lrn");
-    lrn_fwd_run_k<<<grid_for(runs), 256, 0, s>>>(g, x, y, runs);
+    launch_k(lrn_fwd_run_k, grid_for(runs), 256, 0, s, g, x, y, runs);
     PSG_CUDA(cudaGetLastError());
     return;
   }
@@ -520,7 +667,7 @@ void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(tp) * g.C * sizeof(float);
   auto k = g.size == 5 ? lrn_fwd_k<5> : lrn_fwd_k<0>;
   lrn_launch(k, smem);
-  k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, y, tp);
+  launch_k(k, lrn_blocks(g, tp), kLrnThreads, smem, s, g, x, y, tp);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -529,7 +676,7 @@ void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool 
   checked32(static_cast<size_t>(g.pixels) * g.C, "lrn");
   if (lrn_run_ok(g)) {
     const uint32_t runs = checked32(static_cast<size_t>(g.pixels) * (g.C / kLrnRun), "lrn");
-    lrn_bwd_run_k<<<grid_for(runs), 256, 0, s>>>(g, x, dy, dx, accumulate, relu_mask ? 1 : 0,
+    launch_k(lrn_bwd_run_k, grid_for(runs), 256, 0, s, g, x, dy, dx, accumulate, relu_mask ? 1 : 0,
                                                  runs);
     PSG_CUDA(cudaGetLastError());
     return;
@@ -538,7 +685,7 @@ void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool 
   const size_t smem = 4 * static_cast<size_t>(tp) * g.C * sizeof(float);
   auto k = g.size == 5 ? lrn_bwd_k<5> : lrn_bwd_k<0>;
   lrn_launch(k, smem);
-  k<<<lrn_blocks(g, tp), kLrnThreads, smem, s>>>(g, x, dy, dx, accumulate, relu_mask ? 1 : 0,
+  launch_k(k, lrn_blocks(g, tp), kLrnThreads, smem, s, g, x, dy, dx, accumulate, relu_mask ? 1 : 0,
                                                  tp);
   PSG_CUDA(cudaGetLastError());
 }
@@ -546,14 +693,14 @@ void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool 
 void dropout_fwd(const DropGeom& g, const float* x, float* y, const uint64_t* d_step, bool train,
                  cudaStream_t s) {
   const uint32_t n = checked32(static_cast<size_t>(g.n) * g.C * g.H * g.W, "dropout");
-  dropout_fwd_k<<<grid_for(n), 256, 0, s>>>(g, x, y, d_step, train, n);
+  launch_k(dropout_fwd_k, grid_for(n), 256, 0, s, g, x, y, d_step, train, n);
   PSG_CUDA(cudaGetLastError());
 }
 
 void dropout_bwd(const DropGeom& g, const float* dy, float* dx, const uint64_t* d_step,
                  bool accumulate, cudaStream_t s) {
   const uint32_t n = checked32(static_cast<size_t>(g.n) * g.C * g.H * g.W, "dropout");
-  dropout_bwd_k<<<grid_for(n), 256, 0, s>>>(g, dy, dx, d_step, accumulate, n);
+  launch_k(dropout_bwd_k, grid_for(n), 256, 0, s, g, dy, dx, d_step, accumulate, n);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -562,7 +709,7 @@ void gather_batch(const float* ds_images, const int32_t* ds_labels, const uint32
                   int32_t* labels, cudaStream_t s) {
   const size_t per_row = checked32(static_cast<size_t>(pixels) * cs, "gather");
   const int bx = static_cast<int>(std::max<size_t>(1, std::min<size_t>((per_row / 4 + 255) / 256, 64)));
-  gather_k<<<dim3(bx, b), 256, 0, s>>>(ds_images, ds_labels, idx, cursor, b, pixels, C, cs, out,
+  launch_k(gather_k, dim3(bx, b), 256, 0, s, ds_images, ds_labels, idx, cursor, b, pixels, C, cs, out,
                                        labels);
   PSG_CUDA(cudaGetLastError());
 }
@@ -570,7 +717,21 @@ void gather_batch(const float* ds_images, const int32_t* ds_labels, const uint32
 void stage_batch_nchw(const float* src, int n, int C, int H, int W, int cs, float* dst,
                       cudaStream_t s) {
   const uint32_t total = checked32(static_cast<size_t>(n) * H * W * cs, "stage");
-  stage_nchw_k<<<grid_for(total), 256, 0, s>>>(src, C, H, W, cs, dst, total);
+  launch_k(stage_nchw_k, grid_for(total), 256, 0, s, src, C, H, W, cs, dst, total);
+  PSG_CUDA(cudaGetLastError());
+}
+
+bool lrn_maxpool_fusable(const LrnGeom& lg, const PoolGeom& pg) {
+  return lg.size == 5 && lg.C % kLrnRun == 0 && pg.C == lg.C && pg.method == PSG_POOL_MAX &&
+         pg.kh == 3 && pg.kw == 3 && pg.sh == pg.sw && (pg.sh == 1 || pg.sh == 2) &&
+         static_cast<size_t>(pg.n) * pg.H * pg.W * pg.C < (1ULL << 31);
+}
+
+void lrn_maxpool_fwd(const LrnGeom& lg, const PoolGeom& g, const float* x, float* y,
+                     uint8_t* route, cudaStream_t s) {
+  const uint32_t runs =
+      checked32(static_cast<size_t>(g.n) * g.OH * g.OW * (g.C / kLrnRun), "lrn_pool");
+  launch_k(lrn_maxpool_fwd_k, grid_for(runs, 256, 148 * 8), 256, 0, s, lg, g, x, y, route, runs);
   PSG_CUDA(cudaGetLastError());
 }
 

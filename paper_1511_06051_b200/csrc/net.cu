@@ -153,8 +153,22 @@ void invalidate_graph(psg_net* net) {
 }
 
 void plan_fusion(psg_net* net) {
-  for (LayerRt& l : net->L) l.fwd_relu = l.fused_from = l.bwd_by = l.bwd_relu = -1;
+  for (LayerRt& l : net->L)
+    l.fwd_relu = l.fused_from = l.bwd_by = l.bwd_relu = l.lrn_pool = l.pool_lrn = -1;
   if (!net->fuse) return;
+  static const bool lrn_pool = [] {  // PSG_FUSE_LRN_POOL=0: keep LRN and pool separate (A/B)
+    const char* e = std::getenv("PSG_FUSE_LRN_POOL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  for (size_t li = 0; lrn_pool && li < net->L.size(); ++li) {
+    LayerRt& l = net->L[li];
+    if (l.kind != PSG_LAYER_LRN || l.consumers.size() != 1) continue;
+    LayerRt& p = net->L[l.consumers[0]];
+    if (p.kind == PSG_LAYER_POOL && p.inputs.size() == 1 && lrn_maxpool_fusable(l.lg, p.pg)) {
+      l.lrn_pool = l.consumers[0];
+      p.pool_lrn = static_cast<int>(li);
+    }
+  }
   for (size_t ri = 0; ri < net->L.size(); ++ri) {
     LayerRt& r = net->L[ri];
     if (r.kind != PSG_LAYER_RELU) continue;
@@ -191,7 +205,7 @@ void ensure_capacity(psg_net* net, size_t n) {
   for (LayerRt& l : net->L) {
     if (l.kind == PSG_LAYER_LABEL) continue;
     const size_t elems = n * l.vol();
-    if (l.fwd_relu < 0) l.out = dalloc<float>(elems);
+    if (l.fwd_relu < 0 && l.lrn_pool < 0) l.out = dalloc<float>(elems);
     if (l.kind != PSG_LAYER_DATA) l.grad = dalloc<float>(elems);
     if (l.kind == PSG_LAYER_POOL && l.d.pool == PSG_POOL_MAX) l.route = dalloc<uint8_t>(elems);
     if (l.kind == PSG_LAYER_CONV) l.col = dalloc<float>(conv_col_elems(geom_for(l, n), net->mode));
@@ -770,8 +784,7 @@ void net_train(psg_net* net, long steps) {
   if (eager_mode()) {
     PSG_CUDA(cudaEventRecord(net->t0, net->stream));
     for (long s = 0; s < steps; ++s) {
-      gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
-                   d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+      stage_gathered_batch(net, ds->images, ds->labels, net->d_idx, &net->dsc->cursor, b);
       run_forward(net, b, true, true);
       run_backward(net, b);
       run_update(net, true);
@@ -787,8 +800,7 @@ void net_train(psg_net* net, long steps) {
     PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
     int launches = 0;
     try {
-      gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
-                   d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+      stage_gathered_batch(net, ds->images, ds->labels, net->d_idx, &net->dsc->cursor, b);
       ++launches;
       launches += run_forward(net, b, true, true);
       launches += run_backward(net, b);
@@ -822,8 +834,7 @@ void net_grad_step(psg_net* net) {
   const LayerRt& d = net->L[net->data_idx];
   psg_dataset* ds = net->train_ds;
   auto body = [&] {
-    gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
-                 d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+    stage_gathered_batch(net, ds->images, ds->labels, net->d_idx, &net->dsc->cursor, b);
     run_forward(net, b, true, true);
     run_backward(net, b);
   };
@@ -906,8 +917,8 @@ void net_test_begin(psg_net* net, long steps, long first, long stride) {
                            cudaMemcpyHostToDevice, net->stream));
   const LayerRt& d = net->L[net->data_idx];
   for (long s = 0; s < mine; ++s) {
-    gather_batch(net->val_ds->images, net->val_ds->labels, net->d_vidx + s * b, nullptr,
-                 static_cast<int>(b), d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+    stage_gathered_batch(net, net->val_ds->images, net->val_ds->labels, net->d_vidx + s * b,
+                         nullptr, b);
     run_forward(net, b, /*train=*/false, /*seed_grad=*/false);
     argmax_count(net->L[net->loss_idx].out, net->labels, static_cast<int>(b), net->classes,
                  &net->dsc->correct, net->stream);

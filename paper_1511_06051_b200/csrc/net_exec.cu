@@ -66,6 +66,26 @@ struct Scope {
 
 }  // namespace
 
+int stage_gathered_batch(psg_net* net, const float* images, const int32_t* labels,
+                         const uint32_t* idx, const int* cursor, size_t n) {
+  const LayerRt& d = net->L[net->data_idx];
+  net->data_s2d = false;
+  if (net->fuse && d.consumers.size() == 1) {
+    const LayerRt& c = net->L[d.consumers[0]];
+    if (c.kind == PSG_LAYER_CONV && c.col) {
+      const ConvGeom g = geom_n(c, n);
+      if (conv_s2d_input(g, net->mode)) {
+        gather_s2d(g, images, labels, idx, cursor, d.C, c.col, net->labels, net->stream);
+        net->data_s2d = true;
+        return 1;
+      }
+    }
+  }
+  gather_batch(images, labels, idx, cursor, static_cast<int>(n), d.H * d.W, d.C, d.cs, d.out,
+               net->labels, net->stream);
+  return 1;
+}
+
 int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer) {
   cudaStream_t s = net->stream;
   int launches = 0;
@@ -86,9 +106,10 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         const ConvGeom g = geom_n(l, n);
         Scope sc(timer, nm.c_str(), lid, 1, conv_flops(net, l, n), 0.0);
         // fused ReLU: l.out aliases the ReLU's buffer and the epilogue applies max(0, .)
+        const bool xs = net->data_s2d && src.kind == PSG_LAYER_DATA;  // x' already gathered
         conv_fprop(g, src.out, net->w + k.int_off, net->w + b.int_off, l.out, l.fwd_relu >= 0,
-                   net->ws, l.col, net->mode, s);
-        const int c = conv_launches(g, 0, net->mode);
+                   net->ws, l.col, net->mode, s, xs);
+        const int c = conv_launches(g, 0, net->mode) - (xs ? 1 : 0);
         sc.done(c);
         launches += c;
         break;
@@ -97,6 +118,16 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         PoolGeom g = l.pg;
         g.n = static_cast<int>(n);
         const LayerRt& src = net->L[l.inputs[0]];
+        if (l.pool_lrn >= 0) {  // LRN computed in the pool kernel from the LRN's input
+          const LayerRt& x = net->L[src.inputs[0]];
+          Scope sc(timer, nm.c_str(), lid, 1, 0.0, act_bytes(x, n) + act_bytes(l, n) * 1.25);
+          LrnGeom lg = src.lg;
+          lg.pixels = static_cast<int>(n) * src.H * src.W;
+          lrn_maxpool_fwd(lg, g, x.out, l.out, l.route, s);
+          sc.done(1);
+          ++launches;
+          break;
+        }
         Scope sc(timer, nm.c_str(), lid, 1, 0.0,
                  act_bytes(src, n) + act_bytes(l, n) * (l.route ? 1.25 : 1.0));
         pool_fwd(g, src.out, l.out, l.route, s);
@@ -113,6 +144,7 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         break;
       }
       case PSG_LAYER_LRN: {
+        if (l.lrn_pool >= 0) break;  // computed by the consuming pool's kernel
         LrnGeom g = l.lg;
         g.pixels = static_cast<int>(n) * l.H * l.W;
         Scope sc(timer, nm.c_str(), lid, 1, 0.0, 2 * act_bytes(l, n));
@@ -154,6 +186,7 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
       }
     }
   }
+  net->data_s2d = false;  // one-shot: set by stage_gathered_batch for this forward only
   return launches;
 }
 

@@ -21,8 +21,7 @@ void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, 
     OpTimer t(net->stream);
     PSG_CUDA(cudaMemsetAsync(&net->dsc->cursor, 0, sizeof(int), net->stream));
     t.begin("gather", net->data_idx, 0, 0.0, 2.0 * 4.0 * static_cast<double>(b) * d.vol());
-    gather_batch(ds->images, ds->labels, net->d_idx, &net->dsc->cursor, static_cast<int>(b),
-                 d.H * d.W, d.C, d.cs, d.out, net->labels, net->stream);
+    stage_gathered_batch(net, ds->images, ds->labels, net->d_idx, &net->dsc->cursor, b);
     t.end(1);
     run_forward(net, b, true, true, &t);
     run_backward(net, b, &t);

@@ -8,6 +8,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/psg.h"
@@ -127,8 +128,16 @@ struct Workspace {
 // the shared workspace must hold conv_workspace_elems() floats.
 // `col` (conv_col_elems floats, may be null) holds an im2col matrix written by fprop (or by
 // wgrad itself) and read by the same step's wgrad when a TF32 layer takes an im2col route.
+// x_s2d: the space-to-depth input x' is already in `col` (written by gather_s2d).
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
-                bool relu, const Workspace& ws, float* col, Mode mode, cudaStream_t s);
+                bool relu, const Workspace& ws, float* col, Mode mode, cudaStream_t s,
+                bool x_s2d = false);
+// A strided first conv on the space-to-depth route (TF32): its input can be gathered
+// straight into x' (col) from the dataset rows idx[cursor * g.n + b] (+ the labels).
+bool conv_s2d_input(const ConvGeom& g, Mode mode);
+void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_labels,
+                const uint32_t* idx, const int* cursor, int src_cs, float* col, int32_t* labels,
+                cudaStream_t s);
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
                 const Workspace& ws, Mode mode, cudaStream_t s);
 // dW [F][Kp] and db [F] (written, not accumulated).
@@ -161,6 +170,10 @@ void lrn_fwd(const LrnGeom& g, const float* x, float* y, cudaStream_t s);
 // the ReLU's input (the ReLU's own backward is folded in).
 void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool accumulate,
              cudaStream_t s, bool relu_mask = false);
+// LRN -> 3x3 max pool fused (the LRN output is never stored; bitwise the unfused pair).
+bool lrn_maxpool_fusable(const LrnGeom& lg, const PoolGeom& pg);
+void lrn_maxpool_fwd(const LrnGeom& lg, const PoolGeom& g, const float* x, float* y,
+                     uint8_t* route, cudaStream_t s);
 
 struct DropGeom {
   int n = 0, C = 0, H = 1, W = 1;  // logical NCHW dims for the counter index
@@ -208,5 +221,39 @@ void average_ordered_into(float* const* bufs, int K, size_t n, float* out, int* 
                           cudaStream_t s);
 void scale_inplace(float* x, size_t n, float a, int* flag, cudaStream_t s);
 void fill_uniform(float* x, size_t n, uint64_t seed, double lo, double hi, cudaStream_t s);
+
+// ------------------------------------------------- programmatic dependent launch --
+// Every kernel of the library is launched with the PDL attribute (launch_k) and starts
+// with pdl_enter(): it waits for its stream predecessor to complete (memory flushed)
+// before touching global memory, so its launch overlaps the predecessor's tail.  The
+// successor is released at exit (an early griddepcontrol.launch_dependents, built with
+// -DPSG_PDL_EARLY_TRIGGER, parks waiting CTAs next to the persistent GEMMs and measured
+// 2-4% slower on AlexNet / GoogLeNet).  No-ops for a kernel launched without the attribute;
+// PSG_PDL=0 launches without it (A/B measurement).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef PSG_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+#endif
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 }  // namespace psg

@@ -60,6 +60,12 @@ struct LayerRt {
   // it); a ReLU whose only consumer is an LRN has its backward folded into the LRN's
   // (bwd_by = that LRN; the LRN masks with its input and writes the ReLU's input grad).
   int fwd_relu = -1, fused_from = -1, bwd_by = -1, bwd_relu = -1;
+  // LRN -> max pool fusion: the forward of an LRN whose only consumer is a fusable 3x3
+  // max pool is computed inside the pool's kernel (lrn_pool = that pool, pool_lrn = the
+  // LRN), so the LRN output is never materialised; the backward stays two kernels (a fused
+  // gather + LRN backward measured slower: it re-gathers each channel's pool gradient for
+  // its neighbours' windows).
+  int lrn_pool = -1, pool_lrn = -1;
   int kern_t = -1, bias_t = -1;
   ConvGeom cg;  // conv / linear (per-example; n filled per call)
   PoolGeom pg;
@@ -93,6 +99,9 @@ struct psg_net {
   double lr = 0.01, mu = 0.0, wd = 0.0;
   psg::Mode mode = psg::Mode::Strict;
   bool fuse = true;
+  // the current batch was gathered straight into the first conv's space-to-depth input
+  // (stage_gathered_batch); consumed (cleared) by the next run_forward
+  bool data_s2d = false;
   psg::DeviceScalars* dsc = nullptr;
   psg::DeviceScalars* hsc = nullptr;  // pinned mirror
   double* row_loss = nullptr;
@@ -161,6 +170,11 @@ struct OpTimer {
   void end(int launches);
 };
 
+// Gather the step's batch from the HBM-resident dataset rows idx[cursor * n + i]: into the
+// data layer, or (fusion on, TF32) straight into the space-to-depth input of a strided
+// first conv that is the data layer's only consumer.  Returns the launches enqueued.
+int stage_gathered_batch(psg_net* net, const float* images, const int32_t* labels,
+                         const uint32_t* idx, const int* cursor, size_t n);
 int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer = nullptr);
 int run_backward(psg_net* net, size_t n, OpTimer* timer = nullptr);
 int run_update(psg_net* net, bool advance, OpTimer* timer = nullptr);

@@ -36,6 +36,7 @@ __device__ __forceinline__ double normal_at(uint64_t key, uint64_t row, uint64_t
 __global__ void synthetic_rows_k(const float* __restrict__ means, int c, int h, int w,
                                  uint32_t per_class, uint64_t key, float* __restrict__ images,
                                  int32_t* __restrict__ labels) {
+  pdl_enter();
   extern __shared__ float nodes[];
   const uint32_t row = blockIdx.x;
   const int gh = max(1, h / 4), gw = max(1, w / 4), nn = (gh + 1) * (gw + 1);
@@ -69,6 +70,7 @@ __global__ void synthetic_rows_k(const float* __restrict__ means, int c, int h, 
 
 __global__ void u8_to_f32_k(const unsigned char* __restrict__ px, size_t n,
                             float* __restrict__ out) {
+  pdl_enter();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     out[i] = static_cast<float>(static_cast<double>(px[i]) / 255.0);
@@ -78,7 +80,7 @@ __global__ void u8_to_f32_k(const unsigned char* __restrict__ px, size_t n,
 
 void ingest_u8_to_f32(const unsigned char* pixels, size_t n, float* images, cudaStream_t s) {
   const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148 * 16));
-  u8_to_f32_k<<<std::max(1u, blocks), 256, 0, s>>>(pixels, n, images);
+  launch_k(u8_to_f32_k, std::max(1u, blocks), 256, 0, s, pixels, n, images);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -94,7 +96,7 @@ void synthetic_rows_device(const float* d_means, int classes, int c, int h, int 
   if (smem > 48 * 1024)
     PSG_CUDA(cudaFuncSetAttribute(synthetic_rows_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-  synthetic_rows_k<<<static_cast<unsigned>(n), 256, smem, s>>>(
+  launch_k(synthetic_rows_k, static_cast<unsigned>(n), 256, smem, s, 
       d_means, c, h, w, static_cast<uint32_t>(per_class), noise_seed, images, labels);
   PSG_CUDA(cudaGetLastError());
 }

@@ -84,6 +84,27 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
                 "r"(c3), "r"(bar));
 }
 #undef PSG_TMA_ASM
+// im2col mode (4-D NHWC map from cuTensorMapEncodeIm2col): {c, w, h, n} is the first
+// pixel's traversal position inside the map's bounding box, {off_w, off_h} the filter tap;
+// the box is `pixelsPerColumn` consecutive pixels (W, then H, then N) x channelsPerPixel.
+template <bool PAIR = false>
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorMap* map,
+                                                   uint32_t bar, int c0, int c1, int c2, int c3,
+                                                   uint16_t off_w, uint16_t off_h) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if constexpr (PAIR)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "h"(off_w), "h"(off_h)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "h"(off_w), "h"(off_h)
+        : "memory");
+}
 
 // PAIR: cta_group::2 — `bar` may be the peer CTA's mbarrier (a shared::cluster address),
 // so both CTAs of a pair can report their bytes to the leader's barrier.

@@ -16,9 +16,9 @@
 namespace psg {
 namespace tck {
 
-enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3 };
+enum AMode { A_RECT_K = 0, A_2D_K = 1, A_RECT_MN = 2, A_2D_MN = 3, A_IM2COL_K = 4 };
 enum BMode { B_2D_K = 0, B_WT_MN = 1, B_RECT_MN = 2, B_2D_MN = 3, B_COL_MN = 4, B_TAPS_MN = 5,
-             B_3D_K = 6 };
+             B_3D_K = 6, B_TAPS_IM2COL = 7 };
 enum RowMap { ROW_RECT = 0, ROW_LINEAR = 1 };
 
 // Warp roles: 0..3 and 6..7 TMA producers (K block it -> producer it % p.producers),
@@ -77,6 +77,10 @@ struct TcArgs {
   int adv_kb, adv_c0, adv_tap, adv_tv, adv_tu, adv_w, adv_h, adv_b;
   int m_units;            // M work units: m_tiles, or ceil(m_tiles / 2) for pairs
   int b_cols;             // B columns (N) loaded per CTA: n_tile, or n_tile / 2 for pairs
+  // A_IM2COL_K: M = linear pixels (b, y, x) of an out_h x out_w traversal grid; a tile's
+  // first pixel sits at (x + im_lw, y + im_lh) of the source, tap (u, v) adds offsets
+  // (sign > 0 ? v : kw - 1 - v, sign > 0 ? u : kh - 1 - u)
+  int kh, im_lw, im_lh;
 };
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
@@ -216,6 +220,12 @@ __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, 
     case A_2D_K:
       tc::tma_load_2d<PAIR>(sa, map, bar, c.kb * KBLK, t.m * kTileM);
       break;
+    case A_IM2COL_K:
+      tc::tma_load_im2col_4d<PAIR>(
+          sa, map, bar, p.a_c_g * t.g + c.t0 * KBLK, ow0, oh0, rb,
+          static_cast<uint16_t>(p.sign > 0 ? c.tv : p.kw - 1 - c.tv),
+          static_cast<uint16_t>(p.sign > 0 ? c.tu : p.kh - 1 - c.tu));
+      break;
     case A_RECT_MN:
       for (int j = 0; j < p.a_chunks; ++j)
         tc::tma_load_4d<PAIR>(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
@@ -266,6 +276,17 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
           tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, tk.c[j], c.kow + tk.dx[j],
                                 c.koh + tk.dy[j], c.kbi);
       break;
+    case B_TAPS_IM2COL: {  // the same chunks as TMA im2col boxes over linear pixel K blocks
+      const int pix = c.kb * KBLK, r = pix / p.out_w;
+      const int x0 = pix - r * p.out_w + p.im_lw, y0 = r % p.out_h + p.im_lh, b0 = r / p.out_h;
+#pragma unroll
+      for (int j = 0; j < kMaxBChunks; ++j)
+        if (j < nch)
+          tc::tma_load_im2col_4d<PAIR>(sb + j * KBLK * 128, map, bar, tk.c[j], x0, y0, b0,
+                                       static_cast<uint16_t>(tk.dx[j] + p.pw),
+                                       static_cast<uint16_t>(tk.dy[j] + p.ph));
+      break;
+    }
   }
 }
 
@@ -313,6 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base_sh;
+  pdl_enter();  // setup above touched only smem / TMEM: it overlaps the predecessor's tail
 
   const int pw = warp < 4 ? warp : (warp == 6 || warp == 7 ? warp - 2 : -1);
   if (pw >= 0 && pw < p.producers && lane == 0) {
@@ -337,10 +359,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int r = t.m % (p.th * p.tw);
           oh0 = (r / p.tw) * p.rm;
           ow0 = (r % p.tw) * p.wm;
+        } else if (p.a_mode == A_IM2COL_K) {  // the tile's first pixel in traversal coords
+          const int pix = t.m * kTileM, r = pix / p.out_w;
+          ow0 = pix - r * p.out_w + p.im_lw;
+          oh0 = r % p.out_h + p.im_lh;
+          rb = r / p.out_h;
         }
         const int u = t.tap / p.kw, v = t.tap % p.kw;
         TapChunks tk;
-        if (p.b_mode == B_TAPS_MN) tap_chunks(p, t, tk, rank);
+        if (p.b_mode == B_TAPS_MN || p.b_mode == B_TAPS_IM2COL) tap_chunks(p, t, tk, rank);
         const uint32_t it = it_tile + first;
         uint32_t s = it % p.stages, ph = (it / p.stages) & 1;
         KCursor c;

@@ -299,12 +299,14 @@ def test_max_pool_tie_routes_to_lowest_index(gpu):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
-@pytest.mark.parametrize("name", ["cifar10_quick", "caffe_mix"])
+@pytest.mark.parametrize("name", ["cifar10_quick", "caffe_mix", "s2d"])
 def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
-    """psg_net_set_fusion: the ReLU applied in the GEMM epilogue and the ReLU backward
-    folded into the LRN give bitwise-identical training to the unfused graph."""
+    """psg_net_set_fusion: the ReLU applied in the GEMM epilogue, the ReLU backward folded
+    into the LRN, the LRN computed inside the following max pool and the batch gathered
+    straight into the space-to-depth input give bitwise-identical training to the unfused
+    graph."""
     from paper_1511_06051_b200 import data
-    spec = micro_nets()[name]
+    spec = _s2d_net(6) if name == "s2d" else micro_nets()[name]
     d = spec.data_spec().shape
     img, lab = oracle_lib.generate_synthetic(10, d[1], d[2], d[3], 6, 2.0, 12345, 0)
     ds = data.Dataset(f32(img), lab % 5 if name == "caffe_mix" else lab,
@@ -320,12 +322,24 @@ def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
     assert out[0][1] == out[1][1]
 
 
-def test_train_host_matches_device_stream(gpu, oracle_lib):
+def _s2d_net(b):
+    """A strided 3-channel first conv (the space-to-depth route in TF32: the device stream
+    gathers straight into x', host batches are staged NHWC then rearranged)."""
+    return ns.NetSpec([
+        ns.data_layer("data", b, 3, 23, 23), ns.label_layer("label", b),
+        ns.conv_layer("c1", "data", 7, 7, 16, stride=2, pad=3), ns.relu_layer("r1", "c1"),
+        ns.lrn_layer("n1", "r1", 5, 1e-2, 0.75, 1.0),
+        ns.pool_layer("p1", "n1", 3, 3, 2, 2, ceil_mode=True),
+        ns.linear_layer("out", "p1", 10), ns.softmax_loss_layer("loss", "out", "label")])
+
+
+@pytest.mark.parametrize("name", ["cifar10_quick", "s2d"])
+def test_train_host_matches_device_stream(gpu, oracle_lib, name):
     """psg_net_train_host (host batches, double-buffered H2D overlapping the steps) ==
     psg_net_train on the HBM-resident stream with the same batch order, bitwise."""
     from paper_1511_06051_b200 import data
     from paper_1511_06051_b200._lib import PinnedArray
-    spec = ns.make_cifar10_quick(10)
+    spec = ns.make_cifar10_quick(10) if name == "cifar10_quick" else _s2d_net(10)
     ds = _dataset(gpu, oracle_lib, spec, 6)
     shards = data.shard(ds, 1, 4)
     a = gpu.Net(spec, 2, precision="tf32")
@@ -335,7 +349,7 @@ def test_train_host_matches_device_stream(gpu, oracle_lib):
     a.set_training_data(data.make_worker_iterator(shards, 0, 10, 4))
     a.train(5)
     it = data.make_worker_iterator(shards, 0, 10, 4)
-    img = PinnedArray((5, 10, 3, 32, 32), np.float32)
+    img = PinnedArray((5,) + tuple(spec.data_spec().shape), np.float32)
     lab = PinnedArray((5, 10), np.int32)
     for s in range(5):
         idx = it.next_indices().astype(np.int64)
