@@ -36,6 +36,11 @@ WORKLOADS = {
 }
 
 
+# BASELINE.json configs: AlexNet K=8 tau=50, GoogLeNet K=8 tau=20, cifar10_quick tau sweep
+DEFAULT_TAU = {"alexnet": 50, "googlenet": 20, "cifar10_quick": 10, "cq-valid": 10}
+HOST_RING = 10  # e2e: pinned host batches per train_host call (re-sent every call)
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -43,7 +48,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cifar10_quick", choices=list(WORKLOADS))
-    p.add_argument("--tau", type=int, default=10)
+    p.add_argument("--tau", type=int, default=None,
+                   help="local SGD steps per round (default: the BASELINE config's — "
+                        "AlexNet 50, GoogLeNet 20, cifar10_quick 10)")
     p.add_argument("--batch", type=int, default=None,
                    help="per-worker batch override (exploration; default: the config's)")
     # tf32 = tcgen05 tensor cores (north star's fast mode, per-layer parity 1e-2);
@@ -52,7 +59,10 @@ def parse():
     p.add_argument("--average", default="fast", choices=["fast", "ordered"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-json", default=None, help="write the per-op profile here")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.tau is None:
+        a.tau = DEFAULT_TAU.get(a.workload, 10)
+    return a
 
 
 def dist_env():
@@ -285,10 +295,19 @@ def main():
     # --- end to end through the C ABI with host buffers (e2e) ---
     e2e_steps = min(args.steps, 5)
     chw = c * h * w
-    pin_img = PinnedArray((args.tau, b, c, h, w), np.float32)
-    pin_lab = PinnedArray((args.tau, b), np.int32)
+    ring = min(args.tau, HOST_RING)  # bounded pinned buffer; every step still copies H2D
+    pin_img = PinnedArray((ring, b, c, h, w), np.float32)
+    pin_lab = PinnedArray((ring, b), np.int32)
     host_it = pdata.make_worker_iterator(shards, rank, b, 7)
-    for s in range(args.tau):
+
+    def host_round():  # tau host-fed steps: ceil(tau / ring) calls over the pinned ring
+        left = args.tau
+        while left > 0:
+            n = min(ring, left)
+            net.train_host(pin_img.array[:n], pin_lab.array[:n])
+            left -= n
+
+    for s in range(ring):
         idx = host_it.next_indices().astype(np.int64)
         if isinstance(ds, pdata.DeviceSyntheticDataset):  # pixels only in HBM: fetch rows once
             for i, r in enumerate(idx):
@@ -296,12 +315,12 @@ def main():
         else:
             pin_img.array[s] = ds.images[idx]
         pin_lab.array[s] = ds.labels[idx]
-    net.train_host(pin_img.array, pin_lab.array)  # warm-up: capture the host-fed graph
+    host_round()  # warm-up: capture the host-fed graph
     average()
     barrier()
     net.event_record(2)
     for _ in range(e2e_steps):
-        net.train_host(pin_img.array, pin_lab.array)
+        host_round()
         average()
     net.event_record(3)
     net.sync()

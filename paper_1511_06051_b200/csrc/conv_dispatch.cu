@@ -108,11 +108,15 @@ bool s2d_route(const ConvGeom& g) {
 }
 
 // x'[b][hs][ws][c'] for c' = (dy*s + dx)*C + c < s*s*C; 0 beyond (and outside x).
-// Block y = one x' row (b, hs); threads stride over its W' x C'/4 float4 cells (32-bit
-// index math), so every store is a coalesced float4 run.  With `idx` the images come
-// straight from the HBM-resident dataset (row idx[cursor * batch + b], channel stride
-// src_cs) and the block of row hs = 0 also copies the label: the batch gather and the
-// space-to-depth rearrangement in one pass (data.hpp:292-304 gather_batch).
+// Block = one x' row (b, hs).  Thread = one (ws, dy) pair: for fixed dy the s*C values
+// c' = dy*s*C .. dy*s*C + s*C - 1 are one contiguous run of input row ih = s*hs + dy - ph
+// (columns s*ws - pw .. s*ws - pw + s - 1, all channels), so the thread copies a run with
+// one division per run instead of per element; the channel padding past s*s*C is written
+// by the dy = s - 1 thread.  With `idx` the images come straight from the HBM-resident
+// dataset (row idx[cursor * batch + b], channel stride src_cs) and the block of row hs = 0
+// also copies the label: the batch gather and the space-to-depth rearrangement in one pass
+// (data.hpp:292-304 gather_batch).
+template <int RUN>  // RUN = s * C when it is 12 (AlexNet conv1: s = 4, C = 3): float4 stores
 __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, ConvGeom g,
                                                ConvGeom q, float* __restrict__ xs,
                                                const uint32_t* __restrict__ idx,
@@ -120,31 +124,51 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
                                                int src_cs, const int32_t* __restrict__ ds_labels,
                                                int32_t* __restrict__ labels) {
   pdl_enter();
-  const int s = g.sh, C = g.Cgs(), c4n = q.cs_in / 4, row = blockIdx.x;
+  const int s = g.sh, C = g.Cgs(), run = s * C, row = blockIdx.x;
   const int hs = row % q.H, b = row / q.H;
-  float4* out = reinterpret_cast<float4*>(xs) + static_cast<size_t>(row) * q.W * c4n;
+  float* out = xs + static_cast<size_t>(row) * q.W * q.cs_in;
   size_t img = b;
   if (idx) {
     img = idx[static_cast<size_t>(cursor ? *cursor : 0) * batch + b];
     if (hs == 0 && threadIdx.x == 0) labels[b] = ds_labels[img];
   }
   const float* xb = x + img * g.H * g.W * src_cs;
-  for (int j = threadIdx.x; j < q.W * c4n; j += blockDim.x) {
-    const int ws = j / c4n, c0 = (j - ws * c4n) * 4;
-    float v[4];
+  for (int j = threadIdx.x; j < q.W * s; j += blockDim.x) {
+    const int ws = j / s, dy = j - ws * s;
+    const int ih = s * hs + dy - g.ph, iw0 = s * ws - g.pw;
+    float* o = out + ws * q.cs_in + dy * run;
+    const bool row_ok = ih >= 0 && ih < g.H;
+    const float* xr = xb + static_cast<size_t>(ih) * g.W * src_cs;
+    if constexpr (RUN == 12) {
+      float v[12];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int cp = c0 + e;
-      v[e] = 0.f;
-      if (cp < s * s * C) {
-        const int blk = cp / C, c = cp - blk * C;
-        const int ih = s * hs + blk / s - g.ph, iw = s * ws + blk % s - g.pw;
-        if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
-          v[e] = __ldg(xb + (ih * g.W + iw) * src_cs + c);
+      for (int dx = 0; dx < 4; ++dx) {
+        const int iw = iw0 + dx;
+        const bool ok = row_ok && iw >= 0 && iw < g.W;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[dx * 3 + c] = ok ? __ldg(xr + iw * src_cs + c) : 0.f;
+      }
+      float4* o4 = reinterpret_cast<float4*>(o);
+      o4[0] = make_float4(v[0], v[1], v[2], v[3]);
+      o4[1] = make_float4(v[4], v[5], v[6], v[7]);
+      o4[2] = make_float4(v[8], v[9], v[10], v[11]);
+    } else {
+      for (int dx = 0; dx < s; ++dx) {
+        const int iw = iw0 + dx;
+        const bool ok = row_ok && iw >= 0 && iw < g.W;
+        for (int c = 0; c < C; ++c) o[dx * C + c] = ok ? __ldg(xr + iw * src_cs + c) : 0.f;
       }
     }
-    out[j] = make_float4(v[0], v[1], v[2], v[3]);
+    if (dy == s - 1)
+      for (int cp = s * run; cp < q.cs_in; ++cp) out[ws * q.cs_in + cp] = 0.f;
   }
+}
+
+using S2dKernel = void (*)(const float*, ConvGeom, ConvGeom, float*, const uint32_t*, const int*,
+                          int, int, const int32_t*, int32_t*);
+S2dKernel s2d_kernel(const ConvGeom& g, const ConvGeom& q) {
+  // float4 runs: 12-float runs at 16-byte aligned offsets (cs_in % 4 == 0 by construction)
+  return g.sh * g.Cgs() == 12 && q.cs_in % 4 == 0 ? s2d_x_k<12> : s2d_x_k<0>;
 }
 
 // W'[f][tu][tv][c'] = W[f][s*tu + dy][s*tv + dx][c] (0 past the kernel / past s*s*C)
@@ -186,8 +210,8 @@ void s2d_x(const ConvGeom& g, const float* x, float* xs, cudaStream_t st) {
   const ConvGeom q = s2d_geom(g);
   if (static_cast<size_t>(g.H) * g.W * g.cs_in >= (1ULL << 31))
     throw std::invalid_argument("s2d: image too large");
-  launch_k(s2d_x_k, q.n * q.H, 256, 0, st, x, g, q, xs, nullptr, nullptr, 0, g.cs_in, nullptr,
-           nullptr);
+  launch_k(s2d_kernel(g, q), q.n * q.H, 256, 0, st, x, g, q, xs, nullptr, nullptr, 0, g.cs_in,
+           nullptr, nullptr);
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -270,8 +294,8 @@ void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_lab
   const ConvGeom q = s2d_geom(g);
   if (static_cast<size_t>(g.H) * g.W * src_cs >= (1ULL << 31))
     throw std::invalid_argument("s2d: image too large");
-  launch_k(s2d_x_k, q.n * q.H, 256, 0, st, ds_images, g, q, col, idx, cursor, g.n, src_cs,
-           ds_labels, labels);
+  launch_k(s2d_kernel(g, q), q.n * q.H, 256, 0, st, ds_images, g, q, col, idx, cursor, g.n,
+           src_cs, ds_labels, labels);
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -179,42 +179,46 @@ __global__ void __launch_bounds__(256) pool_fwd_k(PoolGeom g, const V* __restric
 
 // model.hpp:492-498 as a deterministic gather: each input sums, in ascending
 // output order, the dy of the covering windows that routed to it.
-template <typename V>
+// KS > 0: kh = kw = KS and sh = sw = SS at compile time (the window / stride divisions and
+// bounds checks become constants; same arithmetic, same summation order).
+template <typename V, int KS, int SS>
 __global__ void __launch_bounds__(256) pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
                                                   const typename RouteOf<V>::T* __restrict__ route,
                                                   V* __restrict__ dx, int accumulate, int cv) {
   pdl_enter();
   constexpr int L = RouteOf<V>::n;
+  const int kh = KS > 0 ? KS : g.kh, kw = KS > 0 ? KS : g.kw;
+  const int sh = KS > 0 ? SS : g.sh, sw = KS > 0 ? SS : g.sw;
   const int h = blockIdx.x % g.H, b = blockIdx.x / g.H;
   // windows with oh*sh - ph <= h < oh*sh - ph + kh
-  const int ohl = max(0, (h + g.ph - g.kh + g.sh) / g.sh);
-  const int ohh = min(g.OH - 1, (h + g.ph) / g.sh);
+  const int ohl = max(0, (h + g.ph - kh + sh) / sh);
+  const int ohh = min(g.OH - 1, (h + g.ph) / sh);
   const uint32_t obase = static_cast<uint32_t>(b) * g.OH * g.OW;
   const size_t xbase = static_cast<size_t>(blockIdx.x) * g.W * cv;
   const int total = g.W * cv, step_c = blockDim.x % cv, step_w = blockDim.x / cv;
   int c = threadIdx.x % cv, w = threadIdx.x / cv;
   for (int j = threadIdx.x; j < total; j += blockDim.x) {
-    const int owl = max(0, (w + g.pw - g.kw + g.sw) / g.sw);
-    const int owh = min(g.OW - 1, (w + g.pw) / g.sw);
+    const int owl = max(0, (w + g.pw - kw + sw) / sw);
+    const int owh = min(g.OW - 1, (w + g.pw) / sw);
     V acc;
 #pragma unroll
     for (int q = 0; q < L; ++q) comp(acc, q) = 0.f;
     for (int oh = ohl; oh <= ohh; ++oh) {
-      const int hs0 = oh * g.sh - g.ph;
-      if (h < hs0 || h >= hs0 + g.kh) continue;
+      const int hs0 = oh * sh - g.ph;
+      if (h < hs0 || h >= hs0 + kh) continue;
       for (int ow = owl; ow <= owh; ++ow) {
-        const int ws0 = ow * g.sw - g.pw;
-        if (w < ws0 || w >= ws0 + g.kw) continue;
+        const int ws0 = ow * sw - g.pw;
+        if (w < ws0 || w >= ws0 + kw) continue;
         const uint32_t o = (obase + oh * g.OW + ow) * cv + c;
         const V d = __ldg(dy + o);
         if (g.method == PSG_POOL_AVE) {
-          const float size = static_cast<float>((min(hs0 + g.kh, g.H + g.ph) - hs0) *
-                                                (min(ws0 + g.kw, g.W + g.pw) - ws0));
+          const float size = static_cast<float>((min(hs0 + kh, g.H + g.ph) - hs0) *
+                                                (min(ws0 + kw, g.W + g.pw) - ws0));
 #pragma unroll
           for (int q = 0; q < L; ++q) comp(acc, q) += comp(d, q) / size;
         } else {
           const typename RouteOf<V>::T r = __ldg(route + o);
-          const uint8_t want = static_cast<uint8_t>((h - hs0) * g.kw + (w - ws0));
+          const uint8_t want = static_cast<uint8_t>((h - hs0) * kw + (w - ws0));
 #pragma unroll
           for (int q = 0; q < L; ++q)
             if (rcomp(r, q) == want) comp(acc, q) += comp(d, q);
@@ -630,12 +634,18 @@ void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* d
               bool accumulate, cudaStream_t s) {
   checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
   const unsigned rows = static_cast<unsigned>(g.n) * g.H;
-  if (g.C % 4 == 0)
-    launch_k(pool_bwd_k<float4>, rows, 256, 0, s, g, reinterpret_cast<const float4*>(dy),
+  const bool k3 = g.kh == 3 && g.kw == 3 && g.sh == g.sw && (g.sh == 1 || g.sh == 2);
+  if (g.C % 4 == 0) {
+    auto kern = !k3 ? pool_bwd_k<float4, 0, 0>
+                    : g.sh == 2 ? pool_bwd_k<float4, 3, 2> : pool_bwd_k<float4, 3, 1>;
+    launch_k(kern, rows, 256, 0, s, g, reinterpret_cast<const float4*>(dy),
              reinterpret_cast<const uchar4*>(route), reinterpret_cast<float4*>(dx), accumulate,
              g.C / 4);
-  else
-    launch_k(pool_bwd_k<float>, rows, 256, 0, s, g, dy, route, dx, accumulate, g.C);
+  } else {
+    auto kern = !k3 ? pool_bwd_k<float, 0, 0>
+                    : g.sh == 2 ? pool_bwd_k<float, 3, 2> : pool_bwd_k<float, 3, 1>;
+    launch_k(kern, rows, 256, 0, s, g, dy, route, dx, accumulate, g.C);
+  }
   PSG_CUDA(cudaGetLastError());
 }
 
