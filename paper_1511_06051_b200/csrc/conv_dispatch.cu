@@ -36,7 +36,7 @@ int tc_launches(const ConvGeom& g, int which);
 void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
               bool relu, const Workspace& ws, cudaStream_t s);
 void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-              const Workspace& ws, cudaStream_t s);
+              const Workspace& ws, cudaStream_t s, const float* relu_mask);
 void tc_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
               const Workspace& ws, cudaStream_t s);
 bool tc_wgrad_col_supported(const ConvGeom& g);
@@ -326,10 +326,14 @@ void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* 
   }
 }
 
+bool conv_dgrad_masks(const ConvGeom& g, Mode m) { return use_tc(g, 1, m); }
+
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-                const Workspace& ws, Mode m, cudaStream_t s) {
+                const Workspace& ws, Mode m, cudaStream_t s, const float* relu_mask) {
   if (use_tc(g, 1, m))
-    tc_dgrad(g, dy, w, dx, accumulate, ws, s);
+    tc_dgrad(g, dy, w, dx, accumulate, ws, s, relu_mask);
+  else if (relu_mask)
+    throw std::logic_error("conv_dgrad: ReLU mask needs the tensor-core path");
   else
     conv_dgrad_simt(g, dy, w, dx, accumulate, ws, s);
 }

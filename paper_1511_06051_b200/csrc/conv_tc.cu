@@ -39,7 +39,7 @@ using namespace tck;
 __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long long stride,
                                 long long total, const float* __restrict__ bias, int ldo,
                                 int valid_cols, int relu, int accumulate,
-                                float* __restrict__ out) {
+                                const float* __restrict__ mask, float* __restrict__ out) {
   pdl_enter();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -53,6 +53,7 @@ __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long l
       s += bias[i % ldo];
       if (relu) s = s > 0.f ? s : 0.f;
     }
+    if (mask && !(mask[i] > 0.f)) s = 0.f;  // folded ReLU backward (dgrad)
     out[i] = accumulate ? out[i] + s : s;
   }
 }
@@ -403,7 +404,7 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     const int blocks = static_cast<int>(std::min<long long>((out_elems + 255) / 256, 148 * 8));
     launch_k(tc_split_reduce, blocks, 256, 0, s, ws, splits, out_elems, out_elems, a0.bias, a0.ldo,
                                            a0.valid_cols ? a0.valid_cols : a0.ldo, a0.relu,
-                                           a0.accumulate, a0.out);
+                                           a0.accumulate, a0.mask, a0.out);
     PSG_CUDA(cudaGetLastError());
   }
 }
@@ -745,13 +746,14 @@ void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bi
 }
 
 void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-              const Workspace& ws, cudaStream_t s) {
+              const Workspace& ws, cudaStream_t s, const float* relu_mask) {
   TcArgs a;
   int kblk;
   if (!plan_dgrad(g, a, kblk)) throw std::logic_error("tc_dgrad: unsupported geometry");
   finish_args(a, kblk, sm_count());
   a.out = dx;
   a.accumulate = accumulate;
+  a.mask = relu_mask;
   CUtensorMap ma, mb;
   if (a.a_mode == A_2D_K) {
     ma = map_2d(dy, g.n, g.F, kblk, kTileM, k_swizzle(kblk));

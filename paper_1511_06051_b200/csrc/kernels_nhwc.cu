@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(256) pool_fwd_k(PoolGeom g, const V* __restric
 template <typename V, int KS, int SS>
 __global__ void __launch_bounds__(256) pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
                                                   const typename RouteOf<V>::T* __restrict__ route,
-                                                  V* __restrict__ dx, int accumulate, int cv) {
+                                                  V* __restrict__ dx, int accumulate, int cv,
+                                                  const V* __restrict__ mask) {
   pdl_enter();
   constexpr int L = RouteOf<V>::n;
   const int kh = KS > 0 ? KS : g.kh, kw = KS > 0 ? KS : g.kw;
@@ -224,6 +225,12 @@ __global__ void __launch_bounds__(256) pool_bwd_k(PoolGeom g, const V* __restric
             if (rcomp(r, q) == want) comp(acc, q) += comp(d, q);
         }
       }
+    }
+    if (mask) {
+      const V m = __ldg(mask + xbase + j);
+#pragma unroll
+      for (int q = 0; q < L; ++q)
+        if (!(comp(m, q) > 0.f)) comp(acc, q) = 0.f;
     }
     if (accumulate) {
       const V o = dx[xbase + j];
@@ -631,7 +638,7 @@ void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaS
 }
 
 void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
-              bool accumulate, cudaStream_t s) {
+              bool accumulate, cudaStream_t s, const float* relu_mask) {
   checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
   const unsigned rows = static_cast<unsigned>(g.n) * g.H;
   const bool k3 = g.kh == 3 && g.kw == 3 && g.sh == g.sw && (g.sh == 1 || g.sh == 2);
@@ -640,11 +647,11 @@ void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* d
                     : g.sh == 2 ? pool_bwd_k<float4, 3, 2> : pool_bwd_k<float4, 3, 1>;
     launch_k(kern, rows, 256, 0, s, g, reinterpret_cast<const float4*>(dy),
              reinterpret_cast<const uchar4*>(route), reinterpret_cast<float4*>(dx), accumulate,
-             g.C / 4);
+             g.C / 4, reinterpret_cast<const float4*>(relu_mask));
   } else {
     auto kern = !k3 ? pool_bwd_k<float, 0, 0>
                     : g.sh == 2 ? pool_bwd_k<float, 3, 2> : pool_bwd_k<float, 3, 1>;
-    launch_k(kern, rows, 256, 0, s, g, dy, route, dx, accumulate, g.C);
+    launch_k(kern, rows, 256, 0, s, g, dy, route, dx, accumulate, g.C, relu_mask);
   }
   PSG_CUDA(cudaGetLastError());
 }

@@ -190,10 +190,29 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
   return launches;
 }
 
+namespace {
+// Fusion: the ReLU whose backward the layer `c` (its only consumer) can fold into its own
+// input-gradient pass (a tensor-core dgrad epilogue or the max/ave pool backward), else -1.
+int foldable_relu(const psg_net* net, const LayerRt& c) {
+  if (!net->fuse || c.inputs.size() != 1) return -1;
+  const int ri = c.inputs[0];
+  const LayerRt& r = net->L[ri];
+  if (r.kind != PSG_LAYER_RELU || r.bwd_by >= 0 || r.consumers.size() != 1 ||
+      net->L[r.inputs[0]].kind == PSG_LAYER_DATA)
+    return -1;
+  if (c.kind == PSG_LAYER_POOL) return ri;
+  if ((c.kind == PSG_LAYER_CONV || c.kind == PSG_LAYER_LINEAR) && net->mode == Mode::Tf32 &&
+      conv_dgrad_masks(c.cg, net->mode))
+    return ri;
+  return -1;
+}
+}  // namespace
+
 int run_backward(psg_net* net, size_t n, OpTimer* timer) {
   cudaStream_t s = net->stream;
   int launches = 0;
   std::vector<char> written(net->L.size(), 0);
+  std::vector<char> relu_folded(net->L.size(), 0);  // backward done by the consumer
   for (const LayerRt& l : net->L)  // every loss seed writes its logits grad
     if (l.kind == PSG_LAYER_SOFTMAX_LOSS) written[l.inputs[0]] = 1;
   for (int li = static_cast<int>(net->L.size()) - 1; li >= 0; --li) {
@@ -238,7 +257,16 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
         }
         if (need_dx) {
           Scope sc(timer, (nm + ".dgrad").c_str(), li, 4, conv_flops(net, l, n), 0.0);
-          conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->ws, net->mode, s);
+          const int ri = foldable_relu(net, l);
+          if (ri >= 0) {  // write the ReLU's input gradient, masked by the ReLU's output
+            const int pi2 = net->L[ri].inputs[0];
+            conv_dgrad(g, l.grad, net->w + k.int_off, net->L[pi2].grad, written[pi2] != 0,
+                       net->ws, net->mode, s, net->L[ri].out);
+            written[pi2] = 1;
+            relu_folded[ri] = 1;
+          } else {
+            conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->ws, net->mode, s);
+          }
           const int c = conv_launches(g, 1, net->mode);
           sc.done(c);
           launches += c;
@@ -251,13 +279,22 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
           g.n = static_cast<int>(n);
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0,
                    act_bytes(src, n) + act_bytes(l, n) * (l.route ? 1.25 : 1.0));
-          pool_bwd(g, l.grad, l.route, src.grad, acc, s);
+          const int ri = foldable_relu(net, l);
+          if (ri >= 0) {  // ReLU backward folded in: mask by the ReLU's output
+            const int pi2 = net->L[ri].inputs[0];
+            pool_bwd(g, l.grad, l.route, net->L[pi2].grad, written[pi2] != 0, s,
+                     net->L[ri].out);
+            written[pi2] = 1;
+            relu_folded[ri] = 1;
+          } else {
+            pool_bwd(g, l.grad, l.route, src.grad, acc, s);
+          }
           sc.done(1);
           ++launches;
         }
         break;
       case PSG_LAYER_RELU:
-        if (l.bwd_by >= 0) break;  // done by the consuming LRN's backward
+        if (l.bwd_by >= 0 || relu_folded[li]) break;  // done by the consumer's backward
         if (need_dx) {
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
           relu_bwd(src.out, l.grad, src.grad, n * l.vol(), acc, s);

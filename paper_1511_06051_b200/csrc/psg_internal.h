@@ -138,8 +138,11 @@ bool conv_s2d_input(const ConvGeom& g, Mode mode);
 void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_labels,
                 const uint32_t* idx, const int* cursor, int src_cs, float* col, int32_t* labels,
                 cudaStream_t s);
+// relu_mask (tensor-core path only, see conv_dgrad_masks): dx = (relu_mask > 0 ? dgrad : 0)
+// (+ dx when accumulating) — the backward of a ReLU whose only consumer is this layer.
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-                const Workspace& ws, Mode mode, cudaStream_t s);
+                const Workspace& ws, Mode mode, cudaStream_t s, const float* relu_mask = nullptr);
+bool conv_dgrad_masks(const ConvGeom& g, Mode mode);
 // dW [F][Kp] and db [F] (written, not accumulated).
 void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
                 const Workspace& ws, float* col, Mode mode, cudaStream_t s);
@@ -153,8 +156,9 @@ struct PoolGeom {
   int method = 0;
 };
 void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaStream_t s);
+// relu_mask: dx = (relu_mask > 0 ? pool gradient : 0) (+ dx) — a folded ReLU backward.
 void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
-              bool accumulate, cudaStream_t s);
+              bool accumulate, cudaStream_t s, const float* relu_mask = nullptr);
 
 void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s);
 void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumulate,

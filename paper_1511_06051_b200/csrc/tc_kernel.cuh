@@ -81,6 +81,9 @@ struct TcArgs {
   // first pixel sits at (x + im_lw, y + im_lh) of the source, tap (u, v) adds offsets
   // (sign > 0 ? v : kw - 1 - v, sign > 0 ? u : kh - 1 - u)
   int kh, im_lw, im_lh;
+  // dgrad with the consumer-side ReLU backward folded in: out = (mask > 0 ? acc : 0), mask
+  // laid out like out (the ReLU's output = this conv's input), applied before accumulate
+  const float* mask;
 };
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
@@ -542,6 +545,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     y.w = y.w > 0.f ? y.w : 0.f;
                   }
                 }
+                if (p.mask) {
+                  const float4 m = *reinterpret_cast<const float4*>(p.mask + row_off + cidx);
+                  y.x = m.x > 0.f ? y.x : 0.f;
+                  y.y = m.y > 0.f ? y.y : 0.f;
+                  y.z = m.z > 0.f ? y.z : 0.f;
+                  y.w = m.w > 0.f ? y.w : 0.f;
+                }
                 if (acc_out) {
                   const float4 o = *dst;
                   y.x += o.x; y.y += o.y; y.z += o.z; y.w += o.w;
@@ -569,6 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     yv += bsh[c + e];
                     if (p.relu) yv = yv > 0.f ? yv : 0.f;
                   }
+                  if (p.mask && !(p.mask[row_off + ce] > 0.f)) yv = 0.f;
                   if (acc_out) yv += rowp[ce];
                 }
                 rowp[ce] = yv;
