@@ -337,6 +337,15 @@ def main():
     barrier()
     images = K * args.steps * args.tau * b
     value = images / (ms / 1000.0)
+    avg_ms = None
+    if comm is not None:  # the K-way weight average alone (north star: < 2% of the round)
+        barrier()
+        net.event_record(2)
+        for _ in range(5):
+            average()
+        net.event_record(3)
+        net.sync()
+        avg_ms = max_over_ranks(net.event_elapsed(2, 3)) / 5
 
     # --- end to end through the C ABI with host buffers (e2e) ---
     e2e_steps = min(args.steps, 5)
@@ -430,6 +439,9 @@ def main():
                     "h2d_bytes_per_step": args.tau * b * (chw * 4 + 4),
                     "d2h_bytes_per_step": args.tau * 8},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "weight_average": None if avg_ms is None else {
+                "ms": avg_ms, "share_of_round": avg_ms / (ms / args.steps),
+                "param_bytes": 4 * sum(c for _, c in net.segments())},
             "gpu_launches": launches}))
     if dist is not None:
         dist.destroy_process_group()

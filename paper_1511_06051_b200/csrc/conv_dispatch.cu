@@ -36,7 +36,9 @@ int tc_launches(const ConvGeom& g, int which);
 void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
               bool relu, const Workspace& ws, cudaStream_t s);
 void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-              const Workspace& ws, cudaStream_t s, const float* relu_mask);
+              const Workspace& ws, cudaStream_t s, const float* relu_mask, const float* wt);
+bool tc_dgrad_wt(const ConvGeom& g);
+void tc_dgrad_wt_transpose(const ConvGeom& g, const float* w, float* wt, cudaStream_t s);
 void tc_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
               const Workspace& ws, cudaStream_t s);
 bool tc_wgrad_col_supported(const ConvGeom& g);
@@ -299,11 +301,20 @@ void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_lab
   PSG_CUDA(cudaGetLastError());
 }
 
-size_t conv_col_elems(const ConvGeom& g, Mode m) {
+namespace {
+size_t col_route_elems(const ConvGeom& g, Mode m) {
   // s2d route: x' (written by fprop, read by wgrad), W', dW'
   if (m == Mode::Tf32 && s2d_route(g)) return s2d_x_elems(g) + 2 * s2d_w_elems(g);
   if (m != Mode::Tf32 || !(fprop_col_route(g) || wgrad_col_route(g))) return 0;
   return static_cast<size_t>(g.G) * g.n * g.OH * g.OW * g.Kp();
+}
+bool dgrad_uses_wt(const ConvGeom& g, Mode m) { return use_tc(g, 1, m) && tc_dgrad_wt(g); }
+}  // namespace
+
+// col = [im2col / space-to-depth scratch][dgrad's transposed weights Wt (32-float aligned)]
+size_t conv_col_elems(const ConvGeom& g, Mode m) {
+  const size_t base = (col_route_elems(g, m) + 31) / 32 * 32;
+  return base + (dgrad_uses_wt(g, m) ? static_cast<size_t>(g.F) * g.kh * g.kw * g.Cgs() : 0);
 }
 
 void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
@@ -329,9 +340,16 @@ void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* 
 bool conv_dgrad_masks(const ConvGeom& g, Mode m) { return use_tc(g, 1, m); }
 
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-                const Workspace& ws, Mode m, cudaStream_t s, const float* relu_mask) {
-  if (use_tc(g, 1, m))
-    tc_dgrad(g, dy, w, dx, accumulate, ws, s, relu_mask);
+                const Workspace& ws, Mode m, cudaStream_t s, const float* relu_mask, float* col) {
+  if (use_tc(g, 1, m)) {
+    float* wt = nullptr;
+    if (tc_dgrad_wt(g)) {
+      if (!col) throw std::logic_error("conv_dgrad: no scratch for the transposed weights");
+      wt = col + (col_route_elems(g, m) + 31) / 32 * 32;
+      tc_dgrad_wt_transpose(g, w, wt, s);
+    }
+    tc_dgrad(g, dy, w, dx, accumulate, ws, s, relu_mask, wt);
+  }
   else if (relu_mask)
     throw std::logic_error("conv_dgrad: ReLU mask needs the tensor-core path");
   else
@@ -375,7 +393,7 @@ int conv_launches(const ConvGeom& g, int which, Mode m) {
     return 1 + tc_launches(col_geom(g), 0);
   if (m == Mode::Tf32 && which == 2 && wgrad_col_route(g))
     return (fprop_col_route(g) ? 0 : 1) + tc_wgrad_col_launches(g);
-  if (use_tc(g, which, m)) return tc_launches(g, which);
+  if (use_tc(g, which, m)) return tc_launches(g, which) + (which == 1 && tc_dgrad_wt(g) ? 1 : 0);
   return conv_launches_simt(g, which);
 }
 

@@ -293,7 +293,10 @@ void finish_args(TcArgs& a, int kblk, int sms) {
     const int v = e ? std::atoi(e) : kMaxProducers;
     return std::max(1, std::min(kMaxProducers, v));
   }();
-  // a producer may only run one ring ahead of the slot it refills (parity waits): <= stages
+  // a producer may only run one ring ahead of the slot it refills (parity waits): <= stages.
+  // (Producers sharing every stage's boxes instead measured 2.5x slower: each producer
+  // then pays every stage's barrier wait and cursor walk, which cost about as much as a
+  // box issue.)
   a.producers = std::min(producers, a.stages);
   // the producers' cursor jump over the other producers' stages, as mixed-radix digits
   {
@@ -484,6 +487,42 @@ bool plan_fprop(const ConvGeom& g, TcArgs& a, int& kblk) {
   return true;
 }
 
+}  // namespace
+
+// dgrad B from a K-major copy of the weights, Wt[g][c][tap][f] (written per step by
+// tc_dgrad_wt_transpose): C/G not a multiple of 64 would otherwise pad an MN-major B to
+// whole 64-column pair halves (AlexNet conv2: 48 -> 64); K-major B splits 48 = 2 x 24 rows.
+bool tc_dgrad_wt(const ConvGeom& g) {
+  static const bool env = [] {
+    const char* e = std::getenv("PSG_TC_DGRAD_WT");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return env && !is_linear(g) && g.sh == 1 && g.sw == 1 && g.Cgs() % 64 != 0 &&
+         g.Cgs() % 16 == 0 && g.Fg() % 32 == 0;
+}
+
+namespace {
+
+__global__ void dgrad_wt_k(const float* __restrict__ w, int Fg, int taps, int Cg, int Kp,
+                           float* __restrict__ wt, int total) {
+  pdl_enter();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int f = i % Fg, r = i / Fg, tap = r % taps, gc = r / taps, g = gc / Cg, c = gc % Cg;
+  wt[i] = w[static_cast<size_t>(g * Fg + f) * Kp + tap * Cg + c];
+}
+
+}  // namespace
+
+void tc_dgrad_wt_transpose(const ConvGeom& g, const float* w, float* wt, cudaStream_t s) {
+  const int taps = g.kh * g.kw, total = g.F * taps * g.Cgs();
+  launch_k(dgrad_wt_k, (total + 255) / 256, 256, 0, s, w, g.Fg(), taps, g.Cgs(), g.Kp(), wt,
+           total);
+  PSG_CUDA(cudaGetLastError());
+}
+
+namespace {
+
 bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   std::memset(&a, 0, sizeof a);
   if (is_linear(g)) {
@@ -511,7 +550,7 @@ bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
     kblk = 32;
   }
   a.a_mode = A_RECT_K;   // dY rectangles, taps reversed
-  a.b_mode = B_WT_MN;    // W^T
+  a.b_mode = tc_dgrad_wt(g) ? B_3D_K : B_WT_MN;  // Wt (K-major copy) or W^T (MN-major)
   a.row_map = ROW_RECT;
   rect_shape(g.W, kTileM, a.rm, a.wm);
   a.th = (g.H + a.rm - 1) / a.rm;
@@ -746,7 +785,7 @@ void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bi
 }
 
 void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-              const Workspace& ws, cudaStream_t s, const float* relu_mask) {
+              const Workspace& ws, cudaStream_t s, const float* relu_mask, const float* wt) {
   TcArgs a;
   int kblk;
   if (!plan_dgrad(g, a, kblk)) throw std::logic_error("tc_dgrad: unsupported geometry");
@@ -764,14 +803,24 @@ void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, boo
                            -g.ph, k_swizzle(kblk));
     else
       ma = map_nhwc(dy, g.n, g.OH, g.OW, g.F, kblk, a.wm, a.rm, k_swizzle(kblk));
-    const uint64_t dims[4] = {static_cast<uint64_t>(g.Cgs()),
-                              static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.Fg()),
-                              static_cast<uint64_t>(g.G)};
-    const uint64_t str[3] = {static_cast<uint64_t>(g.Cgs()) * 4,
-                             static_cast<uint64_t>(g.Kp()) * 4,
-                             static_cast<uint64_t>(g.Fg()) * g.Kp() * 4};
-    const uint32_t box[4] = {32, 1, static_cast<uint32_t>(kblk), 1};
-    mb = make_map(w, 4, dims, str, box, kMnSwizzle);
+    if (a.b_mode == B_3D_K) {  // Wt viewed as [G * C/G][taps][F/G], K-major boxes
+      if (!wt) throw std::logic_error("tc_dgrad: transposed weights missing");
+      const uint64_t taps = static_cast<uint64_t>(g.kh) * g.kw;
+      const uint64_t dims[3] = {static_cast<uint64_t>(g.Fg()), taps,
+                                static_cast<uint64_t>(g.G) * g.Cgs()};
+      const uint64_t str[2] = {static_cast<uint64_t>(g.Fg()) * 4, taps * g.Fg() * 4};
+      const uint32_t box[3] = {static_cast<uint32_t>(kblk), 1, static_cast<uint32_t>(a.b_cols)};
+      mb = make_map(wt, 3, dims, str, box, k_swizzle(kblk));
+    } else {
+      const uint64_t dims[4] = {static_cast<uint64_t>(g.Cgs()),
+                                static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.Fg()),
+                                static_cast<uint64_t>(g.G)};
+      const uint64_t str[3] = {static_cast<uint64_t>(g.Cgs()) * 4,
+                               static_cast<uint64_t>(g.Kp()) * 4,
+                               static_cast<uint64_t>(g.Fg()) * g.Kp() * 4};
+      const uint32_t box[4] = {32, 1, static_cast<uint32_t>(kblk), 1};
+      mb = make_map(w, 4, dims, str, box, kMnSwizzle);
+    }
   }
   launch(a, ma, mb, kblk, static_cast<long long>(g.n) * g.H * g.W * g.cs_in, ws.ptr, ws.elems,
          s);

@@ -261,11 +261,12 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
           if (ri >= 0) {  // write the ReLU's input gradient, masked by the ReLU's output
             const int pi2 = net->L[ri].inputs[0];
             conv_dgrad(g, l.grad, net->w + k.int_off, net->L[pi2].grad, written[pi2] != 0,
-                       net->ws, net->mode, s, net->L[ri].out);
+                       net->ws, net->mode, s, net->L[ri].out, l.col);
             written[pi2] = 1;
             relu_folded[ri] = 1;
           } else {
-            conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->ws, net->mode, s);
+            conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->ws, net->mode, s,
+                       nullptr, l.col);
           }
           const int c = conv_launches(g, 1, net->mode);
           sc.done(c);

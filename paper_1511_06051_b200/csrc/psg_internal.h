@@ -140,8 +140,10 @@ void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_lab
                 cudaStream_t s);
 // relu_mask (tensor-core path only, see conv_dgrad_masks): dx = (relu_mask > 0 ? dgrad : 0)
 // (+ dx when accumulating) — the backward of a ReLU whose only consumer is this layer.
+// col: the layer's conv_col_elems scratch (holds a K-major weight copy for some dgrads).
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
-                const Workspace& ws, Mode mode, cudaStream_t s, const float* relu_mask = nullptr);
+                const Workspace& ws, Mode mode, cudaStream_t s, const float* relu_mask = nullptr,
+                float* col = nullptr);
 bool conv_dgrad_masks(const ConvGeom& g, Mode mode);
 // dW [F][Kp] and db [F] (written, not accumulated).
 void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,

@@ -515,6 +515,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c0 = 0; c0 < c_end; c0 += 32) {
         const bool more = c0 + 32 < c_end;
         if (more) tc::tmem_ld32_async(taddr + c0 + 32, vb);
+        // operands the epilogue reads (ReLU mask, accumulated output): all 8 float4 of the
+        // chunk are loaded before any store, so the loads overlap instead of each waiting
+        // behind the previous store (out / mask may alias as far as the compiler knows)
+        float4 pre_m[8], pre_o[8];
+        const bool vec_pre = row_ok && p.epi_vec && !p.cpt && !p.ws;
+        if (vec_pre && (p.mask || acc_out)) {
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const int c = c0 + 4 * q4;
+            if (c >= nvalid) continue;
+            if (p.mask) pre_m[q4] = __ldg(reinterpret_cast<const float4*>(p.mask + row_off + col0 + c));
+            if (acc_out) pre_o[q4] = *reinterpret_cast<const float4*>(rowp + col0 + c);
+          }
+        }
         if (row_ok) {
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
@@ -546,14 +560,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                   }
                 }
                 if (p.mask) {
-                  const float4 m = *reinterpret_cast<const float4*>(p.mask + row_off + cidx);
+                  const float4 m = vec_pre ? pre_m[q4]
+                                           : *reinterpret_cast<const float4*>(p.mask + row_off + cidx);
                   y.x = m.x > 0.f ? y.x : 0.f;
                   y.y = m.y > 0.f ? y.y : 0.f;
                   y.z = m.z > 0.f ? y.z : 0.f;
                   y.w = m.w > 0.f ? y.w : 0.f;
                 }
                 if (acc_out) {
-                  const float4 o = *dst;
+                  const float4 o = vec_pre ? pre_o[q4] : *dst;
                   y.x += o.x; y.y += o.y; y.z += o.z; y.w += o.w;
                 }
               }
