@@ -212,6 +212,24 @@ void to_im2col(TcArgs& a, const ConvGeom& g, int out_h, int out_w, int sign) {
   a.row_g = 0;
 }
 
+// MN-major [rows][cols] (cols % 32 == 0) as [cols / 32][rows][32]: one box = `chunks`
+// 32-column chunks x box_r rows, landing chunk-major in smem (PSG_TC_ONEBOX=0: per chunk).
+bool one_box_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_TC_ONEBOX");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
+CUtensorMap map_mn_chunks(const float* base, long long rows, long long cols, int box_r,
+                          int chunks) {
+  const uint64_t dims[3] = {32, static_cast<uint64_t>(rows), static_cast<uint64_t>(cols / 32)};
+  const uint64_t str[2] = {static_cast<uint64_t>(cols) * 4, 128};
+  const uint32_t box[3] = {32, static_cast<uint32_t>(box_r), static_cast<uint32_t>(chunks)};
+  return make_map(base, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
 CUtensorMap map_2d(const float* base, long long rows, long long cols, int box_c, int box_r,
                    CUtensorMapSwizzle sw) {
   const uint64_t dims[2] = {static_cast<uint64_t>(cols), static_cast<uint64_t>(rows)};
@@ -796,7 +814,9 @@ void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, boo
   CUtensorMap ma, mb;
   if (a.a_mode == A_2D_K) {
     ma = map_2d(dy, g.n, g.F, kblk, kTileM, k_swizzle(kblk));
-    mb = map_2d(w, g.F, g.cs_in, 32, kblk, kMnSwizzle);
+    a.b_one = one_box_enabled() && g.cs_in % 32 == 0 && a.n_tile % 32 == 0 && a.b_cols % 32 == 0;
+    mb = a.b_one ? map_mn_chunks(w, g.F, g.cs_in, kblk, (a.b_cols + 31) / 32)
+                 : map_2d(w, g.F, g.cs_in, 32, kblk, kMnSwizzle);
   } else {
     if (a.a_mode == A_IM2COL_K)  // traversal grid H x W over dY: lower = -(k-1-p), upper = -p
       ma = map_nhwc_im2col(dy, g.n, g.OH, g.OW, g.F, kblk, kTileM, a.im_lw, a.im_lh, -g.pw,
@@ -811,6 +831,19 @@ void tc_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, boo
       const uint64_t str[2] = {static_cast<uint64_t>(g.Fg()) * 4, taps * g.Fg() * 4};
       const uint32_t box[3] = {static_cast<uint32_t>(kblk), 1, static_cast<uint32_t>(a.b_cols)};
       mb = make_map(wt, 3, dims, str, box, k_swizzle(kblk));
+    } else if (one_box_enabled() && g.Cgs() % 32 == 0 && a.n_tile % 32 == 0 &&
+               a.b_cols % 32 == 0) {  // W as [G][taps][C/G / 32][F/G][32]
+      a.b_one = 1;
+      const uint64_t taps = static_cast<uint64_t>(g.kh) * g.kw;
+      const uint64_t dims[5] = {32, static_cast<uint64_t>(g.Fg()),
+                                static_cast<uint64_t>(g.Cgs() / 32), taps,
+                                static_cast<uint64_t>(g.G)};
+      const uint64_t str[4] = {static_cast<uint64_t>(g.Kp()) * 4, 128,
+                               static_cast<uint64_t>(g.Cgs()) * 4,
+                               static_cast<uint64_t>(g.Fg()) * g.Kp() * 4};
+      const uint32_t box[5] = {32, static_cast<uint32_t>(kblk),
+                               static_cast<uint32_t>((a.b_cols + 31) / 32), 1, 1};
+      mb = make_map(w, 5, dims, str, box, kMnSwizzle);
     } else {
       const uint64_t dims[4] = {static_cast<uint64_t>(g.Cgs()),
                                 static_cast<uint64_t>(g.kh) * g.kw, static_cast<uint64_t>(g.Fg()),
@@ -834,13 +867,21 @@ void tc_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, flo
   finish_args(a, kblk, sm_count());
   a.out = dw;
   CUtensorMap ma, mb;
+  const bool a_one = one_box_enabled() && a.a_mode == A_2D_MN && g.F % 32 == 0 &&
+                     a.a_c_g % 32 == 0;
+  a.a_one = a_one;
   if (a.b_mode == B_TAPS_IM2COL) {
-    ma = map_2d(dy, static_cast<long long>(g.n) * g.OH * g.OW, g.F, 32, kblk, kMnSwizzle);
+    const long long pixels = static_cast<long long>(g.n) * g.OH * g.OW;
+    ma = a_one ? map_mn_chunks(dy, pixels, g.F, kblk, a.a_chunks)
+               : map_2d(dy, pixels, g.F, 32, kblk, kMnSwizzle);
     mb = map_nhwc_im2col(x, g.n, g.H, g.W, g.cs_in, 32, kblk, a.im_lw, a.im_lh,
                          g.pw - (g.kw - 1), g.ph - (g.kh - 1), kMnSwizzle);
   } else if (a.a_mode == A_2D_MN) {
-    ma = map_2d(dy, g.n, g.F, 32, kblk, kMnSwizzle);
-    mb = map_2d(x, g.n, g.cs_in, 32, kblk, kMnSwizzle);
+    ma = a_one ? map_mn_chunks(dy, g.n, g.F, kblk, a.a_chunks)
+               : map_2d(dy, g.n, g.F, 32, kblk, kMnSwizzle);
+    a.b_one = one_box_enabled() && g.cs_in % 32 == 0 && a.n_tile % 32 == 0 && a.b_cols % 32 == 0;
+    mb = a.b_one ? map_mn_chunks(x, g.n, g.cs_in, kblk, (a.b_cols + 31) / 32)
+                 : map_2d(x, g.n, g.cs_in, 32, kblk, kMnSwizzle);
   } else {
     ma = map_nhwc(dy, g.n, g.OH, g.OW, g.F, 32, a.wk, a.rk, kMnSwizzle);
     mb = map_nhwc(x, g.n, g.H, g.W, g.cs_in, 32, a.wk, a.rk, kMnSwizzle);

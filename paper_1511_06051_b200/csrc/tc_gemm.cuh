@@ -83,6 +83,17 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
     PSG_TMA_ASM("4d", "", "{%2, %3, %4, %5}", "%6", "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2),
                 "r"(c3), "r"(bar));
 }
+template <bool PAIR = false>
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if constexpr (PAIR)
+    PSG_TMA_ASM("5d", ".cta_group::2", "{%2, %3, %4, %5, %6}", "%7", "r"(dst), "l"(m), "r"(c0),
+                "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar));
+  else
+    PSG_TMA_ASM("5d", "", "{%2, %3, %4, %5, %6}", "%7", "r"(dst), "l"(m), "r"(c0), "r"(c1),
+                "r"(c2), "r"(c3), "r"(c4), "r"(bar));
+}
 #undef PSG_TMA_ASM
 // im2col mode (4-D NHWC map from cuTensorMapEncodeIm2col): {c, w, h, n} is the first
 // pixel's traversal position inside the map's bounding box, {off_w, off_h} the filter tap;

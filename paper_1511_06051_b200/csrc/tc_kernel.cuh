@@ -75,6 +75,10 @@ struct TcArgs {
   // producer cursor jump over the other producers' stages: D = (producers - 1) * kps K
   // blocks split into the cursors' mixed-radix digits (host-computed, no divisions per stage)
   int adv_kb, adv_c0, adv_tap, adv_tv, adv_tu, adv_w, adv_h, adv_b;
+  // MN-major operand tiles as ONE TMA box (map viewed as [chunks][rows][32 floats]: the
+  // 32-column chunks stacked in smem exactly as the per-chunk boxes would land) instead of
+  // one box per 32-column chunk — TMA issue cost is per box
+  int a_one, b_one;
   int m_units;            // M work units: m_tiles, or ceil(m_tiles / 2) for pairs
   int b_cols;             // B columns (N) loaded per CTA: n_tile, or n_tile / 2 for pairs
   // A_IM2COL_K: M = linear pixels (b, y, x) of an out_h x out_w traversal grid; a tile's
@@ -235,6 +239,10 @@ __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, 
                               c.kow, c.koh, c.kbi);
       break;
     case A_2D_MN:
+      if (p.a_one) {
+        tc::tma_load_3d<PAIR>(sa, map, bar, 0, c.kb * KBLK, (p.a_c_g * t.g + t.m * kTileM) / 32);
+        break;
+      }
       for (int j = 0; j < p.a_chunks; ++j)
         tc::tma_load_2d<PAIR>(sa + j * KBLK * 128, map, bar, p.a_c_g * t.g + t.m * kTileM + 32 * j,
                               c.kb * KBLK);
@@ -253,6 +261,10 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
       tc::tma_load_2d<PAIR>(sb, map, bar, c.kb * KBLK, p.b_r_g * t.g + n0);
       break;
     case B_WT_MN:  // W viewed as [G][F/G][taps][C/G]: filter blocks past F/G read as 0
+      if (p.b_one) {  // [G][taps][C/G / 32][F/G][32]
+        tc::tma_load_5d<PAIR>(sb, map, bar, 0, c.t0 * KBLK, n0 / 32, c.t1, t.g);
+        break;
+      }
       for (int j = 0; j < nch; ++j)
         tc::tma_load_4d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.t1, c.t0 * KBLK, t.g);
       break;
@@ -265,6 +277,10 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
                               c.kow + v - p.pw, c.koh + u - p.ph, c.kbi);
       break;
     case B_2D_MN:
+      if (p.b_one) {
+        tc::tma_load_3d<PAIR>(sb, map, bar, 0, c.kb * KBLK, n0 / 32);
+        break;
+      }
       for (int j = 0; j < nch; ++j)
         tc::tma_load_2d<PAIR>(sb + j * KBLK * 128, map, bar, n0 + 32 * j, c.kb * KBLK);
       break;
