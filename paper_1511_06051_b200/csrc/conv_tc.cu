@@ -272,6 +272,11 @@ bool want_pair(const TcArgs& a) {
   if (!env) return false;
   if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K && a.a_mode != A_IM2COL_K) return false;
   if (a.m_tiles < 2) return false;
+  static const int min_n = [] {  // narrow tiles: the pair's B half is too thin to pay off
+    const char* e = std::getenv("PSG_TC_PAIR_MIN_N");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (a.n_tile < min_n) return false;
   // small GEMMs: halving the number of work units costs more in load balance than the
   // pair gains (cifar10_quick); want >= 2 waves of clusters
   const long long units = static_cast<long long>((a.m_tiles + 1) / 2) * a.n_tiles * a.G * a.taps;
@@ -416,10 +421,18 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     cfg.numAttrs = na;
     PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, a));
   };
-  if (kblk == 32)
-    a.pair ? go(tc_gemm_kernel<32, true>) : go(tc_gemm_kernel<32, false>);
-  else
-    a.pair ? go(tc_gemm_kernel<16, true>) : go(tc_gemm_kernel<16, false>);
+  const bool gen = a.mask || a.accumulate || a.cpt;  // see tc_gemm_kernel's GEN
+  if (kblk == 32) {
+    if (gen)
+      a.pair ? go(tc_gemm_kernel<32, true, true>) : go(tc_gemm_kernel<32, false, true>);
+    else
+      a.pair ? go(tc_gemm_kernel<32, true, false>) : go(tc_gemm_kernel<32, false, false>);
+  } else {
+    if (gen)
+      a.pair ? go(tc_gemm_kernel<16, true, true>) : go(tc_gemm_kernel<16, false, true>);
+    else
+      a.pair ? go(tc_gemm_kernel<16, true, false>) : go(tc_gemm_kernel<16, false, false>);
+  }
   PSG_CUDA(cudaGetLastError());
   if (splits > 1) {
     const int blocks = static_cast<int>(std::min<long long>((out_elems + 255) / 256, 148 * 8));

@@ -309,7 +309,10 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
   }
 }
 
-template <int KBLK, bool PAIR>
+// GEN = false: the fprop epilogue (bias / ReLU / split-K partials) compiled without the
+// dgrad / wgrad operands (ReLU mask, accumulate, multi-tap column map), which cost the
+// narrow-N fprops registers and time; GEN = true: every epilogue feature.
+template <int KBLK, bool PAIR, bool GEN>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const TcArgs p) {
@@ -521,7 +524,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // go straight to global memory as float4 runs of the thread's row (no smem
       // transpose); bias / ReLU / accumulate applied in registers.
       const int c_end = __any_sync(0xffffffffu, row_ok) ? p.n_tile : 0;  // idle rows: skip
-      const bool acc_out = p.accumulate && !p.ws;
+      const bool acc_out = GEN && p.accumulate && !p.ws;
+      const float* mask = GEN ? p.mask : nullptr;
+      const int cpt = p.cpt;  // wgrad multi-tap column map (GEN only)
       float* rowp = base + row_off;
       uint32_t va[32], vb[32];
       if (c_end > 0) {
@@ -535,13 +540,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // chunk are loaded before any store, so the loads overlap instead of each waiting
         // behind the previous store (out / mask may alias as far as the compiler knows)
         float4 pre_m[8], pre_o[8];
-        const bool vec_pre = row_ok && p.epi_vec && !p.cpt && !p.ws;
-        if (vec_pre && (p.mask || acc_out)) {
+#ifdef PSG_EPI_NO_PRELOAD
+        const bool vec_pre = false;
+#else
+        const bool vec_pre = GEN && row_ok && p.epi_vec && !cpt && !p.ws;
+#endif
+        if (vec_pre && (mask || acc_out)) {
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
             const int c = c0 + 4 * q4;
             if (c >= nvalid) continue;
-            if (p.mask) pre_m[q4] = __ldg(reinterpret_cast<const float4*>(p.mask + row_off + col0 + c));
+            if (mask) pre_m[q4] = __ldg(reinterpret_cast<const float4*>(mask + row_off + col0 + c));
             if (acc_out) pre_o[q4] = *reinterpret_cast<const float4*>(rowp + col0 + c);
           }
         }
@@ -551,8 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int c = c0 + 4 * q4;  // column within the tile
             int cidx;
             bool ok;
-            if (p.cpt) {
-              const int vc = t.n * p.n_tile + c, tap = vc / p.cpt, cc = vc % p.cpt;
+            if (GEN && cpt) {
+              const int vc = t.n * p.n_tile + c, tap = vc / cpt, cc = vc % cpt;
               ok = c < p.n_tile && tap < p.ntaps && cc < p.cgs;
               cidx = tap * p.cgs + cc;
             } else {
@@ -575,9 +584,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     y.w = y.w > 0.f ? y.w : 0.f;
                   }
                 }
-                if (p.mask) {
+                if (mask) {
                   const float4 m = vec_pre ? pre_m[q4]
-                                           : *reinterpret_cast<const float4*>(p.mask + row_off + cidx);
+                                           : *reinterpret_cast<const float4*>(mask + row_off + cidx);
                   y.x = m.x > 0.f ? y.x : 0.f;
                   y.y = m.y > 0.f ? y.y : 0.f;
                   y.z = m.z > 0.f ? y.z : 0.f;
@@ -595,8 +604,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int e = 0; e < 4; ++e) {
                 int ce;
                 bool oke;
-                if (p.cpt) {
-                  const int vc = t.n * p.n_tile + c + e, tap = vc / p.cpt, cc = vc % p.cpt;
+                if (GEN && cpt) {
+                  const int vc = t.n * p.n_tile + c + e, tap = vc / cpt, cc = vc % cpt;
                   oke = c + e < p.n_tile && tap < p.ntaps && cc < p.cgs;
                   ce = tap * p.cgs + cc;
                 } else {
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     yv += bsh[c + e];
                     if (p.relu) yv = yv > 0.f ? yv : 0.f;
                   }
-                  if (p.mask && !(p.mask[row_off + ce] > 0.f)) yv = 0.f;
+                  if (mask && !(mask[row_off + ce] > 0.f)) yv = 0.f;
                   if (acc_out) yv += rowp[ce];
                 }
                 rowp[ce] = yv;
