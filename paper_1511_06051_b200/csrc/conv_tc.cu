@@ -421,17 +421,20 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     cfg.numAttrs = na;
     PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, a));
   };
-  const bool gen = a.mask || a.accumulate || a.cpt;  // see tc_gemm_kernel's GEN
+  // tc_gemm_kernel's EPI: wgrad (multi-tap column map), dgrad (mask / accumulate), fprop
+  const int epi = a.cpt ? 2 : (a.mask || a.accumulate) ? 1 : 0;
+  if (a.cpt && (a.mask || a.accumulate)) throw std::logic_error("tc: wgrad epilogue with dgrad operands");
+  auto pick = [&](auto k0, auto k1, auto k2) { epi == 0 ? go(k0) : epi == 1 ? go(k1) : go(k2); };
   if (kblk == 32) {
-    if (gen)
-      a.pair ? go(tc_gemm_kernel<32, true, true>) : go(tc_gemm_kernel<32, false, true>);
+    if (a.pair)
+      pick(tc_gemm_kernel<32, true, 0>, tc_gemm_kernel<32, true, 1>, tc_gemm_kernel<32, true, 2>);
     else
-      a.pair ? go(tc_gemm_kernel<32, true, false>) : go(tc_gemm_kernel<32, false, false>);
+      pick(tc_gemm_kernel<32, false, 0>, tc_gemm_kernel<32, false, 1>, tc_gemm_kernel<32, false, 2>);
   } else {
-    if (gen)
-      a.pair ? go(tc_gemm_kernel<16, true, true>) : go(tc_gemm_kernel<16, false, true>);
+    if (a.pair)
+      pick(tc_gemm_kernel<16, true, 0>, tc_gemm_kernel<16, true, 1>, tc_gemm_kernel<16, true, 2>);
     else
-      a.pair ? go(tc_gemm_kernel<16, true, false>) : go(tc_gemm_kernel<16, false, false>);
+      pick(tc_gemm_kernel<16, false, 0>, tc_gemm_kernel<16, false, 1>, tc_gemm_kernel<16, false, 2>);
   }
   PSG_CUDA(cudaGetLastError());
   if (splits > 1) {

@@ -280,42 +280,76 @@ void softmax_loss(const float* logits, const int32_t* labels, int n, int C, doub
 }
 
 namespace {
-__global__ void concat_copy_k(const float* __restrict__ in, int ci, float* __restrict__ out,
-                              int ctot, int off, size_t total) {
+// Concat copies over (pixel, channel-vector) with 32-bit index math; V = float4 when every
+// channel count / offset is a multiple of 4 (GoogLeNet), else float.
+__device__ __forceinline__ float relu_gate(float m, float v) { return m > 0.f ? v : 0.f; }
+__device__ __forceinline__ float4 relu_gate(float4 m, float4 v) {
+  return make_float4(relu_gate(m.x, v.x), relu_gate(m.y, v.y), relu_gate(m.z, v.z),
+                     relu_gate(m.w, v.w));
+}
+__device__ __forceinline__ float4 operator+(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+template <typename V>
+__global__ void concat_copy_k(const V* __restrict__ in, int ci, V* __restrict__ out, int ctot,
+                              int off, uint32_t total) {
   pdl_enter();
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t p = i / ci, c = i % ci;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t p = i / ci, c = i - p * ci;
     out[p * ctot + off + c] = in[i];
   }
 }
-__global__ void concat_split_k(const float* __restrict__ dy, int ctot, int off,
-                               float* __restrict__ dx, int ci, size_t total, int accumulate) {
+// dx (+)= dy[:, off : off + ci]; with `mask` (a folded ReLU backward) dx (+)= mask > 0 ? . : 0
+template <typename V>
+__global__ void concat_split_k(const V* __restrict__ dy, int ctot, int off, V* __restrict__ dx,
+                               int ci, uint32_t total, int accumulate, const V* __restrict__ mask) {
   pdl_enter();
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t p = i / ci, c = i % ci;
-    const float v = dy[p * ctot + off + c];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t p = i / ci, c = i - p * ci;
+    V v = dy[p * ctot + off + c];
+    if (mask) v = relu_gate(__ldg(mask + i), v);
     dx[i] = accumulate ? dx[i] + v : v;
   }
 }
 unsigned concat_blocks(size_t total) {
   return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((total + 255) / 256, 148 * 16)));
 }
+uint32_t concat_total(size_t pixels, int ctot) {
+  if (pixels * static_cast<size_t>(ctot) >= (1ULL << 31))
+    throw std::invalid_argument("concat: tensor too large");
+  return static_cast<uint32_t>(pixels * static_cast<size_t>(ctot));
+}
 }  // namespace
 
 void concat_copy(const float* in, int ci, float* out, int ctot, int off, size_t pixels,
                  cudaStream_t s) {
-  const size_t total = pixels * ci;
-  launch_k(concat_copy_k, concat_blocks(total), 256, 0, s, in, ci, out, ctot, off, total);
+  concat_total(pixels, ctot);
+  if (ci % 4 == 0 && ctot % 4 == 0 && off % 4 == 0) {
+    const uint32_t total = static_cast<uint32_t>(pixels * ci / 4);
+    launch_k(concat_copy_k<float4>, concat_blocks(total), 256, 0, s,
+             reinterpret_cast<const float4*>(in), ci / 4, reinterpret_cast<float4*>(out), ctot / 4,
+             off / 4, total);
+  } else {
+    const uint32_t total = static_cast<uint32_t>(pixels * ci);
+    launch_k(concat_copy_k<float>, concat_blocks(total), 256, 0, s, in, ci, out, ctot, off, total);
+  }
   PSG_CUDA(cudaGetLastError());
 }
 
 void concat_split(const float* dy, int ctot, int off, float* dx, int ci, size_t pixels,
-                  bool accumulate, cudaStream_t s) {
-  const size_t total = pixels * ci;
-  launch_k(concat_split_k, concat_blocks(total), 256, 0, s, dy, ctot, off, dx, ci, total,
-                                                       accumulate ? 1 : 0);
+                  bool accumulate, cudaStream_t s, const float* relu_mask) {
+  concat_total(pixels, ctot);
+  if (ci % 4 == 0 && ctot % 4 == 0 && off % 4 == 0) {
+    const uint32_t total = static_cast<uint32_t>(pixels * ci / 4);
+    launch_k(concat_split_k<float4>, concat_blocks(total), 256, 0, s,
+             reinterpret_cast<const float4*>(dy), ctot / 4, off / 4, reinterpret_cast<float4*>(dx),
+             ci / 4, total, accumulate ? 1 : 0, reinterpret_cast<const float4*>(relu_mask));
+  } else {
+    const uint32_t total = static_cast<uint32_t>(pixels * ci);
+    launch_k(concat_split_k<float>, concat_blocks(total), 256, 0, s, dy, ctot, off, dx, ci, total,
+             accumulate ? 1 : 0, relu_mask);
+  }
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -193,13 +193,20 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
 namespace {
 // Fusion: the ReLU whose backward the layer `c` (its only consumer) can fold into its own
 // input-gradient pass (a tensor-core dgrad epilogue or the max/ave pool backward), else -1.
-int foldable_relu(const psg_net* net, const LayerRt& c) {
-  if (!net->fuse || c.inputs.size() != 1) return -1;
-  const int ri = c.inputs[0];
+// Input `ri` of a layer, when it is a ReLU whose backward that layer (its only consumer)
+// may fold in, else -1.
+int foldable_relu_input(const psg_net* net, int ri) {
   const LayerRt& r = net->L[ri];
-  if (r.kind != PSG_LAYER_RELU || r.bwd_by >= 0 || r.consumers.size() != 1 ||
+  if (!net->fuse || r.kind != PSG_LAYER_RELU || r.bwd_by >= 0 || r.consumers.size() != 1 ||
       net->L[r.inputs[0]].kind == PSG_LAYER_DATA)
     return -1;
+  return ri;
+}
+
+int foldable_relu(const psg_net* net, const LayerRt& c) {
+  if (!net->fuse || c.inputs.size() != 1) return -1;
+  const int ri = foldable_relu_input(net, c.inputs[0]);
+  if (ri < 0) return -1;
   if (c.kind == PSG_LAYER_POOL) return ri;
   if ((c.kind == PSG_LAYER_CONV || c.kind == PSG_LAYER_LINEAR) && net->mode == Mode::Tf32 &&
       conv_dgrad_masks(c.cg, net->mode))
@@ -227,7 +234,16 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
         const int in = l.inputs[i];
         LayerRt& x = net->L[in];
         if (x.kind == PSG_LAYER_DATA) continue;
-        concat_split(l.grad, l.C, l.coff[i], x.grad, x.C, pixels, written[in] != 0, s);
+        const int ri = foldable_relu_input(net, in);
+        if (ri >= 0) {  // the branch's ReLU backward folded into the split (mask by its output)
+          const int pi2 = net->L[ri].inputs[0];
+          concat_split(l.grad, l.C, l.coff[i], net->L[pi2].grad, x.C, pixels,
+                       written[pi2] != 0, s, x.out);
+          written[pi2] = 1;
+          relu_folded[ri] = 1;
+        } else {
+          concat_split(l.grad, l.C, l.coff[i], x.grad, x.C, pixels, written[in] != 0, s);
+        }
         written[in] = 1;
         ++c;
       }

@@ -201,8 +201,9 @@ void softmax_loss(const float* logits, const int32_t* labels, int n, int C, doub
 // dx_i[pix][c] (+)= dy[pix][off_i + c].
 void concat_copy(const float* in, int ci, float* out, int ctot, int off, size_t pixels,
                  cudaStream_t s);
+// relu_mask: a folded ReLU backward (dx (+)= relu_mask > 0 ? dy slice : 0)
 void concat_split(const float* dy, int ctot, int off, float* dx, int ci, size_t pixels,
-                  bool accumulate, cudaStream_t s);
+                  bool accumulate, cudaStream_t s, const float* relu_mask = nullptr);
 void argmax_count(const float* probs, const int32_t* labels, int n, int C,
                   unsigned long long* correct, cudaStream_t s);
 

@@ -309,10 +309,10 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
   }
 }
 
-// GEN = false: the fprop epilogue (bias / ReLU / split-K partials) compiled without the
-// dgrad / wgrad operands (ReLU mask, accumulate, multi-tap column map), which cost the
-// narrow-N fprops registers and time; GEN = true: every epilogue feature.
-template <int KBLK, bool PAIR, bool GEN>
+// EPI selects the epilogue features compiled in (each costs registers and time even when
+// unused): 0 = fprop (bias / ReLU / split-K partials), 1 = dgrad (+ ReLU mask, accumulate),
+// 2 = wgrad (+ multi-tap column map).
+template <int KBLK, bool PAIR, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const TcArgs p) {
@@ -524,9 +524,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // go straight to global memory as float4 runs of the thread's row (no smem
       // transpose); bias / ReLU / accumulate applied in registers.
       const int c_end = __any_sync(0xffffffffu, row_ok) ? p.n_tile : 0;  // idle rows: skip
-      const bool acc_out = GEN && p.accumulate && !p.ws;
-      const float* mask = GEN ? p.mask : nullptr;
-      const int cpt = p.cpt;  // wgrad multi-tap column map (GEN only)
+      constexpr bool DG = EPI == 1, WG = EPI == 2;
+      const bool acc_out = DG && p.accumulate && !p.ws;
+      const float* mask = DG ? p.mask : nullptr;
+      const int cpt = p.cpt;  // wgrad multi-tap column map (WG only)
       float* rowp = base + row_off;
       uint32_t va[32], vb[32];
       if (c_end > 0) {
@@ -539,19 +540,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         // operands the epilogue reads (ReLU mask, accumulated output): all 8 float4 of the
         // chunk are loaded before any store, so the loads overlap instead of each waiting
         // behind the previous store (out / mask may alias as far as the compiler knows)
-        float4 pre_m[8], pre_o[8];
+        float4 pre[8];  // the ReLU mask, else the accumulated output
 #ifdef PSG_EPI_NO_PRELOAD
         const bool vec_pre = false;
 #else
-        const bool vec_pre = GEN && row_ok && p.epi_vec && !cpt && !p.ws;
+        const bool vec_pre = DG && row_ok && p.epi_vec && !p.ws;
 #endif
         if (vec_pre && (mask || acc_out)) {
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
             const int c = c0 + 4 * q4;
             if (c >= nvalid) continue;
-            if (mask) pre_m[q4] = __ldg(reinterpret_cast<const float4*>(mask + row_off + col0 + c));
-            if (acc_out) pre_o[q4] = *reinterpret_cast<const float4*>(rowp + col0 + c);
+            pre[q4] = mask ? __ldg(reinterpret_cast<const float4*>(mask + row_off + col0 + c))
+                           : *reinterpret_cast<const float4*>(rowp + col0 + c);
           }
         }
         if (row_ok) {
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int c = c0 + 4 * q4;  // column within the tile
             int cidx;
             bool ok;
-            if (GEN && cpt) {
+            if (WG && cpt) {
               const int vc = t.n * p.n_tile + c, tap = vc / cpt, cc = vc % cpt;
               ok = c < p.n_tile && tap < p.ntaps && cc < p.cgs;
               cidx = tap * p.cgs + cc;
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   }
                 }
                 if (mask) {
-                  const float4 m = vec_pre ? pre_m[q4]
+                  const float4 m = vec_pre ? pre[q4]
                                            : *reinterpret_cast<const float4*>(mask + row_off + cidx);
                   y.x = m.x > 0.f ? y.x : 0.f;
                   y.y = m.y > 0.f ? y.y : 0.f;
@@ -593,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   y.w = m.w > 0.f ? y.w : 0.f;
                 }
                 if (acc_out) {
-                  const float4 o = vec_pre ? pre_o[q4] : *dst;
+                  const float4 o = vec_pre && !mask ? pre[q4] : *dst;
                   y.x += o.x; y.y += o.y; y.z += o.z; y.w += o.w;
                 }
               }
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int e = 0; e < 4; ++e) {
                 int ce;
                 bool oke;
-                if (GEN && cpt) {
+                if (WG && cpt) {
                   const int vc = t.n * p.n_tile + c + e, tap = vc / cpt, cc = vc % cpt;
                   oke = c + e < p.n_tile && tap < p.ntaps && cc < p.cgs;
                   ce = tap * p.cgs + cc;

@@ -299,14 +299,25 @@ def test_max_pool_tie_routes_to_lowest_index(gpu):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
-@pytest.mark.parametrize("name", ["cifar10_quick", "caffe_mix", "s2d"])
+def _inception_net(b):
+    """One small inception block (GoogLeNet-style branches, ReLUs feeding a concat)."""
+    layers = [ns.data_layer("data", b, 3, 12, 12), ns.label_layer("label", b),
+              ns.conv_layer("c0", "data", 3, 3, 16, pad=1), ns.relu_layer("r0", "c0")]
+    ns._inception(layers, "inc", "r0", 8, 8, 16, 4, 8, 8, {})
+    layers += [ns.pool_layer("p", "inc/output", 3, 3, 2, 2),
+               ns.linear_layer("out", "p", 10), ns.softmax_loss_layer("loss", "out", "label")]
+    return ns.NetSpec(layers)
+
+
+@pytest.mark.parametrize("name", ["cifar10_quick", "caffe_mix", "s2d", "inception"])
 def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
     """psg_net_set_fusion: the ReLU applied in the GEMM epilogue, the ReLU backward folded
     into the LRN, the LRN computed inside the following max pool and the batch gathered
     straight into the space-to-depth input give bitwise-identical training to the unfused
     graph."""
     from paper_1511_06051_b200 import data
-    spec = _s2d_net(6) if name == "s2d" else micro_nets()[name]
+    spec = (_s2d_net(6) if name == "s2d" else _inception_net(6) if name == "inception"
+            else micro_nets()[name])
     d = spec.data_spec().shape
     img, lab = oracle_lib.generate_synthetic(10, d[1], d[2], d[3], 6, 2.0, 12345, 0)
     ds = data.Dataset(f32(img), lab % 5 if name == "caffe_mix" else lab,
