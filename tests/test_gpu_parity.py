@@ -298,7 +298,6 @@ def test_max_pool_tie_routes_to_lowest_index(gpu):
     np.testing.assert_allclose(dk, [dpool * 1.0, dpool * 2.0], rtol=STRICT)
 
 
-@pytest.mark.parametrize("precision", ["fp32", "tf32"])
 def _inception_net(b):
     """One small inception block (GoogLeNet-style branches, ReLUs feeding a concat)."""
     layers = [ns.data_layer("data", b, 3, 12, 12), ns.label_layer("label", b),
@@ -309,12 +308,13 @@ def _inception_net(b):
     return ns.NetSpec(layers)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
 @pytest.mark.parametrize("name", ["cifar10_quick", "caffe_mix", "s2d", "inception"])
 def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
-    """psg_net_set_fusion: the ReLU applied in the GEMM epilogue, the ReLU backward folded
-    into the LRN, the LRN computed inside the following max pool and the batch gathered
-    straight into the space-to-depth input give bitwise-identical training to the unfused
-    graph."""
+    """psg_net_set_fusion: the ReLU applied in the GEMM epilogue, ReLU backwards folded into
+    the consuming LRN / dgrad epilogue / pool backward / concat split, the LRN computed inside
+    the following max pool and the batch gathered straight into the space-to-depth input
+    give bitwise-identical training to the unfused graph."""
     from paper_1511_06051_b200 import data
     spec = (_s2d_net(6) if name == "s2d" else _inception_net(6) if name == "inception"
             else micro_nets()[name])
