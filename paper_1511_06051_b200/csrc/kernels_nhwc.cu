@@ -527,6 +527,117 @@ __global__ void __launch_bounds__(256) lrn_maxpool_fwd_k(LrnGeom lg, PoolGeom g,
   }
 }
 
+// Backward of the fused pair: thread = (LRN input pixel, 8-channel run) with the runs of a
+// pixel on consecutive lanes of one warp (lp = runs rounded up to a power of two lanes per
+// pixel), so the LRN window halos (x at c0-4 .. c0-1 / c0+8 .. c0+11, and the st / sp
+// terms of channels c0-2, c0-1, c0+8, c0+9) come from the neighbouring lanes by shuffles;
+// each lane gathers the pool gradient of its own 8 channels only, from the covering
+// windows in ascending (oh, ow) order (pool_bwd_k's sum), and evaluates lrn_bwd_run_k's
+// arithmetic unchanged — bitwise the unfused pool backward + LRN backward.
+template <int NW>
+__global__ void __launch_bounds__(256) lrn_maxpool_bwd_k(LrnGeom lg, PoolGeom g,
+                                                         const float* __restrict__ x,
+                                                         const float* __restrict__ dpool,
+                                                         const uint8_t* __restrict__ route,
+                                                         float* __restrict__ dx, int accumulate,
+                                                         int relu_mask, int lp, uint32_t pixels) {
+  pdl_enter();
+  const int C = g.C, runs = C / kLrnRun, ppw = 32 / lp;
+  const float a = lg.alpha / lg.size, ratio = 2.f * lg.alpha * lg.beta / lg.size;
+  const int lane = threadIdx.x & 31, grp = lane / lp, run = lane % lp, c0 = run * kLrnRun;
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / 32; w * ppw < pixels; w += warps) {
+    const uint32_t pix = w * ppw + grp;  // warp-uniform loop: every lane reaches the shuffles
+    const bool act = run < runs && pix < pixels;
+    float v[kLrnRun], d[kLrnRun];
+#pragma unroll
+    for (int i = 0; i < kLrnRun; ++i) v[i] = d[i] = 0.f;
+    size_t base = 0;
+    if (act) {
+      base = static_cast<size_t>(pix) * C + c0;
+      lrn_put4(v, __ldg(reinterpret_cast<const float4*>(x + base)));
+      lrn_put4(v + 4, __ldg(reinterpret_cast<const float4*>(x + base + 4)));
+      const int wq = static_cast<int>(pix % g.W);
+      const uint32_t t = pix / g.W;
+      const int h = static_cast<int>(t % g.H), b = static_cast<int>(t / g.H);
+      const int ohl = max(0, (h + g.ph - g.kh + g.sh) / g.sh);
+      const int ohh = min(g.OH - 1, (h + g.ph) / g.sh);
+      const int owl = max(0, (wq + g.pw - g.kw + g.sw) / g.sw);
+      const int owh = min(g.OW - 1, (wq + g.pw) / g.sw);
+#pragma unroll
+      for (int i = 0; i < NW; ++i)
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+          const int oh = ohl + i, ow = owl + q;
+          const int hs0 = oh * g.sh - g.ph, ws0 = ow * g.sw - g.pw;
+          if (oh > ohh || ow > owh || h < hs0 || h >= hs0 + g.kh || wq < ws0 || wq >= ws0 + g.kw)
+            continue;
+          const uint8_t want = static_cast<uint8_t>((h - hs0) * g.kw + (wq - ws0));
+          const size_t ob = (static_cast<size_t>(b * g.OH + oh) * g.OW + ow) * C + c0;
+          const float4 d0 = __ldg(reinterpret_cast<const float4*>(dpool + ob));
+          const float4 d1 = __ldg(reinterpret_cast<const float4*>(dpool + ob + 4));
+          const uint2 rr = __ldg(reinterpret_cast<const uint2*>(route + ob));
+          const float dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t r8 = ((e < 4 ? rr.x : rr.y) >> (8 * (e & 3))) & 0xffu;
+            if (r8 == want) d[e] += dd[e];
+          }
+        }
+    }
+    // x at channels c0-4 .. c0+11 (neighbour lanes; zero outside [0, C))
+    float xw[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float l = __shfl_up_sync(0xffffffffu, v[4 + k], 1);
+      const float r = __shfl_down_sync(0xffffffffu, v[k], 1);
+      xw[k] = run > 0 ? l : 0.f;
+      xw[12 + k] = run + 1 < runs ? r : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < kLrnRun; ++i) xw[4 + i] = v[i];
+    float st[kLrnRun], sp[kLrnRun];
+#pragma unroll
+    for (int i = 0; i < kLrnRun; ++i) {  // channel c0 + i = xw[i + 4]; window xw[i+2 .. i+6]
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc += xw[i + 2 + q] * xw[i + 2 + q];
+      const float sc = lg.k + a * acc;
+      sp[i] = lrn_pow(sc, lg.beta);
+      st[i] = d[i] * v[i] * sp[i] * __frcp_rn(sc);
+    }
+    // st at channels c0-2 .. c0+9
+    float sw[12];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float l = __shfl_up_sync(0xffffffffu, st[6 + k], 1);
+      const float r = __shfl_down_sync(0xffffffffu, st[k], 1);
+      sw[k] = run > 0 ? l : 0.f;
+      sw[10 + k] = run + 1 < runs ? r : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < kLrnRun; ++i) sw[2 + i] = st[i];
+    if (!act) continue;
+    float out[kLrnRun];
+#pragma unroll
+    for (int i = 0; i < kLrnRun; ++i) {  // channels whose window holds c0 + i: sw[i .. i+4]
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc += sw[i + q];
+      out[i] = d[i] * sp[i] - ratio * v[i] * acc;
+      if (relu_mask && !(v[i] > 0.f)) out[i] = 0.f;
+    }
+    float4* dst = reinterpret_cast<float4*>(dx + base);
+    if (accumulate) {
+      const float4 o0 = dst[0], o1 = dst[1];
+      out[0] += o0.x; out[1] += o0.y; out[2] += o0.z; out[3] += o0.w;
+      out[4] += o1.x; out[5] += o1.y; out[6] += o1.z; out[7] += o1.w;
+    }
+    dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+    dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+  }
+}
+
 // --------------------------------------------------------------- dropout ---
 // Keep-mask = splitmix64(mix(base ^ step) + nchw_index) >> 40 >= ratio * 2^24.
 __device__ __forceinline__ float drop_mask(const DropGeom& g, uint64_t base, uint32_t i,
@@ -739,7 +850,8 @@ void stage_batch_nchw(const float* src, int n, int C, int H, int W, int cs, floa
 }
 
 bool lrn_maxpool_fusable(const LrnGeom& lg, const PoolGeom& pg) {
-  return lg.size == 5 && lg.C % kLrnRun == 0 && pg.C == lg.C && pg.method == PSG_POOL_MAX &&
+  return lg.size == 5 && lg.C % kLrnRun == 0 && lg.C <= 256 && pg.C == lg.C &&
+         pg.method == PSG_POOL_MAX &&
          pg.kh == 3 && pg.kw == 3 && pg.sh == pg.sw && (pg.sh == 1 || pg.sh == 2) &&
          static_cast<size_t>(pg.n) * pg.H * pg.W * pg.C < (1ULL << 31);
 }
@@ -749,6 +861,22 @@ void lrn_maxpool_fwd(const LrnGeom& lg, const PoolGeom& g, const float* x, float
   const uint32_t runs =
       checked32(static_cast<size_t>(g.n) * g.OH * g.OW * (g.C / kLrnRun), "lrn_pool");
   launch_k(lrn_maxpool_fwd_k, grid_for(runs, 256, 148 * 8), 256, 0, s, lg, g, x, y, route, runs);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void lrn_maxpool_bwd(const LrnGeom& lg, const PoolGeom& g, const float* x, const float* dpool,
+                     const uint8_t* route, float* dx, bool accumulate, bool relu_mask,
+                     cudaStream_t s) {
+  const int runs = g.C / kLrnRun;
+  int lp = 1;
+  while (lp < runs) lp <<= 1;
+  if (lp > 32) throw std::invalid_argument("lrn_pool: more than 256 channels");
+  const uint32_t pixels = checked32(static_cast<size_t>(g.n) * g.H * g.W, "lrn_pool");
+  checked32(static_cast<size_t>(pixels) * g.C, "lrn_pool");
+  const size_t warps = (pixels + 32 / lp - 1) / (32 / lp);
+  auto kern = g.sh == 1 ? lrn_maxpool_bwd_k<3> : lrn_maxpool_bwd_k<2>;
+  launch_k(kern, grid_for(warps * 32, 256, 148 * 8), 256, 0, s, lg, g, x, dpool, route, dx,
+           accumulate ? 1 : 0, relu_mask ? 1 : 0, lp, pixels);
   PSG_CUDA(cudaGetLastError());
 }
 

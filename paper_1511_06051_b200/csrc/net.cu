@@ -206,7 +206,7 @@ void ensure_capacity(psg_net* net, size_t n) {
     if (l.kind == PSG_LAYER_LABEL) continue;
     const size_t elems = n * l.vol();
     if (l.fwd_relu < 0 && l.lrn_pool < 0) l.out = dalloc<float>(elems);
-    if (l.kind != PSG_LAYER_DATA) l.grad = dalloc<float>(elems);
+    if (l.kind != PSG_LAYER_DATA && l.lrn_pool < 0) l.grad = dalloc<float>(elems);
     if (l.kind == PSG_LAYER_POOL && l.d.pool == PSG_POOL_MAX) l.route = dalloc<uint8_t>(elems);
     if (l.kind == PSG_LAYER_CONV) l.col = dalloc<float>(conv_col_elems(geom_for(l, n), net->mode));
     if (is_param_layer(l.kind)) {

@@ -291,6 +291,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
         break;
       }
       case PSG_LAYER_POOL:
+        if (l.pool_lrn >= 0) break;  // gathered inside the fused LRN backward
         if (need_dx) {
           PoolGeom g = l.pg;
           g.n = static_cast<int>(n);
@@ -324,12 +325,21 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
           LrnGeom g = l.lg;
           g.pixels = static_cast<int>(n) * l.H * l.W;
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
-          if (l.bwd_relu >= 0) {  // fold the ReLU below: mask by x > 0, write its input grad
+          float* dx = src.grad;  // the ReLU below folded in: mask by x > 0, its input grad
+          bool dacc = acc;
+          if (l.bwd_relu >= 0) {
             const int pi2 = net->L[l.bwd_relu].inputs[0];
-            lrn_bwd(g, src.out, l.grad, net->L[pi2].grad, written[pi2] != 0, s, true);
+            dx = net->L[pi2].grad;
+            dacc = written[pi2] != 0;
             written[pi2] = 1;
+          }
+          if (l.lrn_pool >= 0) {  // the max pool's backward gathered in the same kernel
+            const LayerRt& p = net->L[l.lrn_pool];
+            PoolGeom pg = p.pg;
+            pg.n = static_cast<int>(n);
+            lrn_maxpool_bwd(g, pg, src.out, p.grad, p.route, dx, dacc, l.bwd_relu >= 0, s);
           } else {
-            lrn_bwd(g, src.out, l.grad, src.grad, acc, s);
+            lrn_bwd(g, src.out, l.grad, dx, dacc, s, l.bwd_relu >= 0);
           }
           sc.done(1);
           ++launches;

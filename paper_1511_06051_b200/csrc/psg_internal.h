@@ -180,6 +180,10 @@ void lrn_bwd(const LrnGeom& g, const float* x, const float* dy, float* dx, bool 
 bool lrn_maxpool_fusable(const LrnGeom& lg, const PoolGeom& pg);
 void lrn_maxpool_fwd(const LrnGeom& lg, const PoolGeom& g, const float* x, float* y,
                      uint8_t* route, cudaStream_t s);
+// dx (+)= LRN backward of the pool gradient gathered through `route` (relu_mask as lrn_bwd)
+void lrn_maxpool_bwd(const LrnGeom& lg, const PoolGeom& g, const float* x, const float* dpool,
+                     const uint8_t* route, float* dx, bool accumulate, bool relu_mask,
+                     cudaStream_t s);
 
 struct DropGeom {
   int n = 0, C = 0, H = 1, W = 1;  // logical NCHW dims for the counter index

@@ -60,11 +60,10 @@ struct LayerRt {
   // it); a ReLU whose only consumer is an LRN has its backward folded into the LRN's
   // (bwd_by = that LRN; the LRN masks with its input and writes the ReLU's input grad).
   int fwd_relu = -1, fused_from = -1, bwd_by = -1, bwd_relu = -1;
-  // LRN -> max pool fusion: the forward of an LRN whose only consumer is a fusable 3x3
-  // max pool is computed inside the pool's kernel (lrn_pool = that pool, pool_lrn = the
-  // LRN), so the LRN output is never materialised; the backward stays two kernels (a fused
-  // gather + LRN backward measured slower: it re-gathers each channel's pool gradient for
-  // its neighbours' windows).
+  // LRN -> max pool fusion: an LRN whose only consumer is a fusable 3x3 max pool is
+  // computed inside the pool's kernel (lrn_pool = that pool, pool_lrn = the LRN), and the
+  // pool's backward is gathered inside the LRN backward (lrn_maxpool_bwd), so the LRN output
+  // and gradient are never materialised.
   int lrn_pool = -1, pool_lrn = -1;
   int kern_t = -1, bias_t = -1;
   ConvGeom cg;  // conv / linear (per-example; n filled per call)
