@@ -261,7 +261,7 @@ constexpr int kLrnTileElems = 2048;
 __device__ __forceinline__ float lrn_pow(float s, float beta) {  // s^-beta, s >= k > 0
   float l, r;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(s));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-beta * l));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fmul_rn(-beta, l)));
   return r;
 }
 
@@ -369,6 +369,30 @@ __global__ void __launch_bounds__(kLrnThreads) lrn_bwd_k(LrnGeom g, const float*
 // the neighbouring channels it needs (float4, the neighbours mostly L1 hits) and keeps the
 // window sums in registers (same ascending 5-term sums as the tile kernels).  Channels
 // outside [0, C) read as zero.
+// The streaming LRN kernels (standalone and fused with the max pool) evaluate every
+// channel through these helpers with explicitly rounded operations (no compiler FMA
+// contraction choices), so the fused and unfused paths agree bit for bit.
+__device__ __forceinline__ float lrn_sq5(const float* w) {  // sum of 5 squares, ascending
+  float acc = 0.f;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) acc = __fmaf_rn(w[q], w[q], acc);
+  return acc;
+}
+__device__ __forceinline__ float lrn_sum5(const float* w) {
+  float acc = 0.f;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) acc = __fadd_rn(acc, w[q]);
+  return acc;
+}
+__device__ __forceinline__ float lrn_scale(float k, float a, float sq) { return __fmaf_rn(a, sq, k); }
+// dy * x * s^-beta / s (the term each channel contributes to its neighbours' gradients)
+__device__ __forceinline__ float lrn_st(float d, float x, float sp, float sc) {
+  return __fmul_rn(__fmul_rn(__fmul_rn(d, x), sp), __frcp_rn(sc));
+}
+__device__ __forceinline__ float lrn_dx(float d, float sp, float ratio, float x, float sum_st) {
+  return __fsub_rn(__fmul_rn(d, sp), __fmul_rn(__fmul_rn(ratio, x), sum_st));
+}
+
 constexpr int kLrnRun = 8;
 
 __device__ __forceinline__ float4 lrn_ld4(const float* p, int c, int C) {
@@ -399,10 +423,7 @@ __global__ void __launch_bounds__(256) lrn_fwd_run_k(LrnGeom g, const float* __r
     float out[kLrnRun];
 #pragma unroll
     for (int i = 0; i < kLrnRun; ++i) {  // channel c0 + i = v[i + 4]; window v[i+2 .. i+6]
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) acc += v[i + 2 + q] * v[i + 2 + q];
-      out[i] = v[i + 4] * lrn_pow(g.k + a * acc, g.beta);
+      out[i] = __fmul_rn(v[i + 4], lrn_pow(lrn_scale(g.k, a, lrn_sq5(v + i + 2)), g.beta));
     }
     float4* dst = reinterpret_cast<float4*>(y + static_cast<size_t>(pix) * C + c0);
     dst[0] = make_float4(out[0], out[1], out[2], out[3]);
@@ -431,20 +452,14 @@ __global__ void __launch_bounds__(256) lrn_bwd_run_k(LrnGeom g, const float* __r
     float st[12], sp[12];
 #pragma unroll
     for (int j = 0; j < 12; ++j) {
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) acc += v[j + q] * v[j + q];  // window of channel j + c0 - 2
-      const float sc = g.k + a * acc;
+      const float sc = lrn_scale(g.k, a, lrn_sq5(v + j));  // window of channel j + c0 - 2
       sp[j] = lrn_pow(sc, g.beta);
-      st[j] = d[j + 2] * v[j + 2] * sp[j] * __frcp_rn(sc);  // zero outside [0, C): x = 0
+      st[j] = lrn_st(d[j + 2], v[j + 2], sp[j], sc);  // zero outside [0, C): x = 0
     }
     float out[kLrnRun];
 #pragma unroll
     for (int i = 0; i < kLrnRun; ++i) {  // channels q whose window holds c: [c-2, c+2]
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) acc += st[i + q];
-      out[i] = d[i + 4] * sp[i + 2] - ratio * v[i + 4] * acc;
+      out[i] = lrn_dx(d[i + 4], sp[i + 2], ratio, v[i + 4], lrn_sum5(st + i));
       if (relu_mask && !(v[i + 4] > 0.f)) out[i] = 0.f;
     }
     float4* dst = reinterpret_cast<float4*>(dx + base + c0);
@@ -473,10 +488,7 @@ __device__ __forceinline__ void lrn_run8(const float* xp, int c0, int C, float a
   lrn_put4(v + 12, lrn_ld4(xp, c0 + 8, C));
 #pragma unroll
   for (int i = 0; i < kLrnRun; ++i) {
-    float acc = 0.f;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) acc += v[i + 2 + q] * v[i + 2 + q];
-    out[i] = v[i + 4] * lrn_pow(g.k + a * acc, g.beta);
+    out[i] = __fmul_rn(v[i + 4], lrn_pow(lrn_scale(g.k, a, lrn_sq5(v + i + 2)), g.beta));
   }
 }
 
@@ -527,14 +539,29 @@ __global__ void __launch_bounds__(256) lrn_maxpool_fwd_k(LrnGeom lg, PoolGeom g,
   }
 }
 
-// Backward of the fused pair: thread = (LRN input pixel, 8-channel run) with the runs of a
-// pixel on consecutive lanes of one warp (lp = runs rounded up to a power of two lanes per
-// pixel), so the LRN window halos (x at c0-4 .. c0-1 / c0+8 .. c0+11, and the st / sp
-// terms of channels c0-2, c0-1, c0+8, c0+9) come from the neighbouring lanes by shuffles;
+// Backward of the fused pair: thread = (LRN input pixel, RUN-channel run, RUN = 8 or 6)
+// with the runs of a pixel on consecutive lanes of one warp (lp = runs rounded up to a
+// power of two lanes per pixel), so the LRN window halos (x at c0-4 .. c0-1 /
+// c0+RUN .. c0+RUN+3, and the st terms of c0-2, c0-1, c0+RUN, c0+RUN+1) come from the
+// neighbouring lanes by shuffles;
 // each lane gathers the pool gradient of its own 8 channels only, from the covering
 // windows in ascending (oh, ow) order (pool_bwd_k's sum), and evaluates lrn_bwd_run_k's
 // arithmetic unchanged — bitwise the unfused pool backward + LRN backward.
-template <int NW>
+template <int RUN>  // RUN consecutive channels at p (RUN = 8: float4 x 2, 6: float2 x 3)
+__device__ __forceinline__ void ld_run(const float* p, float* v) {
+  if constexpr (RUN == 8) {
+    lrn_put4(v, __ldg(reinterpret_cast<const float4*>(p)));
+    lrn_put4(v + 4, __ldg(reinterpret_cast<const float4*>(p + 4)));
+  } else {
+#pragma unroll
+    for (int k = 0; k < RUN / 2; ++k) {
+      const float2 q = __ldg(reinterpret_cast<const float2*>(p) + k);
+      v[2 * k] = q.x;
+      v[2 * k + 1] = q.y;
+    }
+  }
+}
+template <int NW, int RUN>
 __global__ void __launch_bounds__(256) lrn_maxpool_bwd_k(LrnGeom lg, PoolGeom g,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ dpool,
@@ -542,21 +569,20 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd_k(LrnGeom lg, PoolGeom g,
                                                          float* __restrict__ dx, int accumulate,
                                                          int relu_mask, int lp, uint32_t pixels) {
   pdl_enter();
-  const int C = g.C, runs = C / kLrnRun, ppw = 32 / lp;
+  const int C = g.C, runs = C / RUN, ppw = 32 / lp;
   const float a = lg.alpha / lg.size, ratio = 2.f * lg.alpha * lg.beta / lg.size;
-  const int lane = threadIdx.x & 31, grp = lane / lp, run = lane % lp, c0 = run * kLrnRun;
+  const int lane = threadIdx.x & 31, grp = lane / lp, run = lane % lp, c0 = run * RUN;
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / 32; w * ppw < pixels; w += warps) {
     const uint32_t pix = w * ppw + grp;  // warp-uniform loop: every lane reaches the shuffles
     const bool act = run < runs && pix < pixels;
-    float v[kLrnRun], d[kLrnRun];
+    float v[RUN], d[RUN];
 #pragma unroll
-    for (int i = 0; i < kLrnRun; ++i) v[i] = d[i] = 0.f;
+    for (int i = 0; i < RUN; ++i) v[i] = d[i] = 0.f;
     size_t base = 0;
     if (act) {
       base = static_cast<size_t>(pix) * C + c0;
-      lrn_put4(v, __ldg(reinterpret_cast<const float4*>(x + base)));
-      lrn_put4(v + 4, __ldg(reinterpret_cast<const float4*>(x + base + 4)));
+      ld_run<RUN>(x + base, v);
       const int wq = static_cast<int>(pix % g.W);
       const uint32_t t = pix / g.W;
       const int h = static_cast<int>(t % g.H), b = static_cast<int>(t / g.H);
@@ -572,69 +598,73 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd_k(LrnGeom lg, PoolGeom g,
           const int hs0 = oh * g.sh - g.ph, ws0 = ow * g.sw - g.pw;
           if (oh > ohh || ow > owh || h < hs0 || h >= hs0 + g.kh || wq < ws0 || wq >= ws0 + g.kw)
             continue;
-          const uint8_t want = static_cast<uint8_t>((h - hs0) * g.kw + (wq - ws0));
+          const uint32_t want = static_cast<uint32_t>((h - hs0) * g.kw + (wq - ws0));
           const size_t ob = (static_cast<size_t>(b * g.OH + oh) * g.OW + ow) * C + c0;
-          const float4 d0 = __ldg(reinterpret_cast<const float4*>(dpool + ob));
-          const float4 d1 = __ldg(reinterpret_cast<const float4*>(dpool + ob + 4));
-          const uint2 rr = __ldg(reinterpret_cast<const uint2*>(route + ob));
-          const float dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint32_t r8 = ((e < 4 ? rr.x : rr.y) >> (8 * (e & 3))) & 0xffu;
-            if (r8 == want) d[e] += dd[e];
+          float dd[RUN];
+          ld_run<RUN>(dpool + ob, dd);
+          uint32_t rr[2];  // RUN route bytes (RUN = 8: 8-byte aligned, 6: 2-byte aligned)
+          if constexpr (RUN == 8) {
+            const uint2 q2 = __ldg(reinterpret_cast<const uint2*>(route + ob));
+            rr[0] = q2.x;
+            rr[1] = q2.y;
+          } else {
+            const uint16_t* r16 = reinterpret_cast<const uint16_t*>(route + ob);
+            rr[0] = __ldg(r16) | (static_cast<uint32_t>(__ldg(r16 + 1)) << 16);
+            rr[1] = __ldg(r16 + 2);
           }
+#pragma unroll
+          for (int e = 0; e < RUN; ++e)
+            if (((rr[e / 4] >> (8 * (e & 3))) & 0xffu) == want) d[e] += dd[e];
         }
     }
-    // x at channels c0-4 .. c0+11 (neighbour lanes; zero outside [0, C))
-    float xw[16];
+    // x at channels c0-4 .. c0+RUN+3 (neighbour lanes; zero outside [0, C))
+    float xw[RUN + 8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float l = __shfl_up_sync(0xffffffffu, v[4 + k], 1);
+      const float l = __shfl_up_sync(0xffffffffu, v[RUN - 4 + k], 1);
       const float r = __shfl_down_sync(0xffffffffu, v[k], 1);
       xw[k] = run > 0 ? l : 0.f;
-      xw[12 + k] = run + 1 < runs ? r : 0.f;
+      xw[RUN + 4 + k] = run + 1 < runs ? r : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < kLrnRun; ++i) xw[4 + i] = v[i];
-    float st[kLrnRun], sp[kLrnRun];
+    for (int i = 0; i < RUN; ++i) xw[4 + i] = v[i];
+    float st[RUN], sp[RUN];
 #pragma unroll
-    for (int i = 0; i < kLrnRun; ++i) {  // channel c0 + i = xw[i + 4]; window xw[i+2 .. i+6]
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) acc += xw[i + 2 + q] * xw[i + 2 + q];
-      const float sc = lg.k + a * acc;
+    for (int i = 0; i < RUN; ++i) {  // channel c0 + i = xw[i + 4]; window xw[i+2 .. i+6]
+      const float sc = lrn_scale(lg.k, a, lrn_sq5(xw + i + 2));
       sp[i] = lrn_pow(sc, lg.beta);
-      st[i] = d[i] * v[i] * sp[i] * __frcp_rn(sc);
+      st[i] = lrn_st(d[i], v[i], sp[i], sc);
     }
-    // st at channels c0-2 .. c0+9
-    float sw[12];
+    // st at channels c0-2 .. c0+RUN+1
+    float sw[RUN + 4];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const float l = __shfl_up_sync(0xffffffffu, st[6 + k], 1);
+      const float l = __shfl_up_sync(0xffffffffu, st[RUN - 2 + k], 1);
       const float r = __shfl_down_sync(0xffffffffu, st[k], 1);
       sw[k] = run > 0 ? l : 0.f;
-      sw[10 + k] = run + 1 < runs ? r : 0.f;
+      sw[RUN + 2 + k] = run + 1 < runs ? r : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < kLrnRun; ++i) sw[2 + i] = st[i];
+    for (int i = 0; i < RUN; ++i) sw[2 + i] = st[i];
     if (!act) continue;
-    float out[kLrnRun];
+    float out[RUN];
 #pragma unroll
-    for (int i = 0; i < kLrnRun; ++i) {  // channels whose window holds c0 + i: sw[i .. i+4]
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) acc += sw[i + q];
-      out[i] = d[i] * sp[i] - ratio * v[i] * acc;
+    for (int i = 0; i < RUN; ++i) {  // channels whose window holds c0 + i: sw[i .. i+4]
+      out[i] = lrn_dx(d[i], sp[i], ratio, v[i], lrn_sum5(sw + i));
       if (relu_mask && !(v[i] > 0.f)) out[i] = 0.f;
     }
-    float4* dst = reinterpret_cast<float4*>(dx + base);
-    if (accumulate) {
-      const float4 o0 = dst[0], o1 = dst[1];
-      out[0] += o0.x; out[1] += o0.y; out[2] += o0.z; out[3] += o0.w;
-      out[4] += o1.x; out[5] += o1.y; out[6] += o1.z; out[7] += o1.w;
+    float* dst = dx + base;
+#pragma unroll
+    for (int k = 0; k < RUN / 2; ++k) {
+      float2 o = make_float2(out[2 * k], out[2 * k + 1]);
+      float2* p2 = reinterpret_cast<float2*>(dst) + k;
+      if (accumulate) {
+        const float2 q = *p2;
+        o.x += q.x;
+        o.y += q.y;
+      }
+      *p2 = o;
     }
-    dst[0] = make_float4(out[0], out[1], out[2], out[3]);
-    dst[1] = make_float4(out[4], out[5], out[6], out[7]);
   }
 }
 
@@ -867,14 +897,23 @@ void lrn_maxpool_fwd(const LrnGeom& lg, const PoolGeom& g, const float* x, float
 void lrn_maxpool_bwd(const LrnGeom& lg, const PoolGeom& g, const float* x, const float* dpool,
                      const uint8_t* route, float* dx, bool accumulate, bool relu_mask,
                      cudaStream_t s) {
-  const int runs = g.C / kLrnRun;
-  int lp = 1;
-  while (lp < runs) lp <<= 1;
+  // channels per lane: 8, or 6 when that fills the pixel's power-of-two lane group better
+  // (C = 96: 16 lanes of 6 instead of 12 of 16 lanes busy; C = 192: 32 instead of 24)
+  auto lanes = [](int runs) {
+    int lp = 1;
+    while (lp < runs) lp <<= 1;
+    return lp;
+  };
+  const int r8 = g.C / 8, l8 = lanes(r8);
+  const bool six = g.C % 6 == 0 && lanes(g.C / 6) <= 32 &&
+                   static_cast<double>(g.C / 6) / lanes(g.C / 6) > static_cast<double>(r8) / l8;
+  const int lp = six ? lanes(g.C / 6) : l8;
   if (lp > 32) throw std::invalid_argument("lrn_pool: more than 256 channels");
   const uint32_t pixels = checked32(static_cast<size_t>(g.n) * g.H * g.W, "lrn_pool");
   checked32(static_cast<size_t>(pixels) * g.C, "lrn_pool");
   const size_t warps = (pixels + 32 / lp - 1) / (32 / lp);
-  auto kern = g.sh == 1 ? lrn_maxpool_bwd_k<3> : lrn_maxpool_bwd_k<2>;
+  auto kern = six ? (g.sh == 1 ? lrn_maxpool_bwd_k<3, 6> : lrn_maxpool_bwd_k<2, 6>)
+                  : (g.sh == 1 ? lrn_maxpool_bwd_k<3, 8> : lrn_maxpool_bwd_k<2, 8>);
   launch_k(kern, grid_for(warps * 32, 256, 148 * 8), 256, 0, s, lg, g, x, dpool, route, dx,
            accumulate ? 1 : 0, relu_mask ? 1 : 0, lp, pixels);
   PSG_CUDA(cudaGetLastError());

@@ -335,10 +335,12 @@ def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
 
 def _s2d_net(b):
     """A strided 3-channel first conv (the space-to-depth route in TF32: the device stream
-    gathers straight into x', host batches are staged NHWC then rearranged)."""
+    gathers straight into x', host batches are staged NHWC then rearranged), then
+    ReLU -> LRN -> 3x3 max pool over 48 channels (the fused LRN / pool kernels, 6-channel
+    lanes in the backward)."""
     return ns.NetSpec([
         ns.data_layer("data", b, 3, 23, 23), ns.label_layer("label", b),
-        ns.conv_layer("c1", "data", 7, 7, 16, stride=2, pad=3), ns.relu_layer("r1", "c1"),
+        ns.conv_layer("c1", "data", 7, 7, 48, stride=2, pad=3), ns.relu_layer("r1", "c1"),
         ns.lrn_layer("n1", "r1", 5, 1e-2, 0.75, 1.0),
         ns.pool_layer("p1", "n1", 3, 3, 2, 2, ceil_mode=True),
         ns.linear_layer("out", "p1", 10), ns.softmax_loss_layer("loss", "out", "label")])
