@@ -15,13 +15,13 @@ void OpTimer::begin(const char* name, int layer, int phase, double flops, double
   r.info.bytes = bytes;
   PSG_CUDA(cudaEventCreate(&r.a));
   PSG_CUDA(cudaEventCreate(&r.b));
-  PSG_CUDA(cudaEventRecord(r.a, stream));
+  PSG_CUDA(cudaEventRecordWithFlags(r.a, stream, cudaEventRecordExternal));  // graph node when captured
   recs.push_back(r);
 }
 
 void OpTimer::end(int launches) {
   recs.back().info.launches = launches;
-  PSG_CUDA(cudaEventRecord(recs.back().b, stream));
+  PSG_CUDA(cudaEventRecordWithFlags(recs.back().b, stream, cudaEventRecordExternal));
 }
 
 OpTimer::~OpTimer() {

@@ -1,6 +1,7 @@
 // Measurement paths of a Net: per-op CUDA-event profile of one training step,
 // and the host-fed (end-to-end) training loop used for bench.py's `e2e` number.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "runtime.h"
@@ -17,15 +18,39 @@ void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, 
   const LayerRt& d = net->L[net->data_idx];
   psg_dataset* ds = net->train_ds;
   std::vector<psg_op_time> acc;
+  // The step is captured with its per-op event records into a CUDA graph and replayed, as
+  // the training loop runs it (eager launches would add the host's launch cost to every
+  // short op); PSG_EAGER=1 profiles eager launches.
+  static const bool eager = [] {
+    const char* e = std::getenv("PSG_EAGER");
+    return e && std::atoi(e) != 0;
+  }();
   for (int r = 0; r <= repeats; ++r) {  // r = 0 is an untimed warm-up
     OpTimer t(net->stream);
-    PSG_CUDA(cudaMemsetAsync(&net->dsc->cursor, 0, sizeof(int), net->stream));
-    t.begin("gather", net->data_idx, 0, 0.0, 2.0 * 4.0 * static_cast<double>(b) * d.vol());
-    stage_gathered_batch(net, ds->images, ds->labels, net->d_idx, &net->dsc->cursor, b);
-    t.end(1);
-    run_forward(net, b, true, true, &t);
-    run_backward(net, b, &t);
-    run_update(net, true, &t);
+    cudaGraph_t graph = nullptr;
+    if (!eager) PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      PSG_CUDA(cudaMemsetAsync(&net->dsc->cursor, 0, sizeof(int), net->stream));
+      t.begin("gather", net->data_idx, 0, 0.0, 2.0 * 4.0 * static_cast<double>(b) * d.vol());
+      stage_gathered_batch(net, ds->images, ds->labels, net->d_idx, &net->dsc->cursor, b);
+      t.end(1);
+      run_forward(net, b, true, true, &t);
+      run_backward(net, b, &t);
+      run_update(net, true, &t);
+    } catch (...) {
+      if (!eager) cudaStreamEndCapture(net->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    if (!eager) {
+      PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
+      cudaGraphExec_t exec = nullptr;
+      PSG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      PSG_CUDA(cudaGraphLaunch(exec, net->stream));
+      PSG_CUDA(cudaStreamSynchronize(net->stream));
+      cudaGraphExecDestroy(exec);
+    }
     PSG_CUDA(cudaStreamSynchronize(net->stream));
     if (r == 0) {
       acc.resize(t.recs.size());
