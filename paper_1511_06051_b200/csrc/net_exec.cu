@@ -6,6 +6,16 @@
 
 namespace psg {
 
+// Under stream capture the record must become an event-record node of the graph
+// (cudaEventRecordExternal); outside capture that flag is rejected.
+cudaError_t OpTimer::record(cudaEvent_t e) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  PSG_CUDA(cudaStreamIsCapturing(stream, &st));
+  return st == cudaStreamCaptureStatusActive
+             ? cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal)
+             : cudaEventRecord(e, stream);
+}
+
 void OpTimer::begin(const char* name, int layer, int phase, double flops, double bytes) {
   Rec r{};
   std::strncpy(r.info.name, name, sizeof(r.info.name) - 1);
@@ -15,13 +25,13 @@ void OpTimer::begin(const char* name, int layer, int phase, double flops, double
   r.info.bytes = bytes;
   PSG_CUDA(cudaEventCreate(&r.a));
   PSG_CUDA(cudaEventCreate(&r.b));
-  PSG_CUDA(cudaEventRecordWithFlags(r.a, stream, cudaEventRecordExternal));  // graph node when captured
+  PSG_CUDA(record(r.a));
   recs.push_back(r);
 }
 
 void OpTimer::end(int launches) {
   recs.back().info.launches = launches;
-  PSG_CUDA(cudaEventRecordWithFlags(recs.back().b, stream, cudaEventRecordExternal));
+  PSG_CUDA(record(recs.back().b));
 }
 
 OpTimer::~OpTimer() {

@@ -167,6 +167,7 @@ struct OpTimer {
   ~OpTimer();
   void begin(const char* name, int layer, int phase, double flops, double bytes);
   void end(int launches);
+  cudaError_t record(cudaEvent_t e);
 };
 
 // Gather the step's batch from the HBM-resident dataset rows idx[cursor * n + i]: into the
