@@ -549,13 +549,59 @@ size_t conv_workspace_elems_simt(const ConvGeom& g) {
   return e;
 }
 
+bool wgrad_small(const ConvGeom& g);
+
 int conv_launches_simt(const ConvGeom& g, int which) {
+  if (which == 2 && wgrad_small(g)) return 1;
   const Split sp = which == 0 ? fprop_split(g) : which == 1 ? dgrad_split(g) : wgrad_split(g);
   return sp.splits == 1 ? 1 : 2;
 }
 
+// Linear wgrad with a small output (the logits layer, e.g. cifar10_quick ip2: 10 x 64 over
+// a batch of 100): one warp per dW / db element, lane l summing batch rows l, l + 32, ...
+// then a fixed xor-shuffle tree (deterministic).  The tiled kernel runs such a GEMM on one
+// block, bound by its K-loop latency (30 us).
+__global__ void wgrad_linear_small(const float* __restrict__ x, const float* __restrict__ dy,
+                                   int n, int D, int F, int Kp, float* __restrict__ dw,
+                                   float* __restrict__ db) {
+  pdl_enter();
+  const int idx = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (idx >= F * (Kp + 1)) return;  // warp-uniform
+  const int f = idx / (Kp + 1), k = idx - f * (Kp + 1);
+  if (k < Kp && k >= D) {
+    if (lane == 0) dw[static_cast<size_t>(f) * Kp + k] = 0.f;  // row padding
+    return;
+  }
+  float acc = 0.f;
+  for (int i = lane; i < n; i += 32) {
+    const float d = __ldg(dy + static_cast<size_t>(i) * F + f);
+    acc = k == Kp ? acc + d : fmaf(d, __ldg(x + static_cast<size_t>(i) * D + k), acc);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    if (k == Kp)
+      db[f] = acc;  // bias column: sum over the batch of dY[:, f]
+    else
+      dw[static_cast<size_t>(f) * Kp + k] = acc;
+  }
+}
+
+bool wgrad_small(const ConvGeom& g) {
+  const bool linear = g.H == 1 && g.W == 1 && g.OH == 1 && g.OW == 1 && g.kh == 1 && g.kw == 1;
+  return linear && g.G == 1 && g.cs_in == g.Kf() &&
+         static_cast<long>(g.F) * (g.Kp() + 1) <= 16384 && g.n <= 4096;
+}
+
 void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
                      const Workspace& ws, cudaStream_t s) {
+  if (wgrad_small(g)) {
+    const int total = g.F * (g.Kp() + 1);  // one warp each
+    launch_k(wgrad_linear_small, (total + 7) / 8, 256, 0, s, x, dy, g.n, g.cs_in, g.F, g.Kp(),
+             dw, db);
+    PSG_CUDA(cudaGetLastError());
+    return;
+  }
   WgradProb p{};
   fill_geom(p, g);
   p.x = x;
