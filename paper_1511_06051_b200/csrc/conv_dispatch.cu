@@ -25,6 +25,7 @@ void conv_fprop_simt(const ConvGeom& g, const float* x, const float* w, const fl
                      float* y, bool relu, const Workspace& ws, cudaStream_t s);
 void conv_dgrad_simt(const ConvGeom& g, const float* dy, const float* w, float* dx,
                      bool accumulate, const Workspace& ws, cudaStream_t s);
+bool linear_small(const ConvGeom& g);  // conv_simt.cu
 void conv_wgrad_simt(const ConvGeom& g, const float* x, const float* dy, float* dw, float* db,
                      const Workspace& ws, cudaStream_t s);
 size_t conv_workspace_elems_simt(const ConvGeom& g);
@@ -330,6 +331,8 @@ void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* 
   } else if (m == Mode::Tf32 && col && fprop_col_route(g)) {
     im2col(g, x, col, s);
     tc_fprop(col_geom(g), col, w, bias, y, relu, ws, s);
+  } else if (linear_small(g)) {  // few-output linear layer: dedicated kernel (any mode)
+    conv_fprop_simt(g, x, w, bias, y, relu, ws, s);
   } else if (use_tc(g, 0, m)) {
     tc_fprop(g, x, w, bias, y, relu, ws, s);
   } else {
@@ -337,11 +340,13 @@ void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* 
   }
 }
 
-bool conv_dgrad_masks(const ConvGeom& g, Mode m) { return use_tc(g, 1, m); }
+bool conv_dgrad_masks(const ConvGeom& g, Mode m) { return use_tc(g, 1, m) && !linear_small(g); }
 
 void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, bool accumulate,
                 const Workspace& ws, Mode m, cudaStream_t s, const float* relu_mask, float* col) {
-  if (use_tc(g, 1, m)) {
+  if (linear_small(g) && !relu_mask) {
+    conv_dgrad_simt(g, dy, w, dx, accumulate, ws, s);
+  } else if (use_tc(g, 1, m)) {
     float* wt = nullptr;
     if (tc_dgrad_wt(g)) {
       if (!col) throw std::logic_error("conv_dgrad: no scratch for the transposed weights");
@@ -393,6 +398,7 @@ int conv_launches(const ConvGeom& g, int which, Mode m) {
     return 1 + tc_launches(col_geom(g), 0);
   if (m == Mode::Tf32 && which == 2 && wgrad_col_route(g))
     return (fprop_col_route(g) ? 0 : 1) + tc_wgrad_col_launches(g);
+  if (which != 2 && linear_small(g)) return 1;
   if (use_tc(g, which, m)) return tc_launches(g, which) + (which == 1 && tc_dgrad_wt(g) ? 1 : 0);
   return conv_launches_simt(g, which);
 }

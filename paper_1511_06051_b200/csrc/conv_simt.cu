@@ -501,8 +501,56 @@ float* split_ws(const Workspace& ws, const Split& sp, int G, int M, int N) {
 
 }  // namespace
 
+// Small linear layers with few outputs (the logits layer, cifar10_quick ip2: 64 -> 10):
+// fprop = one warp per output (lanes split the input features, fixed xor tree); dgrad = one
+// thread per input feature (sum over the <= 32 outputs in order).  The tiled kernels run
+// these on one or two blocks, bound by their K-loop latency.
+bool linear_small(const ConvGeom& g) {
+  const bool linear = g.H == 1 && g.W == 1 && g.OH == 1 && g.OW == 1 && g.kh == 1 && g.kw == 1;
+  return linear && g.G == 1 && g.cs_in == g.Kf() && g.F <= 32 && g.n <= 65536;
+}
+
+__global__ void fprop_linear_small(const float* __restrict__ x, const float* __restrict__ w,
+                                   const float* __restrict__ bias, int n, int D, int F, int Kp,
+                                   int relu, float* __restrict__ y) {
+  pdl_enter();
+  const int o = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (o >= n * F) return;  // warp-uniform
+  const int i = o / F, j = o - i * F;
+  const float* xr = x + static_cast<size_t>(i) * D;
+  const float* wr = w + static_cast<size_t>(j) * Kp;
+  float acc = 0.f;
+  for (int k = lane; k < D; k += 32) acc = fmaf(__ldg(xr + k), __ldg(wr + k), acc);
+#pragma unroll
+  for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (lane == 0) {
+    if (bias) acc += bias[j];
+    y[o] = relu && !(acc > 0.f) ? 0.f : acc;
+  }
+}
+
+__global__ void dgrad_linear_small(const float* __restrict__ dy, const float* __restrict__ w,
+                                   int n, int D, int F, int Kp, int accumulate,
+                                   float* __restrict__ dx) {
+  pdl_enter();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * D) return;
+  const int i = t / D, k = t - i * D;
+  const float* dr = dy + static_cast<size_t>(i) * F;
+  float acc = 0.f;
+  for (int j = 0; j < F; ++j) acc = fmaf(__ldg(dr + j), __ldg(w + static_cast<size_t>(j) * Kp + k), acc);
+  dx[t] = accumulate ? dx[t] + acc : acc;
+}
+
 void conv_fprop_simt(const ConvGeom& g, const float* x, const float* w, const float* bias,
                      float* y, bool relu, const Workspace& ws, cudaStream_t s) {
+  if (linear_small(g)) {
+    const long warps = static_cast<long>(g.n) * g.F;
+    launch_k(fprop_linear_small, static_cast<unsigned>((warps + 7) / 8), 256, 0, s, x, w, bias,
+             g.n, g.cs_in, g.F, g.Kp(), relu ? 1 : 0, y);
+    PSG_CUDA(cudaGetLastError());
+    return;
+  }
   FpropProb p{};
   fill_geom(p, g);
   p.x = x;
@@ -522,6 +570,13 @@ void conv_fprop_simt(const ConvGeom& g, const float* x, const float* w, const fl
 
 void conv_dgrad_simt(const ConvGeom& g, const float* dy, const float* w, float* dx,
                      bool accumulate, const Workspace& ws, cudaStream_t s) {
+  if (linear_small(g)) {
+    const long total = static_cast<long>(g.n) * g.cs_in;
+    launch_k(dgrad_linear_small, static_cast<unsigned>((total + 255) / 256), 256, 0, s, dy, w,
+             g.n, g.cs_in, g.F, g.Kp(), accumulate ? 1 : 0, dx);
+    PSG_CUDA(cudaGetLastError());
+    return;
+  }
   DgradProb p{};
   fill_geom(p, g);
   p.dy = dy;
@@ -551,8 +606,11 @@ size_t conv_workspace_elems_simt(const ConvGeom& g) {
 
 bool wgrad_small(const ConvGeom& g);
 
+bool linear_small(const ConvGeom& g);
+
 int conv_launches_simt(const ConvGeom& g, int which) {
   if (which == 2 && wgrad_small(g)) return 1;
+  if (which != 2 && linear_small(g)) return 1;
   const Split sp = which == 0 ? fprop_split(g) : which == 1 ? dgrad_split(g) : wgrad_split(g);
   return sp.splits == 1 ? 1 : 2;
 }
