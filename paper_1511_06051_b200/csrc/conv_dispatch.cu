@@ -135,13 +135,18 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
     img = idx[static_cast<size_t>(cursor ? *cursor : 0) * batch + b];
     if (hs == 0 && threadIdx.x == 0) labels[b] = ds_labels[img];
   }
-  const float* xb = x + img * g.H * g.W * src_cs;
+  // src_cs > 0: NHWC source with channel stride src_cs; src_cs < 0: NCHW with -src_cs
+  // channels (a host-fed batch in the reference's layout)
+  const bool nchw = src_cs < 0;
+  const int cs = nchw ? -src_cs : src_cs;
+  const int ps = nchw ? 1 : cs, cst = nchw ? g.H * g.W : 1, rs = nchw ? g.W : g.W * cs;
+  const float* xb = x + img * g.H * g.W * cs;
   for (int j = threadIdx.x; j < q.W * s; j += blockDim.x) {
     const int ws = j / s, dy = j - ws * s;
     const int ih = s * hs + dy - g.ph, iw0 = s * ws - g.pw;
     float* o = out + ws * q.cs_in + dy * run;
     const bool row_ok = ih >= 0 && ih < g.H;
-    const float* xr = xb + static_cast<size_t>(ih) * g.W * src_cs;
+    const float* xr = xb + static_cast<size_t>(ih) * rs;
     if constexpr (RUN == 12) {
       float v[12];
 #pragma unroll
@@ -149,7 +154,7 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
         const int iw = iw0 + dx;
         const bool ok = row_ok && iw >= 0 && iw < g.W;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) v[dx * 3 + c] = ok ? __ldg(xr + iw * src_cs + c) : 0.f;
+        for (int c = 0; c < 3; ++c) v[dx * 3 + c] = ok ? __ldg(xr + iw * ps + c * cst) : 0.f;
       }
       float4* o4 = reinterpret_cast<float4*>(o);
       o4[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
       for (int dx = 0; dx < s; ++dx) {
         const int iw = iw0 + dx;
         const bool ok = row_ok && iw >= 0 && iw < g.W;
-        for (int c = 0; c < C; ++c) o[dx * C + c] = ok ? __ldg(xr + iw * src_cs + c) : 0.f;
+        for (int c = 0; c < C; ++c) o[dx * C + c] = ok ? __ldg(xr + iw * ps + c * cst) : 0.f;
       }
     }
     if (dy == s - 1)
@@ -299,6 +304,15 @@ void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_lab
     throw std::invalid_argument("s2d: image too large");
   launch_k(s2d_kernel(g, q), q.n * q.H, 256, 0, st, ds_images, g, q, col, idx, cursor, g.n,
            src_cs, ds_labels, labels);
+  PSG_CUDA(cudaGetLastError());
+}
+
+void stage_s2d_nchw(const ConvGeom& g, const float* src, int C, float* col, cudaStream_t st) {
+  const ConvGeom q = s2d_geom(g);
+  if (static_cast<size_t>(g.H) * g.W * C >= (1ULL << 31))
+    throw std::invalid_argument("s2d: image too large");
+  launch_k(s2d_kernel(g, q), q.n * q.H, 256, 0, st, src, g, q, col, nullptr, nullptr, g.n, -C,
+           nullptr, nullptr);
   PSG_CUDA(cudaGetLastError());
 }
 

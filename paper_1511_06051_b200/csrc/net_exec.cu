@@ -96,6 +96,24 @@ int stage_gathered_batch(psg_net* net, const float* images, const int32_t* label
   return 1;
 }
 
+int stage_host_batch(psg_net* net, const float* src, size_t n) {
+  const LayerRt& d = net->L[net->data_idx];
+  net->data_s2d = false;
+  if (net->fuse && d.consumers.size() == 1) {
+    const LayerRt& c = net->L[d.consumers[0]];
+    if (c.kind == PSG_LAYER_CONV && c.col) {
+      const ConvGeom g = geom_n(c, n);
+      if (conv_s2d_input(g, net->mode)) {
+        stage_s2d_nchw(g, src, d.C, c.col, net->stream);
+        net->data_s2d = true;
+        return 1;
+      }
+    }
+  }
+  stage_batch_nchw(src, static_cast<int>(n), d.C, d.H, d.W, d.cs, d.out, net->stream);
+  return 1;
+}
+
 int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer) {
   cudaStream_t s = net->stream;
   int launches = 0;

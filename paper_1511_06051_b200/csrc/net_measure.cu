@@ -110,8 +110,7 @@ void net_train_host(psg_net* net, const float* images, const int32_t* labels, lo
                                cudaMemcpyHostToDevice, net->stream));
       PSG_CUDA(cudaMemcpyAsync(net->labels, labels + s * b, b * sizeof(int32_t),
                                cudaMemcpyHostToDevice, net->stream));
-      stage_batch_nchw(net->d_stage, static_cast<int>(b), d.C, d.H, d.W, d.cs, d.out,
-                       net->stream);
+      stage_host_batch(net, net->d_stage, b);
       run_forward(net, b, true, true);
       run_backward(net, b);
       run_update(net, true);
@@ -154,8 +153,7 @@ void net_train_host(psg_net* net, const float* images, const int32_t* labels, lo
     try {
       PSG_CUDA(cudaMemcpyAsync(net->labels, net->d_lab2[k], b * sizeof(int32_t),
                                cudaMemcpyDeviceToDevice, net->stream));
-      stage_batch_nchw(net->d_stage2[k], static_cast<int>(b), d.C, d.H, d.W, d.cs, d.out,
-                       net->stream);
+      stage_host_batch(net, net->d_stage2[k], b);
       run_forward(net, b, true, true);
       run_backward(net, b);
       run_update(net, true);

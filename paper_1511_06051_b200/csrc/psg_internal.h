@@ -135,6 +135,8 @@ void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* 
 // A strided first conv on the space-to-depth route (TF32): its input can be gathered
 // straight into x' (col) from the dataset rows idx[cursor * g.n + b] (+ the labels).
 bool conv_s2d_input(const ConvGeom& g, Mode mode);
+// The same from a host-fed NCHW batch already in device memory (no labels).
+void stage_s2d_nchw(const ConvGeom& g, const float* src, int C, float* col, cudaStream_t s);
 void gather_s2d(const ConvGeom& g, const float* ds_images, const int32_t* ds_labels,
                 const uint32_t* idx, const int* cursor, int src_cs, float* col, int32_t* labels,
                 cudaStream_t s);

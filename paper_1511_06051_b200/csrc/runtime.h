@@ -175,6 +175,9 @@ struct OpTimer {
 // first conv that is the data layer's only consumer.  Returns the launches enqueued.
 int stage_gathered_batch(psg_net* net, const float* images, const int32_t* labels,
                          const uint32_t* idx, const int* cursor, size_t n);
+// A host-fed NCHW batch (already copied to the device) into the data layer, or straight
+// into the space-to-depth input of the first conv (as stage_gathered_batch).
+int stage_host_batch(psg_net* net, const float* src, size_t n);
 int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer = nullptr);
 int run_backward(psg_net* net, size_t n, OpTimer* timer = nullptr);
 int run_update(psg_net* net, bool advance, OpTimer* timer = nullptr);
