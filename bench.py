@@ -47,7 +47,12 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="cifar10_quick", choices=list(WORKLOADS))
+    p.add_argument("--workload", default="alexnet", choices=list(WORKLOADS),
+                   help="default: AlexNet b=256 tau=50 (BASELINE.json configs[2], the "
+                        "north-star workload); the cifar10_quick tau sweep at this K "
+                        "(configs[1]) rides along as an extra key")
+    p.add_argument("--no-extra", dest="extra", action="store_false",
+                   help="skip the cifar10_quick tau sweep")
     p.add_argument("--tau", type=int, default=None,
                    help="local SGD steps per round (default: the BASELINE config's — "
                         "AlexNet 50, GoogLeNet 20, cifar10_quick 10)")
@@ -208,67 +213,380 @@ def build_dataset(workload, K):
     return Dataset(img.astype(np.float32), lab, 10)
 
 
-# CPU-baseline sample batch per worker: ~10-30 s of fp64 work on the box's host cores
-CPU_SAMPLE_BATCH = {"cifar10_quick": None, "cq-valid": None, "alexnet": 16, "googlenet": 8}
+# CPU sample: per-worker batch of the bounded sample (~10-30 s of fp64 work on the host cores)
+CPU_SAMPLE_BATCH = {"cifar10_quick": None, "cq-valid": None, "alexnet": 2, "googlenet": 2}
 
 
-def cpu_baseline(workload, b, threads, steps=1):
-    """The oracle port (C, fp64) of run_sparknet on host cores: workers = threads, tau = steps,
-    one round, eval skipped.  cifar10_quick / AlexNet are not expressible by the unmodified
-    reference (no pad / ave pool / LRN), so the C restatement is timed (kind "port");
-    cq-valid runs the reference itself (kind "reference")."""
+def host_cpu():
+    return {"model": lscpu_model(), "hardware_concurrency": os.cpu_count()}
+
+
+class CpuRound:
+    """The reference's CPU path in steady state (the oracle port of run_sparknet's round,
+    schemes.hpp:323-338): K = `threads` worker nets (the port of Net, model.hpp) on K host
+    threads, each running SGD steps (backward + apply_update, model.hpp:111-118) on its own
+    batch of its shard, then get_weights of every worker, weights_mean (weights.hpp:90-107)
+    and set_weights back (the next round's broadcast).  Net construction / init happens
+    once, outside the timed rounds (the reference builds its nets once per run)."""
+
+    def __init__(self, workload, b, threads):
+        import threading
+        from oracle import pyoracle
+        from paper_1511_06051_b200 import netspec
+        self.b = CPU_SAMPLE_BATCH.get(workload) or b
+        self.K = threads
+        self.spec = getattr(netspec, WORKLOADS[workload][0])(self.b)
+        _, _, (c, h, w), _, self.lr, self.mu, self.wd = WORKLOADS[workload]
+        self.lib = pyoracle.OracleLib()
+        per_class = max(1, (self.b * threads + 9) // 10)
+        img, lab = self.lib.generate_synthetic(10, c, h, w, per_class, 2.0, 12345, 0)
+        if (c, h, w) != (3, 32, 32):
+            lab = lab * 97  # ImageNet-shaped nets: labels spread over 1000 classes
+        rows = self.lib.shard(len(lab), threads, 1)
+        self.batches = [(np.ascontiguousarray(img[r[:self.b].astype(np.int64)]),
+                         np.ascontiguousarray(lab[r[:self.b].astype(np.int64)]))
+                        for r in rows]
+        self.nets = [None] * threads
+
+        def make(k):
+            n = self.lib.net(self.spec, 1)
+            n.set_sgd(self.lr, self.mu, self.wd)
+            self.nets[k] = n
+        self._parallel(make, threading)
+        self.threading = threading
+
+    def _parallel(self, fn, threading):
+        ts = [threading.Thread(target=fn, args=(k,)) for k in range(self.K)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    def round(self, steps=1):
+        """One round of `steps` local steps per worker + the average; returns (seconds of
+        the steps, seconds of the average)."""
+        def work(k):
+            n = self.nets[k]
+            x, y = self.batches[k]
+            for _ in range(steps):
+                _, g = n.backward(x, y)
+                n.apply_update(g)
+        t0 = time.perf_counter()
+        self._parallel(work, self.threading)
+        t1 = time.perf_counter()
+        ws = [n.get_weights() for n in self.nets]
+        mean = self.lib.weights_mean(ws)
+        for n in self.nets:
+            n.set_weights(mean)
+        return t1 - t0, time.perf_counter() - t1
+
+    def value_at(self, tau, t_step, t_avg):
+        """images/sec of a round of tau steps: the round is tau sequential steps per worker
+        followed by one average (schemes.hpp:323-336)."""
+        return self.K * tau * self.b / (tau * t_step + t_avg)
+
+
+def cpu_baseline(workload, b, threads, steps=1, rounds=1, tau=None):
+    """The reference's CPU path timed on host cores (see CpuRound).  cifar10_quick / AlexNet /
+    GoogLeNet are not expressible by the unmodified reference (no pad / ave pool / LRN), so
+    the C restatement (oracle/oracle.c) is timed (kind "port"); cq-valid runs the reference
+    itself (kind "reference", oracle/_ref built from /root/reference by oracle/Makefile)."""
     from oracle import pyoracle
-    b = CPU_SAMPLE_BATCH.get(workload) or b
-    spec = getattr(__import__("paper_1511_06051_b200.netspec", fromlist=["x"]),
-                   WORKLOADS[workload][0])(b)
-    _, _, (c, h, w), *_ = WORKLOADS[workload]
-    per_class = max(1, (b * threads + 9) // 10)
-    orc = pyoracle.OracleLib()
-    img, lab = orc.generate_synthetic(10, c, h, w, per_class, 2.0, 12345, 0)
-    ev = (img[:b], lab[:b])
     use_ref = workload == "cq-valid" and os.path.exists(
         os.path.join(ROOT, "oracle", "_ref", "libparasgd_ref.so"))
-    t0 = time.perf_counter()
     if use_ref:
-        pyoracle.RefLib(strict=False).run_sparknet(spec, (img, lab), ev, b, 0.001, 0.9, 1,
-                                                   threads, steps, 1, 0, threads=threads)
+        spec, _ = make_spec(workload, b)
+        _, _, (c, h, w), *_ = WORKLOADS[workload]
+        orc = pyoracle.OracleLib()
+        img, lab = orc.generate_synthetic(10, c, h, w, max(1, (b * threads + 9) // 10), 2.0,
+                                          12345, 0)
+        t0 = time.perf_counter()
+        pyoracle.RefLib(strict=False).run_sparknet(spec, (img, lab), (img[:b], lab[:b]), b,
+                                                   0.001, 0.9, 1, threads, steps, rounds, 0,
+                                                   threads=threads)
+        dt = time.perf_counter() - t0
+        bs = b
+        value = threads * steps * rounds * bs / dt
+        sample = (f"{workload} per-worker batch {bs}: {rounds} round(s) of {threads} workers x "
+                  f"{steps} SGD step(s) on {threads} host threads + the K-way weights_mean "
+                  f"({dt:.1f} s timed)")
     else:
-        orc.run_sparknet(spec, (img, lab), ev, b, 0.001, 0.9, 1, threads, steps, 1, 0,
-                         threads=threads, skip_eval=True)
-    dt = time.perf_counter() - t0
-    value = threads * steps * b / dt
-    return {"value": value, "unit": "images/sec", "cores": threads,
-            "kind": "reference" if use_ref else "port",
-            "sample": f"{workload} b={b}: {threads} workers x {steps} SGD step(s) on {threads} "
-                      f"host threads, 1 round ({dt:.1f} s)"}
+        cr = CpuRound(workload, b, threads)
+        ts = [cr.round(1) for _ in range(rounds)]
+        t_step, t_avg = sum(t for t, _ in ts) / rounds, sum(a for _, a in ts) / rounds
+        tau = tau or 1
+        value, bs = cr.value_at(tau, t_step, t_avg), cr.b
+        sample = (f"{workload} per-worker batch {bs}: {threads} workers x 1 SGD step on "
+                  f"{threads} host threads ({t_step:.2f} s) + the K-way weights_mean / "
+                  f"get / set_weights ({t_avg:.2f} s), round time at tau={tau} = tau x step "
+                  f"+ average")
+    out = {"value": value, "unit": "images/sec", "cores": threads,
+           "kind": "reference" if use_ref else "port", "sample": sample}
+    out.update(host_cpu())
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path (CpuRound: the oracle port of run_sparknet's
+    round; the reference itself for cq-valid) on the box's host cores, all threads, on this
+    arm's workload / metric; each step is a bounded sample — one round of one SGD step per
+    worker thread at a small per-worker batch, plus the K-way average."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    spec, b = make_spec(args.workload, args.batch)
-    threads = max(1, args.gpus)
-    t = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_baseline(args.workload, b, threads, steps=1)
-        if i >= args.warmup:
-            t.append(threads * b / r["value"])
-    sec = sum(t) / len(t)
-    value = threads * b / sec
-    cb = {"value": value, "unit": "images/sec", "cores": threads, "kind": r["kind"],
-          "sample": f"per step: {threads} worker(s) x 1 SGD step of {args.workload} b={b} "
-                    f"on {threads} host thread(s) + the K-way average"}
+    _, b = make_spec(args.workload, args.batch)
+    threads = max(1, os.cpu_count() or 1)
+    if args.workload == "cq-valid":
+        r = cpu_baseline(args.workload, b, threads, rounds=args.steps)
+        value, bs, kind = r["value"], b, r["kind"]
+    else:
+        cr = CpuRound(args.workload, b, threads)
+        for _ in range(args.warmup):
+            cr.round(1)
+        ts = [cr.round(1) for _ in range(args.steps)]
+        t_step = sum(t for t, _ in ts) / args.steps
+        t_avg = sum(a for _, a in ts) / args.steps
+        bs, kind = cr.b, "port"
+        value = cr.value_at(args.tau, t_step, t_avg)
+    cb = {"value": value, "unit": "images/sec", "cores": threads, "kind": kind,
+          "sample": f"per step: {threads} worker(s) x 1 SGD step of {args.workload} at "
+                    f"per-worker batch {bs} on {threads} host thread(s) + the K-way average; "
+                    f"value = K*tau*b / (tau*step + average) at tau={args.tau}"}
+    cb.update(host_cpu())
     print(json.dumps({
         "impl": "reference", "metric": "images/sec", "value": value, "unit": "images/sec",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1000.0, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "global_batch": b * threads, "K": threads,
-                   "tau": 1, "note": "reference CPU path (bounded sample per step)"},
+        "ms_per_step": threads * bs / value * 1000.0, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "global_batch": bs * threads, "K": threads,
+                   "tau": args.tau, "note": "reference CPU path (bounded sample per step)"},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "images/sec", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}))
+
+
+GEMM_PHASES = ("forward", "wgrad", "dgrad")
+
+
+def lscpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def roofline_of(prof, precision, peaks, workload):
+    """Roofline of the dominant op of one step's live per-op profile, plus the aggregate over
+    every GEMM-shaped op (conv / linear fprop, dgrad, wgrad: `gemm_frac`).  TF32 peak: the
+    driver-measured dense bf16 cuBLAS burst figure / 2 (MEASURED_PEAKS.json; tensor-core TF32
+    issues half the bf16 MACs per cycle); the sustained (power-capped) figure / 2 is reported
+    beside it."""
+    step_ms = sum(p["ms"] for p in prof)
+    top = max(prof, key=lambda p: p["ms"])
+    bf16, bf16_s = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained")
+    if precision == "tf32":
+        peak, src = bf16 / 2, f"MEASURED_PEAKS.json bf16_tflops {bf16:.1f} / 2 (burst)"
+        peak_s = bf16_s / 2 if bf16_s else None
+    else:
+        peak, src = peaks.get("fp32_simt_tflops", bf16 / 32), "fp32 SIMT (profiles/peaks_measured.json)"
+        peak_s = None
+    if top["flops"] > 0:
+        achieved = top["flops"] / (top["ms"] * 1e-3) / 1e12
+        roof = {"bound": "tensor" if precision == "tf32" else "fp32-simt", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "peak_source": src}
+    else:
+        achieved = top["bytes"] / (top["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    roof.update({"traffic": None, "kernel": top["name"], "share_of_step": top["ms"] / step_ms,
+                 "algorithmic": top["flops"] or top["bytes"]})
+    gemm = [p for p in prof if p["flops"] > 0 and p["phase"] in GEMM_PHASES]
+    if gemm:
+        fl, ms = sum(p["flops"] for p in gemm), sum(p["ms"] for p in gemm)
+        roof["gemm"] = {"ops": len(gemm), "flops": fl, "ms": ms, "share_of_step": ms / step_ms,
+                        "achieved": fl / (ms * 1e-3) / 1e12}
+        roof["gemm_frac"] = roof["gemm"]["achieved"] / peak
+        tot = sum(p["flops"] for p in prof)
+        roof["step_frac"] = tot / (step_ms * 1e-3) / 1e12 / peak
+        if peak_s:
+            roof["gemm_frac_vs_sustained"] = roof["gemm"]["achieved"] / peak_s
+            roof["peak_sustained"] = peak_s
+    # traffic: DRAM bytes of the same op in the committed ncu capture of this workload
+    # (tools/op_traffic.py; cold-cache serialised replay, one training step)
+    for rnd in ("round2", "round1"):
+        tpath = os.path.join(ROOT, "profiles", rnd, f"{workload}_op_traffic.json")
+        if not os.path.exists(tpath):
+            continue
+        with open(tpath) as f:
+            tr = json.load(f)
+        hit = [o for o in tr["ops"] if o["op"] == top["name"]]
+        if hit and tr.get("precision") == precision:
+            roof["traffic"] = hit[0]["dram_bytes"]
+            roof["traffic_unit"] = "bytes per op launch set (ncu dram__bytes_read+write)"
+            roof["ncu_share_of_step"] = hit[0]["ncu_share"]
+            roof["traffic_source"] = os.path.relpath(tpath, ROOT)
+        break
+    return roof, step_ms
+
+
+class Rank:
+    """This process's rank / device and the gloo group used for barriers and max-reduces."""
+
+    def __init__(self):
+        self.rank, self.world, self.local = dist_env()
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def max(self, x):
+        if self.dist is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def bcast(self, obj):
+        if self.dist is None:
+            return obj
+        box = [obj if self.rank == 0 else None]
+        self.dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+
+class Worker:
+    """One SparkNet worker (this rank's GPU): its net on shard `rank` of the workload's
+    synthetic dataset, and the communicator of the per-round weight average."""
+
+    def __init__(self, R, workload, precision, average, batch=None):
+        from paper_1511_06051_b200 import data as pdata
+        from paper_1511_06051_b200 import model
+        self.R, self.workload, self.avg_mode = R, workload, average
+        self.spec, self.b = make_spec(workload, batch)
+        _, _, self.chw3, _, lr, mu, wd = WORKLOADS[workload]
+        self.ds = build_dataset(workload, R.world)
+        self.shards = pdata.shard(self.ds, R.world, 1)
+        self.net = model.Net(self.spec, 1, device=R.local, precision=precision)
+        self.net.set_sgd(model.SgdOptions(lr, mu, wd))
+        self.net.set_training_data(pdata.make_worker_iterator(self.shards, R.rank, self.b, 1))
+        self.comm = None
+        if R.world > 1:
+            from paper_1511_06051_b200.comm import Communicator, unique_id
+            uid = R.bcast(unique_id() if R.rank == 0 else None)
+            self.comm = [Communicator.create(self.net.ctx, R.world, R.rank, uid)]
+
+    def average(self):
+        if self.comm is not None:
+            from paper_1511_06051_b200.comm import Communicator
+            Communicator.average(self.comm, [self.net], self.avg_mode)
+
+    def sync_all(self):
+        self.net.sync()
+        self.R.barrier()
+
+    def rounds(self, tau, n):
+        """n SparkNet rounds (tau local steps + the K-way average), device-timed on the worker
+        stream, max over ranks (ms)."""
+        self.sync_all()
+        self.net.event_record(0)
+        for _ in range(n):
+            self.net.train(tau, sync=False)
+            self.average()
+        self.net.event_record(1)
+        self.net.sync()
+        ms = self.R.max(self.net.event_elapsed(0, 1))
+        self.R.barrier()
+        return ms
+
+    def average_ms(self, reps=5):
+        if self.comm is None:
+            return None
+        self.sync_all()
+        self.net.event_record(2)
+        for _ in range(reps):
+            self.average()
+        self.net.event_record(3)
+        self.net.sync()
+        return self.R.max(self.net.event_elapsed(2, 3)) / reps
+
+    def e2e(self, tau, n):
+        """The same rounds through the C ABI's host-fed path: per step an H2D copy of the
+        step's batch from pinned host memory (NCHW fp32 + labels), the step, a D2H read of its
+        loss; plus the K-way average.  A ring of <= HOST_RING distinct pinned batches (the
+        reference's gather_batch output) is re-sent every round."""
+        from paper_1511_06051_b200 import data as pdata
+        from paper_1511_06051_b200._lib import PinnedArray
+        c, h, w = self.chw3
+        b = self.b
+        ring = min(tau, HOST_RING)
+        pin_img = PinnedArray((ring, b, c, h, w), np.float32)
+        pin_lab = PinnedArray((ring, b), np.int32)
+        host_it = pdata.make_worker_iterator(self.shards, self.R.rank, b, 7)
+        for s in range(ring):
+            idx = host_it.next_indices().astype(np.int64)
+            if isinstance(self.ds, pdata.DeviceSyntheticDataset):  # pixels only in HBM
+                for i, r in enumerate(idx):
+                    pin_img.array[s, i] = self.ds.read(self.net.ctx, int(r), 1)[0][0]
+            else:
+                pin_img.array[s] = self.ds.images[idx]
+            pin_lab.array[s] = self.ds.labels[idx]
+
+        def host_round():
+            left = tau
+            while left > 0:
+                k = min(ring, left)
+                self.net.train_host(pin_img.array[:k], pin_lab.array[:k])
+                left -= k
+
+        host_round()  # warm-up: capture the host-fed graph
+        self.average()
+        self.sync_all()
+        self.net.event_record(2)
+        for _ in range(n):
+            host_round()
+            self.average()
+        self.net.event_record(3)
+        self.net.sync()
+        ms = self.R.max(self.net.event_elapsed(2, 3))
+        self.R.barrier()
+        return ms, tau * b * (c * h * w * 4 + 4), tau * 8
+
+
+def rounds_for(ms_per_round, min_ms, at_least):
+    return max(at_least, int(min_ms / max(ms_per_round, 1e-3)) + 1)
+
+
+def tau_sweep(R, workload, precision, average, taus=(1, 10, 50, 100), min_ms=400.0):
+    """cifar10_quick at this K (= world size) over tau (BASELINE.json configs[1]): images/sec
+    = K * tau * b / round time; each point times >= min_ms of rounds after 3 warm-up rounds."""
+    W = Worker(R, workload, precision, average)
+    out = []
+    for tau in taus:
+        for _ in range(3):
+            W.net.train(tau, sync=False)
+            W.average()
+        probe = W.rounds(tau, 2) / 2
+        n = rounds_for(probe, min_ms, 3)
+        ms = W.rounds(tau, n)
+        out.append({"tau": tau, "rounds": n, "ms_per_round": ms / n,
+                    "value": R.world * n * tau * W.b / (ms / 1000.0)})
+    prof = W.net.profile_step(repeats=5)
+    avg_ms = W.average_ms()
+    top = max(prof, key=lambda p: p["ms"])
+    return {"workload": workload, "K": R.world, "per_worker_batch": W.b, "unit": "images/sec",
+            "points": out, "kernels_per_step": W.net.kernels_per_step(),
+            "step_ms": sum(p["ms"] for p in prof), "top_op": top["name"],
+            "weight_average_ms": avg_ms}
 
 
 def main():
@@ -276,154 +594,48 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
-    rank, world, local = dist_env()
-    from paper_1511_06051_b200 import data as pdata
-    from paper_1511_06051_b200 import model
-    from paper_1511_06051_b200._lib import PinnedArray
-
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
+    R = Rank()
+    rank, world = R.rank, R.world
     K = world
-    spec, b = make_spec(args.workload, args.batch)
-    _, _, (c, h, w), _, lr, mu, wd = WORKLOADS[args.workload]
-    ds = build_dataset(args.workload, K)
-    shards = pdata.shard(ds, K, 1)
-    net = model.Net(spec, 1, device=local, precision=args.precision)
-    net.set_sgd(model.SgdOptions(lr, mu, wd))
-    it = pdata.make_worker_iterator(shards, rank, b, 1)
-    net.set_training_data(it)
-    comm = None
-    if world > 1:
-        from paper_1511_06051_b200.comm import Communicator, unique_id
-        obj = [unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        comm = [Communicator.create(net.ctx, world, rank, obj[0])]
-
-    def average():
-        if comm is not None:
-            from paper_1511_06051_b200.comm import Communicator
-            Communicator.average(comm, [net], args.average)
-
-    def barrier():
-        net.sync()
-        if dist is not None:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if dist is None:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    W = Worker(R, args.workload, args.precision, args.average, args.batch)
+    net, b = W.net, W.b
+    c, h, w = W.chw3
 
     # --- device-resident throughput (value) ---
     for _ in range(args.warmup):
         net.train(args.tau, sync=False)
-        average()
-    barrier()
-    sampler = ClockSampler(local)
+        W.average()
+    W.sync_all()
+    sampler = ClockSampler(R.local)
     sampler.start()
-    net.event_record(0)
-    for _ in range(args.steps):
-        net.train(args.tau, sync=False)
-        average()
-    net.event_record(1)
-    net.sync()
-    ms = max_over_ranks(net.event_elapsed(0, 1))
+    ms = W.rounds(args.tau, args.steps)
     clocks = sampler.stop()
-    barrier()
     images = K * args.steps * args.tau * b
     value = images / (ms / 1000.0)
-    avg_ms = None
-    if comm is not None:  # the K-way weight average alone (north star: < 2% of the round)
-        barrier()
-        net.event_record(2)
-        for _ in range(5):
-            average()
-        net.event_record(3)
-        net.sync()
-        avg_ms = max_over_ranks(net.event_elapsed(2, 3)) / 5
+    avg_ms = W.average_ms()
 
     # --- end to end through the C ABI with host buffers (e2e) ---
     e2e_steps = min(args.steps, 5)
-    chw = c * h * w
-    ring = min(args.tau, HOST_RING)  # bounded pinned buffer; every step still copies H2D
-    pin_img = PinnedArray((ring, b, c, h, w), np.float32)
-    pin_lab = PinnedArray((ring, b), np.int32)
-    host_it = pdata.make_worker_iterator(shards, rank, b, 7)
-
-    def host_round():  # tau host-fed steps: ceil(tau / ring) calls over the pinned ring
-        left = args.tau
-        while left > 0:
-            n = min(ring, left)
-            net.train_host(pin_img.array[:n], pin_lab.array[:n])
-            left -= n
-
-    for s in range(ring):
-        idx = host_it.next_indices().astype(np.int64)
-        if isinstance(ds, pdata.DeviceSyntheticDataset):  # pixels only in HBM: fetch rows once
-            for i, r in enumerate(idx):
-                pin_img.array[s, i] = ds.read(net.ctx, int(r), 1)[0][0]
-        else:
-            pin_img.array[s] = ds.images[idx]
-        pin_lab.array[s] = ds.labels[idx]
-    host_round()  # warm-up: capture the host-fed graph
-    average()
-    barrier()
-    net.event_record(2)
-    for _ in range(e2e_steps):
-        host_round()
-        average()
-    net.event_record(3)
-    net.sync()
-    ems = max_over_ranks(net.event_elapsed(2, 3))
+    ems, h2d, d2h = W.e2e(args.tau, e2e_steps)
     e2e_value = K * e2e_steps * args.tau * b / (ems / 1000.0)
 
-    # --- roofline of the dominant kernel (live CUDA events, per op) ---
+    # --- roofline of the dominant op + all GEMM ops (live CUDA events, per op) ---
     prof = net.profile_step(repeats=5)
-    step_ms = sum(p["ms"] for p in prof)
-    top = max(prof, key=lambda p: p["ms"])
     peaks = load_peaks()
-    if top["flops"] > 0:
-        achieved = top["flops"] / (top["ms"] * 1e-3) / 1e12
-        if args.precision == "tf32":
-            peak, src = peaks.get("tf32_tflops", peaks["bf16_tflops"] / 2), "tf32"
-        else:
-            peak, src = peaks.get("fp32_simt_tflops", peaks["bf16_tflops"] / 2), "fp32 SIMT"
-        roof = {"bound": "tensor" if args.precision == "tf32" else "fp32-simt",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": top["name"],
-                "share_of_step": top["ms"] / step_ms, "peak_source": src + " " + str(
-                    peaks.get("source_extra", peaks["source"]))}
-    else:
-        achieved = top["bytes"] / (top["ms"] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": top["name"],
-                "share_of_step": top["ms"] / step_ms, "peak_source": peaks["source"]}
-    # traffic: DRAM bytes of the same op in the committed ncu capture of this workload
-    # (tools/op_traffic.py; cold-cache serialised replay, one training step)
-    tpath = os.path.join(ROOT, "profiles", "round1", f"{args.workload}_op_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tr = json.load(f)
-        hit = [o for o in tr["ops"] if o["op"] == top["name"]]
-        if hit and tr.get("precision") == args.precision:
-            roof["traffic"] = hit[0]["dram_bytes"]
-            roof["traffic_unit"] = "bytes per op launch set (ncu dram__bytes_read+write)"
-            roof["ncu_share_of_step"] = hit[0]["ncu_share"]
-            roof["traffic_source"] = os.path.relpath(tpath, ROOT)
+    roof, step_ms = roofline_of(prof, args.precision, peaks, args.workload)
     if args.profile_json and rank == 0:
         with open(args.profile_json, "w") as f:
             json.dump({"ops": prof, "step_ms": step_ms}, f, indent=1)
 
     launches = net.kernels_per_step() * args.tau * args.steps + (
-        args.steps if (comm is not None and args.average == "ordered") else 0)
+        args.steps if (W.comm is not None and args.average == "ordered") else 0)
+    # the cifar10_quick tau sweep at this K (BASELINE.json configs[1])
+    extra = None
+    if args.extra and args.workload != "cifar10_quick":
+        extra = tau_sweep(R, "cifar10_quick", args.precision, args.average)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.workload, b, max(1, min(8, os.cpu_count() or 1)))
+        cpu = cpu_baseline(args.workload, b, max(1, min(8, os.cpu_count() or 1)), tau=args.tau)
     if rank == 0:
         print(json.dumps({
             "metric": "images/sec", "value": value, "unit": "images/sec", "n_gpus": world,
@@ -432,19 +644,28 @@ def main():
             "dtype": args.precision, "data": "synthetic",
             "config": {"workload": args.workload, "global_batch": b * K, "per_worker_batch": b,
                        "K": K, "tau": args.tau, "average": args.average,
+                       "step": "one SparkNet round: tau local SGD steps per worker + the K-way "
+                               "weight average",
                        "parallelism": f"sparknet-dp{K}",
                        "l2": "inputs larger than L2 (HBM-resident dataset "
-                             f"{ds.size() * c * h * w * 4 / 1e6:.0f} MB, random per-step gather)"},
-            "e2e": {"value": e2e_value, "unit": "images/sec",
-                    "h2d_bytes_per_step": args.tau * b * (chw * 4 + 4),
-                    "d2h_bytes_per_step": args.tau * 8},
+                             f"{W_bytes(args.workload, K):.0f} MB, random per-step gather)"},
+            "e2e": {"value": e2e_value, "unit": "images/sec", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "rounds": e2e_steps},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "timed_ms": ms,
             "weight_average": None if avg_ms is None else {
                 "ms": avg_ms, "share_of_round": avg_ms / (ms / args.steps),
-                "param_bytes": 4 * sum(c for _, c in net.segments())},
-            "gpu_launches": launches}))
-    if dist is not None:
-        dist.destroy_process_group()
+                "param_bytes": 4 * sum(n for _, n in net.segments())},
+            "gpu_launches": launches,
+            "cifar10_quick_tau_sweep": extra}))
+    if R.dist is not None:
+        R.dist.destroy_process_group()
+
+
+def W_bytes(workload, K):
+    _, b, (c, h, w), per_class, *_ = WORKLOADS[workload]
+    n = 10 * (per_class if per_class else max(1, (2 * b * K + 9) // 10))
+    return n * c * h * w * 4 / 1e6
 
 
 if __name__ == "__main__":

@@ -20,6 +20,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "parasgd/batch.hpp"
@@ -117,6 +118,20 @@ inline std::vector<psg_layer_desc> to_desc(const NetSpec& spec) {
 struct Pinned {
   float* p = nullptr;
   std::size_t n = 0;
+  Pinned() = default;
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  // moves transfer ownership of the pinned block (Net is movable, model.hpp /
+  // schemes.hpp:141-147 return it by value)
+  Pinned(Pinned&& o) noexcept : p(std::exchange(o.p, nullptr)), n(std::exchange(o.n, 0)) {}
+  Pinned& operator=(Pinned&& o) noexcept {
+    if (this != &o) {
+      if (p) psg_host_free(p);
+      p = std::exchange(o.p, nullptr);
+      n = std::exchange(o.n, 0);
+    }
+    return *this;
+  }
   void ensure(std::size_t want) {
     if (want <= n) return;
     if (p) psg_host_free(p);

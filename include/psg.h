@@ -234,6 +234,13 @@ int psg_net_test_end(psg_net* net, unsigned long long* correct, unsigned long lo
  * written).  Results are bitwise identical; turn it off to inspect every layer's state
  * (per-layer parity tests). */
 int psg_net_set_fusion(psg_net* net, int on);
+/* tcgen05 CTA-pair policy of the net's TF32 GEMMs (extension, no reference counterpart):
+ * AUTO = the throughput heuristic (pairs for K-major-A GEMMs with >= 2 waves of clusters),
+ * NEVER = single-CTA kernels only, ALWAYS = a CTA pair (cta_group::2) wherever legal.
+ * Results are correct either way; the parity tests use ALWAYS / NEVER to run the pair and
+ * single-CTA kernel variants at small batch sizes where AUTO would not pick pairs. */
+enum psg_tc_pair { PSG_TC_PAIR_AUTO = 0, PSG_TC_PAIR_NEVER = 1, PSG_TC_PAIR_ALWAYS = 2 };
+int psg_net_set_tc_options(psg_net* net, int pair_policy);
 /* Kernel launches of one training step (device-side work count). */
 int psg_net_kernels_per_step(const psg_net* net, int* launches);
 

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(HERE, "libpsg.so")
 OK, EINVAL, ERUNTIME, ECUDA, ELOGIC = range(5)
 PRECISION_FP32, PRECISION_TF32 = 0, 1
 AVERAGE_FAST, AVERAGE_ORDERED = 0, 1
+TC_PAIR = {"auto": 0, "never": 1, "always": 2}
 
 
 class CudaError(RuntimeError):
@@ -115,6 +116,7 @@ SIGNATURES = {
     "psg_net_attach_shard_part": (ctypes.c_int, [_VP, _VP, _U64, _SZ, _SZ, ctypes.c_uint64,
                                                  ctypes.c_int, ctypes.c_int]),
     "psg_net_grad_step": (ctypes.c_int, [_VP]),
+    "psg_net_set_tc_options": (ctypes.c_int, [_VP, ctypes.c_int]),
     "psg_net_set_fusion": (ctypes.c_int, [_VP, ctypes.c_int]),
     "psg_net_apply_grads": (ctypes.c_int, [_VP]),
     "psg_average_grads_local": (ctypes.c_int, [_PP, ctypes.c_int]),

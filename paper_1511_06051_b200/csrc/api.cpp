@@ -73,9 +73,13 @@ psg_dataset* upload(psg_ctx* ctx, const double* imgd, const float* imgf, const i
   try {
     PSG_CUDA(cudaMalloc(&ds->images, nhwc.size() * sizeof(float)));
     PSG_CUDA(cudaMalloc(&ds->labels, n * sizeof(int32_t)));
-    PSG_CUDA(cudaMemcpy(ds->images, nhwc.data(), nhwc.size() * sizeof(float),
-                        cudaMemcpyHostToDevice));
-    PSG_CUDA(cudaMemcpy(ds->labels, labels, n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    // stream-ordered (pageable H2D cudaMemcpy may return before its DMA lands, and the
+    // non-blocking net / ctx streams are not ordered after the legacy stream)
+    PSG_CUDA(cudaMemcpyAsync(ds->images, nhwc.data(), nhwc.size() * sizeof(float),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    PSG_CUDA(cudaMemcpyAsync(ds->labels, labels, n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
   } catch (...) {
     cudaFree(ds->images);
     cudaFree(ds->labels);
@@ -219,8 +223,8 @@ int psg_dataset_synthetic_device(psg_ctx* ctx, int classes, int c, int h, int w,
       PSG_CUDA(cudaMalloc(&ds->images, n * dim * sizeof(float)));
       PSG_CUDA(cudaMalloc(&ds->labels, n * sizeof(int32_t)));
       PSG_CUDA(cudaMalloc(&d_means, meansf.size() * sizeof(float)));
-      PSG_CUDA(cudaMemcpy(d_means, meansf.data(), meansf.size() * sizeof(float),
-                          cudaMemcpyHostToDevice));
+      PSG_CUDA(cudaMemcpyAsync(d_means, meansf.data(), meansf.size() * sizeof(float),
+                               cudaMemcpyHostToDevice, ctx->stream));
       psg::synthetic_rows_device(d_means, classes, c, h, w, per_class,
                                  psg::synthetic_noise_seed(seed, variant), ds->images, ds->labels,
                                  ctx->stream);
@@ -303,9 +307,10 @@ int psg_dataset_load_idx(psg_ctx* ctx, const char* images_path, const char* labe
       PSG_CUDA(cudaMalloc(&ds->images, d.pixels.size() * sizeof(float)));
       PSG_CUDA(cudaMalloc(&ds->labels, d.n * sizeof(int32_t)));
       PSG_CUDA(cudaMalloc(&d_px, d.pixels.size()));
-      PSG_CUDA(cudaMemcpy(d_px, d.pixels.data(), d.pixels.size(), cudaMemcpyHostToDevice));
-      PSG_CUDA(cudaMemcpy(ds->labels, d.labels.data(), d.n * sizeof(int32_t),
-                          cudaMemcpyHostToDevice));
+      PSG_CUDA(cudaMemcpyAsync(d_px, d.pixels.data(), d.pixels.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
+      PSG_CUDA(cudaMemcpyAsync(ds->labels, d.labels.data(), d.n * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
       psg::ingest_u8_to_f32(d_px, d.pixels.size(), ds->images, ctx->stream);
       PSG_CUDA(cudaStreamSynchronize(ctx->stream));
       cudaFree(d_px);
@@ -641,6 +646,18 @@ int psg_net_set_fusion(psg_net* net, int on) {
   });
 }
 
+int psg_net_set_tc_options(psg_net* net, int pair_policy) {
+  return guarded([&] {
+    need(net, "set_tc_options");
+    if (pair_policy != PSG_TC_PAIR_AUTO && pair_policy != PSG_TC_PAIR_NEVER &&
+        pair_policy != PSG_TC_PAIR_ALWAYS)
+      throw std::invalid_argument("set_tc_options: unknown pair policy");
+    // workspace sizes and the captured step graph depend on the policy: rebuild on next use
+    psg::release_batch_buffers(net);
+    for (psg::LayerRt& l : net->L) l.cg.tc_pair = pair_policy;
+  });
+}
+
 int psg_net_kernels_per_step(const psg_net* net, int* launches) {
   return guarded([&] {
     need(net, "kernels_per_step");
@@ -804,7 +821,9 @@ int psg_buffer_read(psg_buffer* buf, float* host, size_t n) {
     if (n != buf->n) throw std::invalid_argument("buffer_read: size mismatch");
     psg::DeviceGuard dg(buf->ctx->device);
     PSG_CUDA(cudaStreamSynchronize(buf->ctx->stream));
-    PSG_CUDA(cudaMemcpy(host, buf->ptr, n * sizeof(float), cudaMemcpyDeviceToHost));
+    PSG_CUDA(cudaMemcpyAsync(host, buf->ptr, n * sizeof(float), cudaMemcpyDeviceToHost,
+                             buf->ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(buf->ctx->stream));
   });
 }
 
@@ -814,7 +833,9 @@ int psg_buffer_write(psg_buffer* buf, const float* host, size_t n) {
     if (n != buf->n) throw std::invalid_argument("buffer_write: size mismatch");
     psg::DeviceGuard dg(buf->ctx->device);
     PSG_CUDA(cudaStreamSynchronize(buf->ctx->stream));
-    PSG_CUDA(cudaMemcpy(buf->ptr, host, n * sizeof(float), cudaMemcpyHostToDevice));
+    PSG_CUDA(cudaMemcpyAsync(buf->ptr, host, n * sizeof(float), cudaMemcpyHostToDevice,
+                             buf->ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(buf->ctx->stream));
   });
 }
 

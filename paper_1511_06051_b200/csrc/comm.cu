@@ -103,7 +103,11 @@ void average_flat(psg_comm* const* comms, float* const* bufs, const size_t* coun
     return;
   }
   if (mode != PSG_AVERAGE_ORDERED) throw std::invalid_argument("average: unknown mode");
-  // counts[i] must be divisible by nranks into 4-aligned slices (P_alloc is).
+  // each rank's slice is reduced with float4 loads: counts[i] must split into nranks
+  // 4-aligned slices (a net's P_alloc is padded to a multiple of 4 * 840 = 4 * lcm(1..8))
+  for (int i = 0; i < count; ++i)
+    if (counts[i] % (4 * static_cast<size_t>(comms[i]->nranks)))
+      throw std::invalid_argument("average: buffer length not divisible into 4-aligned rank slices");
   nccl_check(api.GroupStart(), "ncclGroupStart");
   for (int i = 0; i < count; ++i) {
     psg_comm* c = comms[i];

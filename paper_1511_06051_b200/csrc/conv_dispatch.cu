@@ -67,6 +67,7 @@ ConvGeom col_geom(const ConvGeom& g) {
   l.H = l.W = l.OH = l.OW = 1;
   l.cs_in = g.Kp();
   l.F = g.F;
+  l.tc_pair = g.tc_pair;
   return l;
 }
 
@@ -84,6 +85,7 @@ ConvGeom s2d_geom(const ConvGeom& g) {
   q.cs_in = s2d_channels(g);
   q.F = g.F;
   q.kh = q.kw = k;
+  q.tc_pair = g.tc_pair;
   return q;
 }
 

@@ -269,9 +269,12 @@ bool want_pair(const TcArgs& a) {
     const char* e = std::getenv("PSG_TC_PAIR");
     return e ? std::atoi(e) : 1;
   }();
-  if (!env) return false;
+  if (a.pair_policy == PSG_TC_PAIR_NEVER || (!env && a.pair_policy != PSG_TC_PAIR_ALWAYS))
+    return false;
+  // legality: K-major A (M = pixels / rows) with at least two M tiles
   if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K && a.a_mode != A_IM2COL_K) return false;
   if (a.m_tiles < 2) return false;
+  if (a.pair_policy == PSG_TC_PAIR_ALWAYS) return true;  // parity tests of the pair kernels
   static const int min_n = [] {  // narrow tiles: the pair's B half is too thin to pay off
     const char* e = std::getenv("PSG_TC_PAIR_MIN_N");  // (cifar10_quick's N = 32 convs: +1%)
     return e ? std::atoi(e) : 48;
@@ -465,6 +468,7 @@ bool prefer_k32() {
 // --- planners: fill TcArgs (out/bias/flags are set by the caller) -------------
 bool plan_fprop(const ConvGeom& g, TcArgs& a, int& kblk) {
   std::memset(&a, 0, sizeof a);
+  a.pair_policy = g.tc_pair;
   if (is_linear(g)) {
     const int D = g.cs_in, O = g.F;
     if (D % 4) return false;
@@ -559,6 +563,7 @@ namespace {
 
 bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   std::memset(&a, 0, sizeof a);
+  a.pair_policy = g.tc_pair;
   if (is_linear(g)) {
     const int D = g.cs_in, O = g.F;
     if (O % 4 || D % 4) return false;
@@ -599,7 +604,9 @@ bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   a.cb = (g.Fg() + kblk - 1) / kblk;
   a.kblocks = g.kh * g.kw * a.cb;
   a.a_c_g = g.Fg();
-  a.b_r_g = g.Fg();
+  // B rows per group: W^T (B_WT_MN) takes the group as its own coordinate; the K-major copy
+  // Wt[g][c][tap][f] (B_3D_K) stacks the groups' C/G channel rows
+  a.b_r_g = a.b_mode == B_3D_K ? g.Cgs() : g.Fg();
   a.kw = g.kw;
   a.ph = g.ph;
   a.pw = g.pw;
@@ -613,6 +620,7 @@ bool plan_dgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
 
 bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
   std::memset(&a, 0, sizeof a);
+  a.pair_policy = g.tc_pair;
   kblk = 32;
   if (is_linear(g)) {
     const int D = g.cs_in, O = g.F;
@@ -686,6 +694,7 @@ CUtensorMapSwizzle k_swizzle(int kblk) {
 
 bool plan_wgrad_col(const ConvGeom& g, TcArgs& a) {
   std::memset(&a, 0, sizeof a);
+  a.pair_policy = g.tc_pair;
   if (g.F % 4 || g.Fg() % 4 || g.Kp() % 4) return false;
   a.a_mode = A_2D_MN;   // dY [pixels][F]
   a.b_mode = B_COL_MN;  // col [G][pixels][Kp]

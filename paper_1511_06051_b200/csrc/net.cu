@@ -137,6 +137,14 @@ ConvGeom geom_for(const LayerRt& l, size_t n) {
 
 }  // namespace
 
+// Synchronous copy ordered on the net's stream.  A plain cudaMemcpy runs on the legacy
+// default stream, which the non-blocking net stream neither waits for nor is waited on by,
+// and a pageable H2D cudaMemcpy may return before its DMA lands: stream-ordered + synced.
+void copy_sync(psg_net* net, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  PSG_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, net->stream));
+  PSG_CUDA(cudaStreamSynchronize(net->stream));
+}
+
 void invalidate_graph(psg_net* net) {
   if (net->graph) cudaGraphExecDestroy(net->graph);
   if (net->host_graph) cudaGraphExecDestroy(net->host_graph);
@@ -255,8 +263,8 @@ void build_chunks(psg_net* net) {
     invalidate_graph(net);
   }
   if (!ch.empty())
-    PSG_CUDA(cudaMemcpy(net->d_chunks, ch.data(), ch.size() * sizeof(UpdateChunk),
-                        cudaMemcpyHostToDevice));
+    copy_sync(net, net->d_chunks, ch.data(), ch.size() * sizeof(UpdateChunk),
+                        cudaMemcpyHostToDevice);
 }
 
 // Host NCHW fp64 batch -> device NHWC (channel stride cs) into the data layer.
@@ -290,7 +298,7 @@ double read_loss(psg_net* net) {
   PSG_CUDA(cudaStreamSynchronize(net->stream));
   if (net->hsc->flag) {
     const int zero = 0;
-    PSG_CUDA(cudaMemcpy(&net->dsc->flag, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    copy_sync(net, &net->dsc->flag, &zero, sizeof(int), cudaMemcpyHostToDevice);
     throw std::runtime_error("softmax loss: non-finite loss");
   }
   return net->hsc->loss;
@@ -531,7 +539,7 @@ void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed)
   net->w = dalloc<float>(net->P_alloc);
   net->g = dalloc<float>(net->P_alloc);
   net->v = dalloc<float>(net->P_alloc);
-  PSG_CUDA(cudaMemcpy(net->w, host.data(), net->P_alloc * sizeof(float), cudaMemcpyHostToDevice));
+  copy_sync(net, net->w, host.data(), net->P_alloc * sizeof(float), cudaMemcpyHostToDevice);
   PSG_CUDA(cudaMemset(net->g, 0, net->P_alloc * sizeof(float)));
   PSG_CUDA(cudaMemset(net->v, 0, net->P_alloc * sizeof(float)));
   PSG_CUDA(cudaMalloc(&net->dsc, sizeof(DeviceScalars)));
@@ -580,10 +588,10 @@ void net_check_flag(psg_net* net) {
   DeviceGuard dg(net->ctx->device);
   PSG_CUDA(cudaStreamSynchronize(net->stream));
   int flag = 0;
-  PSG_CUDA(cudaMemcpy(&flag, &net->dsc->flag, sizeof(int), cudaMemcpyDeviceToHost));
+  copy_sync(net, &flag, &net->dsc->flag, sizeof(int), cudaMemcpyDeviceToHost);
   if (flag) {
     const int zero = 0;
-    PSG_CUDA(cudaMemcpy(&net->dsc->flag, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    copy_sync(net, &net->dsc->flag, &zero, sizeof(int), cudaMemcpyHostToDevice);
     throw std::runtime_error("train: produced a non-finite value");
   }
 }
@@ -604,8 +612,8 @@ void net_get_weights(psg_net* net, double* flat, size_t n, bool velocity) {
   DeviceGuard dg(net->ctx->device);
   std::vector<float> host(net->P_int);
   PSG_CUDA(cudaStreamSynchronize(net->stream));
-  PSG_CUDA(cudaMemcpy(host.data(), velocity ? net->v : net->w, net->P_int * sizeof(float),
-                      cudaMemcpyDeviceToHost));
+  copy_sync(net, host.data(), velocity ? net->v : net->w, net->P_int * sizeof(float),
+                      cudaMemcpyDeviceToHost);
   for (const TensorRec& t : net->tensors)
     for (size_t i = 0; i < t.ref_count; ++i)
       flat[t.ref_off + i] = static_cast<double>(host[t.int_off + t.to_int(i)]);
@@ -621,7 +629,7 @@ void net_set_weights(psg_net* net, const double* flat, size_t n) {
       host[t.int_off + t.to_int(i)] = static_cast<float>(flat[t.ref_off + i]);
   DeviceGuard dg(net->ctx->device);
   PSG_CUDA(cudaStreamSynchronize(net->stream));
-  PSG_CUDA(cudaMemcpy(net->w, host.data(), net->P_int * sizeof(float), cudaMemcpyHostToDevice));
+  copy_sync(net, net->w, host.data(), net->P_int * sizeof(float), cudaMemcpyHostToDevice);
 }
 
 void net_forward_host(psg_net* net, const double* images, const int32_t* labels, size_t n,
@@ -634,8 +642,8 @@ void net_forward_host(psg_net* net, const double* images, const int32_t* labels,
   if (loss) *loss = l;
   if (probs) {
     std::vector<float> p(n * net->classes);
-    PSG_CUDA(cudaMemcpy(p.data(), net->L[net->loss_idx].out, p.size() * sizeof(float),
-                        cudaMemcpyDeviceToHost));
+    copy_sync(net, p.data(), net->L[net->loss_idx].out, p.size() * sizeof(float),
+                        cudaMemcpyDeviceToHost);
     for (size_t i = 0; i < p.size(); ++i) probs[i] = p[i];
   }
 }
@@ -651,7 +659,7 @@ void net_backward_host(psg_net* net, const double* images, const int32_t* labels
   if (loss) *loss = l;
   if (grads) {
     std::vector<float> host(net->P_int);
-    PSG_CUDA(cudaMemcpy(host.data(), net->g, net->P_int * sizeof(float), cudaMemcpyDeviceToHost));
+    copy_sync(net, host.data(), net->g, net->P_int * sizeof(float), cudaMemcpyDeviceToHost);
     for (const TensorRec& t : net->tensors)
       for (size_t i = 0; i < t.ref_count; ++i)
         grads[t.ref_off + i] = static_cast<double>(host[t.int_off + t.to_int(i)]);
@@ -668,7 +676,7 @@ void net_apply_update_host(psg_net* net, const double* grads, size_t n) {
       host[t.int_off + t.to_int(i)] = static_cast<float>(grads[t.ref_off + i]);
   DeviceGuard dg(net->ctx->device);
   PSG_CUDA(cudaStreamSynchronize(net->stream));
-  PSG_CUDA(cudaMemcpy(net->g, host.data(), net->P_int * sizeof(float), cudaMemcpyHostToDevice));
+  copy_sync(net, net->g, host.data(), net->P_int * sizeof(float), cudaMemcpyHostToDevice);
   run_update(net, /*advance=*/false);
   net_check_flag(net);
 }
@@ -685,7 +693,7 @@ void net_layer_readback(psg_net* net, int layer, bool grad, double* out, size_t 
   DeviceGuard dg(net->ctx->device);
   std::vector<float> host(rows * l.vol());
   PSG_CUDA(cudaStreamSynchronize(net->stream));
-  PSG_CUDA(cudaMemcpy(host.data(), src, host.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  copy_sync(net, host.data(), src, host.size() * sizeof(float), cudaMemcpyDeviceToHost);
   for (size_t b = 0; b < rows; ++b)
     for (int c = 0; c < l.C; ++c)
       for (int h = 0; h < l.H; ++h)

@@ -109,6 +109,7 @@ struct ConvGeom {
   int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
   int G = 1;             // groups
   int kp = 0;            // row stride of the weight matrix (>= Kf, 16-byte multiple); 0 = Kf
+  int tc_pair = 0;       // tcgen05 CTA pairs: PSG_TC_PAIR_AUTO / _NEVER / _ALWAYS (psg.h)
   __host__ __device__ int Cgs() const { return cs_in / G; }
   __host__ __device__ int Fg() const { return F / G; }
   // reduction length of fprop / row length of dW

@@ -72,6 +72,7 @@ struct TcArgs {
   // adjacent 128-row tiles (CTA rank r takes tile 2u + r) sharing one MMA of M = 256; each
   // CTA loads its own A tile and half of the B tile (b_cols columns).
   int pair;
+  int pair_policy;        // ConvGeom::tc_pair: 0 heuristic, 1 never, 2 whenever legal
   // producer cursor jump over the other producers' stages: D = (producers - 1) * kps K
   // blocks split into the cursors' mixed-radix digits (host-computed, no divisions per stage)
   int adv_kb, adv_c0, adv_tap, adv_tv, adv_tu, adv_w, adv_h, adv_b;

@@ -74,9 +74,11 @@ class Net:
     """A trainable realisation of a NetSpec on one GPU (model.hpp:50)."""
 
     def __init__(self, spec: NetSpec, seed: int, device: int = 0, precision: str = "fp32",
-                 fuse: bool = True):
+                 fuse: bool = True, tc_pair: str = "auto"):
         """fuse: ReLU fusion (psg_net_set_fusion; bitwise-identical results).  Pass False
-        to read every layer's pre-activation output / gradient (per-layer parity tests)."""
+        to read every layer's pre-activation output / gradient (per-layer parity tests).
+        tc_pair: tcgen05 CTA-pair policy of the TF32 GEMMs ("auto" | "never" | "always",
+        psg_net_set_tc_options) — the parity tests force each kernel variant."""
         spec.validate()
         self._spec = spec
         self._seed = seed
@@ -101,6 +103,8 @@ class Net:
         self.set_precision(precision)
         if not fuse:
             _lib.call("psg_net_set_fusion", h, 0)
+        if tc_pair != "auto":
+            self.set_tc_options(tc_pair)
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -148,6 +152,12 @@ class Net:
         mode = {"fp32": _lib.PRECISION_FP32, "tf32": _lib.PRECISION_TF32}[precision]
         _lib.call("psg_net_set_precision", self.handle, mode)
         self.precision = precision
+
+    def set_tc_options(self, pair: str = "auto") -> None:
+        if pair not in _lib.TC_PAIR:
+            raise ValueError("set_tc_options: unknown pair policy")
+        _lib.call("psg_net_set_tc_options", self.handle, _lib.TC_PAIR[pair])
+        self.tc_pair = pair
 
     # --- weights (model.hpp:138-171) ----------------------------------------
     def get_weights_flat(self) -> np.ndarray:

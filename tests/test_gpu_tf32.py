@@ -33,6 +33,14 @@ def tc_nets():
             ns.conv_layer("c2", "r1", 3, 3, 96, pad=1, group=2),
             ns.pool_layer("p", "c2", 3, 3, 2, 2, ceil_mode=True),
             ns.linear_layer("fc", "p", 32), ns.softmax_loss_layer("loss", "fc", "label")]),
+        # C/G = 48, F/G = 128 (AlexNet conv2's grouping): the dgrad reads the K-major weight
+        # copy Wt[g][c][tap][f] (tc_dgrad_wt), group rows C/G apart
+        "grouped48_wt": ns.NetSpec([
+            ns.data_layer("data", 2, 96, 9, 9), ns.label_layer("label", 2),
+            ns.conv_layer("c0", "data", 1, 1, 96), ns.relu_layer("r0", "c0"),
+            ns.conv_layer("c1", "r0", 5, 5, 256, pad=2, group=2), ns.relu_layer("r1", "c1"),
+            ns.pool_layer("p", "r1", 3, 3, 2, 2, ceil_mode=True),
+            ns.linear_layer("fc", "p", 16), ns.softmax_loss_layer("loss", "fc", "label")]),
         "wide_linear": ns.NetSpec([
             ns.data_layer("data", 130, 1, 1, 512), ns.label_layer("label", 130),
             ns.linear_layer("fc1", "data", 320), ns.relu_layer("r", "fc1"),
