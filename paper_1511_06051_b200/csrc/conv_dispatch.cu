@@ -72,7 +72,17 @@ ConvGeom col_geom(const ConvGeom& g) {
 }
 
 // ---- space-to-depth route ----
-int s2d_channels(const ConvGeom& g) { return (g.sh * g.sh * g.Cgs() + 15) / 16 * 16; }
+// x' channels: s*s*C rounded up to a multiple of 16 (16-float K blocks), or of 32 when that
+// is more than one 32-block (AlexNet conv1: 48 -> 64, 128-byte rows / SWIZZLE_128B K
+// blocks; PSG_S2D_C32=0 keeps 48)
+int s2d_channels(const ConvGeom& g) {
+  static const bool c32 = [] {
+    const char* e = std::getenv("PSG_S2D_C32");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  const int c = g.sh * g.sh * g.Cgs();
+  return c32 && c > 32 ? (c + 31) / 32 * 32 : (c + 15) / 16 * 16;
+}
 
 ConvGeom s2d_geom(const ConvGeom& g) {
   const int s = g.sh, k = (g.kh + s - 1) / s;
@@ -169,8 +179,14 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
         for (int c = 0; c < C; ++c) o[dx * C + c] = ok ? __ldg(xr + iw * ps + c * cst) : 0.f;
       }
     }
-    if (dy == s - 1)
-      for (int cp = s * run; cp < q.cs_in; ++cp) out[ws * q.cs_in + cp] = 0.f;
+    if (dy == s - 1) {
+      float* z = out + ws * q.cs_in;
+      int cp = s * run;
+      if (RUN == 12)  // 16-byte aligned channel padding (s * run and cs_in multiples of 4)
+        for (; cp + 4 <= q.cs_in; cp += 4)
+          *reinterpret_cast<float4*>(z + cp) = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (; cp < q.cs_in; ++cp) z[cp] = 0.f;
+    }
   }
 }
 

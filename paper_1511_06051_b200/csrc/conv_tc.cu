@@ -264,6 +264,17 @@ int pick_n_tile(int N) {
 // MN-major B is loaded in 32-column chunks, so each half must be whole chunks (N % 64).
 int sm_count();
 
+// TMA-store epilogue staging chunks per epilogue warp (PSG_TC_EPI_TMA: 0 = direct row stores
+// in every epilogue, 1 or 2 chunks; two let a chunk's smem writes overlap the previous
+// chunk's store but take 16 KB more from the stage ring)
+int epi_tma_bufs() {
+  static const int v = [] {
+    const char* e = std::getenv("PSG_TC_EPI_TMA");
+    return e ? std::max(0, std::min(2, std::atoi(e))) : 1;
+  }();
+  return v;
+}
+
 bool want_pair(const TcArgs& a) {
   static const int env = [] {
     const char* e = std::getenv("PSG_TC_PAIR");
@@ -309,10 +320,14 @@ void finish_args(TcArgs& a, int kblk, int sms) {
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
   a.kps = kps_env ? kps_env : std::max(1, std::min(4, 48 * 1024 / a.stage_bytes));  // ~48 KB
-  a.stages = std::min(8, (225 * 1024 - kEpiBytes) / (a.kps * a.stage_bytes));
+  // TMA-store epilogue (not the multi-tap wgrad's scattered column map): its staging
+  // chunks come out of the stage ring's budget
+  a.epi_tma = !a.cpt && a.row_map == ROW_LINEAR ? epi_tma_bufs() : 0;
+  const int budget = 225 * 1024 - kEpiBytes - (a.epi_tma ? 4 * a.epi_tma * kOutChunkBytes + 1024 : 0);
+  a.stages = std::min(8, budget / (a.kps * a.stage_bytes));
   if (a.stages < 2) {
     a.kps = 1;
-    a.stages = std::min(8, (225 * 1024 - kEpiBytes) / a.stage_bytes);
+    a.stages = std::min(8, budget / a.stage_bytes);
   }
   static const int producers = [] {
     const char* e = std::getenv("PSG_TC_PRODUCERS");
@@ -389,15 +404,28 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   // float4 epilogue stores need 16-byte aligned rows and 4-column-aligned validity bounds
   a.epi_vec = a.ldo % 4 == 0 && a.col_g % 4 == 0 && a.col_tap % 4 == 0 &&
               (a.cpt ? a.cgs % 4 == 0 : a.n_valid % 4 == 0);
-  const size_t smem = static_cast<size_t>(a.stages) * a.kps * a.stage_bytes + 1024;  // + static
+  float* dst = splits > 1 ? ws : a.out;
+  if (!a.epi_vec || reinterpret_cast<uintptr_t>(dst) % 16) a.epi_tma = 0;
+  a.ring_bytes = (a.stages * a.kps * a.stage_bytes + 1023) / 1024 * 1024;
+  CUtensorMap mo;
+  std::memset(&mo, 0, sizeof mo);
+  if (a.epi_tma) {  // out [rows][ldo] or the workspace [splits][rows][ldo], 32 x 32 boxes
+    const uint64_t rows = static_cast<uint64_t>(out_elems / a.ldo);
+    const uint64_t dims[3] = {static_cast<uint64_t>(a.ldo), rows, static_cast<uint64_t>(splits)};
+    const uint64_t str[2] = {static_cast<uint64_t>(a.ldo) * 4, rows * a.ldo * 4};
+    const uint32_t box[3] = {32, 32, 1};
+    mo = make_map(dst, splits > 1 ? 3 : 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  const size_t smem = static_cast<size_t>(a.ring_bytes) + 4 * a.epi_tma * kOutChunkBytes +
+                      1024;  // + alignment of the dynamic base
   const int per = a.pair ? 2 : 1;
   static const bool debug = std::getenv("PSG_TC_DEBUG") != nullptr;
   if (debug)
     std::fprintf(stderr,
                  "tc: a%d b%d pair %d m_tiles %d m_units %d n_tile %d x%d G %d taps %d kblocks %d "
-                 "splits %d kps %d stages %d producers %d smem %zu\n",
+                 "splits %d kps %d stages %d producers %d epi_tma %d smem %zu\n",
                  a.a_mode, a.b_mode, a.pair, a.m_tiles, a.m_units, a.n_tile, a.n_tiles, a.G,
-                 a.taps, a.kblocks, splits, a.kps, a.stages, a.producers, smem);
+                 a.taps, a.kblocks, splits, a.kps, a.stages, a.producers, a.epi_tma, smem);
   const unsigned units =
       static_cast<unsigned>(std::min<long long>(a.total_tiles, sm_count() / per));
   auto go = [&](auto kern) {
@@ -422,7 +450,7 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, a));
+    PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, a));
   };
   // tc_gemm_kernel's EPI: wgrad (multi-tap column map), dgrad (mask / accumulate), fprop
   const int epi = a.cpt ? 2 : (a.mask || a.accumulate) ? 1 : 0;

@@ -95,6 +95,32 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
                 "r"(c2), "r"(c3), "r"(c4), "r"(bar));
 }
 #undef PSG_TMA_ASM
+// TMA stores (smem -> global, bulk-group completion): the epilogue's output chunks.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the smem source of all but the newest `N` committed store groups may be reused
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy smem writes made visible to the async proxy (TMA store source)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // im2col mode (4-D NHWC map from cuTensorMapEncodeIm2col): {c, w, h, n} is the first
 // pixel's traversal position inside the map's bounding box, {off_w, off_h} the filter tap;
 // the box is `pixelsPerColumn` consecutive pixels (W, then H, then N) x channelsPerPixel.

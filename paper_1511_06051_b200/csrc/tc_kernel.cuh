@@ -29,6 +29,9 @@ constexpr int kThreads = 384;
 constexpr int kTileM = 128;
 constexpr int kAccCols = 256;                 // one accumulator: 128 lanes x 256 fp32
 constexpr int kEpiBytes = 2 * kAccCols * 4;  // static smem: the bias of each accumulator's tile
+// TMA-store epilogue staging: per epilogue warp one or two 32 x 32-float chunks
+// (SWIZZLE_128B), 4 KB each
+constexpr int kOutChunkBytes = 32 * 32 * 4;
 
 struct TcArgs {
   int a_mode, b_mode, row_map;
@@ -89,6 +92,12 @@ struct TcArgs {
   // dgrad with the consumer-side ReLU backward folded in: out = (mask > 0 ? acc : 0), mask
   // laid out like out (the ReLU's output = this conv's input), applied before accumulate
   const float* mask;
+  // TMA-store epilogue (fprop / dgrad / linear, ROW_LINEAR, float4-aligned outputs): a warp's
+  // 32 rows x 32 columns go through a swizzled smem chunk and one cp.async.bulk.tensor store
+  // (map_o: out [rows][ldo], or the split-K workspace [splits][rows][ldo]) instead of 32
+  // row-strided float4 runs per store instruction; partial column chunks keep direct stores
+  int epi_tma;             // 0, or the staging chunks per epilogue warp (1 or 2)
+  int ring_bytes;          // stage ring bytes (the staging area follows, 1024-aligned)
 };
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
@@ -316,7 +325,8 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
 template <int KBLK, bool PAIR, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, const TcArgs p) {
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_o, const TcArgs p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -334,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&map_a);
     tc::tma_prefetch(&map_b);
+    if (p.epi_tma) tc::tma_prefetch(&map_o);
     for (int s = 0; s < p.stages; ++s) {
       tc::mbar_init(tc::smem_u32(&full_bar[s]), 1);  // the stage's producer warp, lane 0
       tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
@@ -487,6 +498,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue
     const int ew = warp - kEpiWarp0;
     uint32_t local = 0;
+    uint32_t ochunk = 0;  // TMA-store chunks issued by this warp (staging buffer ochunk % 2)
+    uint8_t* const ostage = smem + p.ring_bytes + ew * p.epi_tma * kOutChunkBytes;
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {
       Tile t = decode_tile(p, tt);
       if (PAIR) t.m = 2 * t.m + rank;
@@ -556,7 +569,61 @@ __global__ void __launch_bounds__(kThreads, 1)
                            : *reinterpret_cast<const float4*>(rowp + col0 + c);
           }
         }
-        if (row_ok) {
+        if (EPI != 2 && p.epi_tma && c0 + 32 <= nvalid) {
+          // whole 32-column chunk: registers -> swizzled smem -> one TMA store of the warp's
+          // 32 rows (rows past the output / split are clipped by the map's bounds)
+          uint8_t* buf = ostage + (p.epi_tma == 2 ? (ochunk & 1) * kOutChunkBytes : 0);
+          if (lane == 0) {  // this buffer's previous store has read it
+            if (p.epi_tma == 2)
+              tc::bulk_wait_read<1>();
+            else
+              tc::bulk_wait_read<0>();
+          }
+          __syncwarp();
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const int c = c0 + 4 * q4;
+            float4 y = make_float4(__uint_as_float(va[4 * q4]), __uint_as_float(va[4 * q4 + 1]),
+                                   __uint_as_float(va[4 * q4 + 2]), __uint_as_float(va[4 * q4 + 3]));
+            if (!p.ws) {
+              if (p.bias) {
+                const float4 bb = *reinterpret_cast<const float4*>(bsh + c);
+                y.x += bb.x; y.y += bb.y; y.z += bb.z; y.w += bb.w;
+                if (p.relu) {
+                  y.x = y.x > 0.f ? y.x : 0.f;
+                  y.y = y.y > 0.f ? y.y : 0.f;
+                  y.z = y.z > 0.f ? y.z : 0.f;
+                  y.w = y.w > 0.f ? y.w : 0.f;
+                }
+              }
+              if (row_ok && mask) {
+                const float4 m = vec_pre ? pre[q4]
+                                         : *reinterpret_cast<const float4*>(mask + row_off + col0 + c);
+                y.x = m.x > 0.f ? y.x : 0.f;
+                y.y = m.y > 0.f ? y.y : 0.f;
+                y.z = m.z > 0.f ? y.z : 0.f;
+                y.w = m.w > 0.f ? y.w : 0.f;
+              }
+              if (row_ok && acc_out) {
+                const float4 o = vec_pre && !mask ? pre[q4]
+                                                  : *reinterpret_cast<const float4*>(rowp + col0 + c);
+                y.x += o.x; y.y += o.y; y.z += o.z; y.w += o.w;
+              }
+            }
+            *reinterpret_cast<float4*>(buf + lane * 128 + ((q4 ^ (lane & 7)) << 4)) = y;
+          }
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int orow = static_cast<int>(out_row - lane);  // the warp's first row
+            if (p.ws)
+              tc::tma_store_3d(&map_o, tc::smem_u32(buf), col0 + c0, orow, t.split);
+            else
+              tc::tma_store_2d(&map_o, tc::smem_u32(buf), col0 + c0, orow);
+            tc::bulk_commit();
+          }
+          ++ochunk;
+        } else if (row_ok) {
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
             const int c = c0 + 4 * q4;  // column within the tile
@@ -641,6 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       else
         mbar_arrive(tc::smem_u32(&tempty_bar[acc]));
     }
+    if (EPI != 2 && p.epi_tma && lane == 0) tc::bulk_wait_all();  // stores done before exit
   }
   tc::fence_before_sync();
   if constexpr (PAIR)

@@ -154,3 +154,78 @@ def test_run_naive_two_gpus_matches_one_gpu(oracle_lib, mode):
             assert max_relative_deviation(a, b) <= STRICT
     if mode == "ordered":
         assert a1 == a2
+
+
+def _mlp_fixture():
+    """schemes_test.cpp:17-37: mlp 8-4-2 on generate_synthetic(2, 1, 1, 8, 60, 3.0, 501),
+    plain SGD lr 0.05 (mu = 0)."""
+    from paper_1511_06051_b200 import schemes
+    from paper_1511_06051_b200.data import Dataset, generate_synthetic
+    from paper_1511_06051_b200.model import SgdOptions
+    img, lab = generate_synthetic(2, 1, 1, 8, 60, 3.0, 501, 0)
+    train = Dataset(f32(img), lab, 2)
+    img, lab = generate_synthetic(2, 1, 1, 8, 20, 3.0, 501, 1)
+    evald = Dataset(f32(img), lab, 2)
+
+    def ctx(seed, batch=8, devices=None, mode="ordered"):
+        c = schemes.SchemeContext(net=ns.make_mlp(batch, 1, 1, 8, 2, 4), train_data=train,
+                                  eval_data=evald, batch=batch, sgd=SgdOptions(0.05, 0.0),
+                                  seed=seed, cost=schemes.CostModel(1.0, 0.0, 1.0),
+                                  target_accuracy=2.0, eval_steps=5, devices=devices,
+                                  precision="fp32")
+        c.average_mode = mode
+        return c
+    return train, ctx
+
+
+def test_tau1_equals_big_batch_serial():
+    """schemes_test.cpp:178-213 / acceptance 1b on the device: run_sparknet with K = 2
+    workers, tau = 1, b = 4 (ordered K-way average) == serial SGD with batch K*b on the
+    concatenated worker batches, same initial weights and lr (mu = 0).  The reference's
+    fp64 bar is 1e-10; in fp32 the two paths sum the same gradient terms in different
+    orders (mean of 4, then mean of 2, vs mean of 8): per-round deviations stay at the fp32
+    level."""
+    from paper_1511_06051_b200 import data, schemes
+    from paper_1511_06051_b200.model import Batch, Net, SgdOptions
+    train, ctx = _mlp_fixture()
+    c = ctx(13, batch=4)
+    rounds = []
+    schemes.run_sparknet(c, 2, 1, 30, 0, 1, schemes.SchemeObserver(
+        on_round=lambda r, w: rounds.append(np.concatenate([t.ravel() for _, ts in w
+                                                             for t in ts]))))
+    big = Net(ns.make_mlp(8, 1, 1, 8, 2, 4), 13)
+    big.set_sgd(SgdOptions(0.05, 0.0))
+    shards = data.shard(train, 2, 13)
+    streams = [data.make_worker_iterator(shards, k, 4, 13) for k in range(2)]
+    worst = 0.0
+    for r in range(30):
+        idx = np.concatenate([s.next_indices() for s in streams]).astype(np.int64)
+        _, g = big.backward_flat(Batch(train.images[idx], train.labels[idx]))
+        big.apply_update_flat(g)
+        worst = max(worst, max_relative_deviation(rounds[r], big.get_weights_flat()))
+    assert len(rounds) == 30
+    assert worst <= 1e-5, worst
+
+
+def test_run_sparknet_k_gpus_bitwise_equals_k_nets_on_one_gpu():
+    """schemes_test.cpp:249-260 (threaded == sequential, bitwise) on B200s: K = 2 workers
+    on 2 GPUs with the ordered NCCL average (all-to-all, ascending-k fp64 reduce, allgather)
+    produce bit-identical rounds, warm start and accuracies to the K nets on one GPU
+    (ordered local average)."""
+    if _gpus() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from paper_1511_06051_b200 import schemes
+    _, ctx = _mlp_fixture()
+    runs = []
+    for devs in (None, [0, 1]):
+        ws = []
+        t = schemes.run_sparknet(ctx(19, devices=devs), 2, 3, 10, 5, 1, schemes.SchemeObserver(
+            on_round=lambda r, w: ws.append(np.concatenate([x.ravel() for _, xs in w
+                                                            for x in xs]))))
+        runs.append((ws, t))
+    (wa, ta), (wb, tb) = runs
+    assert len(wa) == len(wb) == 10
+    for a, b in zip(wa, wb):
+        np.testing.assert_array_equal(a, b)
+    assert ta.warm_digest == tb.warm_digest
+    assert [r.accuracy for r in ta.records] == [r.accuracy for r in tb.records]
