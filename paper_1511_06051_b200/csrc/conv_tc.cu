@@ -36,13 +36,23 @@ using namespace tck;
 
 // Fixed-order second stage: out[i] (+)= sum_z ws[z][i] (+ bias[i % ldo], relu); columns
 // i % ldo >= valid_cols (row padding the GEMM never writes) are set to 0.
+// Fused wgrad bias (TcArgs::bias_chunk): db[f] = sum_z db_part[z][f] in the same pass.
 __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long long stride,
                                 long long total, const float* __restrict__ bias, int ldo,
                                 int valid_cols, int relu, int accumulate,
-                                const float* __restrict__ mask, float* __restrict__ out) {
+                                const float* __restrict__ mask, float* __restrict__ out,
+                                const float* __restrict__ db_part, int nb,
+                                float* __restrict__ db) {
   pdl_enter();
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       i < total + nb; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (i >= total) {
+      const int f = static_cast<int>(i - total);
+      float s = 0.f;
+      for (int z = 0; z < splits; ++z) s += db_part[static_cast<long long>(z) * nb + f];
+      db[f] = s;
+      continue;
+    }
     if (valid_cols < ldo && i % ldo >= valid_cols) {
       out[i] = 0.f;
       continue;
@@ -264,6 +274,14 @@ int pick_n_tile(int N) {
 // MN-major B is loaded in 32-column chunks, so each half must be whole chunks (N % 64).
 int sm_count();
 
+bool fuse_wgrad_bias() {  // PSG_TC_WGRAD_BIAS=0: separate bias_grad passes (A/B)
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_TC_WGRAD_BIAS");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 // TMA-store epilogue staging chunks per epilogue warp (PSG_TC_EPI_TMA: 0 = direct row stores
 // in every epilogue, 1 or 2 chunks; two let a chunk's smem writes overlap the previous
 // chunk's store but take 16 KB more from the stage ring)
@@ -391,6 +409,27 @@ int sm_count() {
   return sms;
 }
 
+constexpr CUtensorMapSwizzle kMnSwizzleOnes = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+
+// A 32 x 32 matrix of 1.0f on the current device (the fused wgrad bias's B chunk).
+const float* ones_matrix() {
+  static std::mutex mu;
+  static float* per_dev[64] = {};
+  int dev = 0;
+  PSG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (!per_dev[dev]) {
+    float h[32 * 32];
+    for (float& v : h) v = 1.f;
+    float* d = nullptr;
+    PSG_CUDA(cudaMalloc(&d, sizeof h));
+    PSG_CUDA(cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice));
+    PSG_CUDA(cudaDeviceSynchronize());  // before any stream uses it
+    per_dev[dev] = d;
+  }
+  return per_dev[dev];
+}
+
 void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int kblk,
             long long out_elems, float* ws, size_t ws_elems, cudaStream_t s) {
   TcArgs a = a0;
@@ -409,7 +448,13 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   a.ring_bytes = (a.stages * a.kps * a.stage_bytes + 1023) / 1024 * 1024;
   CUtensorMap mo;
   std::memset(&mo, 0, sizeof mo);
-  if (a.epi_tma) {  // out [rows][ldo] or the workspace [splits][rows][ldo], 32 x 32 boxes
+  if (a.bias_chunk) {  // wgrad: the ones matrix of the bias chunk (KBLK rows x 32)
+    const uint64_t dims[2] = {32, 32};
+    const uint64_t str[1] = {32 * 4};
+    const uint32_t box[2] = {32, static_cast<uint32_t>(kblk)};
+    mo = make_map(ones_matrix(), 2, dims, str, box, kMnSwizzleOnes);
+    if (splits > 1) a.db_part = ws + static_cast<long long>(splits) * out_elems;
+  } else if (a.epi_tma) {  // out [rows][ldo] or the workspace [splits][rows][ldo], 32 x 32 boxes
     const uint64_t rows = static_cast<uint64_t>(out_elems / a.ldo);
     const uint64_t dims[3] = {static_cast<uint64_t>(a.ldo), rows, static_cast<uint64_t>(splits)};
     const uint64_t str[2] = {static_cast<uint64_t>(a.ldo) * 4, rows * a.ldo * 4};
@@ -470,9 +515,10 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   PSG_CUDA(cudaGetLastError());
   if (splits > 1) {
     const int blocks = static_cast<int>(std::min<long long>((out_elems + 255) / 256, 148 * 8));
+    const int nb = a0.bias_chunk ? a0.db_ld : 0;
     launch_k(tc_split_reduce, blocks, 256, 0, s, ws, splits, out_elems, out_elems, a0.bias, a0.ldo,
-                                           a0.valid_cols ? a0.valid_cols : a0.ldo, a0.relu,
-                                           a0.accumulate, a0.mask, a0.out);
+             a0.valid_cols ? a0.valid_cols : a0.ldo, a0.relu, a0.accumulate, a0.mask, a0.out,
+             static_cast<const float*>(a.db_part), nb, a0.db);
     PSG_CUDA(cudaGetLastError());
   }
 }
@@ -708,6 +754,17 @@ bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
     a.im_lh = -g.ph;
     a.kh = g.kh;
     a.kblocks = (g.n * g.OH * g.OW + kblk - 1) / kblk;
+    // a spare chunk in the last N tile (the tiles' chunks exceed the taps' chunks) carries
+    // the bias gradient (TcArgs::bias_chunk) instead of a harmless reload
+    // (or one more chunk per tile when that costs <= ~10% more MMA operand bytes: AlexNet
+    // conv1's 18 chunks in 3 x 6 -> 3 x 7; the separate pass re-reads all of dY)
+    if (fuse_wgrad_bias()) {
+      const int wider = 32 * ((chunks + 1 + a.n_tiles - 1) / a.n_tiles);
+      if (a.n_tiles * (a.n_tile / 32) <= chunks && wider <= 256 &&
+          10 * (128 + wider) <= 11 * (128 + a.n_tile))
+        a.n_tile = wider;
+      if (a.n_tiles * (a.n_tile / 32) > chunks) a.bias_chunk = chunks;
+    }
   }
   return true;
 }
@@ -792,6 +849,7 @@ bool tc_supported(const ConvGeom& g, int which) {
 }
 
 size_t tc_workspace_elems(const ConvGeom& g) {
+  ones_matrix();  // allocated here, outside any stream capture (the nets size workspaces first)
   size_t e = 0;
   TcArgs a;
   int kblk;
@@ -819,7 +877,7 @@ int tc_launches(const ConvGeom& g, int which) {
                              : which == 1 ? plan_dgrad(g, a, kblk) : plan_wgrad(g, a, kblk);
   if (!ok) return -1;
   finish_args(a, kblk, sm_count());
-  return (splits_of(a) > 1 ? 2 : 1) + (which == 2 ? 2 : 0);
+  return (splits_of(a) > 1 ? 2 : 1) + (which == 2 && !a.bias_chunk ? 2 : 0);
 }
 
 void tc_fprop(const ConvGeom& g, const float* x, const float* w, const float* bias, float* y,
@@ -943,8 +1001,12 @@ void tc_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, flo
   // the split-K workspace holds dW partials; bias partials go after them
   const int splits = splits_of(a);
   float* part = ws.ptr + (splits > 1 ? splits * dw_elems : 0);
+  if (a.bias_chunk) {  // dbias from the ones chunk of the same GEMM (+ the split reduce)
+    a.db = db;
+    a.db_ld = g.F;
+  }
   launch(a, ma, mb, kblk, dw_elems, ws.ptr, ws.elems, s);
-  bias_grad(dy, static_cast<long long>(g.n) * g.OH * g.OW, g.F, part, db, s);
+  if (!a.bias_chunk) bias_grad(dy, static_cast<long long>(g.n) * g.OH * g.OW, g.F, part, db, s);
 }
 
 // ---- wgrad of narrow layers against an im2col matrix col[G][n*OH*OW][Kp] ----

@@ -96,6 +96,14 @@ struct TcArgs {
   // 32 rows x 32 columns go through a swizzled smem chunk and one cp.async.bulk.tensor store
   // (map_o: out [rows][ldo], or the split-K workspace [splits][rows][ldo]) instead of 32
   // row-strided float4 runs per store instruction; partial column chunks keep direct stores
+  // multi-tap wgrad with a spare 32-column chunk in its last N tile: that chunk is loaded
+  // from a ones matrix (map_o in EPI 2 kernels), so its columns accumulate
+  // sum_pixels dY[pixel][f] = dbias[f] (model.hpp:560) in the same MMAs; written to db
+  // (one split) or to the split's bias partial row (db_part[split][F])
+  int bias_chunk;          // virtual chunk index of the ones chunk, or 0
+  float* db;
+  float* db_part;
+  int db_ld;               // F
   int epi_tma;             // 0, or the staging chunks per epilogue warp (1 or 2)
   int ring_bytes;          // stage ring bytes (the staging area follows, 1024-aligned)
 };
@@ -132,7 +140,7 @@ __device__ __forceinline__ void tap_chunks(const TcArgs& p, const Tile& t, TapCh
     const int tap = min(vc / p.cpt, p.ntaps - 1);  // chunks past the last tap: harmless reloads
     k.dy[j] = tap / p.kw - p.ph;
     k.dx[j] = tap % p.kw - p.pw;
-    k.c[j] = p.b_n_g * t.g + vc % p.cpt;
+    k.c[j] = p.bias_chunk && (vc >> 5) == p.bias_chunk ? -1 : p.b_n_g * t.g + vc % p.cpt;
   }
 }
 
@@ -261,9 +269,10 @@ __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, 
 }
 
 template <int KBLK, bool PAIR>
-__device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, const Tile& t,
-                                       const KCursor& c, int u, int v, const TapChunks& tk,
-                                       uint32_t sb, uint32_t bar, int rank) {
+__device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map,
+                                       const CUtensorMap* ones, const Tile& t, const KCursor& c,
+                                       int u, int v, const TapChunks& tk, uint32_t sb,
+                                       uint32_t bar, int rank) {
   const int nch = (p.b_cols + 31) / 32;
   const int n0 = t.n * p.n_tile + rank * p.b_cols;  // this CTA's first B column
   switch (p.b_mode) {
@@ -310,10 +319,14 @@ __device__ __forceinline__ void load_b(const TcArgs& p, const CUtensorMap* map, 
       const int x0 = pix - r * p.out_w + p.im_lw, y0 = r % p.out_h + p.im_lh, b0 = r / p.out_h;
 #pragma unroll
       for (int j = 0; j < kMaxBChunks; ++j)
-        if (j < nch)
-          tc::tma_load_im2col_4d<PAIR>(sb + j * KBLK * 128, map, bar, tk.c[j], x0, y0, b0,
-                                       static_cast<uint16_t>(tk.dx[j] + p.pw),
-                                       static_cast<uint16_t>(tk.dy[j] + p.ph));
+        if (j < nch) {
+          if (tk.c[j] < 0)  // the bias chunk: a KBLK x 32 box of ones (same bytes)
+            tc::tma_load_2d<PAIR>(sb + j * KBLK * 128, ones, bar, 0, 0);
+          else
+            tc::tma_load_im2col_4d<PAIR>(sb + j * KBLK * 128, map, bar, tk.c[j], x0, y0, b0,
+                                         static_cast<uint16_t>(tk.dx[j] + p.pw),
+                                         static_cast<uint16_t>(tk.dy[j] + p.ph));
+        }
       break;
     }
   }
@@ -344,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&map_a);
     tc::tma_prefetch(&map_b);
-    if (p.epi_tma) tc::tma_prefetch(&map_o);
+    if (p.epi_tma || p.bias_chunk) tc::tma_prefetch(&map_o);
     for (int s = 0; s < p.stages; ++s) {
       tc::mbar_init(tc::smem_u32(&full_bar[s]), 1);  // the stage's producer warp, lane 0
       tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
@@ -415,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < cnt; ++j, c.next(p)) {
             const uint32_t sa = tc::smem_u32(smem + (s * p.kps + j) * p.stage_bytes);
             load_a<KBLK, PAIR>(p, &map_a, t, c, rb, oh0, ow0, sa, bar);
-            load_b<KBLK, PAIR>(p, &map_b, t, c, u, v, tk, sa + p.a_bytes, bar, rank);
+            load_b<KBLK, PAIR>(p, &map_b, &map_o, t, c, u, v, tk, sa + p.a_bytes, bar, rank);
           }
           c.advance(p);
           s += P;
@@ -633,6 +646,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int vc = t.n * p.n_tile + c, tap = vc / cpt, cc = vc % cpt;
               ok = c < p.n_tile && tap < p.ntaps && cc < p.cgs;
               cidx = tap * p.cgs + cc;
+              if (p.bias_chunk && vc == 32 * p.bias_chunk) {  // every ones column = dbias[f]
+                const float bsum = __uint_as_float(va[4 * q4]);
+                if (p.ws)
+                  p.db_part[static_cast<long long>(t.split) * p.db_ld + out_row] = bsum;
+                else
+                  p.db[out_row] = bsum;
+              }
             } else {
               ok = c < nvalid;
               cidx = col0 + c;
