@@ -244,6 +244,11 @@ int psg_net_set_tc_options(psg_net* net, int pair_policy);
 /* Kernel launches of one training step (device-side work count). */
 int psg_net_kernels_per_step(const psg_net* net, int* launches);
 
+/* Debug (tests; no reference counterpart): with PSG_GUARD=1 in the environment every net
+ * buffer is allocated between two 4 KB guard bands of 0xA5; the count of overwritten guard
+ * bytes over all live (and already freed) net buffers, and the first offender. */
+int psg_debug_guard_violations(unsigned long long* bad_bytes, char* first, size_t first_len);
+
 /* ---- measurement ------------------------------------------------------------ */
 /* One op of a training step: algorithmic work and its CUDA-event device time. */
 typedef struct psg_op_time {

@@ -658,6 +658,17 @@ int psg_net_set_tc_options(psg_net* net, int pair_policy) {
   });
 }
 
+int psg_debug_guard_violations(unsigned long long* bad_bytes, char* first, size_t first_len) {
+  return guarded([&] {
+    std::string f;
+    *bad_bytes = psg::guard_violations(&f);
+    if (first && first_len) {
+      std::strncpy(first, f.c_str(), first_len - 1);
+      first[first_len - 1] = 0;
+    }
+  });
+}
+
 int psg_net_kernels_per_step(const psg_net* net, int* launches) {
   return guarded([&] {
     need(net, "kernels_per_step");

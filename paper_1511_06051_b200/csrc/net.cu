@@ -2,6 +2,8 @@
 // (bit-exact with the reference RNG), flat fp32 parameter / gradient / velocity
 // buffers in HBM, NHWC activations, and one CUDA graph per training step
 // (gather -> forward -> loss -> backward -> fused SGD update).
+#include <mutex>
+#include <unordered_map>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -31,15 +33,76 @@ int pool_out(int in, int k, int s, int p, int ceil_mode) {
   return o;
 }
 
+// Guard bands (PSG_GUARD=1; compute-sanitizer is not available on the GPU pool): every
+// net allocation gets kGuardBytes of 0xA5 before and after it (plus the tail up to the next
+// 256 bytes); psg_debug_guard_violations() / dfree compare them after the kernels ran, so a
+// kernel writing outside any activation / gradient / parameter / workspace buffer is caught.
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+
+bool guard_on() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_GUARD");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
+
+struct GuardAlloc {
+  size_t bytes, padded;
+};
+std::mutex g_guard_mu;
+std::unordered_map<uintptr_t, GuardAlloc> g_guard_live;  // user pointer -> sizes
+unsigned long long g_guard_bad = 0;
+std::string g_guard_first;
+
+unsigned long long guard_check(uintptr_t user, const GuardAlloc& a) {
+  std::vector<unsigned char> h(kGuardBytes + (a.padded - a.bytes) + kGuardBytes);
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(user) - kGuardBytes;
+  PSG_CUDA(cudaMemcpy(h.data(), base, kGuardBytes, cudaMemcpyDeviceToHost));
+  PSG_CUDA(cudaMemcpy(h.data() + kGuardBytes, base + kGuardBytes + a.bytes,
+                      h.size() - kGuardBytes, cudaMemcpyDeviceToHost));
+  unsigned long long bad = 0;
+  for (unsigned char c : h) bad += c != kGuardByte;
+  if (bad && g_guard_first.empty())
+    g_guard_first = "allocation of " + std::to_string(a.bytes) + " bytes: " + std::to_string(bad) +
+                    " guard bytes overwritten";
+  return bad;
+}
+
 template <class T>
 T* dalloc(size_t n) {
   T* p = nullptr;
-  if (n) PSG_CUDA(cudaMalloc(&p, n * sizeof(T)));
-  return p;
+  if (!n) return p;
+  if (!guard_on()) {
+    PSG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return p;
+  }
+  const size_t bytes = n * sizeof(T), padded = (bytes + 255) / 256 * 256;
+  unsigned char* base = nullptr;
+  PSG_CUDA(cudaMalloc(&base, padded + 2 * kGuardBytes));
+  PSG_CUDA(cudaMemset(base, kGuardByte, kGuardBytes));
+  PSG_CUDA(cudaMemset(base + kGuardBytes + bytes, kGuardByte, padded - bytes + kGuardBytes));
+  PSG_CUDA(cudaDeviceSynchronize());  // the non-blocking net streams do not wait for memsets
+  std::lock_guard<std::mutex> lock(g_guard_mu);
+  g_guard_live[reinterpret_cast<uintptr_t>(base + kGuardBytes)] = GuardAlloc{bytes, padded};
+  return reinterpret_cast<T*>(base + kGuardBytes);
 }
 
 void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (!p) return;
+  if (guard_on()) {
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    auto it = g_guard_live.find(reinterpret_cast<uintptr_t>(p));
+    if (it != g_guard_live.end()) {
+      cudaDeviceSynchronize();
+      g_guard_bad += guard_check(it->first, it->second);
+      g_guard_live.erase(it);
+      cudaFree(static_cast<unsigned char*>(p) - kGuardBytes);
+      return;
+    }
+  }
+  cudaFree(p);
 }
 
 std::string lname(const psg_layer_desc& d) { return std::string(d.name); }
@@ -136,6 +199,16 @@ ConvGeom geom_for(const LayerRt& l, size_t n) {
 }
 
 }  // namespace
+
+unsigned long long guard_violations(std::string* first) {
+  if (!guard_on()) throw std::logic_error("guard bands are off (set PSG_GUARD=1)");
+  PSG_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lock(g_guard_mu);
+  unsigned long long bad = g_guard_bad;
+  for (const auto& kv : g_guard_live) bad += guard_check(kv.first, kv.second);
+  if (first) *first = g_guard_first;
+  return bad;
+}
 
 // Synchronous copy ordered on the net's stream.  A plain cudaMemcpy runs on the legacy
 // default stream, which the non-blocking net stream neither waits for nor is waited on by,

@@ -184,6 +184,7 @@ int run_update(psg_net* net, bool advance, OpTimer* timer = nullptr);
 void ensure_capacity(psg_net* net, size_t n);
 void release_batch_buffers(psg_net* net);  // drops activations + graphs; realloc on demand
 void invalidate_graph(psg_net* net);
+unsigned long long guard_violations(std::string* first);
 void copy_sync(psg_net* net, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
 void plan_fusion(psg_net* net);
 
