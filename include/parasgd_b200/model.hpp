@@ -155,14 +155,14 @@ class Net {
 
   Net(NetSpec spec, std::uint64_t seed, int device) : spec_(std::move(spec)), device_(device) {
     spec_.validate();
-    const std::vector<psg_layer_desc> d = b200::to_desc(spec_);
-    psg_net* h = nullptr;
-    b200::check(psg_net_create(b200::context(device), d.data(), static_cast<int>(d.size()), seed,
-                               &h));
-    net_.reset(h);
-    b200::check(psg_net_num_classes(net_.get(), &num_classes_));
-    b200::check(psg_net_param_count(net_.get(), &P_));
-    template_ = structure();
+    create(b200::to_desc(spec_), seed);
+  }
+
+  /// Extension: a graph of psg_layer_desc (Caffe layers the reference's NetSpec cannot
+  /// express — parasgd_b200/presets.hpp: cifar10_quick, AlexNet, GoogLeNet).  spec() is
+  /// then the empty NetSpec; layer names come from the descriptors.
+  Net(std::vector<psg_layer_desc> layers, std::uint64_t seed, int device) : device_(device) {
+    create(std::move(layers), seed);
   }
 
   Net(Net&&) noexcept = default;
@@ -177,9 +177,18 @@ class Net {
     if (!(opts.learning_rate > 0.0)) throw std::invalid_argument("sgd: learning rate must be > 0");
     if (opts.momentum < 0.0 || opts.momentum >= 1.0)
       throw std::invalid_argument("sgd: momentum must be in [0,1)");
-    b200::check(psg_net_set_sgd(net_.get(), opts.learning_rate, opts.momentum, 0.0));
+    b200::check(psg_net_set_sgd(net_.get(), opts.learning_rate, opts.momentum, weight_decay_));
     sgd_ = opts;
   }
+
+  /// Extension: L2 weight decay (v = mu v + g + wd w; 0 = the reference's update), scaled
+  /// per tensor by the layers' decay_mult.
+  void set_weight_decay(double wd) {
+    if (!(wd >= 0.0)) throw std::invalid_argument("sgd: weight decay must be >= 0");
+    b200::check(psg_net_set_sgd(net_.get(), sgd_.learning_rate, sgd_.momentum, wd));
+    weight_decay_ = wd;
+  }
+  double weight_decay() const noexcept { return weight_decay_; }
 
   /// Extension: fp32 SIMT (strict, default) or TF32 tensor cores.
   void set_precision(bool tf32) {
@@ -241,7 +250,7 @@ class Net {
     for (long s = 0; s < num_steps; ++s) {
       const Batch b = train_data_->next();
       check_batch(b);
-      if (b.size() != spec_.data_spec().shape[0]) {
+      if (b.size() != data_shape_[0]) {
         apply_update(backward(b));  // off-spec batch size: explicit path
         continue;
       }
@@ -354,10 +363,25 @@ class Net {
     void operator()(psg_dataset* d) const { psg_dataset_destroy(d); }
   };
 
+  void create(std::vector<psg_layer_desc> layers, std::uint64_t seed) {
+    desc_ = std::move(layers);
+    psg_net* h = nullptr;
+    b200::check(psg_net_create(b200::context(device_), desc_.data(),
+                               static_cast<int>(desc_.size()), seed, &h));
+    net_.reset(h);
+    for (const psg_layer_desc& d : desc_)
+      if (d.kind == PSG_LAYER_DATA)
+        data_shape_ = {static_cast<std::size_t>(d.batch), static_cast<std::size_t>(d.channels),
+                       static_cast<std::size_t>(d.height), static_cast<std::size_t>(d.width)};
+    b200::check(psg_net_num_classes(net_.get(), &num_classes_));
+    b200::check(psg_net_param_count(net_.get(), &P_));
+    template_ = structure();
+  }
+
   WeightCollection structure() const {
     int nt = 0;
     b200::check(psg_net_num_tensors(net_.get(), &nt));
-    std::vector<std::vector<NDArray>> per(spec_.layers.size());
+    std::vector<std::vector<NDArray>> per(desc_.size());
     for (int t = 0; t < nt; ++t) {
       int layer = 0, slot = 0, rank = 0;
       int64_t shape[4];
@@ -367,7 +391,7 @@ class Net {
       per[static_cast<std::size_t>(layer)].emplace_back(shp, 0.0);
     }
     WeightCollection w;
-    for (std::size_t i = 0; i < spec_.layers.size(); ++i) w.add(spec_.layers[i].name, per[i]);
+    for (std::size_t i = 0; i < desc_.size(); ++i) w.add(desc_[i].name, per[i]);
     return w;
   }
 
@@ -408,7 +432,7 @@ class Net {
     const std::size_t n = batch.images.extent(0);
     if (n < 1 || batch.labels.size() != n)
       throw std::invalid_argument("forward: label count does not match batch");
-    const auto& d = spec_.data_spec().shape;
+    const auto& d = data_shape_;
     for (int a = 0; a < 3; ++a)
       if (batch.images.extent(a + 1) != d[a + 1])
         throw std::invalid_argument("forward: batch extents do not match the data layer");
@@ -430,6 +454,9 @@ class Net {
   }
 
   NetSpec spec_;
+  std::vector<psg_layer_desc> desc_;
+  std::vector<std::size_t> data_shape_ = {0, 0, 0, 0};
+  double weight_decay_ = 0.0;
   int device_ = 0;
   std::unique_ptr<psg_net, NetDel> net_;
   int num_classes_ = 0;
