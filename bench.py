@@ -62,6 +62,9 @@ def parse():
     # fp32 = strict SIMT mode (parity 1e-5)
     p.add_argument("--precision", default="tf32", choices=["fp32", "tf32"])
     p.add_argument("--average", default="fast", choices=["fast", "ordered"])
+    p.add_argument("--no-overlap", dest="overlap", action="store_false",
+                   help="fast average after the round instead of per-layer buckets "
+                        "overlapped with the round's last backward (psg_net_train_round)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-json", default=None, help="write the per-op profile here")
     a = p.parse_args()
@@ -468,10 +471,11 @@ class Worker:
     """One SparkNet worker (this rank's GPU): its net on shard `rank` of the workload's
     synthetic dataset, and the communicator of the per-round weight average."""
 
-    def __init__(self, R, workload, precision, average, batch=None):
+    def __init__(self, R, workload, precision, average, batch=None, overlap=True):
         from paper_1511_06051_b200 import data as pdata
         from paper_1511_06051_b200 import model
         self.R, self.workload, self.avg_mode = R, workload, average
+        self.overlap = overlap and average == "fast" and R.world > 1
         self.spec, self.b = make_spec(workload, batch)
         _, _, self.chw3, _, lr, mu, wd = WORKLOADS[workload]
         self.ds = build_dataset(workload, R.world)
@@ -479,11 +483,34 @@ class Worker:
         self.net = model.Net(self.spec, 1, device=R.local, precision=precision)
         self.net.set_sgd(model.SgdOptions(lr, mu, wd))
         self.net.set_training_data(pdata.make_worker_iterator(self.shards, R.rank, self.b, 1))
+        # overlap the average with the last backward when it moves enough bytes to matter
+        # (cifar10_quick's 0.58 MB: the per-layer collectives' latency exceeds the overlap)
+        if 4 * self.net.P < 8e6:
+            self.overlap = False
         self.comm = None
         if R.world > 1:
             from paper_1511_06051_b200.comm import Communicator, unique_id
             uid = R.bcast(unique_id() if R.rank == 0 else None)
             self.comm = [Communicator.create(self.net.ctx, R.world, R.rank, uid)]
+
+    def round(self, tau):
+        """tau local steps + the K-way average (overlapped with the last backward in fast
+        mode, psg_net_train_round), enqueued."""
+        if self.overlap:
+            self.net.train_round(tau, self.comm[0], sync=False)
+        else:
+            self.net.train(tau, sync=False)
+            self.average()
+
+    def close(self):
+        """Net (and its captured round graph) first, then the communicator."""
+        self.net.sync()
+        self.net = None
+        import gc
+        gc.collect()
+        for c in self.comm or []:
+            c.close()
+        self.comm = None
 
     def average(self):
         if self.comm is not None:
@@ -500,8 +527,7 @@ class Worker:
         self.sync_all()
         self.net.event_record(0)
         for _ in range(n):
-            self.net.train(tau, sync=False)
-            self.average()
+            self.round(tau)
         self.net.event_record(1)
         self.net.sync()
         ms = self.R.max(self.net.event_elapsed(0, 1))
@@ -566,15 +592,15 @@ def rounds_for(ms_per_round, min_ms, at_least):
     return max(at_least, int(min_ms / max(ms_per_round, 1e-3)) + 1)
 
 
-def tau_sweep(R, workload, precision, average, taus=(1, 10, 50, 100), min_ms=400.0):
+def tau_sweep(R, workload, precision, average, taus=(1, 10, 50, 100), min_ms=400.0,
+              overlap=True):
     """cifar10_quick at this K (= world size) over tau (BASELINE.json configs[1]): images/sec
     = K * tau * b / round time; each point times >= min_ms of rounds after 3 warm-up rounds."""
-    W = Worker(R, workload, precision, average)
+    W = Worker(R, workload, precision, average, overlap=overlap)
     out = []
     for tau in taus:
         for _ in range(3):
-            W.net.train(tau, sync=False)
-            W.average()
+            W.round(tau)
         probe = W.rounds(tau, 2) / 2
         n = rounds_for(probe, min_ms, 3)
         ms = W.rounds(tau, n)
@@ -583,10 +609,12 @@ def tau_sweep(R, workload, precision, average, taus=(1, 10, 50, 100), min_ms=400
     prof = W.net.profile_step(repeats=5)
     avg_ms = W.average_ms()
     top = max(prof, key=lambda p: p["ms"])
-    return {"workload": workload, "K": R.world, "per_worker_batch": W.b, "unit": "images/sec",
-            "points": out, "kernels_per_step": W.net.kernels_per_step(),
-            "step_ms": sum(p["ms"] for p in prof), "top_op": top["name"],
-            "weight_average_ms": avg_ms}
+    res = {"workload": workload, "K": R.world, "per_worker_batch": W.b, "unit": "images/sec",
+           "points": out, "kernels_per_step": W.net.kernels_per_step(),
+           "step_ms": sum(p["ms"] for p in prof), "top_op": top["name"],
+           "weight_average_ms": avg_ms}
+    W.close()
+    return res
 
 
 def main():
@@ -597,14 +625,13 @@ def main():
     R = Rank()
     rank, world = R.rank, R.world
     K = world
-    W = Worker(R, args.workload, args.precision, args.average, args.batch)
+    W = Worker(R, args.workload, args.precision, args.average, args.batch, args.overlap)
     net, b = W.net, W.b
     c, h, w = W.chw3
 
     # --- device-resident throughput (value) ---
     for _ in range(args.warmup):
-        net.train(args.tau, sync=False)
-        W.average()
+        W.round(args.tau)
     W.sync_all()
     sampler = ClockSampler(R.local)
     sampler.start()
@@ -629,10 +656,15 @@ def main():
 
     launches = net.kernels_per_step() * args.tau * args.steps + (
         args.steps if (W.comm is not None and args.average == "ordered") else 0)
+    param_bytes = 4 * sum(n for _, n in net.segments())
+    overlapped = W.overlap
+    net = None
+    W.close()  # before the sweep's net / communicator (one communicator alive at a time)
     # the cifar10_quick tau sweep at this K (BASELINE.json configs[1])
     extra = None
     if args.extra and args.workload != "cifar10_quick":
-        extra = tau_sweep(R, "cifar10_quick", args.precision, args.average)
+        extra = tau_sweep(R, "cifar10_quick", args.precision, args.average,
+                          overlap=args.overlap)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.workload, b, max(1, min(8, os.cpu_count() or 1)), tau=args.tau)
@@ -644,6 +676,7 @@ def main():
             "dtype": args.precision, "data": "synthetic",
             "config": {"workload": args.workload, "global_batch": b * K, "per_worker_batch": b,
                        "K": K, "tau": args.tau, "average": args.average,
+                       "average_overlapped": overlapped,
                        "step": "one SparkNet round: tau local SGD steps per worker + the K-way "
                                "weight average",
                        "parallelism": f"sparknet-dp{K}",
@@ -655,7 +688,7 @@ def main():
             "timed_ms": ms,
             "weight_average": None if avg_ms is None else {
                 "ms": avg_ms, "share_of_round": avg_ms / (ms / args.steps),
-                "param_bytes": 4 * sum(n for _, n in net.segments())},
+                "param_bytes": param_bytes},
             "gpu_launches": launches,
             "cifar10_quick_tau_sweep": extra}))
     if R.dist is not None:

@@ -216,6 +216,12 @@ int psg_net_set_stream_position(psg_net* net, uint64_t epoch, uint64_t cursor);
  * value raises PSG_ERUNTIME at the next psg_net_sync (sticky device flag). */
 int psg_net_train(psg_net* net, long steps);
 int psg_net_sync(psg_net* net);
+/* One SparkNet round of this worker (schemes.hpp:323-336 for one worker): train(steps)
+ * followed by the fast K-way weight average over `comm` (as psg_comm_average(FAST)), the
+ * average overlapped with the last step's backward: each parameter layer's update and
+ * ncclAllReduce(avg) are issued as soon as its gradients are done, on a side stream,
+ * in reverse layer order (extension). */
+int psg_net_train_round(psg_net* net, long steps, psg_comm* comm);
 /* Device time of the last psg_net_train call's kernels (CUDA events on the
  * net's stream), ms; valid after psg_net_sync. */
 int psg_net_last_train_ms(psg_net* net, float* ms);

@@ -39,7 +39,10 @@ class Communicator:
         _lib.call("psg_comm_create_all", arr, len(ctxs), out)
         return [cls(ctypes.c_void_p(out[i]), ctxs[i]) for i in range(len(ctxs))]
 
-    def __del__(self):
+    def close(self) -> None:
+        """Destroy the communicator (ncclCommDestroy).  With several communicators per
+        process, close them in the same order on every rank, after the nets whose captured
+        round graphs use them."""
         h = getattr(self, "handle", None)
         if h:
             try:
@@ -47,6 +50,9 @@ class Communicator:
             except Exception:
                 pass
             self.handle = None
+
+    def __del__(self):
+        self.close()
 
     @staticmethod
     def average(comms: Sequence["Communicator"], nets: Sequence, mode: str = "fast") -> None:

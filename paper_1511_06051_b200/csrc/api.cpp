@@ -581,6 +581,13 @@ int psg_net_train(psg_net* net, long steps) {
   });
 }
 
+int psg_net_train_round(psg_net* net, long steps, psg_comm* comm) {
+  return guarded([&] {
+    need(net, "train_round");
+    psg::net_train_round(net, steps, comm);
+  });
+}
+
 int psg_net_sync(psg_net* net) {
   return guarded([&] {
     need(net, "sync");

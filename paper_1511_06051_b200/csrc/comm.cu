@@ -219,6 +219,12 @@ void comm_average_nets(psg_comm* const* comms, psg_net* const* nets, int count, 
   average_flat(comms, bufs.data(), counts.data(), streams.data(), flags.data(), count, mode);
 }
 
+int comm_device(const psg_comm* c) { return c->ctx->device; }
+
+void comm_allreduce_avg(psg_comm* c, float* ptr, size_t count, cudaStream_t s) {
+  nccl_check(nccl().AllReduce(ptr, ptr, count, ncclFloat, ncclAvg, c->comm, s), "ncclAllReduce");
+}
+
 void comm_broadcast_nets(psg_comm* const* comms, psg_net* const* nets, int count, int root) {
   const NcclApi& api = nccl();
   nccl_check(api.GroupStart(), "ncclGroupStart");

@@ -226,6 +226,9 @@ void invalidate_graph(psg_net* net) {
     gx = nullptr;
   }
   if (net->grad_graph) cudaGraphExecDestroy(net->grad_graph);
+  if (net->round_graph) cudaGraphExecDestroy(net->round_graph);
+  net->round_graph = nullptr;
+  net->round_graph_batch = 0;
   net->graph = nullptr;
   net->host_graph = nullptr;
   net->grad_graph = nullptr;
@@ -319,7 +322,11 @@ void ensure_stage(psg_net* net, size_t floats, size_t rows) {
 void build_chunks(psg_net* net) {
   std::vector<UpdateChunk> ch;
   constexpr uint32_t piece = 8192;
+  for (LayerRt& l : net->L) l.chunk0 = l.nchunk = 0;
   for (const TensorRec& t : net->tensors) {
+    LayerRt& l = net->L[t.layer];
+    if (l.nchunk == 0) l.chunk0 = static_cast<int>(ch.size());
+    l.nchunk += static_cast<int>((t.int_count + piece - 1) / piece);
     const float lr = static_cast<float>(net->lr * t.lr_mult);
     const float wd = static_cast<float>(net->wd * t.decay_mult);
     for (size_t b = t.int_off; b < t.int_off + t.int_count; b += piece) {
@@ -648,6 +655,9 @@ void net_free(psg_net* net) {
     if (net->consumed[k]) cudaEventDestroy(net->consumed[k]);
   }
   if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
+  if (net->side_stream) cudaStreamDestroy(net->side_stream);
+  if (net->side_join) cudaEventDestroy(net->side_join);
+  for (cudaEvent_t e : net->bucket_ev) cudaEventDestroy(e);
   if (net->h_losses) cudaFreeHost(net->h_losses);
   for (cudaEvent_t e : net->slots)
     if (e) cudaEventDestroy(e);
@@ -898,6 +908,86 @@ void net_train(psg_net* net, long steps) {
   }
   PSG_CUDA(cudaEventRecord(net->t0, net->stream));
   for (long s = 0; s < steps; ++s) PSG_CUDA(cudaGraphLaunch(net->graph, net->stream));
+  PSG_CUDA(cudaEventRecord(net->t1, net->stream));
+  net->timed = true;
+  net->last_n = b;
+}
+
+// One SparkNet round of this worker with the fast K-way average overlapped across layers
+// (SURVEY §8(e)): steps - 1 ordinary graph replays, then the round's last step as its own
+// graph in which every parameter layer's SGD update is issued right after its wgrad /
+// dgrad and its weights are averaged by an ncclAllReduce(avg) on a side stream while the
+// backward of the layers below runs; the side stream joins before the step ends.  Same
+// arithmetic as train(steps) + psg_comm_average(fast) (for K = 2 bitwise: the average of
+// two values does not depend on the allreduce's chunking).
+void net_train_round(psg_net* net, long steps, psg_comm* comm) {
+  if (steps < 1) throw std::invalid_argument("train_round: tau must be >= 1");
+  if (!net->train_ds) throw std::runtime_error("train: no training data attached");
+  if (!comm || comm_device(comm) != net->ctx->device)
+    throw std::invalid_argument("train_round: communicator on another device");
+  DeviceGuard dg(net->ctx->device);
+  if (steps > 1)
+    net_train(net, steps - 1);  // records t0 at the round's start
+  else
+    PSG_CUDA(cudaEventRecord(net->t0, net->stream));
+  const size_t b = net->it_batch / static_cast<size_t>(net->it_parts);
+  ensure_capacity(net, b);
+  upload_stream_indices(net, 1);
+  psg_dataset* ds = net->train_ds;
+  if (!net->side_stream) {
+    PSG_CUDA(cudaStreamCreateWithFlags(&net->side_stream, cudaStreamNonBlocking));
+    PSG_CUDA(cudaEventCreateWithFlags(&net->side_join, cudaEventDisableTiming));
+  }
+  int nbuckets = 0, last = -1;
+  for (size_t li = 0; li < net->L.size(); ++li)
+    if (net->L[li].nchunk) {
+      ++nbuckets;
+      if (last < 0) last = static_cast<int>(li);  // first param layer = last in backward
+    }
+  while (static_cast<int>(net->bucket_ev.size()) < nbuckets) {
+    cudaEvent_t e;
+    PSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    net->bucket_ev.push_back(e);
+  }
+  auto body = [&] {
+    RoundOverlap ov;
+    ov.comm = comm;
+    ov.side = net->side_stream;
+    ov.ready = net->bucket_ev;
+    ov.last_param_layer = last;
+    int launches = stage_gathered_batch(net, ds->images, ds->labels, net->d_idx,
+                                        &net->dsc->cursor, b);
+    launches += run_forward(net, b, true, true);
+    // fork: the side stream joins the capture / the stream order here
+    PSG_CUDA(cudaEventRecord(net->side_join, net->stream));
+    PSG_CUDA(cudaStreamWaitEvent(net->side_stream, net->side_join, 0));
+    launches += run_backward(net, b, nullptr, &ov);
+    PSG_CUDA(cudaEventRecord(net->side_join, net->side_stream));
+    PSG_CUDA(cudaStreamWaitEvent(net->stream, net->side_join, 0));
+    return launches;
+  };
+  if (eager_mode()) {
+    body();
+  } else {
+    if (!net->round_graph || net->round_graph_batch != b || net->round_comm != comm) {
+      if (net->round_graph) cudaGraphExecDestroy(net->round_graph);
+      net->round_graph = nullptr;
+      cudaGraph_t graph;
+      PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        body();
+      } catch (...) {
+        cudaStreamEndCapture(net->stream, &graph);
+        throw;
+      }
+      PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
+      PSG_CUDA(cudaGraphInstantiate(&net->round_graph, graph, 0));
+      cudaGraphDestroy(graph);
+      net->round_graph_batch = b;
+      net->round_comm = comm;
+    }
+    PSG_CUDA(cudaGraphLaunch(net->round_graph, net->stream));
+  }
   PSG_CUDA(cudaEventRecord(net->t1, net->stream));
   net->timed = true;
   net->last_n = b;

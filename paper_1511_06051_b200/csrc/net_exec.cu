@@ -243,7 +243,7 @@ int foldable_relu(const psg_net* net, const LayerRt& c) {
 }
 }  // namespace
 
-int run_backward(psg_net* net, size_t n, OpTimer* timer) {
+int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
   cudaStream_t s = net->stream;
   int launches = 0;
   std::vector<char> written(net->L.size(), 0);
@@ -315,6 +315,18 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer) {
           const int c = conv_launches(g, 1, net->mode);
           sc.done(c);
           launches += c;
+        }
+        if (ov && l.nchunk) {  // bucket li: update, then its average on the side stream
+          const bool last = static_cast<int>(li) == ov->last_param_layer;
+          sgd_update(net->d_chunks + l.chunk0, l.nchunk, net->w, net->v, net->g,
+                     static_cast<float>(net->mu), &net->dsc->flag,
+                     last ? &net->dsc->cursor : nullptr, last ? &net->dsc->step : nullptr, s);
+          cudaEvent_t ev = ov->ready[ov->buckets++];
+          PSG_CUDA(cudaEventRecord(ev, s));
+          PSG_CUDA(cudaStreamWaitEvent(ov->side, ev, 0));
+          const size_t lo = k.int_off, hi = b.int_off + b.int_count;
+          comm_allreduce_avg(ov->comm, net->w + lo, hi - lo, ov->side);
+          launches += 1;
         }
         break;
       }

@@ -45,6 +45,7 @@ struct TensorRec {
 
 struct LayerRt {
   psg_layer_desc d{};
+  int chunk0 = 0, nchunk = 0;  // this layer's SGD-update chunks (UpdateChunk table range)
   int kind = 0;
   std::vector<int> inputs, consumers;
   int C = 0, H = 1, W = 1;  // logical per-example dims
@@ -133,6 +134,12 @@ struct psg_net {
   cudaGraphExec_t graph = nullptr;
   size_t graph_batch = 0;
   cudaGraphExec_t grad_graph = nullptr;  // gather + forward + backward (run_naive parts)
+  cudaGraphExec_t round_graph = nullptr;  // last step of an overlapped round (+ NCCL)
+  size_t round_graph_batch = 0;
+  psg_comm* round_comm = nullptr;
+  cudaStream_t side_stream = nullptr;
+  std::vector<cudaEvent_t> bucket_ev;
+  cudaEvent_t side_join = nullptr;
   size_t grad_graph_batch = 0;
   int launches_per_step = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -179,7 +186,19 @@ int stage_gathered_batch(psg_net* net, const float* images, const int32_t* label
 // into the space-to-depth input of the first conv (as stage_gathered_batch).
 int stage_host_batch(psg_net* net, const float* src, size_t n);
 int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer = nullptr);
-int run_backward(psg_net* net, size_t n, OpTimer* timer = nullptr);
+// The last step of a SparkNet round with the K-way average overlapped across layers: as soon
+// as a parameter layer's wgrad and dgrad are enqueued, its SGD update runs and its weights
+// go to an ncclAllReduce(avg) on the side stream while the backward of the layers below
+// continues (the bucket of layer L is final once dgrad_L has read W_L).
+struct RoundOverlap {
+  psg_comm* comm = nullptr;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ready;  // per bucket: update done on the main stream
+  cudaEvent_t join = nullptr;      // side stream done
+  int last_param_layer = -1;       // the last bucket in backward order advances the counters
+  int buckets = 0;
+};
+int run_backward(psg_net* net, size_t n, OpTimer* timer = nullptr, RoundOverlap* ov = nullptr);
 int run_update(psg_net* net, bool advance, OpTimer* timer = nullptr);
 void ensure_capacity(psg_net* net, size_t n);
 void release_batch_buffers(psg_net* net);  // drops activations + graphs; realloc on demand
@@ -207,6 +226,11 @@ void net_layer_readback(psg_net* net, int layer, bool grad, double* out, size_t 
 void net_attach_shard(psg_net* net, psg_dataset* ds, const uint64_t* idx, size_t count,
                       size_t batch, uint64_t seed, int part = 0, int parts = 1);
 void net_train(psg_net* net, long steps);
+// train(tau) + the fast K-way average, the average's buckets overlapped with the last
+// step's backward
+void net_train_round(psg_net* net, long steps, psg_comm* comm);
+void comm_allreduce_avg(psg_comm* c, float* ptr, size_t count, cudaStream_t s);
+int comm_device(const psg_comm* c);
 void net_grad_step(psg_net* net);
 void net_apply_grads(psg_net* net);
 void net_attach_validation(psg_net* net, psg_dataset* ds, size_t batch);

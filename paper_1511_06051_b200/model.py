@@ -319,6 +319,20 @@ class Net:
         if sync:
             self.sync()
 
+    def train_round(self, num_steps: int, comm, sync: bool = True) -> None:
+        """One SparkNet round of this worker: train(num_steps) + the fast K-way weight
+        average over `comm`, the average overlapped with the last step's backward
+        (psg_net_train_round)."""
+        if num_steps < 1:
+            raise ValueError("train_round: tau must be >= 1")
+        if self._train_it is None:
+            raise RuntimeError("train: no training data attached")
+        self._sync_stream_in()
+        _lib.call("psg_net_train_round", self.handle, num_steps, comm.handle)
+        self._sync_stream_out()
+        if sync:
+            self.sync()
+
     def grad_step(self) -> None:
         """One run_naive part (schemes.hpp:233-247): next batch (this net's rows) ->
         forward + backward; the gradient stays on the device (enqueued, no sync)."""

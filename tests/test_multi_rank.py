@@ -99,3 +99,20 @@ def test_bench_two_ranks():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload,tau", [("cifar10_quick", 1), ("cifar10_quick", 3)])
+def test_overlapped_round_bitwise_equals_train_then_average(workload, tau):
+    """psg_net_train_round (per-layer average buckets during the last backward) leaves
+    weights and velocities bit-identical to train(tau) + one ncclAllReduce(avg) at K = 2."""
+    if _gpus() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tools", "overlap_check.py"), "--workload", workload,
+           "--tau", str(tau), "--rounds", "5"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert res["bitwise_equal"], res
