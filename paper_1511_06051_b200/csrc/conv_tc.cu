@@ -68,6 +68,70 @@ __global__ void tc_split_reduce(const float* __restrict__ ws, int splits, long l
   }
 }
 
+// The same per element, four consecutive elements of one row per thread (ldo, valid_cols
+// and the pointers 16-byte aligned): identical arithmetic and order, a quarter of the
+// instructions and 16-byte accesses.
+__global__ void tc_split_reduce4(const float4* __restrict__ ws, int splits, long long stride4,
+                                 long long total4, const float* __restrict__ bias, int ldo,
+                                 int valid_cols, int relu, int accumulate,
+                                 const float4* __restrict__ mask, float4* __restrict__ out,
+                                 const float* __restrict__ db_part, int nb,
+                                 float* __restrict__ db) {
+  pdl_enter();
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       i < total4 + nb; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (i >= total4) {
+      const int f = static_cast<int>(i - total4);
+      float s = 0.f;
+      for (int z = 0; z < splits; ++z) s += db_part[static_cast<long long>(z) * nb + f];
+      db[f] = s;
+      continue;
+    }
+    const int col = static_cast<int>((4 * i) % ldo);
+    if (valid_cols < ldo && col >= valid_cols) {
+      out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int z = 0; z < splits; ++z) {
+      const float4 v = ws[z * stride4 + i];
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    if (bias) {
+      const float4 bb = *reinterpret_cast<const float4*>(bias + col);
+      s.x += bb.x;
+      s.y += bb.y;
+      s.z += bb.z;
+      s.w += bb.w;
+      if (relu) {
+        s.x = s.x > 0.f ? s.x : 0.f;
+        s.y = s.y > 0.f ? s.y : 0.f;
+        s.z = s.z > 0.f ? s.z : 0.f;
+        s.w = s.w > 0.f ? s.w : 0.f;
+      }
+    }
+    if (mask) {  // folded ReLU backward (dgrad)
+      const float4 m = mask[i];
+      if (!(m.x > 0.f)) s.x = 0.f;
+      if (!(m.y > 0.f)) s.y = 0.f;
+      if (!(m.z > 0.f)) s.z = 0.f;
+      if (!(m.w > 0.f)) s.w = 0.f;
+    }
+    if (accumulate) {
+      const float4 o = out[i];
+      s.x = o.x + s.x;
+      s.y = o.y + s.y;
+      s.z = o.z + s.z;
+      s.w = o.w + s.w;
+    }
+    out[i] = s;
+  }
+}
+
 // db[c] = sum over rows of dy[r][c] in a fixed order.  Stage 1: block (cb, chunk) owns a
 // contiguous row chunk and up to 256 column units (float4 when cols % 4 == 0); thread
 // (ty, tx) sums rows r0 + ty, r0 + ty + rpi, ... of unit tx, then row-lanes combine in
@@ -514,11 +578,23 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   }
   PSG_CUDA(cudaGetLastError());
   if (splits > 1) {
-    const int blocks = static_cast<int>(std::min<long long>((out_elems + 255) / 256, 148 * 8));
     const int nb = a0.bias_chunk ? a0.db_ld : 0;
-    launch_k(tc_split_reduce, blocks, 256, 0, s, ws, splits, out_elems, out_elems, a0.bias, a0.ldo,
-             a0.valid_cols ? a0.valid_cols : a0.ldo, a0.relu, a0.accumulate, a0.mask, a0.out,
-             static_cast<const float*>(a.db_part), nb, a0.db);
+    const int vcols = a0.valid_cols ? a0.valid_cols : a0.ldo;
+    auto al16 = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+    if (a0.ldo % 4 == 0 && vcols % 4 == 0 && out_elems % 4 == 0 && al16(ws) && al16(a0.out) &&
+        (!a0.bias || al16(a0.bias)) && (!a0.mask || al16(a0.mask))) {
+      const long long total4 = out_elems / 4;
+      const int blocks = static_cast<int>(std::min<long long>((total4 + nb + 255) / 256, 148 * 8));
+      launch_k(tc_split_reduce4, blocks, 256, 0, s, reinterpret_cast<const float4*>(ws), splits,
+               total4, total4, a0.bias, a0.ldo, vcols, a0.relu, a0.accumulate,
+               reinterpret_cast<const float4*>(a0.mask), reinterpret_cast<float4*>(a0.out),
+               static_cast<const float*>(a.db_part), nb, a0.db);
+    } else {
+      const int blocks = static_cast<int>(std::min<long long>((out_elems + nb + 255) / 256, 148 * 8));
+      launch_k(tc_split_reduce, blocks, 256, 0, s, ws, splits, out_elems, out_elems, a0.bias,
+               a0.ldo, vcols, a0.relu, a0.accumulate, a0.mask, a0.out,
+               static_cast<const float*>(a.db_part), nb, a0.db);
+    }
     PSG_CUDA(cudaGetLastError());
   }
 }
