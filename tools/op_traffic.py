@@ -56,6 +56,13 @@ def load_ncu(path):
     return [kern[k] for k in sorted(kern)]
 
 
+def _wavg(kernels, metric):
+    t = sum(k.get("gpu__time_duration.sum", 0) for k in kernels if metric in k)
+    if not t:
+        return None
+    return sum(k[metric] * k.get("gpu__time_duration.sum", 0) for k in kernels if metric in k) / t
+
+
 def summarize(a):
     ks = load_ncu(a.csv)
     prof = json.load(open(a.ops))
@@ -73,6 +80,9 @@ def summarize(a):
                     "dram_bytes": sum(k.get("dram__bytes_read.sum", 0) +
                                       k.get("dram__bytes_write.sum", 0) for k in mine),
                     "ncu_us": sum(k.get("gpu__time_duration.sum", 0) for k in mine),
+                    # tcgen05 pipe activity of the op's GEMM (time-weighted over its kernels)
+                    "tensor_pipe_pct": _wavg(mine, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                    "tc_pipe_pct": _wavg(mine, "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                     "algorithmic_flops": o["flops"], "algorithmic_bytes": o["bytes"]})
     total = sum(x["ncu_us"] for x in out)
     for x in out:
