@@ -667,7 +667,7 @@ def main():
                           overlap=args.overlap)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.workload, b, max(1, min(8, os.cpu_count() or 1)), tau=args.tau)
+        cpu = cpu_baseline(args.workload, b, max(1, os.cpu_count() or 1), tau=args.tau)
     if rank == 0:
         print(json.dumps({
             "metric": "images/sec", "value": value, "unit": "images/sec", "n_gpus": world,
