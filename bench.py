@@ -38,7 +38,6 @@ WORKLOADS = {
 
 # BASELINE.json configs: AlexNet K=8 tau=50, GoogLeNet K=8 tau=20, cifar10_quick tau sweep
 DEFAULT_TAU = {"alexnet": 50, "googlenet": 20, "cifar10_quick": 10, "cq-valid": 10}
-HOST_RING = 10  # e2e: pinned host batches per train_host call (re-sent every call)
 
 
 def parse():
@@ -546,35 +545,31 @@ class Worker:
         return self.R.max(self.net.event_elapsed(2, 3)) / reps
 
     def e2e(self, tau, n):
-        """The same rounds through the C ABI's host-fed path: per step an H2D copy of the
-        step's batch from pinned host memory (NCHW fp32 + labels), the step, a D2H read of its
-        loss; plus the K-way average.  A ring of <= HOST_RING distinct pinned batches (the
-        reference's gather_batch output) is re-sent every round."""
+        """The same rounds through the C ABI's host-fed path (psg_net_train_host_rows): per
+        step, host threads gather the step's rows of this worker's shard from a host copy of
+        the dataset (NCHW fp32) into pinned staging — the reference's gather_batch — while
+        the GPU runs the previous step; then the H2D copy, the step, a D2H read of its loss;
+        plus the K-way average.  Everything from the batch indices on is inside the timed
+        region."""
         from paper_1511_06051_b200 import data as pdata
-        from paper_1511_06051_b200._lib import PinnedArray
         c, h, w = self.chw3
         b = self.b
-        ring = min(tau, HOST_RING)
-        pin_img = PinnedArray((ring, b, c, h, w), np.float32)
-        pin_lab = PinnedArray((ring, b), np.int32)
+        mine = np.sort(np.asarray(self.shards[self.R.rank].indices, np.int64))
+        if isinstance(self.ds, pdata.DeviceSyntheticDataset):  # pixels only in HBM: copy once
+            host_img = np.empty((mine.size, c, h, w), np.float32)
+            for j, r in enumerate(mine):
+                host_img[j] = self.ds.read(self.net.ctx, int(r), 1)[0][0]
+        else:
+            host_img = np.ascontiguousarray(self.ds.images[mine], np.float32)
+        host_lab = np.ascontiguousarray(self.ds.labels[mine], np.int32)
         host_it = pdata.make_worker_iterator(self.shards, self.R.rank, b, 7)
-        for s in range(ring):
-            idx = host_it.next_indices().astype(np.int64)
-            if isinstance(self.ds, pdata.DeviceSyntheticDataset):  # pixels only in HBM
-                for i, r in enumerate(idx):
-                    pin_img.array[s, i] = self.ds.read(self.net.ctx, int(r), 1)[0][0]
-            else:
-                pin_img.array[s] = self.ds.images[idx]
-            pin_lab.array[s] = self.ds.labels[idx]
+        threads = max(1, (os.cpu_count() or 1) // self.R.world)
 
         def host_round():
-            left = tau
-            while left > 0:
-                k = min(ring, left)
-                self.net.train_host(pin_img.array[:k], pin_lab.array[:k])
-                left -= k
+            rows = np.concatenate([host_it.next_indices() for _ in range(tau)]).astype(np.int64)
+            self.net.train_host_rows(host_img, host_lab, np.searchsorted(mine, rows), threads)
 
-        host_round()  # warm-up: capture the host-fed graph
+        host_round()  # warm-up: capture the host-fed graphs
         self.average()
         self.sync_all()
         self.net.event_record(2)
@@ -585,7 +580,7 @@ class Worker:
         self.net.sync()
         ms = self.R.max(self.net.event_elapsed(2, 3))
         self.R.barrier()
-        return ms, tau * b * (c * h * w * 4 + 4), tau * 8
+        return ms, tau * b * (c * h * w * 4 + 4), tau * 8, threads
 
 
 def rounds_for(ms_per_round, min_ms, at_least):
@@ -643,7 +638,7 @@ def main():
 
     # --- end to end through the C ABI with host buffers (e2e) ---
     e2e_steps = min(args.steps, 5)
-    ems, h2d, d2h = W.e2e(args.tau, e2e_steps)
+    ems, h2d, d2h, gthreads = W.e2e(args.tau, e2e_steps)
     e2e_value = K * e2e_steps * args.tau * b / (ems / 1000.0)
 
     # --- roofline of the dominant op + all GEMM ops (live CUDA events, per op) ---
@@ -683,7 +678,11 @@ def main():
                        "l2": "inputs larger than L2 (HBM-resident dataset "
                              f"{W_bytes(args.workload, K):.0f} MB, random per-step gather)"},
             "e2e": {"value": e2e_value, "unit": "images/sec", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "rounds": e2e_steps},
+                    "d2h_bytes_per_step": d2h, "rounds": e2e_steps,
+                    "host_gather_threads": gthreads,
+                    "path": "psg_net_train_host_rows: host-thread gather of each step's rows "
+                            "from the host dataset into pinned staging (overlapping the "
+                            "previous step), H2D, the step, D2H of its loss; + the average"},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "timed_ms": ms,
             "weight_average": None if avg_ms is None else {

@@ -274,6 +274,13 @@ int psg_net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_op
  * end-to-end path of the C ABI (pinned memory from psg_host_alloc is fastest). */
 int psg_net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,
                        double* losses);
+/* train(steps) with a host-side loader: per step `threads` host threads gather the step's
+ * rows ds_images[rows[s*b + i]] (NCHW fp32, row = c*h*w floats) and their labels into a
+ * pinned staging buffer (gather_batch, data.hpp:292-304) while the GPU runs the previous
+ * step, then H2D copy, the step, and a D2H read of its loss. */
+int psg_net_train_host_rows(psg_net* net, const float* ds_images, const int32_t* ds_labels,
+                            size_t ds_rows, const uint64_t* rows, long steps, double* losses,
+                            int threads);
 int psg_host_alloc(size_t bytes, void** ptr);
 int psg_host_free(void* ptr);
 /* Event slots (0..15) on the net's stream for device-side timing of regions. */

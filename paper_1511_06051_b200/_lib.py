@@ -119,6 +119,7 @@ SIGNATURES = {
     "psg_net_set_tc_options": (ctypes.c_int, [_VP, ctypes.c_int]),
     "psg_debug_guard_violations": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_char_p, _SZ]),
     "psg_net_train_round": (ctypes.c_int, [_VP, ctypes.c_long, _VP]),
+    "psg_net_train_host_rows": (ctypes.c_int, [_VP, _F, _I32, _SZ, _U64, ctypes.c_long, _D, ctypes.c_int]),
     "psg_net_set_fusion": (ctypes.c_int, [_VP, ctypes.c_int]),
     "psg_net_apply_grads": (ctypes.c_int, [_VP]),
     "psg_average_grads_local": (ctypes.c_int, [_PP, ctypes.c_int]),

@@ -698,6 +698,15 @@ int psg_net_train_host(psg_net* net, const float* images, const int32_t* labels,
   });
 }
 
+int psg_net_train_host_rows(psg_net* net, const float* ds_images, const int32_t* ds_labels,
+                            size_t ds_rows, const uint64_t* rows, long steps, double* losses,
+                            int threads) {
+  return guarded([&] {
+    need(net, "train_host_rows");
+    psg::net_train_host_rows(net, ds_images, ds_labels, ds_rows, rows, steps, losses, threads);
+  });
+}
+
 int psg_host_alloc(size_t bytes, void** ptr) {
   return guarded([&] { PSG_CUDA(cudaMallocHost(ptr, std::max<size_t>(bytes, 1))); });
 }

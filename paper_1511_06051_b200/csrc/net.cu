@@ -659,6 +659,11 @@ void net_free(psg_net* net) {
   if (net->side_join) cudaEventDestroy(net->side_join);
   for (cudaEvent_t e : net->bucket_ev) cudaEventDestroy(e);
   if (net->h_losses) cudaFreeHost(net->h_losses);
+  for (int k = 0; k < 2; ++k) {
+    if (net->h_ring[k]) cudaFreeHost(net->h_ring[k]);
+    if (net->h_ring_lab[k]) cudaFreeHost(net->h_ring_lab[k]);
+    if (net->h_ring_ev[k]) cudaEventDestroy(net->h_ring_ev[k]);
+  }
   for (cudaEvent_t e : net->slots)
     if (e) cudaEventDestroy(e);
   if (net->idx_ev) cudaEventDestroy(net->idx_ev);

@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "runtime.h"
 
@@ -72,6 +74,82 @@ void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, 
   *n_ops = static_cast<int>(acc.size());
 }
 
+// Two device staging buffers and their step graphs (host-fed training).
+void host_graphs_prepare(psg_net* net, size_t b, size_t chw) {
+  // Graph path: two staging buffers, the H2D copies on a copy stream.  Step s waits for
+  // its buffer's copy; the copy of step s+1 (other buffer) runs during step s.
+  if (net->d_stage2_cap < b * chw) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    for (int k = 0; k < 2; ++k) {
+      if (net->d_stage2[k]) cudaFree(net->d_stage2[k]);
+      if (net->d_lab2[k]) cudaFree(net->d_lab2[k]);
+      PSG_CUDA(cudaMalloc(&net->d_stage2[k], b * chw * sizeof(float)));
+      PSG_CUDA(cudaMalloc(&net->d_lab2[k], b * sizeof(int32_t)));
+      if (net->host_graph2[k]) cudaGraphExecDestroy(net->host_graph2[k]);
+      net->host_graph2[k] = nullptr;
+    }
+    net->d_stage2_cap = b * chw;
+  }
+  if (!net->copy_stream) {
+    PSG_CUDA(cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      PSG_CUDA(cudaEventCreateWithFlags(&net->copied[k], cudaEventDisableTiming));
+      PSG_CUDA(cudaEventCreateWithFlags(&net->consumed[k], cudaEventDisableTiming));
+    }
+  }
+  if (net->graph_batch != b) invalidate_graph(net);
+  for (int k = 0; k < 2; ++k) {
+    if (net->host_graph2[k]) continue;
+    cudaGraph_t graph;
+    PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      PSG_CUDA(cudaMemcpyAsync(net->labels, net->d_lab2[k], b * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice, net->stream));
+      stage_host_batch(net, net->d_stage2[k], b);
+      run_forward(net, b, true, true);
+      run_backward(net, b);
+      run_update(net, true);
+    } catch (...) {
+      cudaStreamEndCapture(net->stream, &graph);
+      throw;
+    }
+    PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
+    PSG_CUDA(cudaGraphInstantiate(&net->host_graph2[k], graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  net->graph_batch = b;
+}
+
+// Step s of a host-fed run: H2D of its batch into buffer s % 2 (copy stream, after the
+// buffer's previous step consumed it), the step graph, the D2H of its loss.
+void host_step_enqueue(psg_net* net, const float* img, const int32_t* lab, long s, size_t b,
+                       size_t chw) {
+  const int k = static_cast<int>(s & 1);
+  PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->consumed[k], 0));
+  PSG_CUDA(cudaMemcpyAsync(net->d_stage2[k], img, b * chw * sizeof(float),
+                           cudaMemcpyHostToDevice, net->copy_stream));
+  PSG_CUDA(cudaMemcpyAsync(net->d_lab2[k], lab, b * sizeof(int32_t), cudaMemcpyHostToDevice,
+                           net->copy_stream));
+  PSG_CUDA(cudaEventRecord(net->copied[k], net->copy_stream));
+  PSG_CUDA(cudaStreamWaitEvent(net->stream, net->copied[k], 0));
+  PSG_CUDA(cudaGraphLaunch(net->host_graph2[k], net->stream));
+  PSG_CUDA(cudaEventRecord(net->consumed[k], net->stream));
+  PSG_CUDA(cudaMemcpyAsync(net->h_losses + s, &net->dsc->loss, sizeof(double),
+                           cudaMemcpyDeviceToHost, net->stream));
+}
+
+// Device staging + pinned loss slots for `steps` host-fed steps.
+void host_steps_prepare(psg_net* net, size_t b, size_t chw, long steps) {
+  ensure_capacity(net, b);
+  if (net->h_losses_cap < static_cast<size_t>(steps)) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    if (net->h_losses) cudaFreeHost(net->h_losses);
+    PSG_CUDA(cudaMallocHost(&net->h_losses, steps * sizeof(double)));
+    net->h_losses_cap = static_cast<size_t>(steps);
+  }
+  (void)chw;
+}
+
 void net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,
                     double* losses) {
   if (steps < 0) throw std::invalid_argument("train: negative step count");
@@ -124,66 +202,81 @@ void net_train_host(psg_net* net, const float* images, const int32_t* labels, lo
     if (losses) std::memcpy(losses, net->h_losses, steps * sizeof(double));
     return;
   }
-  // Graph path: two staging buffers, the H2D copies on a copy stream.  Step s waits for
-  // its buffer's copy; the copy of step s+1 (other buffer) runs during step s.
-  if (net->d_stage2_cap < b * chw) {
-    PSG_CUDA(cudaStreamSynchronize(net->stream));
-    for (int k = 0; k < 2; ++k) {
-      if (net->d_stage2[k]) cudaFree(net->d_stage2[k]);
-      if (net->d_lab2[k]) cudaFree(net->d_lab2[k]);
-      PSG_CUDA(cudaMalloc(&net->d_stage2[k], b * chw * sizeof(float)));
-      PSG_CUDA(cudaMalloc(&net->d_lab2[k], b * sizeof(int32_t)));
-      if (net->host_graph2[k]) cudaGraphExecDestroy(net->host_graph2[k]);
-      net->host_graph2[k] = nullptr;
-    }
-    net->d_stage2_cap = b * chw;
-  }
-  if (!net->copy_stream) {
-    PSG_CUDA(cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking));
-    for (int k = 0; k < 2; ++k) {
-      PSG_CUDA(cudaEventCreateWithFlags(&net->copied[k], cudaEventDisableTiming));
-      PSG_CUDA(cudaEventCreateWithFlags(&net->consumed[k], cudaEventDisableTiming));
-    }
-  }
-  if (net->graph_batch != b) invalidate_graph(net);
-  for (int k = 0; k < 2; ++k) {
-    if (net->host_graph2[k]) continue;
-    cudaGraph_t graph;
-    PSG_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeThreadLocal));
-    try {
-      PSG_CUDA(cudaMemcpyAsync(net->labels, net->d_lab2[k], b * sizeof(int32_t),
-                               cudaMemcpyDeviceToDevice, net->stream));
-      stage_host_batch(net, net->d_stage2[k], b);
-      run_forward(net, b, true, true);
-      run_backward(net, b);
-      run_update(net, true);
-    } catch (...) {
-      cudaStreamEndCapture(net->stream, &graph);
-      throw;
-    }
-    PSG_CUDA(cudaStreamEndCapture(net->stream, &graph));
-    PSG_CUDA(cudaGraphInstantiate(&net->host_graph2[k], graph, 0));
-    cudaGraphDestroy(graph);
-  }
-  net->graph_batch = b;
+  host_graphs_prepare(net, b, chw);
   PSG_CUDA(cudaEventRecord(net->t0, net->stream));
   PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->t0, 0));  // copies inside the timing
   for (int k = 0; k < 2; ++k) {  // buffers are free once the stream's prior work is done
     PSG_CUDA(cudaEventRecord(net->consumed[k], net->stream));
   }
+  for (long s = 0; s < steps; ++s)
+    host_step_enqueue(net, images + s * b * chw, labels + s * b, s, b, chw);
+  PSG_CUDA(cudaEventRecord(net->t1, net->stream));
+  net->timed = true;
+  net->last_n = b;
+  net_check_flag(net);
+  if (losses) std::memcpy(losses, net->h_losses, steps * sizeof(double));
+}
+
+// train(steps) fed by a host-side loader: per step, `threads` host threads gather the step's
+// rows (NCHW fp32 ds_images[rows[s * b + i]]) and labels into one of two pinned staging
+// buffers — the reference's gather_batch (data.hpp:292-304) on the host — while the GPU runs
+// the previous step; then the same H2D copy / step graph / D2H of the loss as
+// net_train_host.  A staging buffer is refilled once its copy to the device has completed.
+void net_train_host_rows(psg_net* net, const float* ds_images, const int32_t* ds_labels,
+                         size_t ds_rows, const uint64_t* rows, long steps, double* losses,
+                         int threads) {
+  if (steps < 0) throw std::invalid_argument("train: negative step count");
+  if (steps == 0) return;
+  threads = std::max(1, threads);
+  DeviceGuard dg(net->ctx->device);
+  const LayerRt& d = net->L[net->data_idx];
+  const size_t b = static_cast<size_t>(net->spec_batch);
+  const size_t chw = static_cast<size_t>(d.C) * d.H * d.W;
+  for (long s = 0; s < steps; ++s)
+    for (size_t i = 0; i < b; ++i) {
+      const uint64_t r = rows[s * b + i];
+      if (r >= ds_rows) throw std::invalid_argument("gather: row index out of range");
+      if (ds_labels[r] < 0 || ds_labels[r] >= net->classes)
+        throw std::invalid_argument("forward: label out of range");
+    }
+  host_steps_prepare(net, b, chw, steps);
+  host_graphs_prepare(net, b, chw);
+  if (net->h_ring_cap < b * chw) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    for (int k = 0; k < 2; ++k) {
+      if (net->h_ring[k]) cudaFreeHost(net->h_ring[k]);
+      if (net->h_ring_lab[k]) cudaFreeHost(net->h_ring_lab[k]);
+      PSG_CUDA(cudaMallocHost(&net->h_ring[k], b * chw * sizeof(float)));
+      PSG_CUDA(cudaMallocHost(&net->h_ring_lab[k], b * sizeof(int32_t)));
+      if (!net->h_ring_ev[k])
+        PSG_CUDA(cudaEventCreateWithFlags(&net->h_ring_ev[k], cudaEventDisableTiming));
+    }
+    net->h_ring_cap = b * chw;
+  }
+  PSG_CUDA(cudaEventRecord(net->t0, net->stream));
+  PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->t0, 0));
+  for (int k = 0; k < 2; ++k) {
+    PSG_CUDA(cudaEventRecord(net->consumed[k], net->stream));
+    PSG_CUDA(cudaEventRecord(net->h_ring_ev[k], net->copy_stream));
+  }
   for (long s = 0; s < steps; ++s) {
     const int k = static_cast<int>(s & 1);
-    PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->consumed[k], 0));
-    PSG_CUDA(cudaMemcpyAsync(net->d_stage2[k], images + s * b * chw, b * chw * sizeof(float),
-                             cudaMemcpyHostToDevice, net->copy_stream));
-    PSG_CUDA(cudaMemcpyAsync(net->d_lab2[k], labels + s * b, b * sizeof(int32_t),
-                             cudaMemcpyHostToDevice, net->copy_stream));
-    PSG_CUDA(cudaEventRecord(net->copied[k], net->copy_stream));
-    PSG_CUDA(cudaStreamWaitEvent(net->stream, net->copied[k], 0));
-    PSG_CUDA(cudaGraphLaunch(net->host_graph2[k], net->stream));
-    PSG_CUDA(cudaEventRecord(net->consumed[k], net->stream));
-    PSG_CUDA(cudaMemcpyAsync(net->h_losses + s, &net->dsc->loss, sizeof(double),
-                             cudaMemcpyDeviceToHost, net->stream));
+    PSG_CUDA(cudaEventSynchronize(net->h_ring_ev[k]));  // this buffer's last H2D is done
+    float* dst = net->h_ring[k];
+    const uint64_t* rs = rows + s * b;
+    auto work = [&](size_t i0, size_t i1) {
+      for (size_t i = i0; i < i1; ++i)
+        std::memcpy(dst + i * chw, ds_images + rs[i] * chw, chw * sizeof(float));
+    };
+    const size_t per = (b + threads - 1) / threads;
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads && static_cast<size_t>(t) * per < b; ++t)
+      pool.emplace_back(work, t * per, std::min(b, (t + 1) * per));
+    work(0, std::min(b, per));
+    for (std::thread& th : pool) th.join();
+    for (size_t i = 0; i < b; ++i) net->h_ring_lab[k][i] = ds_labels[rs[i]];
+    host_step_enqueue(net, dst, net->h_ring_lab[k], s, b, chw);
+    PSG_CUDA(cudaEventRecord(net->h_ring_ev[k], net->copy_stream));  // after its H2D
   }
   PSG_CUDA(cudaEventRecord(net->t1, net->stream));
   net->timed = true;

@@ -156,6 +156,11 @@ struct psg_net {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
   double* h_losses = nullptr;
+  // host-side loader (net_train_host_rows): two pinned batches gathered on the host
+  float* h_ring[2] = {nullptr, nullptr};
+  int32_t* h_ring_lab[2] = {nullptr, nullptr};
+  cudaEvent_t h_ring_ev[2] = {nullptr, nullptr};
+  size_t h_ring_cap = 0;
   size_t h_losses_cap = 0;
   cudaEvent_t slots[16] = {};
 };
@@ -210,6 +215,9 @@ void plan_fusion(psg_net* net);
 void net_profile_step(psg_net* net, int repeats, psg_op_time* out, int max_ops, int* n_ops);
 void net_train_host(psg_net* net, const float* images, const int32_t* labels, long steps,
                     double* losses);
+void net_train_host_rows(psg_net* net, const float* ds_images, const int32_t* ds_labels,
+                         size_t ds_rows, const uint64_t* rows, long steps, double* losses,
+                         int threads);
 
 void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed);
 void net_free(psg_net* net);

@@ -372,6 +372,24 @@ class Net:
                   labels.ctypes.data_as(_lib._I32), steps, losses.ctypes.data_as(_lib._D))
         return losses
 
+    def train_host_rows(self, images: np.ndarray, labels: np.ndarray, rows: np.ndarray,
+                        threads: int = 8) -> np.ndarray:
+        """End-to-end path with a host loader: steps = rows.size // b; per step `threads`
+        host threads gather rows `rows[s*b:(s+1)*b]` of the host dataset (NCHW fp32,
+        int32 labels) into pinned staging while the GPU runs the previous step, then the
+        H2D copy, the step and a D2H read of its loss.  Returns the per-step losses."""
+        assert images.dtype == np.float32 and images.flags.c_contiguous
+        assert labels.dtype == np.int32 and labels.flags.c_contiguous
+        rows = np.ascontiguousarray(rows, np.uint64)
+        b = self._spec.data_spec().shape[0]
+        steps = rows.size // b
+        losses = np.empty(steps, np.float64)
+        _lib.call("psg_net_train_host_rows", self.handle, images.ctypes.data_as(_lib._F),
+                  labels.ctypes.data_as(_lib._I32), images.shape[0],
+                  rows.ctypes.data_as(_lib._U64), steps, losses.ctypes.data_as(_lib._D),
+                  threads)
+        return losses
+
     def profile_step(self, repeats: int = 5):
         """Per-op CUDA-event times of one training step (list of dicts)."""
         cap = 512

@@ -371,3 +371,25 @@ def test_train_host_matches_device_stream(gpu, oracle_lib, name):
     losses = b.train_host(img.array, lab.array)
     np.testing.assert_array_equal(a.get_weights_flat(), b.get_weights_flat())
     assert losses[-1] == a.last_loss()
+
+
+@pytest.mark.parametrize("name,threads", [("cifar10_quick", 1), ("cifar10_quick", 4), ("s2d", 3)])
+def test_train_host_rows_matches_device_stream(gpu, oracle_lib, name, threads):
+    """psg_net_train_host_rows (host threads gather each step's rows into pinned staging while
+    the GPU runs the previous step) == psg_net_train on the HBM-resident stream, bitwise."""
+    from paper_1511_06051_b200 import data
+    spec = ns.make_cifar10_quick(10) if name == "cifar10_quick" else _s2d_net(10)
+    ds = _dataset(gpu, oracle_lib, spec, 6)
+    shards = data.shard(ds, 1, 4)
+    a = gpu.Net(spec, 2, precision="tf32")
+    b = gpu.Net(spec, 2, precision="tf32")
+    for n in (a, b):
+        n.set_sgd(gpu.SgdOptions(0.01, 0.9, 0.004))
+    a.set_training_data(data.make_worker_iterator(shards, 0, 10, 4))
+    a.train(7)
+    it = data.make_worker_iterator(shards, 0, 10, 4)
+    rows = np.concatenate([it.next_indices() for _ in range(7)])
+    img = np.ascontiguousarray(ds.images, np.float32)
+    losses = b.train_host_rows(img, np.ascontiguousarray(ds.labels, np.int32), rows, threads)
+    np.testing.assert_array_equal(a.get_weights_flat(), b.get_weights_flat())
+    assert losses.size == 7 and losses[-1] == a.last_loss()
