@@ -561,13 +561,33 @@ __device__ __forceinline__ void ld_run(const float* p, float* v) {
     }
   }
 }
-template <int NW, int RUN>
+// n / d and n % d for a fixed divisor from a host-computed magic multiplier (n < 2^31)
+// (mul = ceil(2^(32+s) / d) < 2^33 with s = ceil(log2 d): n * mul < 2^64, and the rounding
+// error n * (mul * d - 2^(32+s)) / (d * 2^(32+s)) < 1 / (2d) never crosses an integer)
+struct FastDiv {
+  uint64_t mul = 0;
+  uint32_t d = 1, shift = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    while ((1ull << shift) < d) ++shift;
+    mul = ((1ull << (32 + shift)) + d - 1) / d;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return static_cast<uint32_t>((static_cast<uint64_t>(n) * mul) >> (32 + shift));
+  }
+};
+
+// S > 0: the specialised case (3x3 windows, stride S, no padding, compile time): the
+// covering windows of a pixel come from shifts, their bounds checks are implied by the
+// range, and the route bytes of 4 channels compare in one SIMD op.  S = 0: any geometry.
+template <int NW, int RUN, int S>
 __global__ void __launch_bounds__(256) lrn_maxpool_bwd_k(LrnGeom lg, PoolGeom g,
                                                          const float* __restrict__ x,
                                                          const float* __restrict__ dpool,
                                                          const uint8_t* __restrict__ route,
                                                          float* __restrict__ dx, int accumulate,
-                                                         int relu_mask, int lp, uint32_t pixels) {
+                                                         int relu_mask, int lp, uint32_t pixels,
+                                                         FastDiv fw, FastDiv fh) {
   pdl_enter();
   const int C = g.C, runs = C / RUN, ppw = 32 / lp;
   const float a = lg.alpha / lg.size, ratio = 2.f * lg.alpha * lg.beta / lg.size;
@@ -580,7 +600,46 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd_k(LrnGeom lg, PoolGeom g,
 #pragma unroll
     for (int i = 0; i < RUN; ++i) v[i] = d[i] = 0.f;
     size_t base = 0;
-    if (act) {
+    if constexpr (S > 0) {
+     if (act) {
+      base = static_cast<size_t>(pix) * C + c0;
+      ld_run<RUN>(x + base, v);
+      const uint32_t t = fw.div(pix), bq = fh.div(t);
+      const int wq = static_cast<int>(pix - t * g.W), h = static_cast<int>(t - bq * g.H);
+      const int ohl = max(0, (h - 3 + S) / S), ohh = min(g.OH - 1, h / S);
+      const int owl = max(0, (wq - 3 + S) / S), owh = min(g.OW - 1, wq / S);
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        const int oh = ohl + i;
+        if (oh > ohh) break;
+        const size_t orow = (static_cast<size_t>(bq) * g.OH + oh) * g.OW;
+        const uint32_t u3 = static_cast<uint32_t>(h - oh * S) * 3u;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+          const int ow = owl + q;
+          if (ow > owh) break;
+          const uint32_t want = (u3 + static_cast<uint32_t>(wq - ow * S)) * 0x01010101u;
+          const size_t ob = (orow + ow) * C + c0;
+          float dd[RUN];
+          ld_run<RUN>(dpool + ob, dd);
+          uint32_t rr[2];
+          if constexpr (RUN == 8) {
+            const uint2 q2 = __ldg(reinterpret_cast<const uint2*>(route + ob));
+            rr[0] = q2.x;
+            rr[1] = q2.y;
+          } else {
+            const uint16_t* r16 = reinterpret_cast<const uint16_t*>(route + ob);
+            rr[0] = __ldg(r16) | (static_cast<uint32_t>(__ldg(r16 + 1)) << 16);
+            rr[1] = __ldg(r16 + 2);
+          }
+          const uint32_t m0 = __vcmpeq4(rr[0], want), m1 = __vcmpeq4(rr[1], want);
+#pragma unroll
+          for (int e = 0; e < RUN; ++e)  // select, not "+ 0": same values as the generic path
+            d[e] = ((e < 4 ? m0 : m1) >> (8 * (e & 3))) & 1u ? d[e] + dd[e] : d[e];
+        }
+      }
+     }
+    } else if (act) {
       base = static_cast<size_t>(pix) * C + c0;
       ld_run<RUN>(x + base, v);
       const int wq = static_cast<int>(pix % g.W);
@@ -912,10 +971,18 @@ void lrn_maxpool_bwd(const LrnGeom& lg, const PoolGeom& g, const float* x, const
   const uint32_t pixels = checked32(static_cast<size_t>(g.n) * g.H * g.W, "lrn_pool");
   checked32(static_cast<size_t>(pixels) * g.C, "lrn_pool");
   const size_t warps = (pixels + 32 / lp - 1) / (32 / lp);
-  auto kern = six ? (g.sh == 1 ? lrn_maxpool_bwd_k<3, 6> : lrn_maxpool_bwd_k<2, 6>)
-                  : (g.sh == 1 ? lrn_maxpool_bwd_k<3, 8> : lrn_maxpool_bwd_k<2, 8>);
+  static const bool spec_env = [] {  // PSG_LRN_BWD_SPEC=0: the generic window path (A/B)
+    const char* e = std::getenv("PSG_LRN_BWD_SPEC");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  const bool spec = spec_env && g.ph == 0 && g.pw == 0;  // fusable: 3x3, stride 1 or 2
+  auto kern = spec ? (six ? (g.sh == 1 ? lrn_maxpool_bwd_k<3, 6, 1> : lrn_maxpool_bwd_k<2, 6, 2>)
+                          : (g.sh == 1 ? lrn_maxpool_bwd_k<3, 8, 1> : lrn_maxpool_bwd_k<2, 8, 2>))
+                   : (six ? (g.sh == 1 ? lrn_maxpool_bwd_k<3, 6, 0> : lrn_maxpool_bwd_k<2, 6, 0>)
+                          : (g.sh == 1 ? lrn_maxpool_bwd_k<3, 8, 0> : lrn_maxpool_bwd_k<2, 8, 0>));
   launch_k(kern, grid_for(warps * 32, 256, 148 * 8), 256, 0, s, lg, g, x, dpool, route, dx,
-           accumulate ? 1 : 0, relu_mask ? 1 : 0, lp, pixels);
+           accumulate ? 1 : 0, relu_mask ? 1 : 0, lp, pixels,
+           FastDiv(static_cast<uint32_t>(g.W)), FastDiv(static_cast<uint32_t>(g.H)));
   PSG_CUDA(cudaGetLastError());
 }
 
