@@ -266,26 +266,35 @@ class CpuRound:
 
     def round(self, steps=1):
         """One round of `steps` local steps per worker + the average; returns (seconds of
-        the steps, seconds of the average)."""
+        forward + backward, seconds of apply_update — both the slowest worker's, per step —
+        and seconds of the average)."""
+        fb, upd = [0.0] * self.K, [0.0] * self.K
+
         def work(k):
             n = self.nets[k]
             x, y = self.batches[k]
             for _ in range(steps):
+                t0 = time.perf_counter()
                 _, g = n.backward(x, y)
+                t1 = time.perf_counter()
                 n.apply_update(g)
-        t0 = time.perf_counter()
+                fb[k] += t1 - t0
+                upd[k] += time.perf_counter() - t1
         self._parallel(work, self.threading)
         t1 = time.perf_counter()
         ws = [n.get_weights() for n in self.nets]
         mean = self.lib.weights_mean(ws)
         for n in self.nets:
             n.set_weights(mean)
-        return t1 - t0, time.perf_counter() - t1
+        return max(fb) / steps, max(upd) / steps, time.perf_counter() - t1
 
-    def value_at(self, tau, t_step, t_avg):
-        """images/sec of a round of tau steps: the round is tau sequential steps per worker
-        followed by one average (schemes.hpp:323-336)."""
-        return self.K * tau * self.b / (tau * t_step + t_avg)
+    def value_at(self, tau, b_cfg, t_fb, t_upd, t_avg):
+        """images/sec of the configuration's round: tau sequential steps per worker — the
+        forward / backward time scaled from the sample's batch to the configuration's
+        (per-image work), the update per step as measured — then one average
+        (schemes.hpp:323-336)."""
+        t_step = t_fb * b_cfg / self.b + t_upd
+        return self.K * tau * b_cfg / (tau * t_step + t_avg)
 
 
 def cpu_baseline(workload, b, threads, steps=1, rounds=1, tau=None):
@@ -315,13 +324,14 @@ def cpu_baseline(workload, b, threads, steps=1, rounds=1, tau=None):
     else:
         cr = CpuRound(workload, b, threads)
         ts = [cr.round(1) for _ in range(rounds)]
-        t_step, t_avg = sum(t for t, _ in ts) / rounds, sum(a for _, a in ts) / rounds
+        t_fb, t_upd, t_avg = (sum(t[i] for t in ts) / rounds for i in range(3))
         tau = tau or 1
-        value, bs = cr.value_at(tau, t_step, t_avg), cr.b
-        sample = (f"{workload} per-worker batch {bs}: {threads} workers x 1 SGD step on "
-                  f"{threads} host threads ({t_step:.2f} s) + the K-way weights_mean / "
-                  f"get / set_weights ({t_avg:.2f} s), round time at tau={tau} = tau x step "
-                  f"+ average")
+        value, bs = cr.value_at(tau, b, t_fb, t_upd, t_avg), cr.b
+        sample = (f"{workload}: {threads} workers on {threads} host threads, sample batch "
+                  f"{bs} per worker (forward+backward {t_fb:.2f} s, apply_update {t_upd:.2f} s "
+                  f"per step) + the K-way weights_mean / get / set_weights ({t_avg:.2f} s); "
+                  f"round at tau={tau}, batch {b}: tau x (fwd+bwd x {b}/{bs} + update) + "
+                  f"average")
     out = {"value": value, "unit": "images/sec", "cores": threads,
            "kind": "reference" if use_ref else "port", "sample": sample}
     out.update(host_cpu())
@@ -346,22 +356,23 @@ def run_reference(args):
         for _ in range(args.warmup):
             cr.round(1)
         ts = [cr.round(1) for _ in range(args.steps)]
-        t_step = sum(t for t, _ in ts) / args.steps
-        t_avg = sum(a for _, a in ts) / args.steps
+        t_fb, t_upd, t_avg = (sum(t[i] for t in ts) / args.steps for i in range(3))
         bs, kind = cr.b, "port"
-        value = cr.value_at(args.tau, t_step, t_avg)
+        value = cr.value_at(args.tau, b, t_fb, t_upd, t_avg)
     cb = {"value": value, "unit": "images/sec", "cores": threads, "kind": kind,
           "sample": f"per step: {threads} worker(s) x 1 SGD step of {args.workload} at "
-                    f"per-worker batch {bs} on {threads} host thread(s) + the K-way average; "
-                    f"value = K*tau*b / (tau*step + average) at tau={args.tau}"}
+                    f"sample batch {bs} on {threads} host thread(s) + the K-way average; "
+                    f"value = K*tau*b / (tau*(fwd_bwd*b/{bs} + update) + average) at "
+                    f"tau={args.tau}, b={b}"}
     cb.update(host_cpu())
     print(json.dumps({
         "impl": "reference", "metric": "images/sec", "value": value, "unit": "images/sec",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": threads * bs / value * 1000.0, "higher_is_better": True,
+        "ms_per_step": threads * b / value * 1000.0, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "global_batch": bs * threads, "K": threads,
-                   "tau": args.tau, "note": "reference CPU path (bounded sample per step)"},
+        "config": {"workload": args.workload, "global_batch": b * threads, "K": threads,
+                   "tau": args.tau, "per_worker_batch": b, "sample_batch": bs,
+                   "note": "reference CPU path (bounded sample per step)"},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "images/sec", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}))
