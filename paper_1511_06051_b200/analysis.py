@@ -168,8 +168,11 @@ def _for_workers(ctx: SchemeContext, k: int) -> SchemeContext:
 def _measured(trace: RunTrace, tau: int) -> Tuple[float, float]:
     if not trace.compute_ms:
         return 0.0, 0.0
-    # median over rounds: the first round also pays the one-time CUDA-graph capture
-    return lower_median(trace.compute_ms) / tau, lower_median(trace.sync_ms)
+    # median over rounds after the first, which also pays the one-time CUDA-graph capture
+    # and the communicators' connection setup (the first round alone if it is the only one)
+    comp = trace.compute_ms[1:] or trace.compute_ms
+    sync = trace.sync_ms[1:] or trace.sync_ms
+    return lower_median(comp) / tau, lower_median(sync)
 
 
 def sweep_heatmap(base: SchemeContext, spec: HeatmapSpec) -> HeatmapResult:

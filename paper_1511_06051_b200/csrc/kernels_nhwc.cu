@@ -752,15 +752,18 @@ __global__ void dropout_fwd_k(DropGeom g, const float* __restrict__ x, float* __
   GRID_STRIDE32(i, total) y[i] = x[i] * drop_mask(g, base, i, thresh, keep);
 }
 
+// relu_mask: the backward of a ReLU whose only consumer is this dropout, folded in
+// (dx = relu_mask > 0 ? dy * mask : 0, written to the ReLU's input gradient).
 __global__ void dropout_bwd_k(DropGeom g, const float* __restrict__ dy, float* __restrict__ dx,
                               const uint64_t* __restrict__ d_step, int accumulate,
-                              uint32_t total) {
+                              const float* __restrict__ relu_mask, uint32_t total) {
   pdl_enter();
   const uint64_t base = mix64(g.base_seed ^ *d_step);
   const uint32_t thresh = static_cast<uint32_t>(static_cast<double>(g.ratio) * 16777216.0);
   const float keep = static_cast<float>(1.0 / (1.0 - static_cast<double>(g.ratio)));
   GRID_STRIDE32(i, total) {
-    const float v = dy[i] * drop_mask(g, base, i, thresh, keep);
+    float v = dy[i] * drop_mask(g, base, i, thresh, keep);
+    if (relu_mask && !(relu_mask[i] > 0.f)) v = 0.f;
     dx[i] = accumulate ? dx[i] + v : v;
   }
 }
@@ -915,9 +918,9 @@ void dropout_fwd(const DropGeom& g, const float* x, float* y, const uint64_t* d_
 }
 
 void dropout_bwd(const DropGeom& g, const float* dy, float* dx, const uint64_t* d_step,
-                 bool accumulate, cudaStream_t s) {
+                 bool accumulate, cudaStream_t s, const float* relu_mask) {
   const uint32_t n = checked32(static_cast<size_t>(g.n) * g.C * g.H * g.W, "dropout");
-  launch_k(dropout_bwd_k, grid_for(n), 256, 0, s, g, dy, dx, d_step, accumulate, n);
+  launch_k(dropout_bwd_k, grid_for(n), 256, 0, s, g, dy, dx, d_step, accumulate, relu_mask, n);
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -235,7 +235,7 @@ int foldable_relu(const psg_net* net, const LayerRt& c) {
   if (!net->fuse || c.inputs.size() != 1) return -1;
   const int ri = foldable_relu_input(net, c.inputs[0]);
   if (ri < 0) return -1;
-  if (c.kind == PSG_LAYER_POOL) return ri;
+  if (c.kind == PSG_LAYER_POOL || c.kind == PSG_LAYER_DROPOUT) return ri;
   if ((c.kind == PSG_LAYER_CONV || c.kind == PSG_LAYER_LINEAR) && net->mode == Mode::Tf32 &&
       conv_dgrad_masks(c.cg, net->mode))
     return ri;
@@ -390,7 +390,16 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           DropGeom g = l.dg;
           g.n = static_cast<int>(n);
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 2 * act_bytes(l, n));
-          dropout_bwd(g, l.grad, src.grad, &net->dsc->step, acc, s);
+          const int ri = foldable_relu(net, l);
+          if (ri >= 0) {  // ReLU backward folded in: mask by the ReLU's output
+            const int pi2 = net->L[ri].inputs[0];
+            dropout_bwd(g, l.grad, net->L[pi2].grad, &net->dsc->step, written[pi2] != 0, s,
+                        net->L[ri].out);
+            written[pi2] = 1;
+            relu_folded[ri] = 1;
+          } else {
+            dropout_bwd(g, l.grad, src.grad, &net->dsc->step, acc, s);
+          }
           sc.done(1);
           ++launches;
         }

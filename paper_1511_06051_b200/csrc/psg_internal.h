@@ -195,8 +195,9 @@ struct DropGeom {
 };
 void dropout_fwd(const DropGeom& g, const float* x, float* y, const uint64_t* d_step, bool train,
                  cudaStream_t s);
+// relu_mask: a folded ReLU backward (dx (+)= relu_mask > 0 ? dy * mask : 0)
 void dropout_bwd(const DropGeom& g, const float* dy, float* dx, const uint64_t* d_step,
-                 bool accumulate, cudaStream_t s);
+                 bool accumulate, cudaStream_t s, const float* relu_mask = nullptr);
 
 // Softmax + mean cross-entropy (x loss_weight) + the loss seed; per-row loss
 // terms in fp64, reduced in fixed order into *loss.
