@@ -254,6 +254,11 @@ int psg_net_kernels_per_step(const psg_net* net, int* launches);
  * buffer is allocated between two 4 KB guard bands of 0xA5; the count of overwritten guard
  * bytes over all live (and already freed) net buffers, and the first offender. */
 int psg_debug_guard_violations(unsigned long long* bad_bytes, char* first, size_t first_len);
+/* Debug (profiling tools; no reference counterpart): with PSG_TC_PROF=1 in the environment
+ * every tcgen05 GEMM launch records clock64 counters of its pipeline waits; one line per
+ * launch: "index|plan label|loop wait_full wait_acc stages prod_wait prod_loop epi_wait
+ * epi_loop" (cycles summed over the leader CTAs).  reset != 0 zeroes the counters. */
+int psg_debug_tc_prof(char* buf, size_t len, int reset);
 
 /* ---- measurement ------------------------------------------------------------ */
 /* One op of a training step: algorithmic work and its CUDA-event device time. */

@@ -118,6 +118,7 @@ SIGNATURES = {
     "psg_net_grad_step": (ctypes.c_int, [_VP]),
     "psg_net_set_tc_options": (ctypes.c_int, [_VP, ctypes.c_int]),
     "psg_debug_guard_violations": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_char_p, _SZ]),
+    "psg_debug_tc_prof": (ctypes.c_int, [ctypes.c_char_p, _SZ, ctypes.c_int]),
     "psg_net_train_round": (ctypes.c_int, [_VP, ctypes.c_long, _VP]),
     "psg_net_train_host_rows": (ctypes.c_int, [_VP, _F, _I32, _SZ, _U64, ctypes.c_long, _D, ctypes.c_int]),
     "psg_net_set_fusion": (ctypes.c_int, [_VP, ctypes.c_int]),

@@ -665,6 +665,16 @@ int psg_net_set_tc_options(psg_net* net, int pair_policy) {
   });
 }
 
+int psg_debug_tc_prof(char* buf, size_t len, int reset) {
+  return guarded([&] {
+    const std::string r = psg::tc_prof_report(reset != 0);
+    if (buf && len) {
+      std::strncpy(buf, r.c_str(), len - 1);
+      buf[len - 1] = 0;
+    }
+  });
+}
+
 int psg_debug_guard_violations(unsigned long long* bad_bytes, char* first, size_t first_len) {
   return guarded([&] {
     std::string f;

@@ -505,6 +505,29 @@ const float* ones_matrix() {
   return per_dev[dev];
 }
 
+// PSG_TC_PROF=1: every launch gets its own 8 clock64 counters (TcArgs::prof) and a label;
+// psg_debug_tc_prof prints them.  The counter block is allocated with the workspaces,
+// outside any stream capture.
+struct TcProf {
+  std::mutex mu;
+  bool on = std::getenv("PSG_TC_PROF") != nullptr;
+  unsigned long long* dev = nullptr;
+  std::vector<std::string> labels;
+};
+constexpr int kProfMax = 1024;
+TcProf& tc_prof() {
+  static TcProf p;
+  return p;
+}
+void tc_prof_alloc() {
+  TcProf& pr = tc_prof();
+  std::lock_guard<std::mutex> lock(pr.mu);
+  if (!pr.on || pr.dev) return;
+  PSG_CUDA(cudaMalloc(&pr.dev, kProfMax * 8 * sizeof(unsigned long long)));
+  PSG_CUDA(cudaMemset(pr.dev, 0, kProfMax * 8 * sizeof(unsigned long long)));
+  PSG_CUDA(cudaDeviceSynchronize());
+}
+
 void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int kblk,
             long long out_elems, float* ws, size_t ws_elems, cudaStream_t s) {
   TcArgs a = a0;
@@ -539,6 +562,19 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   const size_t smem = static_cast<size_t>(a.ring_bytes) + 4 * a.epi_tma * kOutChunkBytes +
                       1024;  // + alignment of the dynamic base
   const int per = a.pair ? 2 : 1;
+  {
+    TcProf& pr = tc_prof();
+    std::lock_guard<std::mutex> lock(pr.mu);
+    if (pr.dev && pr.labels.size() < static_cast<size_t>(kProfMax)) {
+      a.prof = pr.dev + pr.labels.size() * 8;
+      char buf[160];
+      std::snprintf(buf, sizeof buf,
+                    "kblk%d a%d b%d pair%d n%dx%d m%d G%d taps%d kb%d splits%d kps%d stages%d",
+                    kblk, a.a_mode, a.b_mode, a.pair, a.n_tile, a.n_tiles, a.m_tiles, a.G,
+                    a.taps, a.kblocks, splits, a.kps, a.stages);
+      pr.labels.push_back(buf);
+    }
+  }
   static const bool debug = std::getenv("PSG_TC_DEBUG") != nullptr;
   if (debug)
     std::fprintf(stderr,
@@ -937,6 +973,7 @@ bool tc_supported(const ConvGeom& g, int which) {
 
 size_t tc_workspace_elems(const ConvGeom& g) {
   ones_matrix();  // allocated here, outside any stream capture (the nets size workspaces first)
+  tc_prof_alloc();
   size_t e = 0;
   TcArgs a;
   int kblk;
@@ -1140,6 +1177,28 @@ void tc_wgrad_col(const ConvGeom& g, const float* col, const float* dy, float* d
   float* part = ws.ptr + (splits > 1 ? splits * dw_elems : 0);
   launch(a, ma, mb, 32, dw_elems, ws.ptr, ws.elems, s);
   bias_grad(dy, pixels, g.F, part, db, s);
+}
+
+
+// Labels and counters of the PSG_TC_PROF launches, one line each (see TcArgs::prof).
+std::string tc_prof_report(bool reset) {
+  TcProf& pr = tc_prof();
+  std::lock_guard<std::mutex> lock(pr.mu);
+  std::string out;
+  if (!pr.dev) return out;
+  std::vector<unsigned long long> h(pr.labels.size() * 8);
+  if (!h.empty())
+    PSG_CUDA(cudaMemcpy(h.data(), pr.dev, h.size() * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < pr.labels.size(); ++i) {
+    char buf[320];
+    std::snprintf(buf, sizeof buf, "%zu|%s|%llu %llu %llu %llu %llu %llu %llu %llu\n", i,
+                  pr.labels[i].c_str(), h[i * 8], h[i * 8 + 1], h[i * 8 + 2], h[i * 8 + 3],
+                  h[i * 8 + 4], h[i * 8 + 5], h[i * 8 + 6], h[i * 8 + 7]);
+    out += buf;
+  }
+  if (reset) PSG_CUDA(cudaMemset(pr.dev, 0, kProfMax * 8 * sizeof(unsigned long long)));
+  return out;
 }
 
 }  // namespace psg

@@ -271,4 +271,7 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   PSG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
+// PSG_TC_PROF=1 launch counters, one "index|label|8 counters" line per GEMM launch
+std::string tc_prof_report(bool reset);
+
 }  // namespace psg

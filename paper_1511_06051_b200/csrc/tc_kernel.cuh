@@ -106,6 +106,11 @@ struct TcArgs {
   int db_ld;               // F
   int epi_tma;             // 0, or the staging chunks per epilogue warp (1 or 2)
   int ring_bytes;          // stage ring bytes (the staging area follows, 1024-aligned)
+  // PSG_TC_PROF=1: per-launch clock64 counters (rank-0 CTAs): [0] MMA-loop cycles, [1] MMA
+  // warp waiting for a full stage, [2] ... for a free accumulator, [3] stages consumed,
+  // [4] producer 0 waiting for an empty slot, [5] producer-0 loop cycles, [6] epilogue warp 0
+  // waiting for a finished accumulator, [7] epilogue-warp-0 loop cycles; null = off
+  unsigned long long* prof;
 };
 
 // Per-tile B_TAPS_MN chunk table: tap shift and channel offset of each 32-column chunk.
@@ -227,12 +232,12 @@ struct KCursor {
   }
 };
 
-// Operand loads of one K block, all issued by the producer warp's elected lane.  A TMA
-// issue occupies its thread for a few hundred cycles whatever the box size
-// (tools/tma_bench.cu), and the lanes of one warp are serialised anyway (the tensor-map
-// operands must be warp-uniform), so throughput comes from several producer warps working
-// on different stages, and boxes stay as large as the layout allows (a whole K-major
-// operand tile is one box; MN-major operands are 32-float chunks).
+// Operand loads of one K block, all issued by the producer warp's elected lane; throughput
+// comes from several producer warps working on different stages, and boxes stay as large
+// as the layout allows (a whole K-major operand tile is one box; MN-major operands are
+// 32-float chunks).  Dealing one stage's boxes to several issuers measured slower on
+// AlexNet: 2 or 4 lanes of the producer warp -12%, 2 / 3 producer warps -8% / -26%
+// (tools/tc_prof.py: the MMA warp waited longer for full stages).
 template <int KBLK, bool PAIR>
 __device__ __forceinline__ void load_a(const TcArgs& p, const CUtensorMap* map, const Tile& t,
                                        const KCursor& c, int rb, int oh0, int ow0, uint32_t sa,
@@ -391,6 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // pairs: the leader posts both CTAs' bytes (identical per CTA); the peer only loads
     const uint32_t bytes = (p.a_tx + (p.stage_bytes - p.a_bytes)) * (PAIR ? 2 : 1);
     const int P = p.producers;
+    const bool prof = p.prof != nullptr && pw == 0 && rank == 0;
+    long long prof_t0 = prof ? clock64() : 0, prof_w = 0;
     uint32_t it_tile = 0;  // global stage index of the tile's first stage
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep) {
       Tile t = decode_tile(p, tt);
@@ -423,7 +430,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int cnt = min(p.kps, kb1 - (kb0 + si * p.kps));
           const uint32_t bar = PAIR ? tc::mapa(tc::smem_u32(&full_bar[s]), 0)
                                     : tc::smem_u32(&full_bar[s]);
-          tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
+          if (prof) {
+            const long long w0 = clock64();
+            tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
+            prof_w += clock64() - w0;
+          } else {
+            tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
+          }
           if (rank == 0) tc::mbar_arrive_expect_tx(tc::smem_u32(&full_bar[s]), bytes * cnt);
           for (int j = 0; j < cnt; ++j, c.next(p)) {
             const uint32_t sa = tc::smem_u32(smem + (s * p.kps + j) * p.stage_bytes);
@@ -439,6 +452,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       it_tile += nst;
+    }
+    if (prof) {
+      atomicAdd(p.prof + 4, static_cast<unsigned long long>(prof_w));
+      atomicAdd(p.prof + 5, static_cast<unsigned long long>(clock64() - prof_t0));
     }
   } else if (warp == kMmaWarp && rank == 0) {
     // ------------------------------------------------------------ MMA issue
@@ -459,19 +476,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t a_step = (a_mn ? 1024u : 32u) >> 4, b_step = (b_mn ? 1024u : 32u) >> 4;
     const uint32_t slot_step = static_cast<uint32_t>(p.stage_bytes) >> 4;
     const bool leader = tc::elect_one();
+    const bool prof = p.prof != nullptr;
+    long long prof_t0 = prof ? clock64() : 0, prof_wf = 0, prof_wt = 0, prof_n = 0;
     uint32_t st = 0, ph = 0, local = 0;  // ring slot and its parity
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {
       const Tile t = decode_tile(p, tt);
       const int kb0 = t.split * p.kb_per_split;
       const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
       const uint32_t acc = local & 1;
-      tc::mbar_wait(tc::smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
+      if (prof) {
+        const long long w0 = clock64();
+        tc::mbar_wait(tc::smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
+        prof_wt += clock64() - w0;
+      } else {
+        tc::mbar_wait(tc::smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
+      }
       tc::fence_after_sync();
       const uint32_t d = tmem + acc * kAccCols;
       for (int i = 0; i < nkb;) {
         const int cnt = min(p.kps, nkb - i);
         const uint32_t s = st;
-        tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
+        if (prof) {
+          const long long w0 = clock64();
+          tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
+          prof_wf += clock64() - w0;
+          ++prof_n;
+        } else {
+          tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
+        }
         tc::fence_after_sync();
         if (leader) {
           uint32_t off = s * static_cast<uint32_t>(p.kps) * slot_step;
@@ -507,12 +539,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     }
+    if (prof && lane == 0) {
+      atomicAdd(p.prof + 0, static_cast<unsigned long long>(clock64() - prof_t0));
+      atomicAdd(p.prof + 1, static_cast<unsigned long long>(prof_wf));
+      atomicAdd(p.prof + 2, static_cast<unsigned long long>(prof_wt));
+      atomicAdd(p.prof + 3, static_cast<unsigned long long>(prof_n));
+    }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - kEpiWarp0;
     uint32_t local = 0;
     uint32_t ochunk = 0;  // TMA-store chunks issued by this warp (staging buffer ochunk % 2)
     uint8_t* const ostage = smem + p.ring_bytes + ew * p.epi_tma * kOutChunkBytes;
+    const bool prof = p.prof != nullptr && ew == 0 && rank == 0;
+    long long prof_t0 = prof ? clock64() : 0, prof_w = 0;
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {
       Tile t = decode_tile(p, tt);
       if (PAIR) t.m = 2 * t.m + rank;
@@ -543,7 +583,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           bias_sh[acc][i] = i < nvalid ? p.bias[col0 + i] : 0.f;
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
-      tc::mbar_wait(tc::smem_u32(&tfull_bar[acc]), (local >> 1) & 1);
+      if (prof) {
+        const long long w0 = clock64();
+        tc::mbar_wait(tc::smem_u32(&tfull_bar[acc]), (local >> 1) & 1);
+        prof_w += clock64() - w0;
+      } else {
+        tc::mbar_wait(tc::smem_u32(&tfull_bar[acc]), (local >> 1) & 1);
+      }
       tc::fence_after_sync();
       const uint32_t taddr = tmem + acc * kAccCols + (static_cast<uint32_t>(ew * 32) << 16);
       // Thread = one accumulator row (its TMEM lane): the 32-column chunks stream out of
@@ -729,6 +775,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(tc::smem_u32(&tempty_bar[acc]));
     }
     if (EPI != 2 && p.epi_tma && lane == 0) tc::bulk_wait_all();  // stores done before exit
+    if (prof && lane == 0) {
+      atomicAdd(p.prof + 6, static_cast<unsigned long long>(prof_w));
+      atomicAdd(p.prof + 7, static_cast<unsigned long long>(clock64() - prof_t0));
+    }
   }
   tc::fence_before_sync();
   if constexpr (PAIR)
