@@ -376,7 +376,11 @@ bool want_pair(const TcArgs& a) {
   // small GEMMs: halving the number of work units costs more in load balance than the
   // pair gains (cifar10_quick); want >= 2 waves of clusters
   const long long units = static_cast<long long>((a.m_tiles + 1) / 2) * a.n_tiles * a.G * a.taps;
-  return env > 1 || units >= sm_count();
+  // long-K linear layers (AlexNet fc6 / fc7 at b = 256: two M tiles, split K restores the
+  // parallelism): the pair reads each weight tile from L2 once instead of per M tile,
+  // fc6 fwd / dgrad -10%
+  const bool long_linear = a.a_mode == A_2D_K && a.kblocks >= 64;
+  return env > 1 || units >= sm_count() || long_linear;
 }
 
 // PSG_TC_SPLIT_CHARGE: K blocks charged for splitting at all.  24 (vs 8): cifar10_quick
