@@ -338,66 +338,6 @@ __global__ void __launch_bounds__(256) k_copy_multi(const __grid_constant__ CUte
   if (who == 0) cyc[blockIdx.x] = clock64() - t0;
 }
 
-// TMA multicast: clusters of CS CTAs; per round every CTA's 4 issuer warps post expect_tx for
-// their `depth` 16 KB slots, then each slot's data is read from L2 ONCE (by CTA
-// slot % CS) and multicast into all CS CTAs (mc = 1), or every CTA loads its own copy
-// (mc = 0).  Delivered bytes / time against the ~20 TB/s L2 -> SM ceiling.
-template <int CS>
-__global__ void __launch_bounds__(128) k_copy_mc(const __grid_constant__ CUtensorMap map,
-                                                  long long chunks, int iters, int depth, int mc,
-                                                  long long* cyc) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~1023ull);
-  __shared__ __align__(8) uint64_t full[4][4], empty[4][4];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_rank();
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < 4; ++w)
-      for (int i = 0; i < depth; ++i) {
-        mbar_init(smem_u32(&full[w][i]), 1);
-        mbar_init(smem_u32(&empty[w][i]), mc ? CS : 1);
-      }
-    fence_barrier_init();
-  }
-  cluster_sync();
-  const uint32_t base = smem_u32(smem) + warp * depth * 16384;
-  const long long cl = blockIdx.x / CS;
-  long long t0 = clock64();
-  if (lane == 0) {
-    for (int i = 0; i < iters; ++i) {
-      const int s = i % depth, k = i / depth;
-      const uint32_t fb = smem_u32(&full[warp][s]);
-      if (k > 0) mbar_wait(fb, (k - 1) & 1);
-      mbar_arrive_expect_tx(fb, 16384);
-      const uint32_t owner = mc ? static_cast<uint32_t>(s % CS) : rank;
-      mbar_arrive_cluster(mapa(smem_u32(&empty[warp][s]), owner));
-      if (owner == rank) {
-        mbar_wait(smem_u32(&empty[warp][s]), k & 1);
-        const long long ch = (cl * 7919 + warp * 131 + i * 1184LL + (mc ? 0 : rank * 77)) % chunks;
-        if (mc) {
-          const uint16_t mask = static_cast<uint16_t>((1u << CS) - 1);
-          asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-              " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(base + s * 16384),
-              "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(static_cast<int>(ch * 128)), "r"(fb),
-              "h"(mask)
-              : "memory");
-        } else {
-          tma_load_2d(base + s * 16384, &map, fb, 0, static_cast<int>(ch * 128));
-        }
-      }
-    }
-    // drain: the last `depth` uses
-    for (int i = iters; i < iters + depth; ++i) {
-      const int s = i % depth, k = i / depth;
-      if (k > 0) mbar_wait(smem_u32(&full[warp][s]), (k - 1) & 1);
-    }
-  }
-  __syncwarp();
-  if (threadIdx.x == 0) cyc[blockIdx.x] = clock64() - t0;
-  cluster_sync();
-}
-
 // Multicast bandwidth without a consumer protocol: per round every CTA expects 512 KB on
 // one barrier; its 4 issuer warps fire 8 boxes each (mc = 0: all 32 boxes loaded locally;
 // mc = 1: box b is read once by CTA b % CS and multicast to the whole cluster).  Slots are
@@ -573,7 +513,7 @@ int main(int argc, char** argv) {
                  depth, bytes / (ms * 1e6), bytes / (ms * 1e-3) / grid / 1.9e9);
         }
     printf("# multicast2: delivered bytes per SM (512 KB per CTA per round)\n");
-    for (int cs : {1, 2, 4})
+    for (int cs : {1, 2})  // (4-CTA clusters with multicast hung in this harness)
       for (int mc : {0, 1}) {
         if (cs == 1 && mc) continue;
         const int rounds = 200;
@@ -592,8 +532,6 @@ int main(int argc, char** argv) {
             cudaLaunchKernelEx(&cfg, k_copy_mc2<1>, map, rows / 128, rr, mc, dc); }
           if (cs == 2) { cudaFuncSetAttribute(k_copy_mc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             cudaLaunchKernelEx(&cfg, k_copy_mc2<2>, map, rows / 128, rr, mc, dc); }
-          if (cs == 4) { cudaFuncSetAttribute(k_copy_mc2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            cudaLaunchKernelEx(&cfg, k_copy_mc2<4>, map, rows / 128, rr, mc, dc); }
         };
         launch(10);
         cudaEventRecord(e0);
@@ -607,47 +545,6 @@ int main(int argc, char** argv) {
         printf("cluster=%d multicast=%d delivered=%.0f GB/s per-SM=%.1f B/clk@1.9GHz  L2 reads=%.0f GB/s\n", cs, mc,
                bytes / (ms * 1e6), bytes / (ms * 1e-3) / g / 1.9e9, bytes / (ms * 1e6) / (mc ? cs : 1));
       }
-    printf("# multicast: delivered bytes per SM (4 issuers x depth 16 KB per round)\n");
-    for (int cs : {2, 4})
-      for (int mc : {0, 1})
-        for (int depth : {2, 3}) {
-          const int rounds = 2000;
-          const size_t sm = 4 * depth * 16384 + 1024;
-          cudaEvent_t e0, e1;
-          cudaEventCreate(&e0);
-          cudaEventCreate(&e1);
-          auto launch = [&](int rr) {
-            if (cs == 2) {
-              cudaFuncSetAttribute(k_copy_mc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-              cudaLaunchConfig_t cfg = {};
-              cfg.gridDim = dim3(dev_sms); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = sm;
-              cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
-              at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-              cfg.attrs = at; cfg.numAttrs = 1;
-              cudaLaunchKernelEx(&cfg, k_copy_mc<2>, map, rows / 128, rr, depth, mc, dc);
-            } else {
-              cudaFuncSetAttribute(k_copy_mc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-              cudaLaunchConfig_t cfg = {};
-              cfg.gridDim = dim3(dev_sms / 4 * 4); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = sm;
-              cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
-              at[0].val.clusterDim.x = 4; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-              cfg.attrs = at; cfg.numAttrs = 1;
-              cudaLaunchKernelEx(&cfg, k_copy_mc<4>, map, rows / 128, rr, depth, mc, dc);
-            }
-          };
-          launch(20);
-          cudaEventRecord(e0);
-          launch(rounds);
-          cudaEventRecord(e1);
-          cudaError_t err = cudaDeviceSynchronize();
-          if (err != cudaSuccess) { printf("mc launch failed: %s\n", cudaGetErrorString(err)); return 1; }
-          float ms;
-          cudaEventElapsedTime(&ms, e0, e1);
-          const int g = cs == 2 ? dev_sms : dev_sms / 4 * 4;
-          const double bytes = static_cast<double>(g) * 4.0 * rounds * 16384.0;
-          printf("cluster=%d multicast=%d depth=%d delivered=%.0f GB/s per-SM=%.1f B/clk@1.9GHz\n", cs, mc,
-                 depth, bytes / (ms * 1e6), bytes / (ms * 1e-3) / g / 1.9e9);
-        }
     printf("# pairs + TMA writers / TMEM readers: cycles per M=256 MMA (K=8)\n");
     cudaFuncSetAttribute(k_bench_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kABytes + kBBytes + 4 * 32768 + 1024);
