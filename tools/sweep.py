@@ -32,6 +32,8 @@ def main():
     p.add_argument("--target", type=float, default=None,
                    help="fixed target accuracy (default: derived at half the serial budget)")
     p.add_argument("--lr", type=float, default=0.01)
+    p.add_argument("--separation", type=float, default=2.0,
+                   help="generate_synthetic class separation (distance between class means)")
     p.add_argument("--precision", default="tf32")
     p.add_argument("--out", default="sweep_out")
     a = p.parse_args()
@@ -39,8 +41,8 @@ def main():
     ngpu = max(1, torch.cuda.device_count())
     spec = (netspec.make_cifar10_quick(a.batch) if a.net == "cifar10_quick"
             else netspec.make_cq_valid(a.batch))
-    train = DeviceSyntheticDataset(10, 3, 32, 32, a.per_class, 2.0, 12345, 0)
-    evald = DeviceSyntheticDataset(10, 3, 32, 32, max(1, a.per_class // 10), 2.0, 12345, 1)
+    train = DeviceSyntheticDataset(10, 3, 32, 32, a.per_class, a.separation, 12345, 0)
+    evald = DeviceSyntheticDataset(10, 3, 32, 32, max(1, a.per_class // 10), a.separation, 12345, 1)
     ctx = schemes.SchemeContext(net=spec, train_data=train, eval_data=evald, batch=a.batch,
                                 sgd=SgdOptions(a.lr, 0.9, 0.004 if a.net == "cifar10_quick"
                                                else 0.0),
