@@ -364,8 +364,15 @@ bool want_pair(const TcArgs& a) {
   }();
   if (a.pair_policy == PSG_TC_PAIR_NEVER || (!env && a.pair_policy != PSG_TC_PAIR_ALWAYS))
     return false;
-  // legality: K-major A (M = pixels / rows) with at least two M tiles
-  if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K && a.a_mode != A_IM2COL_K) return false;
+  // legality: K-major A (M = pixels / rows) or a one-box MN-major A (wgrad: M = filters),
+  // with at least two M tiles
+  static const bool pair_mn = [] {  // PSG_TC_PAIR_MN=0: single-CTA MN-major-A GEMMs only
+    const char* e = std::getenv("PSG_TC_PAIR_MN");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (a.a_mode != A_RECT_K && a.a_mode != A_2D_K && a.a_mode != A_IM2COL_K &&
+      !(a.a_mode == A_2D_MN && pair_mn))
+    return false;
   if (a.m_tiles < 2) return false;
   if (a.pair_policy == PSG_TC_PAIR_ALWAYS) return true;  // parity tests of the pair kernels
   static const int min_n = [] {  // narrow tiles: the pair's B half is too thin to pay off
@@ -379,7 +386,7 @@ bool want_pair(const TcArgs& a) {
   // long-K linear layers (AlexNet fc6 / fc7 at b = 256: two M tiles, split K restores the
   // parallelism): the pair reads each weight tile from L2 once instead of per M tile,
   // fc6 fwd / dgrad -10%
-  const bool long_linear = a.a_mode == A_2D_K && a.kblocks >= 64;
+  const bool long_linear = (a.a_mode == A_2D_K || a.a_mode == A_2D_MN) && a.kblocks >= 64;
   return env > 1 || units >= sm_count() || long_linear;
 }
 
