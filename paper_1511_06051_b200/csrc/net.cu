@@ -186,6 +186,10 @@ void free_batch_buffers(psg_net* net) {
   dfree(net->row_loss);
   dfree(net->labels);
   dfree(net->ws.ptr);
+  for (Workspace& w : net->ws_lane) {
+    dfree(w.ptr);
+    w = Workspace{};
+  }
   net->row_loss = nullptr;
   net->labels = nullptr;
   net->ws = Workspace{};
@@ -271,6 +275,44 @@ void plan_fusion(psg_net* net) {
   }
 }
 
+// Branch lanes (psg_net::lane_of): a layer inherits its input's lane; the k-th consumer of a
+// layer with several consumers takes lane (lane + k) % kLanes; joins (several inputs) and the
+// loss layers (they accumulate one device loss in layer order) run on lane 0.  Off for nets
+// without fan-out and with PSG_LANES=0.
+void assign_lanes(psg_net* net) {
+  const char* lanes_env = std::getenv("PSG_LANES");  // read per build (tests toggle it)
+  const bool env = !lanes_env || std::atoi(lanes_env) != 0;
+  const int nl = static_cast<int>(net->L.size());
+  net->lane_of.assign(nl, 0);
+  bool fanout = false;
+  for (const LayerRt& l : net->L)
+    if (l.kind != PSG_LAYER_DATA && l.kind != PSG_LAYER_LABEL && l.consumers.size() > 1)
+      fanout = true;
+  net->lanes_on = env && fanout;
+  if (!net->lanes_on) return;
+  for (int li = 0; li < nl; ++li) {
+    const LayerRt& l = net->L[li];
+    if (l.inputs.size() != 1 || l.kind == PSG_LAYER_SOFTMAX_LOSS) continue;  // lane 0
+    const LayerRt& p = net->L[l.inputs[0]];
+    int k = 0;
+    if (p.kind != PSG_LAYER_DATA && p.consumers.size() > 1)
+      for (size_t c = 0; c < p.consumers.size(); ++c)
+        if (p.consumers[c] == li) k = static_cast<int>(c);
+    net->lane_of[li] = (net->lane_of[l.inputs[0]] + k) % psg_net::kLanes;
+  }
+  for (int k = 1; k < psg_net::kLanes; ++k)
+    PSG_CUDA(cudaStreamCreateWithFlags(&net->lane_stream[k], cudaStreamNonBlocking));
+  PSG_CUDA(cudaEventCreateWithFlags(&net->lane_fork, cudaEventDisableTiming));
+  for (int k = 0; k < psg_net::kLanes; ++k)
+    PSG_CUDA(cudaEventCreateWithFlags(&net->lane_join[k], cudaEventDisableTiming));
+  net->ev_fwd.resize(nl);
+  net->ev_bwd.resize(nl);
+  for (int li = 0; li < nl; ++li) {
+    PSG_CUDA(cudaEventCreateWithFlags(&net->ev_fwd[li], cudaEventDisableTiming));
+    PSG_CUDA(cudaEventCreateWithFlags(&net->ev_bwd[li], cudaEventDisableTiming));
+  }
+}
+
 void release_batch_buffers(psg_net* net) {
   DeviceGuard dg(net->ctx->device);
   PSG_CUDA(cudaStreamSynchronize(net->stream));
@@ -305,6 +347,10 @@ void ensure_capacity(psg_net* net, size_t n) {
   net->labels = dalloc<int32_t>(n);
   net->ws.ptr = dalloc<float>(ws);
   net->ws.elems = ws;
+  for (int k = 1; net->lanes_on && k < psg_net::kLanes; ++k) {
+    net->ws_lane[k].ptr = dalloc<float>(ws);
+    net->ws_lane[k].elems = ws;
+  }
   net->cap = n;
 }
 
@@ -628,6 +674,7 @@ void net_build(psg_net* net, const psg_layer_desc* layers, int n, uint64_t seed)
   PSG_CUDA(cudaEventCreateWithFlags(&net->idx_ev, cudaEventDisableTiming));
   PSG_CUDA(cudaEventCreate(&net->t0));
   PSG_CUDA(cudaEventCreate(&net->t1));
+  assign_lanes(net);
   build_chunks(net);
 }
 
@@ -655,6 +702,13 @@ void net_free(psg_net* net) {
     if (net->consumed[k]) cudaEventDestroy(net->consumed[k]);
   }
   if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
+  for (cudaStream_t ls : net->lane_stream)
+    if (ls) cudaStreamDestroy(ls);
+  if (net->lane_fork) cudaEventDestroy(net->lane_fork);
+  for (cudaEvent_t e : net->lane_join)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : net->ev_fwd) cudaEventDestroy(e);
+  for (cudaEvent_t e : net->ev_bwd) cudaEventDestroy(e);
   if (net->side_stream) cudaStreamDestroy(net->side_stream);
   if (net->side_join) cudaEventDestroy(net->side_join);
   for (cudaEvent_t e : net->bucket_ev) cudaEventDestroy(e);

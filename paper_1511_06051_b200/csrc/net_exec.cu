@@ -64,6 +64,51 @@ double conv_flops(const psg_net* net, const LayerRt& l, size_t n) {
 
 double act_bytes(const LayerRt& l, size_t n) { return 4.0 * static_cast<double>(n) * l.vol(); }
 
+// Branch lanes (psg_net::lane_of), off when profiling per op (the timer's events are on the
+// main stream).
+struct Lanes {
+  psg_net* net;
+  bool on;
+  int lane(int li) const { return on ? net->lane_of[li] : 0; }
+  cudaStream_t s(int li) const {
+    const int k = lane(li);
+    return k ? net->lane_stream[k] : net->stream;
+  }
+  const Workspace& ws(int li) const {
+    const int k = lane(li);
+    return k ? net->ws_lane[k] : net->ws;
+  }
+  void fork() const {  // every lane joins the main stream's order (and a capture)
+    if (!on) return;
+    PSG_CUDA(cudaEventRecord(net->lane_fork, net->stream));
+    for (int k = 1; k < psg_net::kLanes; ++k)
+      PSG_CUDA(cudaStreamWaitEvent(net->lane_stream[k], net->lane_fork, 0));
+  }
+  void join() const {
+    if (!on) return;
+    for (int k = 1; k < psg_net::kLanes; ++k) {
+      PSG_CUDA(cudaEventRecord(net->lane_join[k], net->lane_stream[k]));
+      PSG_CUDA(cudaStreamWaitEvent(net->stream, net->lane_join[k], 0));
+    }
+  }
+  // layer li waits for the forward / backward event of layer `other` (< 0: none) when that
+  // ran on another lane
+  void after_fwd(int li, int other) const {
+    if (on && other >= 0 && lane(other) != lane(li))
+      PSG_CUDA(cudaStreamWaitEvent(s(li), net->ev_fwd[other], 0));
+  }
+  void after_bwd(int li, int other) const {
+    if (on && other >= 0 && lane(other) != lane(li))
+      PSG_CUDA(cudaStreamWaitEvent(s(li), net->ev_bwd[other], 0));
+  }
+  void record_fwd(int li) const {
+    if (on) PSG_CUDA(cudaEventRecord(net->ev_fwd[li], s(li)));
+  }
+  void record_bwd(int li) const {
+    if (on) PSG_CUDA(cudaEventRecord(net->ev_bwd[li], s(li)));
+  }
+};
+
 struct Scope {
   OpTimer* t;
   Scope(OpTimer* t_, const char* name, int layer, int phase, double flops, double bytes) : t(t_) {
@@ -115,13 +160,16 @@ int stage_host_batch(psg_net* net, const float* src, size_t n) {
 }
 
 int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* timer) {
-  cudaStream_t s = net->stream;
+  const Lanes ln{net, net->lanes_on && !timer};
+  ln.fork();
   int launches = 0;
   bool first_loss = true;  // the total loss sums every loss layer's weighted mean
   for (size_t li = 0; li < net->L.size(); ++li) {
     LayerRt& l = net->L[li];
     const int lid = static_cast<int>(li);
     const std::string nm = std::string(l.d.name) + ".fwd";
+    cudaStream_t s = ln.s(lid);
+    for (int p : l.inputs) ln.after_fwd(lid, p);
     switch (l.kind) {
       case PSG_LAYER_DATA:
       case PSG_LAYER_LABEL:
@@ -136,7 +184,7 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         // fused ReLU: l.out aliases the ReLU's buffer and the epilogue applies max(0, .)
         const bool xs = net->data_s2d && src.kind == PSG_LAYER_DATA;  // x' already gathered
         conv_fprop(g, src.out, net->w + k.int_off, net->w + b.int_off, l.out, l.fwd_relu >= 0,
-                   net->ws, l.col, net->mode, s, xs);
+                   ln.ws(lid), l.col, net->mode, s, xs);
         const int c = conv_launches(g, 0, net->mode) - (xs ? 1 : 0);
         sc.done(c);
         launches += c;
@@ -213,7 +261,14 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
         break;
       }
     }
+    if (ln.on)
+      for (int c : l.consumers)
+        if (ln.lane(c) != ln.lane(lid)) {
+          ln.record_fwd(lid);
+          break;
+        }
   }
+  ln.join();
   net->data_s2d = false;  // one-shot: set by stage_gathered_batch for this forward only
   return launches;
 }
@@ -244,16 +299,27 @@ int foldable_relu(const psg_net* net, const LayerRt& c) {
 }  // namespace
 
 int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
-  cudaStream_t s = net->stream;
+  const Lanes ln{net, net->lanes_on && !timer};
+  ln.fork();
   int launches = 0;
   std::vector<char> written(net->L.size(), 0);
   std::vector<char> relu_folded(net->L.size(), 0);  // backward done by the consumer
+  // lanes: the layer whose backward last wrote / accumulated into each gradient buffer; a
+  // reader or the next accumulator on another lane waits for its event (same order as one
+  // stream, so the sums are bitwise those of one stream)
+  std::vector<int> last_writer(net->L.size(), -1);
   for (const LayerRt& l : net->L)  // every loss seed writes its logits grad
     if (l.kind == PSG_LAYER_SOFTMAX_LOSS) written[l.inputs[0]] = 1;
   for (int li = static_cast<int>(net->L.size()) - 1; li >= 0; --li) {
     LayerRt& l = net->L[li];
     if (l.kind == PSG_LAYER_DATA || l.kind == PSG_LAYER_LABEL || l.kind == PSG_LAYER_SOFTMAX_LOSS)
       continue;
+    cudaStream_t s = ln.s(li);
+    ln.after_bwd(li, last_writer[li]);
+    auto writes = [&](int buf) {  // li is about to write / accumulate into L[buf].grad
+      ln.after_bwd(li, last_writer[buf]);
+      last_writer[buf] = li;
+    };
     if (l.kind == PSG_LAYER_CONCAT) {  // dx_i (+)= dy[:, off_i : off_i + C_i]
       const size_t pixels = n * static_cast<size_t>(l.H) * l.W;
       Scope sc(timer, (std::string(l.d.name) + ".bwd").c_str(), li, 5, 0.0, 2 * act_bytes(l, n));
@@ -265,11 +331,13 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
         const int ri = foldable_relu_input(net, in);
         if (ri >= 0) {  // the branch's ReLU backward folded into the split (mask by its output)
           const int pi2 = net->L[ri].inputs[0];
+          writes(pi2);
           concat_split(l.grad, l.C, l.coff[i], net->L[pi2].grad, x.C, pixels,
                        written[pi2] != 0, s, x.out);
           written[pi2] = 1;
           relu_folded[ri] = 1;
         } else {
+          writes(in);
           concat_split(l.grad, l.C, l.coff[i], x.grad, x.C, pixels, written[in] != 0, s);
         }
         written[in] = 1;
@@ -277,6 +345,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
       }
       sc.done(c);
       launches += c;
+      ln.record_bwd(li);
       continue;
     }
     const int pi = l.inputs[0];
@@ -293,7 +362,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
         const ConvGeom g = geom_n(l, n);
         {
           Scope sc(timer, (nm + ".wgrad").c_str(), li, 3, conv_flops(net, l, n), 0.0);
-          conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off, net->ws, l.col,
+          conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off, ln.ws(li), l.col,
                      net->mode, s);
           const int c = conv_launches(g, 2, net->mode);
           sc.done(c);
@@ -304,12 +373,14 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           const int ri = foldable_relu(net, l);
           if (ri >= 0) {  // write the ReLU's input gradient, masked by the ReLU's output
             const int pi2 = net->L[ri].inputs[0];
+            writes(pi2);
             conv_dgrad(g, l.grad, net->w + k.int_off, net->L[pi2].grad, written[pi2] != 0,
-                       net->ws, net->mode, s, net->L[ri].out, l.col);
+                       ln.ws(li), net->mode, s, net->L[ri].out, l.col);
             written[pi2] = 1;
             relu_folded[ri] = 1;
           } else {
-            conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, net->ws, net->mode, s,
+            writes(pi);
+            conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, ln.ws(li), net->mode, s,
                        nullptr, l.col);
           }
           const int c = conv_launches(g, 1, net->mode);
@@ -340,11 +411,13 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           const int ri = foldable_relu(net, l);
           if (ri >= 0) {  // ReLU backward folded in: mask by the ReLU's output
             const int pi2 = net->L[ri].inputs[0];
+            writes(pi2);
             pool_bwd(g, l.grad, l.route, net->L[pi2].grad, written[pi2] != 0, s,
                      net->L[ri].out);
             written[pi2] = 1;
             relu_folded[ri] = 1;
           } else {
+            writes(pi);
             pool_bwd(g, l.grad, l.route, src.grad, acc, s);
           }
           sc.done(1);
@@ -355,6 +428,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
         if (l.bwd_by >= 0 || relu_folded[li]) break;  // done by the consumer's backward
         if (need_dx) {
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
+          writes(pi);
           relu_bwd(src.out, l.grad, src.grad, n * l.vol(), acc, s);
           sc.done(1);
           ++launches;
@@ -372,9 +446,13 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
             dx = net->L[pi2].grad;
             dacc = written[pi2] != 0;
             written[pi2] = 1;
+            writes(pi2);
+          } else {
+            writes(pi);
           }
           if (l.lrn_pool >= 0) {  // the max pool's backward gathered in the same kernel
             const LayerRt& p = net->L[l.lrn_pool];
+            ln.after_bwd(li, last_writer[l.lrn_pool]);
             PoolGeom pg = p.pg;
             pg.n = static_cast<int>(n);
             lrn_maxpool_bwd(g, pg, src.out, p.grad, p.route, dx, dacc, l.bwd_relu >= 0, s);
@@ -393,11 +471,13 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           const int ri = foldable_relu(net, l);
           if (ri >= 0) {  // ReLU backward folded in: mask by the ReLU's output
             const int pi2 = net->L[ri].inputs[0];
+            writes(pi2);
             dropout_bwd(g, l.grad, net->L[pi2].grad, &net->dsc->step, written[pi2] != 0, s,
                         net->L[ri].out);
             written[pi2] = 1;
             relu_folded[ri] = 1;
           } else {
+            writes(pi);
             dropout_bwd(g, l.grad, src.grad, &net->dsc->step, acc, s);
           }
           sc.done(1);
@@ -407,7 +487,9 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
       default:
         break;
     }
+    ln.record_bwd(li);
   }
+  ln.join();
   return launches;
 }
 

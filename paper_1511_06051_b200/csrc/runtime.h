@@ -107,6 +107,18 @@ struct psg_net {
   double* row_loss = nullptr;
   int32_t* labels = nullptr;
   psg::Workspace ws;
+  // Branch lanes (nets whose layers fan out, e.g. GoogLeNet's inception modules): layer li
+  // runs on lane lane_of[li] (0 = stream, k = lane_stream[k]); a layer waits for the events
+  // of its inputs (forward) / of the last writer of the gradient it reads or accumulates into
+  // (backward) when they ran on another lane; each lane has its own GEMM workspace.  The
+  // launch order per buffer is unchanged, so results are bitwise those of one stream.
+  static constexpr int kLanes = 4;
+  bool lanes_on = false;
+  std::vector<int> lane_of;
+  cudaStream_t lane_stream[kLanes] = {};
+  cudaEvent_t lane_fork = nullptr, lane_join[kLanes] = {};
+  std::vector<cudaEvent_t> ev_fwd, ev_bwd;
+  psg::Workspace ws_lane[kLanes];
   size_t cap = 0;       // batch capacity of the activation buffers
   size_t last_n = 0;    // batch of the last forward
   // training stream (ShardBatchIterator, data.hpp:312-351)

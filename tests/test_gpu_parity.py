@@ -333,6 +333,27 @@ def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
     assert out[0][1] == out[1][1]
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_branch_lanes_are_bitwise_neutral(gpu, oracle_lib, precision, monkeypatch):
+    """Branch lanes (the inception block's branches on their own streams, cross-lane event
+    edges, per-lane GEMM workspaces) train bitwise like one stream (PSG_LANES=0)."""
+    from paper_1511_06051_b200 import data
+    spec = _inception_net(6)
+    d = spec.data_spec().shape
+    img, lab = oracle_lib.generate_synthetic(10, d[1], d[2], d[3], 6, 2.0, 12345, 0)
+    ds = data.Dataset(f32(img), lab, 10)
+    out = []
+    for lanes in ("1", "0"):
+        monkeypatch.setenv("PSG_LANES", lanes)
+        net = gpu.Net(spec, 3, precision=precision)
+        net.set_sgd(gpu.SgdOptions(0.01, 0.9, 0.001))
+        net.set_training_data(data.make_worker_iterator(data.shard(ds, 1, 1), 0, d[0], 1))
+        net.train(3)
+        out.append((net.get_weights_flat(), net.last_loss()))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 def _s2d_net(b):
     """A strided 3-channel first conv (the space-to-depth route in TF32: the device stream
     gathers straight into x', host batches are staged NHWC then rearranged), then
