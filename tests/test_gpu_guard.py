@@ -3,7 +3,8 @@ kernel variants run in a subprocess with PSG_GUARD=1, where every net buffer (ac
 gradients, routes, parameters, split-K workspaces, im2col / space-to-depth scratch) sits
 between two 4 KB guard bands of 0xA5; afterwards no guard byte may have changed.  Covers
 AlexNet (TF32 CTA pairs and single-CTA, fused and unfused), GoogLeNet, cifar10_quick (strict
-and TF32) and the grouped C/G = 48 transposed-weight dgrad."""
+and TF32), the parity micro nets (strict / TF32, fused / unfused) and the grouped C/G = 48
+transposed-weight dgrad."""
 import os
 import subprocess
 import sys
@@ -42,6 +43,12 @@ SCRIPT = textwrap.dedent("""
             run(ns.make_alexnet(2), "tf32", pair, fuse, 1000)
             run(ns.make_cifar10_quick(8), "tf32", pair, fuse)
             run(grouped, "tf32", pair, fuse, 16)
+    sys.path.insert(0, %r + "/tests")
+    import test_gpu_parity as T
+    for name, spec in T.micro_nets().items():
+        for precision in ("fp32", "tf32"):
+            for fuse in (True, False):
+                run(spec, precision, "auto", fuse, 5 if name == "caffe_mix" else 10)
     run(ns.make_googlenet(2), "tf32", "always", True, 1000)
     run(ns.make_cifar10_quick(8), "fp32", "auto", True)
     run(ns.make_alexnet(2), "fp32", "auto", False, 1000)
@@ -49,7 +56,7 @@ SCRIPT = textwrap.dedent("""
     first = ctypes.create_string_buffer(256)
     _lib.call("psg_debug_guard_violations", ctypes.byref(bad), first, 256)
     print("GUARD", bad.value, first.value.decode())
-""") % ROOT
+""") % (ROOT, ROOT)
 
 
 def test_no_kernel_writes_outside_its_buffers():
