@@ -694,9 +694,12 @@ def main():
             "e2e": {"value": e2e_value, "unit": "images/sec", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "rounds": e2e_steps,
                     "host_gather_threads": gthreads,
-                    "path": "psg_net_train_host_rows: host-thread gather of each step's rows "
-                            "from the host dataset into pinned staging (overlapping the "
-                            "previous step), H2D, the step, D2H of its loss; + the average"},
+                    "path": "psg_net_train_host_rows: each step's rows gathered from the host "
+                            "dataset (host threads into pinned staging + one H2D, or — rows "
+                            ">= 64 KB with < 12 host threads per rank — one DMA copy per row "
+                            "from the registered dataset straight into device staging), "
+                            "overlapping the previous step; the step; D2H of its loss; + the "
+                            "average"},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "timed_ms": ms,
             "weight_average": None if avg_ms is None else {

@@ -713,6 +713,7 @@ void net_free(psg_net* net) {
   if (net->side_join) cudaEventDestroy(net->side_join);
   for (cudaEvent_t e : net->bucket_ev) cudaEventDestroy(e);
   if (net->h_losses) cudaFreeHost(net->h_losses);
+  if (net->h_reg) cudaHostUnregister(const_cast<void*>(net->h_reg));
   for (int k = 0; k < 2; ++k) {
     if (net->h_ring[k]) cudaFreeHost(net->h_ring[k]);
     if (net->h_ring_lab[k]) cudaFreeHost(net->h_ring_lab[k]);

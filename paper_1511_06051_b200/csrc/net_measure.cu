@@ -253,6 +253,34 @@ void net_train_host_rows(psg_net* net, const float* ds_images, const int32_t* ds
     }
     net->h_ring_cap = b * chw;
   }
+  // Large rows can be gathered by the DMA engine straight from the (registered,
+  // page-locked) dataset into device staging — no host copy — instead of host threads
+  // copying them into pinned staging for one H2D.  Measured on AlexNet's 618 KB rows with a
+  // 16-thread host: 1 GPU (16 threads) host 59.7–67K vs DMA 59.5–60K img/s e2e; 2 GPUs
+  // (8 threads per rank) 93K vs 118K; 4 GPUs (4 per rank) 101K vs 172K — so the DMA engine
+  // takes every row when a rank has fewer than 12 host threads (rows >= 64 KB), the host
+  // otherwise.  A split (both in parallel) was slower than either: the copies serialise on
+  // the copy engine.  PSG_HOST_ROW_DMA_FRAC (0..1) sets the DMA share of the rows.
+  const size_t row_bytes = chw * sizeof(float);
+  double frac = row_bytes >= (size_t{64} << 10) && threads < 12 ? 1.0 : 0.0;
+  if (const char* e = std::getenv("PSG_HOST_ROW_DMA_FRAC")) frac = std::atof(e);
+  const size_t nd = std::min(b, static_cast<size_t>(std::max(0.0, frac) * b + 0.5));
+  if (nd && (net->h_reg != ds_images || net->h_reg_bytes != ds_rows * row_bytes)) {
+    PSG_CUDA(cudaStreamSynchronize(net->stream));
+    PSG_CUDA(cudaStreamSynchronize(net->copy_stream));
+    if (net->h_reg) PSG_CUDA(cudaHostUnregister(const_cast<void*>(net->h_reg)));
+    net->h_reg = nullptr;
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, ds_images) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // unregistered host memory: not an error worth keeping
+    if (!pinned) {
+      PSG_CUDA(cudaHostRegister(const_cast<float*>(ds_images), ds_rows * row_bytes,
+                                cudaHostRegisterDefault));
+      net->h_reg = ds_images;
+      net->h_reg_bytes = ds_rows * row_bytes;
+    }
+  }
   PSG_CUDA(cudaEventRecord(net->t0, net->stream));
   PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->t0, 0));
   for (int k = 0; k < 2; ++k) {
@@ -264,19 +292,35 @@ void net_train_host_rows(psg_net* net, const float* ds_images, const int32_t* ds
     PSG_CUDA(cudaEventSynchronize(net->h_ring_ev[k]));  // this buffer's last H2D is done
     float* dst = net->h_ring[k];
     const uint64_t* rs = rows + s * b;
+    // DMA rows first (asynchronous: they stream while the host threads gather the rest)
+    PSG_CUDA(cudaStreamWaitEvent(net->copy_stream, net->consumed[k], 0));
+    for (size_t i = 0; i < nd; ++i)
+      PSG_CUDA(cudaMemcpyAsync(net->d_stage2[k] + i * chw, ds_images + rs[i] * chw, row_bytes,
+                               cudaMemcpyHostToDevice, net->copy_stream));
+    const size_t nh = b - nd;
     auto work = [&](size_t i0, size_t i1) {
       for (size_t i = i0; i < i1; ++i)
-        std::memcpy(dst + i * chw, ds_images + rs[i] * chw, chw * sizeof(float));
+        std::memcpy(dst + i * chw, ds_images + rs[nd + i] * chw, row_bytes);
     };
-    const size_t per = (b + threads - 1) / threads;
+    const size_t per = (nh + threads - 1) / threads;
     std::vector<std::thread> pool;
-    for (int t = 1; t < threads && static_cast<size_t>(t) * per < b; ++t)
-      pool.emplace_back(work, t * per, std::min(b, (t + 1) * per));
-    work(0, std::min(b, per));
+    for (int t = 1; t < threads && static_cast<size_t>(t) * per < nh; ++t)
+      pool.emplace_back(work, t * per, std::min(nh, (t + 1) * per));
+    work(0, std::min(nh, per));
     for (std::thread& th : pool) th.join();
     for (size_t i = 0; i < b; ++i) net->h_ring_lab[k][i] = ds_labels[rs[i]];
-    host_step_enqueue(net, dst, net->h_ring_lab[k], s, b, chw);
+    if (nh)
+      PSG_CUDA(cudaMemcpyAsync(net->d_stage2[k] + nd * chw, dst, nh * row_bytes,
+                               cudaMemcpyHostToDevice, net->copy_stream));
+    PSG_CUDA(cudaMemcpyAsync(net->d_lab2[k], net->h_ring_lab[k], b * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, net->copy_stream));
     PSG_CUDA(cudaEventRecord(net->h_ring_ev[k], net->copy_stream));  // after its H2D
+    PSG_CUDA(cudaEventRecord(net->copied[k], net->copy_stream));
+    PSG_CUDA(cudaStreamWaitEvent(net->stream, net->copied[k], 0));
+    PSG_CUDA(cudaGraphLaunch(net->host_graph2[k], net->stream));
+    PSG_CUDA(cudaEventRecord(net->consumed[k], net->stream));
+    PSG_CUDA(cudaMemcpyAsync(net->h_losses + s, &net->dsc->loss, sizeof(double),
+                             cudaMemcpyDeviceToHost, net->stream));
   }
   PSG_CUDA(cudaEventRecord(net->t1, net->stream));
   net->timed = true;

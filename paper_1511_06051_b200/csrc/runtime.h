@@ -173,6 +173,10 @@ struct psg_net {
   int32_t* h_ring_lab[2] = {nullptr, nullptr};
   cudaEvent_t h_ring_ev[2] = {nullptr, nullptr};
   size_t h_ring_cap = 0;
+  // net_train_host_rows' DMA share of large rows: the dataset registered (page-locked) once
+  // and those rows copied by the DMA engine straight into device staging
+  const void* h_reg = nullptr;
+  size_t h_reg_bytes = 0;
   size_t h_losses_cap = 0;
   cudaEvent_t slots[16] = {};
 };

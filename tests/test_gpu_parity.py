@@ -394,11 +394,15 @@ def test_train_host_matches_device_stream(gpu, oracle_lib, name):
     assert losses[-1] == a.last_loss()
 
 
-@pytest.mark.parametrize("name,threads", [("cifar10_quick", 1), ("cifar10_quick", 4), ("s2d", 3)])
-def test_train_host_rows_matches_device_stream(gpu, oracle_lib, name, threads):
+@pytest.mark.parametrize("name,threads,dma", [("cifar10_quick", 1, "0"), ("cifar10_quick", 4, "0"),
+                                              ("s2d", 3, "0"), ("cifar10_quick", 2, "0.5"),
+                                              ("s2d", 1, "1")])
+def test_train_host_rows_matches_device_stream(gpu, oracle_lib, name, threads, dma, monkeypatch):
     """psg_net_train_host_rows (host threads gather each step's rows into pinned staging while
-    the GPU runs the previous step) == psg_net_train on the HBM-resident stream, bitwise."""
+    the GPU runs the previous step; the DMA share of the rows copied straight from the
+    registered dataset) == psg_net_train on the HBM-resident stream, bitwise."""
     from paper_1511_06051_b200 import data
+    monkeypatch.setenv("PSG_HOST_ROW_DMA_FRAC", dma)
     spec = ns.make_cifar10_quick(10) if name == "cifar10_quick" else _s2d_net(10)
     ds = _dataset(gpu, oracle_lib, spec, 6)
     shards = data.shard(ds, 1, 4)
