@@ -282,7 +282,11 @@ int psg_net_train_host(psg_net* net, const float* images, const int32_t* labels,
 /* train(steps) with a host-side loader: per step `threads` host threads gather the step's
  * rows ds_images[rows[s*b + i]] (NCHW fp32, row = c*h*w floats) and their labels into a
  * pinned staging buffer (gather_batch, data.hpp:292-304) while the GPU runs the previous
- * step, then H2D copy, the step, and a D2H read of its loss. */
+ * step, then H2D copy, the step, and a D2H read of its loss.  Rows of >= 64 KB with fewer
+ * than 12 threads (PSG_HOST_ROW_DMA_FRAC overrides the share) are instead copied row by row
+ * by the DMA engine straight into device staging: ds_images is then page-locked with
+ * cudaHostRegister (unless already pinned) until the net is freed or another dataset
+ * pointer is passed — it must stay allocated that long. */
 int psg_net_train_host_rows(psg_net* net, const float* ds_images, const int32_t* ds_labels,
                             size_t ds_rows, const uint64_t* rows, long steps, double* losses,
                             int threads);
