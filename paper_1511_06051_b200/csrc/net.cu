@@ -277,8 +277,8 @@ void plan_fusion(psg_net* net) {
 
 // Branch lanes (psg_net::lane_of): a layer inherits its input's lane; the k-th consumer of a
 // layer with several consumers takes lane (lane + k) % kLanes; joins (several inputs) and the
-// loss layers (they accumulate one device loss in layer order) run on lane 0.  Off for nets
-// without fan-out and with PSG_LANES=0.
+// loss layers (they accumulate one device loss in layer order) run on lane 0.  Fan-out lanes
+// are off for nets without fan-out; PSG_LANES=0 turns every lane (and the wgrad lane) off.
 void assign_lanes(psg_net* net) {
   const char* lanes_env = std::getenv("PSG_LANES");  // read per build (tests toggle it)
   const bool env = !lanes_env || std::atoi(lanes_env) != 0;
@@ -288,9 +288,11 @@ void assign_lanes(psg_net* net) {
   for (const LayerRt& l : net->L)
     if (l.kind != PSG_LAYER_DATA && l.kind != PSG_LAYER_LABEL && l.consumers.size() > 1)
       fanout = true;
-  net->lanes_on = env && fanout;
+  const char* wl = std::getenv("PSG_WGRAD_LANE");
+  net->wgrad_lane = env && (!wl || std::atoi(wl) != 0);
+  net->lanes_on = (env && fanout) || net->wgrad_lane;
   if (!net->lanes_on) return;
-  for (int li = 0; li < nl; ++li) {
+  for (int li = 0; li < nl && fanout; ++li) {
     const LayerRt& l = net->L[li];
     if (l.inputs.size() != 1 || l.kind == PSG_LAYER_SOFTMAX_LOSS) continue;  // lane 0
     const LayerRt& p = net->L[l.inputs[0]];

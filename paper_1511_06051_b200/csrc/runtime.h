@@ -114,6 +114,9 @@ struct psg_net {
   // launch order per buffer is unchanged, so results are bitwise those of one stream.
   static constexpr int kLanes = 4;
   bool lanes_on = false;
+  // wgrad lane (PSG_WGRAD_LANE, default on): the weight gradients of lane-0 layers run on
+  // lane 1 — after the last writer of the gradient they read — overlapping the dgrad chain
+  bool wgrad_lane = false;
   std::vector<int> lane_of;
   cudaStream_t lane_stream[kLanes] = {};
   cudaEvent_t lane_fork = nullptr, lane_join[kLanes] = {};

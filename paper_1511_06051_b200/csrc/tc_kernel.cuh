@@ -360,6 +360,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long long ustep = PAIR ? gridDim.x / 2 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
+    tc::tma_descriptor_acquire(&map_a);
+    tc::tma_descriptor_acquire(&map_b);
+    tc::tma_descriptor_acquire(&map_o);
     tc::tma_prefetch(&map_a);
     tc::tma_prefetch(&map_b);
     if (p.epi_tma || p.bias_chunk) tc::tma_prefetch(&map_o);
@@ -396,6 +399,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // pairs: the leader posts both CTAs' bytes (identical per CTA); the peer only loads
     const uint32_t bytes = (p.a_tx + (p.stage_bytes - p.a_bytes)) * (PAIR ? 2 : 1);
     const int P = p.producers;
+    // the grid's own tensor maps, not a descriptor cached for the same parameter address by
+    // another grid of this kernel (concurrent launches on other streams)
+    tc::tma_descriptor_acquire(&map_a);
+    tc::tma_descriptor_acquire(&map_b);
+    tc::tma_descriptor_acquire(&map_o);
     const bool prof = p.prof != nullptr && pw == 0 && rank == 0;
     long long prof_t0 = prof ? clock64() : 0, prof_w = 0;
     uint32_t it_tile = 0;  // global stage index of the tile's first stage
@@ -551,6 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t local = 0;
     uint32_t ochunk = 0;  // TMA-store chunks issued by this warp (staging buffer ochunk % 2)
     uint8_t* const ostage = smem + p.ring_bytes + ew * p.epi_tma * kOutChunkBytes;
+    if (p.epi_tma && lane == 0) tc::tma_descriptor_acquire(&map_o);
     const bool prof = p.prof != nullptr && ew == 0 && rank == 0;
     long long prof_t0 = prof ? clock64() : 0, prof_w = 0;
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {

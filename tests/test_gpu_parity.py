@@ -334,18 +334,24 @@ def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
-def test_branch_lanes_are_bitwise_neutral(gpu, oracle_lib, precision, monkeypatch):
-    """Branch lanes (the inception block's branches on their own streams, cross-lane event
-    edges, per-lane GEMM workspaces) train bitwise like one stream (PSG_LANES=0)."""
+@pytest.mark.parametrize("name", ["inception", "caffe_mix", "cifar10_quick"])
+@pytest.mark.parametrize("fuse", [True, False])
+def test_lanes_are_bitwise_neutral(gpu, oracle_lib, name, precision, fuse, monkeypatch):
+    """Lanes — the inception block's branches on their own streams, every lane-0 layer's wgrad
+    on a second stream overlapping the dgrad chain, cross-lane event edges, per-lane GEMM
+    workspaces, concurrent grids of the same tcgen05 kernel — train bitwise like one stream
+    (PSG_LANES=0)."""
     from paper_1511_06051_b200 import data
-    spec = _inception_net(6)
+    spec = (_inception_net(6) if name == "inception" else micro_nets()[name] if name == "caffe_mix"
+            else ns.make_cifar10_quick(10))
     d = spec.data_spec().shape
     img, lab = oracle_lib.generate_synthetic(10, d[1], d[2], d[3], 6, 2.0, 12345, 0)
-    ds = data.Dataset(f32(img), lab, 10)
+    classes = 5 if name == "caffe_mix" else 10
+    ds = data.Dataset(f32(img), lab % classes, classes)
     out = []
     for lanes in ("1", "0"):
         monkeypatch.setenv("PSG_LANES", lanes)
-        net = gpu.Net(spec, 3, precision=precision)
+        net = gpu.Net(spec, 3, precision=precision, fuse=fuse)
         net.set_sgd(gpu.SgdOptions(0.01, 0.9, 0.001))
         net.set_training_data(data.make_worker_iterator(data.shard(ds, 1, 1), 0, d[0], 1))
         net.train(3)
