@@ -13,7 +13,7 @@ echo "sweep rc $?"; cat gpurun_out/avg_sweep_${N}gpu.jsonl | cut -c1-200
 nvidia-smi nvlink -gt d > gpurun_out/nvlink_after_$N.txt 2>&1
 for t in 1 50; do
   timeout 600 python -m torch.distributed.run --nproc-per-node $N --master-addr 127.0.0.1 \
-    --master-port 2952$t tools/overlap_check.py --workload alexnet --tau $t --rounds 10 \
+    --master-port $((29520 + t)) tools/overlap_check.py --workload alexnet --tau $t --rounds 10 \
     > gpurun_out/overlap_alexnet_tau${t}_${N}gpu.json 2> gpurun_out/overlap_tau${t}_${N}gpu.err
   echo "overlap tau $t rc $?"; tail -1 gpurun_out/overlap_alexnet_tau${t}_${N}gpu.json
 done
