@@ -257,9 +257,50 @@ __global__ void fill_uniform_k(float* x, size_t n, uint64_t seed, double lo, dou
 
 }  // namespace
 
+// dst = ((dst + src[0]) + src[1]) + ... — the branch gradients a fan-out layer received in
+// scratch buffers (lanes), added in the order the single-stream backward accumulates them
+// (each accumulating pass adds its new value to the old one once), so bitwise equal to it.
+struct GradSrcs {
+  const float* p[8];
+};
+__global__ void grad_accumulate_k(float* __restrict__ dst, GradSrcs src, int k, size_t n) {
+  pdl_enter();
+  const size_t n4 = n / 4;
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  GRID_STRIDE(i, n4) {
+    float4 v = d4[i];
+    for (int j = 0; j < k; ++j) {
+      const float4 o = reinterpret_cast<const float4*>(src.p[j])[i];
+      v.x += o.x;
+      v.y += o.y;
+      v.z += o.z;
+      v.w += o.w;
+    }
+    d4[i] = v;
+  }
+  GRID_STRIDE(j, n - n4 * 4) {
+    const size_t i = n4 * 4 + j;
+    float v = dst[i];
+    for (int q = 0; q < k; ++q) v += src.p[q][i];
+    dst[i] = v;
+  }
+}
+
 void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s) {
   launch_k(relu_fwd_k, grid_for(n / 4 + 1), 256, 0, s, x, y, n);
   PSG_CUDA(cudaGetLastError());
+}
+
+int grad_accumulate(float* dst, float* const* src, int k, size_t n, cudaStream_t s) {
+  int launches = 0;
+  for (int j0 = 0; j0 < k; j0 += 8, ++launches) {
+    GradSrcs g{};
+    const int c = std::min(8, k - j0);
+    for (int j = 0; j < c; ++j) g.p[j] = src[j0 + j];
+    launch_k(grad_accumulate_k, grid_for(n / 4 + 1), 256, 0, s, dst, g, c, n);
+    PSG_CUDA(cudaGetLastError());
+  }
+  return launches;
 }
 
 void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumulate,

@@ -180,6 +180,8 @@ void free_batch_buffers(psg_net* net) {
     dfree(l.grad);
     dfree(l.route);
     dfree(l.col);
+    for (float* p : l.acc_scratch) dfree(p);
+    l.acc_scratch.clear();
     l.out = l.grad = l.col = nullptr;
     l.route = nullptr;
   }
@@ -288,9 +290,10 @@ void assign_lanes(psg_net* net) {
   for (const LayerRt& l : net->L)
     if (l.kind != PSG_LAYER_DATA && l.kind != PSG_LAYER_LABEL && l.consumers.size() > 1)
       fanout = true;
-  const char* wl = std::getenv("PSG_WGRAD_LANE");
-  net->wgrad_lane = env && (!wl || std::atoi(wl) != 0);
+  const char* wl = std::getenv("PSG_WGRAD_LANE");  // opt-in: see DESIGN §3 (wgrad lane)
+  net->wgrad_lane = env && wl && std::atoi(wl) != 0;
   net->lanes_on = (env && fanout) || net->wgrad_lane;
+  net->fanout = env && fanout;
   if (!net->lanes_on) return;
   for (int li = 0; li < nl && fanout; ++li) {
     const LayerRt& l = net->L[li];
@@ -309,9 +312,11 @@ void assign_lanes(psg_net* net) {
     PSG_CUDA(cudaEventCreateWithFlags(&net->lane_join[k], cudaEventDisableTiming));
   net->ev_fwd.resize(nl);
   net->ev_bwd.resize(nl);
+  net->ev_sum.resize(nl);
   for (int li = 0; li < nl; ++li) {
     PSG_CUDA(cudaEventCreateWithFlags(&net->ev_fwd[li], cudaEventDisableTiming));
     PSG_CUDA(cudaEventCreateWithFlags(&net->ev_bwd[li], cudaEventDisableTiming));
+    PSG_CUDA(cudaEventCreateWithFlags(&net->ev_sum[li], cudaEventDisableTiming));
   }
 }
 
@@ -344,6 +349,15 @@ void ensure_capacity(psg_net* net, size_t n) {
   }
   for (LayerRt& l : net->L)
     if (l.fwd_relu >= 0) l.out = net->L[l.fwd_relu].out;
+  // branch lanes: scratch for every gradient writer after the first (consumers, and the
+  // consumers of a single-consumer ReLU among them that fold its backward)
+  for (LayerRt& l : net->L) {
+    if (!net->fanout || !l.grad) continue;
+    size_t writers = l.consumers.size();
+    for (int c : l.consumers)
+      if (net->L[c].kind == PSG_LAYER_RELU) writers += net->L[c].consumers.size();
+    for (size_t j = 1; j < writers; ++j) l.acc_scratch.push_back(dalloc<float>(n * l.vol()));
+  }
   // the data layer's grad is never produced (first-layer dgrad is skipped)
   net->row_loss = dalloc<double>(n);
   net->labels = dalloc<int32_t>(n);
@@ -711,6 +725,7 @@ void net_free(psg_net* net) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : net->ev_fwd) cudaEventDestroy(e);
   for (cudaEvent_t e : net->ev_bwd) cudaEventDestroy(e);
+  for (cudaEvent_t e : net->ev_sum) cudaEventDestroy(e);
   if (net->side_stream) cudaStreamDestroy(net->side_stream);
   if (net->side_join) cudaEventDestroy(net->side_join);
   for (cudaEvent_t e : net->bucket_ev) cudaEventDestroy(e);

@@ -109,6 +109,11 @@ struct Lanes {
   }
 };
 
+struct Dst {
+  float* p;
+  bool acc;
+};
+
 struct Scope {
   OpTimer* t;
   Scope(OpTimer* t_, const char* name, int layer, int phase, double flops, double bytes) : t(t_) {
@@ -308,6 +313,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
   // reader or the next accumulator on another lane waits for its event (same order as one
   // stream, so the sums are bitwise those of one stream)
   std::vector<int> last_writer(net->L.size(), -1);
+  std::vector<std::vector<int>> pend(net->L.size());  // scratch writers per gradient, in order
   for (const LayerRt& l : net->L)  // every loss seed writes its logits grad
     if (l.kind == PSG_LAYER_SOFTMAX_LOSS) written[l.inputs[0]] = 1;
   for (int li = static_cast<int>(net->L.size()) - 1; li >= 0; --li) {
@@ -315,10 +321,37 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
     if (l.kind == PSG_LAYER_DATA || l.kind == PSG_LAYER_LABEL || l.kind == PSG_LAYER_SOFTMAX_LOSS)
       continue;
     cudaStream_t s = ln.s(li);
-    ln.after_bwd(li, last_writer[li]);
-    auto writes = [&](int buf) {  // li is about to write / accumulate into L[buf].grad
+    // gradient scratch of this layer (lanes): add the later writers' buffers, in writer
+    // order, into the first writer's gradient before anything reads it
+    bool summed = false;
+    if (!pend[li].empty()) {
+      ln.after_bwd(li, last_writer[li]);
+      for (int w : pend[li]) ln.after_bwd(li, w);
+      launches += grad_accumulate(l.grad, l.acc_scratch.data(), static_cast<int>(pend[li].size()),
+                                  n * l.vol(), s);
+      PSG_CUDA(cudaEventRecord(net->ev_sum[li], s));
+      pend[li].clear();
+      last_writer[li] = li;  // later readers wait for this layer's own event
+      summed = true;
+    } else {
+      ln.after_bwd(li, last_writer[li]);
+    }
+    // destination of li's write into L[buf].grad: the gradient itself (waiting for its last
+    // writer when that ran on another lane), or — a fan-out layer's 2nd, 3rd, ... writer under
+    // branch lanes — a scratch buffer written without waiting (summed in order above)
+    auto dest = [&](int buf) -> Dst {
+      LayerRt& X = net->L[buf];
+      if (ln.on && written[buf] && !X.acc_scratch.empty()) {
+        const size_t j = pend[buf].size();
+        if (j >= X.acc_scratch.size()) throw std::logic_error("backward: gradient scratch exhausted");
+        pend[buf].push_back(li);
+        return {X.acc_scratch[j], false};
+      }
       ln.after_bwd(li, last_writer[buf]);
       last_writer[buf] = li;
+      const bool a = written[buf] != 0;
+      written[buf] = 1;
+      return {X.grad, a};
     };
     if (l.kind == PSG_LAYER_CONCAT) {  // dx_i (+)= dy[:, off_i : off_i + C_i]
       const size_t pixels = n * static_cast<size_t>(l.H) * l.W;
@@ -331,16 +364,14 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
         const int ri = foldable_relu_input(net, in);
         if (ri >= 0) {  // the branch's ReLU backward folded into the split (mask by its output)
           const int pi2 = net->L[ri].inputs[0];
-          writes(pi2);
-          concat_split(l.grad, l.C, l.coff[i], net->L[pi2].grad, x.C, pixels,
-                       written[pi2] != 0, s, x.out);
-          written[pi2] = 1;
+          const Dst d = dest(pi2);
+          concat_split(l.grad, l.C, l.coff[i], d.p, x.C, pixels, d.acc, s, x.out);
           relu_folded[ri] = 1;
+          written[in] = 1;
         } else {
-          writes(in);
-          concat_split(l.grad, l.C, l.coff[i], x.grad, x.C, pixels, written[in] != 0, s);
+          const Dst d = dest(in);
+          concat_split(l.grad, l.C, l.coff[i], d.p, x.C, pixels, d.acc, s);
         }
-        written[in] = 1;
         ++c;
       }
       sc.done(c);
@@ -351,8 +382,7 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
     const int pi = l.inputs[0];
     LayerRt& src = net->L[pi];
     const bool need_dx = src.kind != PSG_LAYER_DATA;
-    const bool acc = written[pi] != 0;
-    if (need_dx) written[pi] = 1;
+
     const std::string nm = std::string(l.d.name);
     switch (l.kind) {
       case PSG_LAYER_CONV:
@@ -370,7 +400,9 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           cudaStream_t sw = s;
           if (wl) {
             sw = net->lane_stream[1];
-            if (last_writer[li] >= 0)
+            if (summed)
+              PSG_CUDA(cudaStreamWaitEvent(sw, net->ev_sum[li], 0));
+            else if (last_writer[li] >= 0)
               PSG_CUDA(cudaStreamWaitEvent(sw, net->ev_bwd[last_writer[li]], 0));
           }
           conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off,
@@ -384,14 +416,13 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           const int ri = foldable_relu(net, l);
           if (ri >= 0) {  // write the ReLU's input gradient, masked by the ReLU's output
             const int pi2 = net->L[ri].inputs[0];
-            writes(pi2);
-            conv_dgrad(g, l.grad, net->w + k.int_off, net->L[pi2].grad, written[pi2] != 0,
-                       ln.ws(li), net->mode, s, net->L[ri].out, l.col);
-            written[pi2] = 1;
+            const Dst d = dest(pi2);
+            conv_dgrad(g, l.grad, net->w + k.int_off, d.p, d.acc, ln.ws(li), net->mode, s,
+                       net->L[ri].out, l.col);
             relu_folded[ri] = 1;
           } else {
-            writes(pi);
-            conv_dgrad(g, l.grad, net->w + k.int_off, src.grad, acc, ln.ws(li), net->mode, s,
+            const Dst d = dest(pi);
+            conv_dgrad(g, l.grad, net->w + k.int_off, d.p, d.acc, ln.ws(li), net->mode, s,
                        nullptr, l.col);
           }
           const int c = conv_launches(g, 1, net->mode);
@@ -422,14 +453,12 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           const int ri = foldable_relu(net, l);
           if (ri >= 0) {  // ReLU backward folded in: mask by the ReLU's output
             const int pi2 = net->L[ri].inputs[0];
-            writes(pi2);
-            pool_bwd(g, l.grad, l.route, net->L[pi2].grad, written[pi2] != 0, s,
-                     net->L[ri].out);
-            written[pi2] = 1;
+            const Dst d = dest(pi2);
+            pool_bwd(g, l.grad, l.route, d.p, d.acc, s, net->L[ri].out);
             relu_folded[ri] = 1;
           } else {
-            writes(pi);
-            pool_bwd(g, l.grad, l.route, src.grad, acc, s);
+            const Dst d = dest(pi);
+            pool_bwd(g, l.grad, l.route, d.p, d.acc, s);
           }
           sc.done(1);
           ++launches;
@@ -439,8 +468,8 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
         if (l.bwd_by >= 0 || relu_folded[li]) break;  // done by the consumer's backward
         if (need_dx) {
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
-          writes(pi);
-          relu_bwd(src.out, l.grad, src.grad, n * l.vol(), acc, s);
+          const Dst d = dest(pi);
+          relu_bwd(src.out, l.grad, d.p, n * l.vol(), d.acc, s);
           sc.done(1);
           ++launches;
         }
@@ -450,17 +479,10 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           LrnGeom g = l.lg;
           g.pixels = static_cast<int>(n) * l.H * l.W;
           Scope sc(timer, (nm + ".bwd").c_str(), li, 5, 0.0, 3 * act_bytes(l, n));
-          float* dx = src.grad;  // the ReLU below folded in: mask by x > 0, its input grad
-          bool dacc = acc;
-          if (l.bwd_relu >= 0) {
-            const int pi2 = net->L[l.bwd_relu].inputs[0];
-            dx = net->L[pi2].grad;
-            dacc = written[pi2] != 0;
-            written[pi2] = 1;
-            writes(pi2);
-          } else {
-            writes(pi);
-          }
+          // the ReLU below folded in: mask by x > 0, write its input grad
+          const Dst d = dest(l.bwd_relu >= 0 ? net->L[l.bwd_relu].inputs[0] : pi);
+          float* dx = d.p;
+          const bool dacc = d.acc;
           if (l.lrn_pool >= 0) {  // the max pool's backward gathered in the same kernel
             const LayerRt& p = net->L[l.lrn_pool];
             ln.after_bwd(li, last_writer[l.lrn_pool]);
@@ -482,14 +504,12 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
           const int ri = foldable_relu(net, l);
           if (ri >= 0) {  // ReLU backward folded in: mask by the ReLU's output
             const int pi2 = net->L[ri].inputs[0];
-            writes(pi2);
-            dropout_bwd(g, l.grad, net->L[pi2].grad, &net->dsc->step, written[pi2] != 0, s,
-                        net->L[ri].out);
-            written[pi2] = 1;
+            const Dst d = dest(pi2);
+            dropout_bwd(g, l.grad, d.p, &net->dsc->step, d.acc, s, net->L[ri].out);
             relu_folded[ri] = 1;
           } else {
-            writes(pi);
-            dropout_bwd(g, l.grad, src.grad, &net->dsc->step, acc, s);
+            const Dst d = dest(pi);
+            dropout_bwd(g, l.grad, d.p, &net->dsc->step, d.acc, s);
           }
           sc.done(1);
           ++launches;

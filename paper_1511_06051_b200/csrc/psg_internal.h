@@ -166,6 +166,8 @@ void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* d
               bool accumulate, cudaStream_t s, const float* relu_mask = nullptr);
 
 void relu_fwd(const float* x, float* y, size_t n, cudaStream_t s);
+// dst += src[0], += src[1], ... in that order (k scratch gradients); returns launches
+int grad_accumulate(float* dst, float* const* src, int k, size_t n, cudaStream_t s);
 void relu_bwd(const float* x, const float* dy, float* dx, size_t n, bool accumulate,
               cudaStream_t s);
 

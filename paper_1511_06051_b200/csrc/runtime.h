@@ -67,6 +67,9 @@ struct LayerRt {
   // and gradient are never materialised.
   int lrn_pool = -1, pool_lrn = -1;
   int kern_t = -1, bias_t = -1;
+  // lanes: gradient scratch for the 2nd, 3rd, ... writer into this layer's gradient when
+  // its consumers run on several lanes (summed into grad, in writer order, before use)
+  std::vector<float*> acc_scratch;
   ConvGeom cg;  // conv / linear (per-example; n filled per call)
   PoolGeom pg;
   LrnGeom lg;
@@ -114,7 +117,9 @@ struct psg_net {
   // launch order per buffer is unchanged, so results are bitwise those of one stream.
   static constexpr int kLanes = 4;
   bool lanes_on = false;
-  // wgrad lane (PSG_WGRAD_LANE, default on): the weight gradients of lane-0 layers run on
+  bool fanout = false;                // branch lanes active (some layer fans out)
+  std::vector<cudaEvent_t> ev_sum;    // per layer: its scratch gradients summed
+  // wgrad lane (PSG_WGRAD_LANE=1, opt-in): the weight gradients of lane-0 layers run on
   // lane 1 — after the last writer of the gradient they read — overlapping the dgrad chain
   bool wgrad_lane = false;
   std::vector<int> lane_of;

@@ -99,3 +99,26 @@ def test_googlenet_trains_tf32():
     net.set_training_data(data.make_worker_iterator(data.shard(ds, 1, 1), 0, 8, 1))
     net.train(4)
     assert np.isfinite(net.last_loss())
+
+
+def test_googlenet_branch_lanes_bitwise(monkeypatch):
+    """GoogLeNet (TF32, b = 2) with its inception branches and auxiliary heads on their own
+    streams trains bitwise like one stream (PSG_LANES=0), twice in a row."""
+    from paper_1511_06051_b200 import data, model
+    from paper_1511_06051_b200 import netspec as ns
+    spec = ns.make_googlenet(2)
+    d = spec.data_spec().shape
+    rng = np.random.default_rng(3)
+    img = rng.uniform(-1, 1, size=(8,) + tuple(d[1:])).astype(np.float32).astype(np.float64)
+    ds = data.Dataset(img, (np.arange(8) % 1000).astype(np.int32), 1000)
+    out = []
+    for lanes in ("1", "0", "1"):
+        monkeypatch.setenv("PSG_LANES", lanes)
+        net = model.Net(spec, 5, precision="tf32")
+        net.set_sgd(model.SgdOptions(0.01, 0.9, 0.0002))
+        net.set_training_data(data.make_worker_iterator(data.shard(ds, 1, 1), 0, d[0], 1))
+        net.train(3)
+        out.append(net.get_weights_flat())
+    np.testing.assert_array_equal(out[0], out[1])
+    np.testing.assert_array_equal(out[0], out[2])
+
