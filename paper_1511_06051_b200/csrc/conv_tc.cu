@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
 
 #include "psg_internal.h"
 #include "tc_gemm.cuh"
@@ -596,8 +597,7 @@ void launch(const TcArgs& a0, const CUtensorMap& ma, const CUtensorMap& mb, int 
   const unsigned units =
       static_cast<unsigned>(std::min<long long>(a.total_tiles, sm_count() / per));
   auto go = [&](auto kern) {
-    PSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    allow_max_dynamic_smem(reinterpret_cast<const void*>(kern));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units * per);
     cfg.blockDim = dim3(kThreads);

@@ -4,10 +4,33 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "psg_internal.h"
 
 namespace psg {
+
+// Raise a kernel's dynamic shared memory limit to the device maximum once (per device and
+// kernel), instead of setting it to each launch's size right before the launch: two host
+// threads launching the same kernel with different sizes (nets driven from several threads)
+// could otherwise lower the limit between the other thread's set and launch
+// (cudaLaunchKernelEx: invalid argument).
+void allow_max_dynamic_smem(const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int d = 0;
+  PSG_CUDA(cudaGetDevice(&d));
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done.insert({d, kern}).second) return;
+  int optin = 0;
+  PSG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d));
+  cudaFuncAttributes fa{};
+  PSG_CUDA(cudaFuncGetAttributes(&fa, kern));
+  PSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - static_cast<int>(fa.sharedSizeBytes)));
+}
 
 bool pdl_enabled() {
   static const bool on = [] {

@@ -868,9 +868,7 @@ int lrn_blocks(const LrnGeom& g, int tp) {
 
 template <class K>
 void lrn_launch(K kernel, size_t smem) {
-  if (smem > 48 * 1024)
-    PSG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+  if (smem > 48 * 1024) allow_max_dynamic_smem(reinterpret_cast<const void*>(kernel));
 }
 
 bool lrn_run_ok(const LrnGeom& g) { return g.size == 5 && g.C % kLrnRun == 0; }

@@ -290,8 +290,8 @@ void assign_lanes(psg_net* net) {
   for (const LayerRt& l : net->L)
     if (l.kind != PSG_LAYER_DATA && l.kind != PSG_LAYER_LABEL && l.consumers.size() > 1)
       fanout = true;
-  const char* wl = std::getenv("PSG_WGRAD_LANE");  // opt-in: see DESIGN §3 (wgrad lane)
-  net->wgrad_lane = env && wl && std::atoi(wl) != 0;
+  const char* wl = std::getenv("PSG_WGRAD_LANE");
+  net->wgrad_lane = env && (!wl || std::atoi(wl) != 0);
   net->lanes_on = (env && fanout) || net->wgrad_lane;
   net->fanout = env && fanout;
   if (!net->lanes_on) return;

@@ -256,6 +256,8 @@ __device__ __forceinline__ void pdl_enter() {
 }
 #endif
 bool pdl_enabled();
+// a kernel's dynamic shared memory limit raised to the device maximum, once per device
+void allow_max_dynamic_smem(const void* kern);
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

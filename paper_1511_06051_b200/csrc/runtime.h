@@ -119,7 +119,7 @@ struct psg_net {
   bool lanes_on = false;
   bool fanout = false;                // branch lanes active (some layer fans out)
   std::vector<cudaEvent_t> ev_sum;    // per layer: its scratch gradients summed
-  // wgrad lane (PSG_WGRAD_LANE=1, opt-in): the weight gradients of lane-0 layers run on
+  // wgrad lane (PSG_WGRAD_LANE, default on): the weight gradients of lane-0 layers run on
   // lane 1 — after the last writer of the gradient they read — overlapping the dgrad chain
   bool wgrad_lane = false;
   std::vector<int> lane_of;

@@ -93,9 +93,7 @@ void synthetic_rows_device(const float* d_means, int classes, int c, int h, int 
   const int gh = std::max(1, h / 4), gw = std::max(1, w / 4);
   const size_t smem = static_cast<size_t>(c) * (gh + 1) * (gw + 1) * sizeof(float);
   if (smem > 200 * 1024) throw std::invalid_argument("synthetic: node grid too large");
-  if (smem > 48 * 1024)
-    PSG_CUDA(cudaFuncSetAttribute(synthetic_rows_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+  if (smem > 48 * 1024) allow_max_dynamic_smem(reinterpret_cast<const void*>(synthetic_rows_k));
   launch_k(synthetic_rows_k, static_cast<unsigned>(n), 256, smem, s, 
       d_means, c, h, w, static_cast<uint32_t>(per_class), noise_seed, images, labels);
   PSG_CUDA(cudaGetLastError());

@@ -44,13 +44,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 // ----------------------------------------------------------------------- TMA
-// Acquire the tensor map at `map` for the async (TMA) proxy: drops a descriptor the
-// tensormap cache may still hold for the same address from another grid.
-__device__ __forceinline__ void tma_descriptor_acquire(const CUtensorMap* map) {
-  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
-                   reinterpret_cast<uint64_t>(map))
-               : "memory");
-}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

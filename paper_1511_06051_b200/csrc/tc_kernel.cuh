@@ -360,9 +360,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long long ustep = PAIR ? gridDim.x / 2 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
-    tc::tma_descriptor_acquire(&map_a);
-    tc::tma_descriptor_acquire(&map_b);
-    tc::tma_descriptor_acquire(&map_o);
     tc::tma_prefetch(&map_a);
     tc::tma_prefetch(&map_b);
     if (p.epi_tma || p.bias_chunk) tc::tma_prefetch(&map_o);
@@ -399,11 +396,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // pairs: the leader posts both CTAs' bytes (identical per CTA); the peer only loads
     const uint32_t bytes = (p.a_tx + (p.stage_bytes - p.a_bytes)) * (PAIR ? 2 : 1);
     const int P = p.producers;
-    // the grid's own tensor maps, not a descriptor cached for the same parameter address by
-    // another grid of this kernel (concurrent launches on other streams)
-    tc::tma_descriptor_acquire(&map_a);
-    tc::tma_descriptor_acquire(&map_b);
-    tc::tma_descriptor_acquire(&map_o);
     const bool prof = p.prof != nullptr && pw == 0 && rank == 0;
     long long prof_t0 = prof ? clock64() : 0, prof_w = 0;
     uint32_t it_tile = 0;  // global stage index of the tile's first stage
@@ -559,7 +551,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t local = 0;
     uint32_t ochunk = 0;  // TMA-store chunks issued by this warp (staging buffer ochunk % 2)
     uint8_t* const ostage = smem + p.ring_bytes + ew * p.epi_tma * kOutChunkBytes;
-    if (p.epi_tma && lane == 0) tc::tma_descriptor_acquire(&map_o);
     const bool prof = p.prof != nullptr && ew == 0 && rank == 0;
     long long prof_t0 = prof ? clock64() : 0, prof_w = 0;
     for (long long tt = unit0; tt < p.total_tiles; tt += ustep, ++local) {
@@ -606,6 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // go straight to global memory as float4 runs of the thread's row (no smem
       // transpose); bias / ReLU / accumulate applied in registers.
       const int c_end = __any_sync(0xffffffffu, row_ok) ? p.n_tile : 0;  // idle rows: skip
+      const bool tma_rows = p.row_g == 0 || __all_sync(0xffffffffu, row_ok);
       constexpr bool DG = EPI == 1, WG = EPI == 2;
       const bool acc_out = DG && p.accumulate && !p.ws;
       const float* mask = DG ? p.mask : nullptr;
@@ -637,9 +629,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                            : *reinterpret_cast<const float4*>(rowp + col0 + c);
           }
         }
-        if (EPI != 2 && p.epi_tma && c0 + 32 <= nvalid) {
+        if (EPI != 2 && p.epi_tma && c0 + 32 <= nvalid && tma_rows) {
           // whole 32-column chunk: registers -> swizzled smem -> one TMA store of the warp's
-          // 32 rows (rows past the output / split are clipped by the map's bounds)
+          // 32 rows (rows past the output / split are clipped by the map's bounds; with
+          // per-group row ranges (row_g > 0) only when all 32 rows are the tile's own — a
+          // partial chunk would overwrite the next group's rows, which another CTA writes)
           uint8_t* buf = ostage + (p.epi_tma == 2 ? (ochunk & 1) * kOutChunkBytes : 0);
           if (lane == 0) {  // this buffer's previous store has read it
             if (p.epi_tma == 2)

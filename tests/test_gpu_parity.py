@@ -334,13 +334,14 @@ def test_relu_fusion_is_bitwise_neutral(gpu, oracle_lib, name, precision):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
-@pytest.mark.parametrize("name", ["inception"])
+@pytest.mark.parametrize("name", ["inception", "caffe_mix", "cifar10_quick"])
 @pytest.mark.parametrize("fuse", [True, False])
 def test_lanes_are_bitwise_neutral(gpu, oracle_lib, name, precision, fuse, monkeypatch):
-    """Branch lanes — the inception block's branches on their own streams, cross-lane event
-    edges, per-lane GEMM workspaces, the later branch gradients into the block input written to
-    scratch and summed in order, concurrent grids of the same tcgen05 kernel — train bitwise
-    like one stream (PSG_LANES=0)."""
+    """Lanes — the inception block's branches on their own streams, every lane-0 layer's wgrad
+    on a second stream overlapping the dgrad chain, cross-lane event edges, per-lane GEMM
+    workspaces, the later branch gradients into the block input written to scratch and summed
+    in order, concurrent grids of the tcgen05 kernel — train bitwise like one stream
+    (PSG_LANES=0)."""
     from paper_1511_06051_b200 import data
     spec = (_inception_net(6) if name == "inception" else micro_nets()[name] if name == "caffe_mix"
             else ns.make_cifar10_quick(10))
