@@ -305,10 +305,10 @@ void assign_lanes(psg_net* net) {
         if (p.consumers[c] == li) k = static_cast<int>(c);
     net->lane_of[li] = (net->lane_of[l.inputs[0]] + k) % psg_net::kLanes;
   }
-  for (int k = 1; k < psg_net::kLanes; ++k)
+  for (int k = 1; k < psg_net::kStreams; ++k)
     PSG_CUDA(cudaStreamCreateWithFlags(&net->lane_stream[k], cudaStreamNonBlocking));
   PSG_CUDA(cudaEventCreateWithFlags(&net->lane_fork, cudaEventDisableTiming));
-  for (int k = 0; k < psg_net::kLanes; ++k)
+  for (int k = 0; k < psg_net::kStreams; ++k)
     PSG_CUDA(cudaEventCreateWithFlags(&net->lane_join[k], cudaEventDisableTiming));
   net->ev_fwd.resize(nl);
   net->ev_bwd.resize(nl);
@@ -363,7 +363,7 @@ void ensure_capacity(psg_net* net, size_t n) {
   net->labels = dalloc<int32_t>(n);
   net->ws.ptr = dalloc<float>(ws);
   net->ws.elems = ws;
-  for (int k = 1; net->lanes_on && k < psg_net::kLanes; ++k) {
+  for (int k = 1; net->lanes_on && k < psg_net::kStreams; ++k) {
     net->ws_lane[k].ptr = dalloc<float>(ws);
     net->ws_lane[k].elems = ws;
   }

@@ -81,12 +81,12 @@ struct Lanes {
   void fork() const {  // every lane joins the main stream's order (and a capture)
     if (!on) return;
     PSG_CUDA(cudaEventRecord(net->lane_fork, net->stream));
-    for (int k = 1; k < psg_net::kLanes; ++k)
+    for (int k = 1; k < psg_net::kStreams; ++k)
       PSG_CUDA(cudaStreamWaitEvent(net->lane_stream[k], net->lane_fork, 0));
   }
   void join() const {
     if (!on) return;
-    for (int k = 1; k < psg_net::kLanes; ++k) {
+    for (int k = 1; k < psg_net::kStreams; ++k) {
       PSG_CUDA(cudaEventRecord(net->lane_join[k], net->lane_stream[k]));
       PSG_CUDA(cudaStreamWaitEvent(net->stream, net->lane_join[k], 0));
     }
@@ -392,21 +392,21 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
         const ConvGeom g = geom_n(l, n);
         {
           Scope sc(timer, (nm + ".wgrad").c_str(), li, 3, conv_flops(net, l, n), 0.0);
-          // wgrad lane: a lane-0 layer's weight gradient on lane 1, overlapping its dgrad and
-          // the layers below; it reads l.grad (complete at its last writer's event) and the
-          // forward activations, writes only its own gradients and lane 1's workspace (the
+          // wgrad lane: a lane-0 layer's weight gradient on its own stream, overlapping its
+          // dgrad and the layers below; it reads l.grad (complete at its last writer's event)
+          // and the forward activations, writes only its own gradients and workspace (the
           // overlapped-average path keeps it on the layer's lane: the bucket update follows)
           const bool wl = ln.on && net->wgrad_lane && !ov && ln.lane(li) == 0;
           cudaStream_t sw = s;
           if (wl) {
-            sw = net->lane_stream[1];
+            sw = net->lane_stream[psg_net::kWgLane];
             if (summed)
               PSG_CUDA(cudaStreamWaitEvent(sw, net->ev_sum[li], 0));
             else if (last_writer[li] >= 0)
               PSG_CUDA(cudaStreamWaitEvent(sw, net->ev_bwd[last_writer[li]], 0));
           }
           conv_wgrad(g, src.out, l.grad, net->g + k.int_off, net->g + b.int_off,
-                     wl ? net->ws_lane[1] : ln.ws(li), l.col, net->mode, sw);
+                     wl ? net->ws_lane[psg_net::kWgLane] : ln.ws(li), l.col, net->mode, sw);
           const int c = conv_launches(g, 2, net->mode);
           sc.done(c);
           launches += c;

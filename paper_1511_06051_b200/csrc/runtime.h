@@ -115,18 +115,21 @@ struct psg_net {
   // of its inputs (forward) / of the last writer of the gradient it reads or accumulates into
   // (backward) when they ran on another lane; each lane has its own GEMM workspace.  The
   // launch order per buffer is unchanged, so results are bitwise those of one stream.
-  static constexpr int kLanes = 4;
+  static constexpr int kLanes = 4;             // branch lanes (0 = stream)
+  static constexpr int kWgLane = kLanes;       // the wgrad lane's own stream
+  static constexpr int kStreams = kLanes + 1;
   bool lanes_on = false;
   bool fanout = false;                // branch lanes active (some layer fans out)
   std::vector<cudaEvent_t> ev_sum;    // per layer: its scratch gradients summed
   // wgrad lane (PSG_WGRAD_LANE, default on): the weight gradients of lane-0 layers run on
-  // lane 1 — after the last writer of the gradient they read — overlapping the dgrad chain
+  // their own stream (kWgLane) — after the last writer of the gradient they read —
+  // overlapping the dgrad chain
   bool wgrad_lane = false;
   std::vector<int> lane_of;
-  cudaStream_t lane_stream[kLanes] = {};
-  cudaEvent_t lane_fork = nullptr, lane_join[kLanes] = {};
+  cudaStream_t lane_stream[kStreams] = {};
+  cudaEvent_t lane_fork = nullptr, lane_join[kStreams] = {};
   std::vector<cudaEvent_t> ev_fwd, ev_bwd;
-  psg::Workspace ws_lane[kLanes];
+  psg::Workspace ws_lane[kStreams];
   size_t cap = 0;       // batch capacity of the activation buffers
   size_t last_n = 0;    // batch of the last forward
   // training stream (ShardBatchIterator, data.hpp:312-351)
