@@ -347,6 +347,14 @@ bool fuse_wgrad_bias() {  // PSG_TC_WGRAD_BIAS=0: separate bias_grad passes (A/B
   return v;
 }
 
+bool bias_tile_enabled() {  // PSG_TC_BIAS_TILE=0: no extra N tile for the bias chunk (A/B)
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_TC_BIAS_TILE");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 // TMA-store epilogue staging chunks per epilogue warp (PSG_TC_EPI_TMA: 0 = direct row stores
 // in every epilogue, 1 or 2 chunks; two let a chunk's smem writes overlap the previous
 // chunk's store but take 16 KB more from the stage ring)
@@ -408,6 +416,7 @@ void finish_args(TcArgs& a, int kblk, int sms) {
     a.n_tile = std::min(256, (a.n_tile + 63) / 64 * 64);  // pad: the extra columns read 0
     a.n_tiles = (a.n_valid + a.n_tile - 1) / a.n_tile;
   }
+  if (a.bias_chunk && a.n_tiles * (a.n_tile / 32) <= a.bias_chunk) a.bias_chunk = 0;
   a.b_cols = a.pair ? a.n_tile / 2 : a.n_tile;
   a.m_units = a.pair ? (a.m_tiles + 1) / 2 : a.m_tiles;
   const int nb = b_mn ? (a.b_cols + 31) / 32 * 32 : a.b_cols;
@@ -897,6 +906,16 @@ bool plan_wgrad(const ConvGeom& g, TcArgs& a, int& kblk) {
       if (a.n_tiles * (a.n_tile / 32) <= chunks && wider <= 256 &&
           10 * (128 + wider) <= 11 * (128 + a.n_tile))
         a.n_tile = wider;
+      // (or, one filter tile, one more N tile: the bias pass's dY re-read and its two
+      // launches traded for a second read of the dY tiles — GoogLeNet's 1x1 wgrads over 256
+      // / 512 channels)
+      if (a.n_tiles * (a.n_tile / 32) <= chunks && a.m_tiles == 1 && bias_tile_enabled()) {
+        const int nt = a.n_tiles + 1, w = 32 * ((chunks + 1 + nt - 1) / nt);
+        if (w <= 256) {
+          a.n_tiles = nt;
+          a.n_tile = w;
+        }
+      }
       if (a.n_tiles * (a.n_tile / 32) > chunks) a.bias_chunk = chunks;
     }
   }

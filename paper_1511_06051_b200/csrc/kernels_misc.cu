@@ -376,6 +376,68 @@ __global__ void concat_split_k(const V* __restrict__ dy, int ctot, int off, V* _
     dx[i] = accumulate ? dx[i] + v : v;
   }
 }
+// One launch over every (pixel, vector) of the concat: segment j owns vectors
+// [off[j], off[j + 1]) of a pixel (off[k] = ctot); writes / reads coalesced over the concat row.
+template <typename V>
+struct ConcatAll {
+  const V* src[kConcatMax];
+  V* dst[kConcatMax];
+  const V* mask[kConcatMax];
+  int ci[kConcatMax];
+  int off[kConcatMax + 1];
+  int acc[kConcatMax];
+  int k;
+};
+template <typename V>
+__device__ __forceinline__ int concat_seg(const ConcatAll<V>& a, uint32_t c) {
+  int j = 0;
+  while (j + 1 < a.k && c >= static_cast<uint32_t>(a.off[j + 1])) ++j;
+  return j;
+}
+template <typename V>
+__global__ void concat_copy_all_k(ConcatAll<V> a, V* __restrict__ out, int ctot, uint32_t total) {
+  pdl_enter();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t p = i / ctot, c = i - p * ctot;
+    const int j = concat_seg(a, c);
+    out[i] = a.src[j][p * a.ci[j] + (c - a.off[j])];
+  }
+}
+template <typename V>
+__global__ void concat_split_all_k(const V* __restrict__ dy, ConcatAll<V> a, int ctot,
+                                   uint32_t total) {
+  pdl_enter();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t p = i / ctot, c = i - p * ctot;
+    const int j = concat_seg(a, c);
+    V* dx = a.dst[j];
+    if (!dx) continue;
+    const uint32_t q = p * a.ci[j] + (c - a.off[j]);
+    V v = dy[i];
+    if (a.mask[j]) v = relu_gate(__ldg(a.mask[j] + q), v);
+    dx[q] = a.acc[j] ? dx[q] + v : v;
+  }
+}
+template <typename V>
+bool concat_pack(const ConcatSeg* seg, int k, int ctot, int vw, ConcatAll<V>& a) {
+  if (k < 1 || k > kConcatMax || ctot % vw) return false;
+  a.k = k;
+  int expect = 0;
+  for (int j = 0; j < k; ++j) {
+    if (seg[j].ci % vw || seg[j].off % vw || seg[j].off != expect) return false;
+    for (int i = 0; i < j; ++i)
+      if (seg[j].dst && seg[j].dst == seg[i].dst) return false;
+    a.src[j] = reinterpret_cast<const V*>(seg[j].src);
+    a.dst[j] = reinterpret_cast<V*>(seg[j].dst);
+    a.mask[j] = reinterpret_cast<const V*>(seg[j].mask);
+    a.ci[j] = seg[j].ci / vw;
+    a.off[j] = seg[j].off / vw;
+    a.acc[j] = seg[j].acc ? 1 : 0;
+    expect += seg[j].ci;
+  }
+  a.off[k] = ctot / vw;
+  return expect == ctot;
+}
 unsigned concat_blocks(size_t total) {
   return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((total + 255) / 256, 148 * 16)));
 }
@@ -415,6 +477,44 @@ void concat_split(const float* dy, int ctot, int off, float* dx, int ci, size_t 
              accumulate ? 1 : 0, relu_mask);
   }
   PSG_CUDA(cudaGetLastError());
+}
+
+bool concat_copy_all(const ConcatSeg* seg, int k, float* out, int ctot, size_t pixels,
+                     cudaStream_t s) {
+  concat_total(pixels, ctot);
+  ConcatAll<float4> a4;
+  ConcatAll<float> a1;
+  if (concat_pack(seg, k, ctot, 4, a4)) {
+    const uint32_t total = static_cast<uint32_t>(pixels * ctot / 4);
+    launch_k(concat_copy_all_k<float4>, concat_blocks(total), 256, 0, s, a4,
+             reinterpret_cast<float4*>(out), ctot / 4, total);
+  } else if (concat_pack(seg, k, ctot, 1, a1)) {
+    const uint32_t total = static_cast<uint32_t>(pixels * ctot);
+    launch_k(concat_copy_all_k<float>, concat_blocks(total), 256, 0, s, a1, out, ctot, total);
+  } else {
+    return false;
+  }
+  PSG_CUDA(cudaGetLastError());
+  return true;
+}
+
+bool concat_split_all(const float* dy, int ctot, const ConcatSeg* seg, int k, size_t pixels,
+                      cudaStream_t s) {
+  concat_total(pixels, ctot);
+  ConcatAll<float4> a4;
+  ConcatAll<float> a1;
+  if (concat_pack(seg, k, ctot, 4, a4)) {
+    const uint32_t total = static_cast<uint32_t>(pixels * ctot / 4);
+    launch_k(concat_split_all_k<float4>, concat_blocks(total), 256, 0, s,
+             reinterpret_cast<const float4*>(dy), a4, ctot / 4, total);
+  } else if (concat_pack(seg, k, ctot, 1, a1)) {
+    const uint32_t total = static_cast<uint32_t>(pixels * ctot);
+    launch_k(concat_split_all_k<float>, concat_blocks(total), 256, 0, s, dy, a1, ctot, total);
+  } else {
+    return false;
+  }
+  PSG_CUDA(cudaGetLastError());
+  return true;
 }
 
 void argmax_count(const float* probs, const int32_t* labels, int n, int C,

@@ -62,6 +62,12 @@ double conv_flops(const psg_net* net, const LayerRt& l, size_t n) {
   return 2.0 * macs;
 }
 
+// PSG_CONCAT_SINGLE=0: one concat copy / split launch per input (A/B; read when recording)
+bool concat_single() {
+  const char* e = std::getenv("PSG_CONCAT_SINGLE");
+  return !e || std::atoi(e) != 0;
+}
+
 double act_bytes(const LayerRt& l, size_t n) { return 4.0 * static_cast<double>(n) * l.vol(); }
 
 // Branch lanes (psg_net::lane_of), off when profiling per op (the timer's events are on the
@@ -257,12 +263,22 @@ int run_forward(psg_net* net, size_t n, bool train, bool seed_grad, OpTimer* tim
       case PSG_LAYER_CONCAT: {
         const size_t pixels = n * static_cast<size_t>(l.H) * l.W;
         Scope sc(timer, nm.c_str(), lid, 1, 0.0, 2 * act_bytes(l, n));
-        for (size_t i = 0; i < l.inputs.size(); ++i) {
+        ConcatSeg seg[kConcatMax];
+        const int k = static_cast<int>(l.inputs.size());
+        for (int i = 0; i < k && i < kConcatMax; ++i) {
           const LayerRt& x = net->L[l.inputs[i]];
-          concat_copy(x.out, x.C, l.out, l.C, l.coff[i], pixels, s);
+          seg[i] = {x.out, nullptr, nullptr, x.C, l.coff[i], false};
         }
-        sc.done(static_cast<int>(l.inputs.size()));
-        launches += static_cast<int>(l.inputs.size());
+        int c = 1;
+        if (!concat_single() || !concat_copy_all(seg, k, l.out, l.C, pixels, s)) {
+          for (int i = 0; i < k; ++i) {
+            const LayerRt& x = net->L[l.inputs[i]];
+            concat_copy(x.out, x.C, l.out, l.C, l.coff[i], pixels, s);
+          }
+          c = k;
+        }
+        sc.done(c);
+        launches += c;
         break;
       }
     }
@@ -356,23 +372,38 @@ int run_backward(psg_net* net, size_t n, OpTimer* timer, RoundOverlap* ov) {
     if (l.kind == PSG_LAYER_CONCAT) {  // dx_i (+)= dy[:, off_i : off_i + C_i]
       const size_t pixels = n * static_cast<size_t>(l.H) * l.W;
       Scope sc(timer, (std::string(l.d.name) + ".bwd").c_str(), li, 5, 0.0, 2 * act_bytes(l, n));
+      // one launch for every branch (concat_split_all), else one per branch
+      const int k = static_cast<int>(l.inputs.size());
+      std::vector<ConcatSeg> seg(k);
       int c = 0;
-      for (size_t i = 0; i < l.inputs.size(); ++i) {
+      for (int i = 0; i < k; ++i) {
         const int in = l.inputs[i];
         LayerRt& x = net->L[in];
+        seg[i] = {nullptr, nullptr, nullptr, x.C, l.coff[i], false};
         if (x.kind == PSG_LAYER_DATA) continue;
         const int ri = foldable_relu_input(net, in);
         if (ri >= 0) {  // the branch's ReLU backward folded into the split (mask by its output)
-          const int pi2 = net->L[ri].inputs[0];
-          const Dst d = dest(pi2);
-          concat_split(l.grad, l.C, l.coff[i], d.p, x.C, pixels, d.acc, s, x.out);
+          const Dst d = dest(net->L[ri].inputs[0]);
+          seg[i].dst = d.p;
+          seg[i].acc = d.acc;
+          seg[i].mask = x.out;
           relu_folded[ri] = 1;
           written[in] = 1;
         } else {
           const Dst d = dest(in);
-          concat_split(l.grad, l.C, l.coff[i], d.p, x.C, pixels, d.acc, s);
+          seg[i].dst = d.p;
+          seg[i].acc = d.acc;
         }
         ++c;
+      }
+      if (c > 0 && concat_single() &&
+          concat_split_all(l.grad, l.C, seg.data(), k, pixels, s)) {
+        c = 1;
+      } else {
+        for (int i = 0; i < k; ++i)
+          if (seg[i].dst)
+            concat_split(l.grad, l.C, seg[i].off, seg[i].dst, seg[i].ci, pixels, seg[i].acc, s,
+                         seg[i].mask);
       }
       sc.done(c);
       launches += c;

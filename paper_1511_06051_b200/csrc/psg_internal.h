@@ -214,6 +214,22 @@ void concat_copy(const float* in, int ci, float* out, int ctot, int off, size_t 
 // relu_mask: a folded ReLU backward (dx (+)= relu_mask > 0 ? dy slice : 0)
 void concat_split(const float* dy, int ctot, int off, float* dx, int ci, size_t pixels,
                   bool accumulate, cudaStream_t s, const float* relu_mask = nullptr);
+// All inputs of a concat in one launch (same values as the per-input calls above).
+// ConcatSeg i: channels [off_i, off_i + ci) of the concat; forward reads `src`; backward
+// writes dx (+)= the slice into `dst` (skipped when null; `mask` = a folded ReLU backward).
+// k <= kConcatMax segments, every dst distinct; false = not applicable (caller loops).
+constexpr int kConcatMax = 8;
+struct ConcatSeg {
+  const float* src;
+  float* dst;
+  const float* mask;
+  int ci, off;
+  bool acc;
+};
+bool concat_copy_all(const ConcatSeg* seg, int k, float* out, int ctot, size_t pixels,
+                     cudaStream_t s);
+bool concat_split_all(const float* dy, int ctot, const ConcatSeg* seg, int k, size_t pixels,
+                      cudaStream_t s);
 void argmax_count(const float* probs, const int32_t* labels, int n, int C,
                   unsigned long long* correct, cudaStream_t s);
 

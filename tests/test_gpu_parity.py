@@ -361,6 +361,45 @@ def test_lanes_are_bitwise_neutral(gpu, oracle_lib, name, precision, fuse, monke
     assert out[0][1] == out[1][1]
 
 
+def _concat_edge_net(b):
+    """A concat over the data layer (no gradient), a ReLU'd branch taken twice (the same
+    gradient written by two slices: per-slice launches) and an odd channel count (scalar
+    path)."""
+    return ns.NetSpec([
+        ns.data_layer("data", b, 3, 6, 6), ns.label_layer("label", b),
+        ns.conv_layer("a", "data", 1, 1, 4), ns.relu_layer("ra", "a"),
+        ns.conv_layer("b", "data", 3, 3, 5, pad=1),
+        ns.concat_layer("cat", ["data", "ra", "b", "ra"]),
+        ns.pool_layer("p", "cat", 3, 3, 2, 2),
+        ns.linear_layer("out", "p", 10), ns.softmax_loss_layer("loss", "out", "label")])
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("name", ["inception", "concat_edge"])
+@pytest.mark.parametrize("lanes", ["1", "0"])
+def test_single_launch_concat_is_bitwise_neutral(gpu, oracle_lib, name, precision, lanes,
+                                                 monkeypatch):
+    """The concat forward and its backward split as ONE launch over all inputs
+    (concat_copy_all / concat_split_all) train bitwise like one launch per input
+    (PSG_CONCAT_SINGLE=0), with and without branch lanes."""
+    from paper_1511_06051_b200 import data
+    spec = _inception_net(6) if name == "inception" else _concat_edge_net(6)
+    d = spec.data_spec().shape
+    img, lab = oracle_lib.generate_synthetic(10, d[1], d[2], d[3], 6, 2.0, 12345, 0)
+    ds = data.Dataset(f32(img), lab, 10)
+    monkeypatch.setenv("PSG_LANES", lanes)
+    out = []
+    for single in ("1", "0"):
+        monkeypatch.setenv("PSG_CONCAT_SINGLE", single)
+        net = gpu.Net(spec, 3, precision=precision)
+        net.set_sgd(gpu.SgdOptions(0.01, 0.9, 0.001))
+        net.set_training_data(data.make_worker_iterator(data.shard(ds, 1, 1), 0, d[0], 1))
+        net.train(3)
+        out.append((net.get_weights_flat(), net.last_loss()))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 def _s2d_net(b):
     """A strided 3-channel first conv (the space-to-depth route in TF32: the device stream
     gathers straight into x', host batches are staged NHWC then rearranged), then
