@@ -185,7 +185,7 @@ template <typename V, int KS, int SS>
 __global__ void __launch_bounds__(256) pool_bwd_k(PoolGeom g, const V* __restrict__ dy,
                                                   const typename RouteOf<V>::T* __restrict__ route,
                                                   V* __restrict__ dx, int accumulate, int cv,
-                                                  const V* __restrict__ mask) {
+                                                  const V* __restrict__ mask, int loads_first) {
   pdl_enter();
   constexpr int L = RouteOf<V>::n;
   const int kh = KS > 0 ? KS : g.kh, kw = KS > 0 ? KS : g.kw;
@@ -198,6 +198,69 @@ __global__ void __launch_bounds__(256) pool_bwd_k(PoolGeom g, const V* __restric
   const size_t xbase = static_cast<size_t>(blockIdx.x) * g.W * cv;
   const int total = g.W * cv, step_c = blockDim.x % cv, step_w = blockDim.x / cv;
   int c = threadIdx.x % cv, w = threadIdx.x / cv;
+  if constexpr (KS > 0) {
+    if (g.method == PSG_POOL_MAX && loads_first) {
+      // every covering window's dy and route loaded before any is used (NW x NW candidates,
+      // predicated), then summed in the same ascending (oh, ow) order as the loop below
+      constexpr int NW = (KS + SS - 1) / SS;
+      using RT = typename RouteOf<V>::T;
+      for (int j = threadIdx.x; j < total; j += blockDim.x) {
+        const int owl = max(0, (w + g.pw - kw + sw) / sw);
+        const int owh = min(g.OW - 1, (w + g.pw) / sw);
+        V dd[NW][NW];
+        RT rr[NW][NW];
+        bool ok[NW][NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i)
+#pragma unroll
+          for (int q = 0; q < NW; ++q) {
+            const int oh = ohl + i, ow = owl + q;
+            const int hs0 = oh * sh - g.ph, ws0 = ow * sw - g.pw;
+            ok[i][q] = oh <= ohh && ow <= owh && h >= hs0 && h < hs0 + kh && w >= ws0 &&
+                       w < ws0 + kw;
+            if (ok[i][q]) {
+              const uint32_t o = (obase + oh * g.OW + ow) * cv + c;
+              dd[i][q] = __ldg(dy + o);
+              rr[i][q] = __ldg(route + o);
+            }
+          }
+        V m, o;
+        if (mask) m = __ldg(mask + xbase + j);
+        if (accumulate) o = dx[xbase + j];
+        V acc;
+#pragma unroll
+        for (int e = 0; e < L; ++e) comp(acc, e) = 0.f;
+#pragma unroll
+        for (int i = 0; i < NW; ++i)
+#pragma unroll
+          for (int q = 0; q < NW; ++q) {
+            const int hs0 = (ohl + i) * sh - g.ph, ws0 = (owl + q) * sw - g.pw;
+            const uint8_t want = static_cast<uint8_t>((h - hs0) * kw + (w - ws0));
+            if (!ok[i][q]) continue;
+#pragma unroll
+            for (int e = 0; e < L; ++e)
+              if (rcomp(rr[i][q], e) == want) comp(acc, e) += comp(dd[i][q], e);
+          }
+        if (mask) {
+#pragma unroll
+          for (int e = 0; e < L; ++e)
+            if (!(comp(m, e) > 0.f)) comp(acc, e) = 0.f;
+        }
+        if (accumulate) {
+#pragma unroll
+          for (int e = 0; e < L; ++e) comp(acc, e) += comp(o, e);
+        }
+        dx[xbase + j] = acc;
+        c += step_c;
+        w += step_w;
+        if (c >= cv) {
+          c -= cv;
+          ++w;
+        }
+      }
+      return;
+    }
+  }
   for (int j = threadIdx.x; j < total; j += blockDim.x) {
     const int owl = max(0, (w + g.pw - kw + sw) / sw);
     const int owh = min(g.OW - 1, (w + g.pw) / sw);
@@ -842,6 +905,11 @@ void pool_fwd(const PoolGeom& g, const float* x, float* y, uint8_t* route, cudaS
 
 void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* dx,
               bool accumulate, cudaStream_t s, const float* relu_mask) {
+  // PSG_POOL_BWD_LOADS_FIRST=0: the window loop for the compile-time 3x3 windows too (A/B)
+  static const int loads_first = [] {
+    const char* e = std::getenv("PSG_POOL_BWD_LOADS_FIRST");
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : 1;
+  }();
   checked32(static_cast<size_t>(g.n) * g.H * g.W * g.C, "pool");
   const unsigned rows = static_cast<unsigned>(g.n) * g.H;
   const bool k3 = g.kh == 3 && g.kw == 3 && g.sh == g.sw && (g.sh == 1 || g.sh == 2);
@@ -850,11 +918,11 @@ void pool_bwd(const PoolGeom& g, const float* dy, const uint8_t* route, float* d
                     : g.sh == 2 ? pool_bwd_k<float4, 3, 2> : pool_bwd_k<float4, 3, 1>;
     launch_k(kern, rows, 256, 0, s, g, reinterpret_cast<const float4*>(dy),
              reinterpret_cast<const uchar4*>(route), reinterpret_cast<float4*>(dx), accumulate,
-             g.C / 4, reinterpret_cast<const float4*>(relu_mask));
+             g.C / 4, reinterpret_cast<const float4*>(relu_mask), loads_first);
   } else {
     auto kern = !k3 ? pool_bwd_k<float, 0, 0>
                     : g.sh == 2 ? pool_bwd_k<float, 3, 2> : pool_bwd_k<float, 3, 1>;
-    launch_k(kern, rows, 256, 0, s, g, dy, route, dx, accumulate, g.C, relu_mask);
+    launch_k(kern, rows, 256, 0, s, g, dy, route, dx, accumulate, g.C, relu_mask, loads_first);
   }
   PSG_CUDA(cudaGetLastError());
 }
