@@ -366,7 +366,15 @@ int epi_tma_bufs() {
   return v;
 }
 
-bool want_pair(const TcArgs& a) {
+bool pair_k16_off() {  // PSG_TC_PAIR_K16=1: pairs for narrow 16-float-K-block GEMMs too (A/B)
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_TC_PAIR_K16");
+    return !e || std::atoi(e) == 0;
+  }();
+  return v;
+}
+
+bool want_pair(const TcArgs& a, int kblk) {
   static const int env = [] {
     const char* e = std::getenv("PSG_TC_PAIR");
     return e ? std::atoi(e) : 1;
@@ -389,6 +397,9 @@ bool want_pair(const TcArgs& a) {
     return e ? std::atoi(e) : 48;
   }();
   if (a.n_tile < min_n) return false;
+  // 16-float K blocks and N <= 64 (GoogLeNet's space-to-depth conv1 fprop: x' at 16
+  // channels, 64 filters): each stage is too small for the pair to pay, 101 -> 87 us single
+  if (kblk == 16 && a.n_tile <= 64 && pair_k16_off()) return false;
   // small GEMMs: halving the number of work units costs more in load balance than the
   // pair gains (cifar10_quick); want >= 2 waves of clusters
   const long long units = static_cast<long long>((a.m_tiles + 1) / 2) * a.n_tiles * a.G * a.taps;
@@ -411,7 +422,7 @@ int split_charge() {
 
 void finish_args(TcArgs& a, int kblk, int sms) {
   const bool b_mn = a.b_mode != B_2D_K && a.b_mode != B_3D_K;
-  a.pair = want_pair(a) ? 1 : 0;
+  a.pair = want_pair(a, kblk) ? 1 : 0;
   if (a.pair && b_mn && a.n_tile % 64) {
     a.n_tile = std::min(256, (a.n_tile + 63) / 64 * 64);  // pad: the extra columns read 0
     a.n_tiles = (a.n_valid + a.n_tile - 1) / a.n_tile;
