@@ -406,7 +406,14 @@ bool want_pair(const TcArgs& a, int kblk) {
   // long-K linear layers (AlexNet fc6 / fc7 at b = 256: two M tiles, split K restores the
   // parallelism): the pair reads each weight tile from L2 once instead of per M tile,
   // fc6 fwd / dgrad -10%
-  const bool long_linear = (a.a_mode == A_2D_K || a.a_mode == A_2D_MN) && a.kblocks >= 64;
+  // (MN-major A — the wgrads over linear pixels — from 512 K blocks: GoogLeNet's 14 x 14
+  // wgrads at 196 lose 5-10% as pairs, AlexNet's conv2-5 wgrads at 1352+ gain)
+  static const int mn_kb = [] {  // PSG_TC_PAIR_MN_KB: that threshold (A/B)
+    const char* e = std::getenv("PSG_TC_PAIR_MN_KB");
+    return e ? std::atoi(e) : 512;
+  }();
+  const bool long_linear = (a.a_mode == A_2D_K && a.kblocks >= 64) ||
+                           (a.a_mode == A_2D_MN && a.kblocks >= mn_kb);
   return env > 1 || units >= sm_count() || long_linear;
 }
 
