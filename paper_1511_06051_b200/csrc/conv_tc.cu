@@ -400,6 +400,13 @@ bool want_pair(const TcArgs& a, int kblk) {
   // 16-float K blocks and N <= 64 (GoogLeNet's space-to-depth conv1 fprop: x' at 16
   // channels, 64 filters): each stage is too small for the pair to pay, 101 -> 87 us single
   if (kblk == 16 && a.n_tile <= 64 && pair_k16_off()) return false;
+  // short K (GoogLeNet's 1x1 convs over 64 / 192 channels: 2 / 6 K blocks): the pair's
+  // cluster overhead is not repaid; GoogLeNet +0.4%
+  static const int k_kb = [] {  // PSG_TC_PAIR_K_KB: fewest K blocks for a K-major-A pair
+    const char* e = std::getenv("PSG_TC_PAIR_K_KB");
+    return e ? std::atoi(e) : 8;
+  }();
+  if (a.a_mode != A_2D_MN && a.kblocks < k_kb) return false;
   // small GEMMs: halving the number of work units costs more in load balance than the
   // pair gains (cifar10_quick); want >= 2 waves of clusters
   const long long units = static_cast<long long>((a.m_tiles + 1) / 2) * a.n_tiles * a.G * a.taps;
