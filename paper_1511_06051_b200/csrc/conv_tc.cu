@@ -777,8 +777,15 @@ bool tc_dgrad_wt(const ConvGeom& g) {
     const char* e = std::getenv("PSG_TC_DGRAD_WT");
     return e ? std::atoi(e) != 0 : true;
   }();
+  // small layers (GoogLeNet's 28 x 28 and smaller, cifar10_quick): the transpose launch
+  // costs more than the MN-major B's padding; PSG_TC_DGRAD_WT_MIN_PX: the pixel threshold
+  static const long long min_px = [] {
+    const char* e = std::getenv("PSG_TC_DGRAD_WT_MIN_PX");
+    return e ? std::atoll(e) : 65536LL;
+  }();
   return env && !is_linear(g) && g.sh == 1 && g.sw == 1 && g.Cgs() % 64 != 0 &&
-         g.Cgs() % 16 == 0 && g.Fg() % 32 == 0;
+         g.Cgs() % 16 == 0 && g.Fg() % 32 == 0 &&
+         static_cast<long long>(g.n) * g.H * g.W >= min_px;
 }
 
 namespace {

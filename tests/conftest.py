@@ -8,6 +8,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# The small parity nets take the K-major transposed-weight dgrad (tc_dgrad_wt) wherever
+# it is legal, as AlexNet's conv2 does at full size (by default only layers of >= 64K
+# pixels do); test_gpu_tf32.py::test_tf32_parity_default_routes re-runs the parity
+# cases with the production defaults in a fresh process.
+if not os.environ.get("PSG_TEST_DEFAULT_ROUTES"):
+    os.environ.setdefault("PSG_TC_DGRAD_WT_MIN_PX", "0")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs under gpurun)")

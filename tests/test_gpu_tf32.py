@@ -108,3 +108,20 @@ def test_tf32_train_steps_track_strict(gpu, oracle_lib):
     # multi-step trajectories drift (SURVEY §7 hard part 3); the per-step bar is TF32
     assert max_relative_deviation(nets[1].get_weights_flat(), nets[0].get_weights_flat(),
                                   nets[0].segments()) <= 5 * TF32
+
+
+def test_tf32_parity_default_routes():
+    """The per-layer TF32 parity cases and the tiny-AlexNet parity again, in a fresh process
+    with the production route defaults (conftest.py points the small parity nets at the
+    transposed-weight dgrad; by default layers under 64K pixels use the MN-major W^T B)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PSG_TEST_DEFAULT_ROUTES="1")
+    env.pop("PSG_TC_DGRAD_WT_MIN_PX", None)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        "tests/test_gpu_tf32.py::test_tf32_per_layer_parity",
+                        "tests/test_gpu_alexnet.py::test_alexnet_per_layer_parity"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
