@@ -131,7 +131,9 @@ bool s2d_route(const ConvGeom& g) {
 // dataset (row idx[cursor * batch + b], channel stride src_cs) and the block of row hs = 0
 // also copies the label: the batch gather and the space-to-depth rearrangement in one pass
 // (data.hpp:292-304 gather_batch).
-template <int RUN>  // RUN = s * C when it is 12 (AlexNet conv1: s = 4, C = 3): float4 stores
+// RUN = s * C when it is 12 (AlexNet conv1: s = 4, C = 3): float4 stores; 6 (GoogLeNet
+// conv1: s = 2, C = 3): float2 stores
+template <int RUN>
 __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, ConvGeom g,
                                                ConvGeom q, float* __restrict__ xs,
                                                const uint32_t* __restrict__ idx,
@@ -172,6 +174,19 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
       o4[0] = make_float4(v[0], v[1], v[2], v[3]);
       o4[1] = make_float4(v[4], v[5], v[6], v[7]);
       o4[2] = make_float4(v[8], v[9], v[10], v[11]);
+    } else if constexpr (RUN == 6) {
+      float v[6];
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const int iw = iw0 + dx;
+        const bool ok = row_ok && iw >= 0 && iw < g.W;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[dx * 3 + c] = ok ? __ldg(xr + iw * ps + c * cst) : 0.f;
+      }
+      float2* o2 = reinterpret_cast<float2*>(o);
+      o2[0] = make_float2(v[0], v[1]);
+      o2[1] = make_float2(v[2], v[3]);
+      o2[2] = make_float2(v[4], v[5]);
     } else {
       for (int dx = 0; dx < s; ++dx) {
         const int iw = iw0 + dx;
@@ -182,7 +197,7 @@ __global__ void __launch_bounds__(256) s2d_x_k(const float* __restrict__ x, Conv
     if (dy == s - 1) {
       float* z = out + ws * q.cs_in;
       int cp = s * run;
-      if (RUN == 12)  // 16-byte aligned channel padding (s * run and cs_in multiples of 4)
+      if (RUN > 0)  // 16-byte aligned channel padding (s * run and cs_in multiples of 4)
         for (; cp + 4 <= q.cs_in; cp += 4)
           *reinterpret_cast<float4*>(z + cp) = make_float4(0.f, 0.f, 0.f, 0.f);
       for (; cp < q.cs_in; ++cp) z[cp] = 0.f;
@@ -194,7 +209,10 @@ using S2dKernel = void (*)(const float*, ConvGeom, ConvGeom, float*, const uint3
                           int, int, const int32_t*, int32_t*);
 S2dKernel s2d_kernel(const ConvGeom& g, const ConvGeom& q) {
   // float4 runs: 12-float runs at 16-byte aligned offsets (cs_in % 4 == 0 by construction)
-  return g.sh * g.Cgs() == 12 && q.cs_in % 4 == 0 ? s2d_x_k<12> : s2d_x_k<0>;
+  // (6-float runs at 8-byte aligned offsets)
+  if (q.cs_in % 4 == 0 && g.Cgs() == 3 && g.sh == 4) return s2d_x_k<12>;
+  if (q.cs_in % 4 == 0 && g.Cgs() == 3 && g.sh == 2) return s2d_x_k<6>;
+  return s2d_x_k<0>;
 }
 
 // W'[f][tu][tv][c'] = W[f][s*tu + dy][s*tv + dx][c] (0 past the kernel / past s*s*C)
