@@ -328,6 +328,21 @@ bool use_tc(const ConvGeom& g, int which, Mode m) {
   return m == Mode::Tf32 && tc_supported(g, which);
 }
 
+// A 1x1 / stride-1 / unpadded conv over whole 32-channel blocks is a linear layer over its
+// pixels: its wgrad as the linear plan (dY^T X, the fprop-style epilogue with TMA stores, the
+// bias as a separate pass) instead of the one-tap multi-tap plan.  PSG_TC_1X1_LINEAR=0: the
+// multi-tap plan (A/B).
+bool wgrad_1x1_linear(const ConvGeom& g, Mode m) {
+  static const bool env = [] {
+    const char* e = std::getenv("PSG_TC_1X1_LINEAR");
+    return !e || std::atoi(e) != 0;
+  }();
+  return env && m == Mode::Tf32 && !is_linear(g) && g.G == 1 && g.kh == 1 && g.kw == 1 &&
+         g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.H == g.OH && g.W == g.OW &&
+         g.cs_in == g.Cgs() && g.Kp() == g.cs_in && g.cs_in % 32 == 0 &&
+         tc_supported(col_geom(g), 2);
+}
+
 }  // namespace
 
 bool conv_s2d_input(const ConvGeom& g, Mode m) { return m == Mode::Tf32 && s2d_route(g); }
@@ -423,6 +438,8 @@ void conv_wgrad(const ConvGeom& g, const float* x, const float* dy, float* dw, f
   } else if (m == Mode::Tf32 && col && wgrad_col_route(g)) {
     if (!fprop_col_route(g)) im2col(g, x, col, s);  // else written by this step's fprop
     tc_wgrad_col(g, col, dy, dw, db, ws, s);
+  } else if (wgrad_1x1_linear(g, m)) {
+    tc_wgrad(col_geom(g), x, dy, dw, db, ws, s);
   } else if (use_tc(g, 2, m)) {
     tc_wgrad(g, x, dy, dw, db, ws, s);
   } else {
@@ -437,6 +454,7 @@ size_t conv_workspace_elems(const ConvGeom& g, Mode m) {
     if (s2d_route(g)) e = std::max(e, tc_workspace_elems(s2d_geom(g)));
     if (fprop_col_route(g)) e = std::max(e, tc_workspace_elems(col_geom(g)));
     if (wgrad_col_route(g)) e = std::max(e, tc_wgrad_col_ws_elems(g));
+    if (wgrad_1x1_linear(g, m)) e = std::max(e, tc_workspace_elems(col_geom(g)));
   }
   return e;
 }
@@ -448,6 +466,7 @@ int conv_launches(const ConvGeom& g, int which, Mode m) {
     return 1 + tc_launches(col_geom(g), 0);
   if (m == Mode::Tf32 && which == 2 && wgrad_col_route(g))
     return (fprop_col_route(g) ? 0 : 1) + tc_wgrad_col_launches(g);
+  if (which == 2 && wgrad_1x1_linear(g, m)) return tc_launches(col_geom(g), 2);
   if (which != 2 && linear_small(g)) return 1;
   if (use_tc(g, which, m)) return tc_launches(g, which) + (which == 1 && tc_dgrad_wt(g) ? 1 : 0);
   return conv_launches_simt(g, which);

@@ -41,6 +41,14 @@ def tc_nets():
             ns.conv_layer("c1", "r0", 5, 5, 256, pad=2, group=2), ns.relu_layer("r1", "c1"),
             ns.pool_layer("p", "r1", 3, 3, 2, 2, ceil_mode=True),
             ns.linear_layer("fc", "p", 16), ns.softmax_loss_layer("loss", "fc", "label")]),
+        # 1x1 convs over whole 32-channel blocks: the wgrad as a linear layer over pixels
+        # (wgrad_1x1_linear, GoogLeNet's inception 1x1s), beside a 1x1 over 48 channels
+        "conv1x1_linear": ns.NetSpec([
+            ns.data_layer("data", 3, 64, 9, 9), ns.label_layer("label", 3),
+            ns.conv_layer("a", "data", 1, 1, 48), ns.relu_layer("ra", "a"),
+            ns.conv_layer("b", "ra", 1, 1, 32), ns.relu_layer("rb", "b"),
+            ns.conv_layer("c", "rb", 1, 1, 96),
+            ns.linear_layer("fc", "c", 10), ns.softmax_loss_layer("loss", "fc", "label")]),
         "wide_linear": ns.NetSpec([
             ns.data_layer("data", 130, 1, 1, 512), ns.label_layer("label", 130),
             ns.linear_layer("fc1", "data", 320), ns.relu_layer("r", "fc1"),
