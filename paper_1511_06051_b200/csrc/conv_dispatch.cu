@@ -328,18 +328,18 @@ bool use_tc(const ConvGeom& g, int which, Mode m) {
   return m == Mode::Tf32 && tc_supported(g, which);
 }
 
-// A 1x1 / stride-1 / unpadded conv over whole 32-channel blocks is a linear layer over its
+// A 1x1 / stride-1 / unpadded conv (C % 4 == 0) is a linear layer over its
 // pixels: its wgrad as the linear plan (dY^T X, the fprop-style epilogue with TMA stores, the
 // bias as a separate pass) instead of the one-tap multi-tap plan.  PSG_TC_1X1_LINEAR=0: the
 // multi-tap plan (A/B).
 bool wgrad_1x1_linear(const ConvGeom& g, Mode m) {
-  static const bool env = [] {
+  static const int env = [] {  // 1 = whole 32-channel blocks, 2 (default) = any C % 4 == 0
     const char* e = std::getenv("PSG_TC_1X1_LINEAR");
-    return !e || std::atoi(e) != 0;
+    return e ? std::atoi(e) : 2;
   }();
   return env && m == Mode::Tf32 && !is_linear(g) && g.G == 1 && g.kh == 1 && g.kw == 1 &&
          g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.H == g.OH && g.W == g.OW &&
-         g.cs_in == g.Cgs() && g.Kp() == g.cs_in && g.cs_in % 32 == 0 &&
+         g.cs_in == g.Cgs() && g.Kp() == g.cs_in && g.cs_in % (env == 1 ? 32 : 4) == 0 &&
          tc_supported(col_geom(g), 2);
 }
 
