@@ -332,14 +332,28 @@ bool use_tc(const ConvGeom& g, int which, Mode m) {
 // pixels: its wgrad as the linear plan (dY^T X, the fprop-style epilogue with TMA stores, the
 // bias as a separate pass) instead of the one-tap multi-tap plan.  PSG_TC_1X1_LINEAR=0: the
 // multi-tap plan (A/B).
+bool conv1x1_as_linear(const ConvGeom& g, Mode m, int cmod);
 bool wgrad_1x1_linear(const ConvGeom& g, Mode m) {
   static const int env = [] {  // 1 = whole 32-channel blocks, 2 (default) = any C % 4 == 0
     const char* e = std::getenv("PSG_TC_1X1_LINEAR");
     return e ? std::atoi(e) : 2;
   }();
-  return env && m == Mode::Tf32 && !is_linear(g) && g.G == 1 && g.kh == 1 && g.kw == 1 &&
+  return env && conv1x1_as_linear(g, m, env == 1 ? 32 : 4);
+}
+// ... and its fprop / dgrad (linear rows instead of pixel rectangles, the TMA-store epilogue);
+// PSG_TC_1X1_LINEAR_FD=0: the rectangle plans (A/B)
+bool fd_1x1_linear(const ConvGeom& g, Mode m) {
+  static const bool env = [] {
+    const char* e = std::getenv("PSG_TC_1X1_LINEAR_FD");
+    return !e || std::atoi(e) != 0;
+  }();
+  return env && conv1x1_as_linear(g, m, 4) && tc_supported(col_geom(g), 0) &&
+         tc_supported(col_geom(g), 1);
+}
+bool conv1x1_as_linear(const ConvGeom& g, Mode m, int cmod) {
+  return m == Mode::Tf32 && !is_linear(g) && g.G == 1 && g.kh == 1 && g.kw == 1 &&
          g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0 && g.H == g.OH && g.W == g.OW &&
-         g.cs_in == g.Cgs() && g.Kp() == g.cs_in && g.cs_in % (env == 1 ? 32 : 4) == 0 &&
+         g.cs_in == g.Cgs() && g.Kp() == g.cs_in && g.cs_in % cmod == 0 &&
          tc_supported(col_geom(g), 2);
 }
 
@@ -398,6 +412,8 @@ void conv_fprop(const ConvGeom& g, const float* x, const float* w, const float* 
     tc_fprop(col_geom(g), col, w, bias, y, relu, ws, s);
   } else if (linear_small(g)) {  // few-output linear layer: dedicated kernel (any mode)
     conv_fprop_simt(g, x, w, bias, y, relu, ws, s);
+  } else if (fd_1x1_linear(g, m)) {
+    tc_fprop(col_geom(g), x, w, bias, y, relu, ws, s);
   } else if (use_tc(g, 0, m)) {
     tc_fprop(g, x, w, bias, y, relu, ws, s);
   } else {
@@ -411,6 +427,8 @@ void conv_dgrad(const ConvGeom& g, const float* dy, const float* w, float* dx, b
                 const Workspace& ws, Mode m, cudaStream_t s, const float* relu_mask, float* col) {
   if (linear_small(g) && !relu_mask) {
     conv_dgrad_simt(g, dy, w, dx, accumulate, ws, s);
+  } else if (fd_1x1_linear(g, m)) {
+    tc_dgrad(col_geom(g), dy, w, dx, accumulate, ws, s, relu_mask, nullptr);
   } else if (use_tc(g, 1, m)) {
     float* wt = nullptr;
     if (tc_dgrad_wt(g)) {
@@ -454,7 +472,8 @@ size_t conv_workspace_elems(const ConvGeom& g, Mode m) {
     if (s2d_route(g)) e = std::max(e, tc_workspace_elems(s2d_geom(g)));
     if (fprop_col_route(g)) e = std::max(e, tc_workspace_elems(col_geom(g)));
     if (wgrad_col_route(g)) e = std::max(e, tc_wgrad_col_ws_elems(g));
-    if (wgrad_1x1_linear(g, m)) e = std::max(e, tc_workspace_elems(col_geom(g)));
+    if (wgrad_1x1_linear(g, m) || fd_1x1_linear(g, m))
+      e = std::max(e, tc_workspace_elems(col_geom(g)));
   }
   return e;
 }
@@ -467,6 +486,7 @@ int conv_launches(const ConvGeom& g, int which, Mode m) {
   if (m == Mode::Tf32 && which == 2 && wgrad_col_route(g))
     return (fprop_col_route(g) ? 0 : 1) + tc_wgrad_col_launches(g);
   if (which == 2 && wgrad_1x1_linear(g, m)) return tc_launches(col_geom(g), 2);
+  if (which != 2 && fd_1x1_linear(g, m)) return tc_launches(col_geom(g), which);
   if (which != 2 && linear_small(g)) return 1;
   if (use_tc(g, which, m)) return tc_launches(g, which) + (which == 1 && tc_dgrad_wt(g) ? 1 : 0);
   return conv_launches_simt(g, which);
